@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark: fixed-iteration scenario-MPC solves on B200 (BASELINE.json metric).
+
+A step is one SMPC solve: ``--iters`` (500) fixed APG iterations on the
+configs[1] workload (Barcelona-dimension network, horizon 24, 128-scenario
+tree ``[2]*7``, 2,430 nodes, fp64) followed by the duality-gap certificate the
+reference always runs at max_iter, and the control action u0.
+
+* ``value``: APG iterations/s with the instance resident in HBM (device time,
+  CUDA events on the solver's stream, max over ranks).
+* ``e2e``: the same metric through the public API — ``factor_step(inst,
+  structure_from=cache)`` + ``solve(inst, cfg, cache)`` per step, with the
+  per-node inputs in pinned host memory and every result array read back.
+* ``roofline``: the APG iteration (the CUDA graph of all stage kernels)
+  against HBM: algorithmic 10,016 B per node per iteration.
+* ``cpu_baseline``: the oracle port (numpy restatement of the reference) on a
+  bounded sample on this host's cores.
+
+``--impl reference`` times the reference's CPU implementation of the path (the
+oracle port; the Python reference cannot travel to the GPU box) on the same
+config and prints the same JSON line with ``"impl": "reference"``.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "APG iterations/s and ms per SMPC solve (fixed iters) vs scenarios, 1/2/4/8 B200"
+UNIT = "APG iterations/s"
+BYTES_PER_NODE_ITER = 8 * (9 * 63 + 6 * 114 + 1)  # 10,016 B
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--iters", type=int, default=500)
+    ap.add_argument("--cpu-sample-iters", type=int, default=30)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(cfg: str) -> dict:
+    from paper_1904_10548_b200.synthetic import CONFIGS
+    br = CONFIGS[cfg]
+    return {"workload": f"barcelona-63t-114u-88d-17m H=24 tree{br} ({cfg})", "branching": br,
+            "horizon": 24, "fixed_iters": None, "precision": "fp64"}
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        cmd = ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+               "--format=csv,noheader,nounits"]
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(cmd, capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for name, val in zip(names, s[2:]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ dist helpers
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ----------------------------------------------------------- CPU baseline
+
+def cpu_baseline(cfg: str, iters: int, sample_iters: int) -> dict:
+    """Oracle port (numpy restatement of the reference solve) on a bounded
+    sample: `sample_iters` APG iterations + one certificate, extrapolated to
+    one `iters`-iteration solve."""
+    from oracle import port
+    from paper_1904_10548_b200.synthetic import config_instance
+    inst = config_instance(cfg)
+    t0 = time.perf_counter()
+    fac, e_off = port.factor(inst)
+    t_factor = time.perf_counter() - t0
+    gamma = 1.0 / 2.0e9
+    t0 = time.perf_counter()
+    res = port.apg_solve(inst, gamma, max_iter=sample_iters, tol=1e-30,
+                         gap_check_every=sample_iters + 1, fac=fac, e_off=e_off,
+                         reference_cost_accounting=True, final_certificate=True)
+    total = time.perf_counter() - t0
+    per_iter = res.loop_time_s / sample_iters
+    t_cert = total - res.loop_time_s
+    solve_s = iters * per_iter + t_cert
+    threads = os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS")
+    cores = int(threads) if threads else (os.cpu_count() or 1)
+    return {"value": iters / solve_s, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{cfg}: {sample_iters} APG iterations ({per_iter * 1e3:.1f} ms/it) + 1 certificate "
+                      f"({t_cert:.2f} s), extrapolated to a {iters}-iteration solve ({solve_s:.1f} s); "
+                      f"per-node factor part {t_factor * 1e3:.0f} ms; numpy/OpenBLAS fp64",
+            "ms_per_solve_extrapolated": solve_s * 1e3, "ms_per_iteration": per_iter * 1e3}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    W, K = args.warmup, args.steps
+    # each step: a bounded sample (a few iterations + certificate) of the solve
+    sample = max(2, min(args.cpu_sample_iters, 10))
+    vals = []
+    cb = None
+    for i in range(W + K):
+        cb = cpu_baseline(args.config, args.iters, sample)
+        if i >= W:
+            vals.append(cb["value"])
+    value = float(np.median(vals))
+    cfgd = workload(args.config)
+    cfgd["fixed_iters"] = args.iters
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": K, "warmup": W, "ms_per_step": args.iters / value * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfgd,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb["cores"], "kind": "port",
+                             "sample": cb["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- ours
+
+def load_peaks() -> tuple[float, str]:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(cfg: str):
+    """Per-iteration DRAM bytes from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(cfg)
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    world, rank, local = dist_env()
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    from paper_1904_10548_b200 import SolverConfig, estimate_lipschitz, factor_step, solve
+    from paper_1904_10548_b200 import _native as nat
+    from paper_1904_10548_b200 import solver as S
+    from paper_1904_10548_b200.synthetic import config_instance
+
+    S.set_device(local if world > 1 else 0)
+    inst = config_instance(args.config)
+    n = inst.n_nonroot
+    cache = factor_step(inst)
+    L = estimate_lipschitz(cache, inst)
+    gamma = 1.0 / L
+    iters = args.iters
+    cfg = SolverConfig(max_iter=iters, tol=1e-30, gamma=gamma, gap_check_every=iters + 1)
+    ctx = cache._bind()
+    theta = S.theta_sequence(iters)
+    beta = S._beta_table(theta)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
+
+    def device_step():
+        """One solve with the instance resident in HBM; returns (step ms, loop ms)."""
+        ctx.call("wmpc_timer_start")
+        ctx.call("wmpc_apg_begin", float(gamma), iters, nat.ptr(theta), nat.ptr(beta))
+        loop = nat.C.c_float(0.0)
+        ctx.call("wmpc_apg_run_timed", iters, nat.C.byref(loop))
+        S._certificate(ctx)
+        S._read(ctx, inst, True, u0=True, primal=False, avg=False, dual=False)
+        ms = nat.C.c_float(0.0)
+        ctx.call("wmpc_timer_stop", nat.C.byref(ms))
+        return float(ms.value), float(loop.value)
+
+    for _ in range(args.warmup):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        device_step()
+    l0 = nat.load().wmpc_launch_count(ctx.h)
+    step_ms, loop_ms = [], []
+    clocks = ClockSampler(local if world > 1 else 0)
+    barrier(world)
+    torch.cuda.synchronize()
+    with clocks:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            a, b = device_step()
+            step_ms.append(a)
+            loop_ms.append(b)
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = nat.load().wmpc_launch_count(ctx.h) - l0
+    total_ms = max_over_ranks(sum(step_ms), world)
+    loop_total = max_over_ranks(sum(loop_ms), world)
+    K = args.steps
+    value = world * K * iters / (total_ms / 1e3)
+    ms_per_step = total_ms / K
+
+    # roofline: the APG iteration (graph of stage kernels) against HBM
+    t_iter = loop_total / (K * iters) / 1e3
+    alg_bytes = BYTES_PER_NODE_ITER * n
+    peak, peak_src = load_peaks()
+    achieved = alg_bytes / t_iter / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": ncu_traffic(args.config),
+            "kernel": f"APG iteration = CUDA graph of {2 * 24 + 1} launches (k_bwd_stage x24, "
+                      f"k_fwd_stage x24, k_advance)",
+            "algorithmic_bytes_per_launch": alg_bytes, "us_per_iteration": t_iter * 1e6,
+            "peak_source": peak_src}
+
+    # e2e through the public API with pinned inputs
+    e2e = None
+    if not args.no_e2e:
+        from paper_1904_10548_b200.problem import ProblemInstance  # noqa: F401
+        pin = nat.pinned_copy
+        inst.demand = pin(inst.demand)
+        inst.demand_gd = pin(inst.demand_gd)
+        inst.econ = pin(inst.econ)
+        for _ in range(max(1, args.warmup)):
+            c2 = factor_step(inst, structure_from=cache)
+            solve(inst, cfg, cache=c2)
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(K):
+            c2 = factor_step(inst, structure_from=cache)
+            res = solve(inst, cfg, cache=c2)
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+        m = inst.model
+        h2d = 8 * (n * (m.n_demands + m.n_tanks + 2 * m.n_inputs) + m.n_mixing * m.n_demands
+                   + 3 * m.n_tanks + 4 * m.n_inputs + 2 * iters)
+        d2h = 8 * (m.n_inputs + 2 * inst.n_primal + inst.n_dual + 8)
+        e2e = {"value": world * K * iters / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s / K * 1e3,
+               "api": "factor_step(structure_from) + solve() per step"}
+        assert res.iterations == iters
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, iters, args.cpu_sample_iters)
+    if rank == 0:
+        cfgd = workload(args.config)
+        cfgd.update({"fixed_iters": iters, "nodes": n, "gamma": "1/L (device power iteration)",
+                     "l2": "flushed between steps (256 MiB write); one solve's working set is "
+                           "L2-resident by design",
+                     "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                     "step": "500 fixed APG iterations + duality-gap certificate + u0"})
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": cfgd, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clocks.summary(),
+                "loop_ms_per_solve": loop_total / K}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,142 @@
+/*
+ * wmpc.h — C ABI of the B200 scenario-tree dual-APG solver (libwmpc.so).
+ *
+ * The reference (watermpc, /root/reference/pkg/src/watermpc) has no FFI: its
+ * boundary is the Python API of watermpc.solver / watermpc.problem. Each entry
+ * point below replaces one piece of that API; the Python facade
+ * (paper_1904_10548_b200/solver.py) binds them with ctypes.
+ *
+ * Conventions: host pointers are C-contiguous float64 (or int64 for indices),
+ * node-major in breadth-first row order (row r = tree node r+1). Every call
+ * returns 0 on success, a negative WMPC_E_* code otherwise; the message is in
+ * wmpc_last_error(). A context is bound to one CUDA device and one tree
+ * structure and is not thread-safe (one solve per context at a time).
+ */
+#ifndef WMPC_H
+#define WMPC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WMPC_OK 0
+#define WMPC_E_ARG -1        /* bad argument / shape            -> ValueError   */
+#define WMPC_E_CUDA -2       /* CUDA runtime failure            -> RuntimeError */
+#define WMPC_E_INFEASIBLE -3 /* coupling infeasible at a node   -> ValueError   */
+#define WMPC_E_NONFINITE -4  /* non-finite iterate              -> RuntimeError */
+#define WMPC_E_STATE -5      /* call order violated             -> RuntimeError */
+
+typedef struct wmpc_ctx wmpc_ctx;
+
+typedef struct wmpc_dims {
+  int64_t n_nodes;   /* non-root nodes n                           */
+  int32_t horizon;   /* H (stages 1..H)                            */
+  int32_t n_tanks;   /* n_t                                        */
+  int32_t n_inputs;  /* n_u                                        */
+  int32_t n_demands; /* n_d                                        */
+  int32_t n_mixing;  /* n_s (rows of E; may be 0)                  */
+  int32_t device;    /* CUDA ordinal                               */
+} wmpc_dims;
+
+/* Create a context; allocates every device buffer for n_nodes.
+ * Replaces the allocation part of solver.py:427-436. */
+int wmpc_create(const wmpc_dims* dims, wmpc_ctx** out);
+void wmpc_destroy(wmpc_ctx* ctx);
+const char* wmpc_last_error(const wmpc_ctx* ctx);
+/* Errors raised before a context exists. */
+const char* wmpc_global_error(void);
+
+/* Tree + stage factors (FactorCache structural members, solver.py:150-205).
+ * A (nt*nt), B (nt*nu), Wu (nu*nu), T/D/Lam (H*nu*nu, stage-major),
+ * anc_row (n; -1 = stage 1), stage_off (H+1), prob (n), E (ns*nu),
+ * e_pinv (nu*ns). */
+int wmpc_set_structure(wmpc_ctx* ctx, const double* A, const double* B, const double* Wu,
+                       const double* T, const double* D, const double* Lam,
+                       const int64_t* anc_row, const int64_t* stage_off, const double* prob,
+                       const double* E, const double* e_pinv);
+
+/* Per-node factor state (u_part, e_offset, child-aggregated offsets, coupling
+ * shift, demand_gd) lives in its own device object so FactorCaches sharing one
+ * tree structure (solver.py:163-170 reuse) share one context without copies. */
+typedef struct wmpc_nodes wmpc_nodes;
+int wmpc_nodes_create(wmpc_ctx* ctx, wmpc_nodes** out);
+void wmpc_nodes_destroy(wmpc_nodes* nodes);
+/* Make `nodes` the node state used by subsequent calls on ctx. */
+int wmpc_bind_nodes(wmpc_ctx* ctx, wmpc_nodes* nodes);
+
+/* Factor step per-node part on the GPU (solver.py:206-225) into `nodes`
+ * (and bind it): demand (n*nd), Ed (ns*nd), demand_gd (n*nt), econ (n*nu).
+ * Returns WMPC_E_INFEASIBLE with *bad_row = first infeasible row (node-1). */
+int wmpc_set_node_data(wmpc_ctx* ctx, wmpc_nodes* nodes, const double* demand, const double* Ed,
+                       const double* demand_gd, const double* econ, int64_t* bad_row);
+/* Read back u_part / e_offset of `nodes` (n*nu each; FactorCache fields). */
+int wmpc_get_offsets(wmpc_ctx* ctx, wmpc_nodes* nodes, double* u_part, double* e_offset);
+
+/* Mutable per-solve data (tests mutate these after factor_step): state box,
+ * safety level, input box, penalty weights, measured state p, previous input q,
+ * economic rows econ (n*nu, nullable = keep). */
+int wmpc_set_bounds(wmpc_ctx* ctx, const double* x_min, const double* x_max,
+                    const double* x_safe, const double* u_min, const double* u_max,
+                    double w_x, double w_s, const double* p, const double* q,
+                    const double* econ);
+
+/* Dual gradient (solver.py:242-306): y (n*(2nt+nu)) -> z (n*(nu+nt)) and the
+ * attained value f(z) + <H'y, z>. value may be NULL. */
+int wmpc_dual_gradient(wmpc_ctx* ctx, const double* y, double* z, double* value);
+
+/* Row-wise prox (problem.py:313-327): conjugate=0 -> prox_{gamma g}(v);
+ * conjugate=1 -> prox_{gamma g*}(v) via Moreau, the solver's expression order
+ * (solver.py:563-575). Bit-exact with numpy on identical inputs. */
+int wmpc_prox(wmpc_ctx* ctx, const double* v, double gamma, int conjugate, double* out);
+
+/* Power iteration for the dual Lipschitz constant (solver.py:326-387).
+ * v0 (n_dual) is the normalised start vector; returns the raw Rayleigh
+ * quotient in *lam (no safety factor) and whether it settled. */
+int wmpc_power_iteration(wmpc_ctx* ctx, const double* v0, double rel_tol, int max_iter,
+                         double* lam, int* settled, int* iters);
+/* Trace-bound fallback: sum_i <e_i, Op e_i> (solver.py:376-382). */
+int wmpc_operator_trace(wmpc_ctx* ctx, double* trace);
+
+/* APG loop (solver.py:398-543). begin: step gamma, theta/beta tables of
+ * length max_iter (theta_nu and beta_nu = theta_nu (1/theta_{nu-1} - 1)),
+ * y0 = 0. run: iterations [it, it + count) on the device, CUDA-graph replayed.
+ * check: scalars of the last completed iteration. */
+int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* theta,
+                   const double* beta);
+int wmpc_apg_run(wmpc_ctx* ctx, int count);
+int wmpc_apg_check(wmpc_ctx* ctx, double* primal_residual, double* image_scale,
+                   double* dual_change, int* first_nonfinite_nu);
+/* Duality-gap certificate at the current dual iterate (solver.py:449-457):
+ * Dykstra restoration of the averaged inputs, rollout, primal value, dual value. */
+int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective);
+/* Results: u0 (nu), primal/primal_avg (n*(nu+nt)), dual (n*(2nt+nu)); any may
+ * be NULL. averaged selects the ergodic average for u0. */
+int wmpc_apg_read(wmpc_ctx* ctx, int averaged, double* u0, double* primal,
+                  double* primal_avg, double* dual);
+/* Iterations completed since wmpc_apg_begin. */
+int wmpc_apg_iterations(const wmpc_ctx* ctx);
+
+/* Kernels launched per APG iteration (bench accounting). */
+int wmpc_kernel_launches_per_iteration(const wmpc_ctx* ctx);
+
+/* Timing helpers for bench.py: run `count` iterations between CUDA events on
+ * the context's stream; *ms = elapsed device time. */
+int wmpc_apg_run_timed(wmpc_ctx* ctx, int count, float* ms);
+
+/* Device-time bracket on the context's stream (bench.py): start records an
+ * event; stop records a second one, waits for it and returns the elapsed ms. */
+int wmpc_timer_start(wmpc_ctx* ctx);
+int wmpc_timer_stop(wmpc_ctx* ctx, float* ms);
+/* Kernels this context has launched so far (graph replays counted per node). */
+int64_t wmpc_launch_count(const wmpc_ctx* ctx);
+
+/* Page-locked host buffers for end-to-end transfers (bench.py e2e leg). */
+int wmpc_host_alloc(uint64_t bytes, void** out);
+void wmpc_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WMPC_H */

@@ -1,0 +1,192 @@
+"""ctypes binding of ``libwmpc.so`` (C ABI declared in ``include/wmpc.h``).
+
+The library is built in-tree by ``paper_1904_10548_b200.build.build_native``
+(called from ``__graft_entry__.build()``). There is no fallback: if the
+library or a CUDA device is missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libwmpc.so")
+
+WMPC_OK = 0
+WMPC_E_ARG = -1
+WMPC_E_CUDA = -2
+WMPC_E_INFEASIBLE = -3
+WMPC_E_NONFINITE = -4
+WMPC_E_STATE = -5
+
+
+class wmpc_dims(C.Structure):
+    _fields_ = [
+        ("n_nodes", C.c_int64),
+        ("horizon", C.c_int32),
+        ("n_tanks", C.c_int32),
+        ("n_inputs", C.c_int32),
+        ("n_demands", C.c_int32),
+        ("n_mixing", C.c_int32),
+        ("device", C.c_int32),
+    ]
+
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int64)
+_vp = C.c_void_p
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "wmpc_create": (C.c_int, [C.POINTER(wmpc_dims), C.POINTER(_vp)]),
+    "wmpc_destroy": (None, [_vp]),
+    "wmpc_last_error": (C.c_char_p, [_vp]),
+    "wmpc_global_error": (C.c_char_p, []),
+    "wmpc_set_structure": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _dp, _ip, _ip, _dp, _dp, _dp]),
+    "wmpc_nodes_create": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "wmpc_nodes_destroy": (None, [_vp]),
+    "wmpc_bind_nodes": (C.c_int, [_vp, _vp]),
+    "wmpc_set_node_data": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp, _ip]),
+    "wmpc_get_offsets": (C.c_int, [_vp, _vp, _dp, _dp]),
+    "wmpc_set_bounds": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, C.c_double, C.c_double, _dp, _dp, _dp]),
+    "wmpc_dual_gradient": (C.c_int, [_vp, _dp, _dp, _dp]),
+    "wmpc_prox": (C.c_int, [_vp, _dp, C.c_double, C.c_int, _dp]),
+    "wmpc_power_iteration": (C.c_int, [_vp, _dp, C.c_double, C.c_int, _dp, C.POINTER(C.c_int),
+                                       C.POINTER(C.c_int)]),
+    "wmpc_operator_trace": (C.c_int, [_vp, _dp]),
+    "wmpc_apg_begin": (C.c_int, [_vp, C.c_double, C.c_int, _dp, _dp]),
+    "wmpc_apg_run": (C.c_int, [_vp, C.c_int]),
+    "wmpc_apg_run_timed": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_float)]),
+    "wmpc_apg_check": (C.c_int, [_vp, _dp, _dp, _dp, C.POINTER(C.c_int)]),
+    "wmpc_certificate": (C.c_int, [_vp, _dp, _dp]),
+    "wmpc_apg_read": (C.c_int, [_vp, C.c_int, _dp, _dp, _dp, _dp]),
+    "wmpc_apg_iterations": (C.c_int, [_vp]),
+    "wmpc_kernel_launches_per_iteration": (C.c_int, [_vp]),
+    "wmpc_timer_start": (C.c_int, [_vp]),
+    "wmpc_timer_stop": (C.c_int, [_vp, C.POINTER(C.c_float)]),
+    "wmpc_launch_count": (C.c_int64, [_vp]),
+    "wmpc_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_vp)]),
+    "wmpc_host_free": (None, [_vp]),
+}
+
+_LIB = None
+
+
+def load() -> C.CDLL:
+    """Load the in-tree library (raises if it has not been built)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"native library missing: {LIB_PATH}; build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = lib
+    return _LIB
+
+
+def ptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    if a.dtype == np.int64:
+        return a.ctypes.data_as(_ip)
+    return a.ctypes.data_as(_dp)
+
+
+def f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+class Context:
+    """Owns one ``wmpc_ctx`` (device buffers for one tree size)."""
+
+    def __init__(self, n, horizon, n_tanks, n_inputs, n_demands, n_mixing, device=0):
+        self.lib = load()
+        dims = wmpc_dims(n, horizon, n_tanks, n_inputs, n_demands, n_mixing, device)
+        h = _vp()
+        rc = self.lib.wmpc_create(C.byref(dims), C.byref(h))
+        if rc != WMPC_OK:
+            msg = self.lib.wmpc_global_error().decode()
+            if rc == WMPC_E_ARG:
+                raise ValueError(msg)
+            raise NativeError(f"wmpc_create failed: {msg}")
+        self.h = h
+        self.dims = (n, horizon, n_tanks, n_inputs, n_demands, n_mixing)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            try:
+                self.lib.wmpc_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def err(self) -> str:
+        return self.lib.wmpc_last_error(self.h).decode()
+
+    def call(self, name, *args):
+        rc = getattr(self.lib, name)(self.h, *args)
+        if rc == WMPC_OK:
+            return
+        msg = self.err()
+        if rc in (WMPC_E_ARG, WMPC_E_INFEASIBLE):
+            raise ValueError(msg)
+        raise NativeError(f"{name}: {msg}")
+
+
+class NodeSet:
+    """Owns one ``wmpc_nodes`` (per-node factor state) of a context."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx  # keeps the context alive
+        h = _vp()
+        ctx.call("wmpc_nodes_create", C.byref(h))
+        self.h = h
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            try:
+                self.ctx.lib.wmpc_nodes_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+
+class _Pinned:
+    def __init__(self, nbytes):
+        self.lib = load()
+        p = _vp()
+        if self.lib.wmpc_host_alloc(nbytes, C.byref(p)) != WMPC_OK:
+            raise NativeError(self.lib.wmpc_global_error().decode())
+        self.p = p
+
+    def __del__(self):
+        if getattr(self, "p", None):
+            self.lib.wmpc_host_free(self.p)
+            self.p = None
+
+
+def pinned_copy(a) -> np.ndarray:
+    """Copy of ``a`` in page-locked host memory (keeps its buffer alive)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    buf = _Pinned(max(a.nbytes, 8))
+    raw = (C.c_double * max(a.size, 1)).from_address(buf.p.value)
+    out = np.frombuffer(raw, dtype=np.float64, count=a.size).reshape(a.shape)
+    out[...] = a
+    _PINNED_KEEP[id(out)] = buf
+    return out
+
+
+_PINNED_KEEP: dict = {}

@@ -1,0 +1,890 @@
+// wmpc.cu — C ABI (include/wmpc.h) over the sm_100a kernels.
+//
+// The context owns every device buffer of one tree structure; the APG
+// iteration (2H stage kernels + 1 counter kernel) is captured once per
+// wmpc_apg_begin into a CUDA graph and replayed; nothing leaves HBM between
+// iterations except the scalars read at check iterations.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "wmpc.h"
+#include "wmpc_kernels.cuh"
+
+using namespace wmpc;
+
+static thread_local std::string g_global_err;
+
+struct wmpc_nodes {
+  int dev = 0;
+  size_t n = 0;
+  double *u_part = nullptr, *e_off = nullptr, *R = nullptr, *shift = nullptr, *g = nullptr;
+  bool ready = false;
+};
+
+struct wmpc_ctx {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  int n = 0, H = 0, nt = 0, nu = 0, nd = 0, ns = 0, W = 0, P = 0;
+  int a_identity = 0, w_scalar = 0;
+  double w_c = 0.0;
+  std::vector<int> off;  // H+1
+  bool have_structure = false, have_nodes = false, have_bounds = false;
+  // device buffers
+  int *stage_of = nullptr, *anc = nullptr, *cptr = nullptr, *cidx = nullptr;
+  double *prob = nullptr, *A = nullptr, *At = nullptr, *Bt = nullptr, *Wu = nullptr;
+  double *T = nullptr, *Lam = nullptr, *Mb = nullptr, *Mf = nullptr, *E = nullptr, *e_pinv = nullptr;
+  wmpc_nodes* nodes = nullptr;  // bound per-node state (not owned)
+  NodePtrs* d_np = nullptr;     // device copy of the bound node pointers
+  double *econ = nullptr, *tmp = nullptr, *demand = nullptr, *Ed = nullptr;
+  double *xmin = nullptr, *xmax = nullptr, *xsafe = nullptr, *umin = nullptr, *umax = nullptr;
+  double *p = nullptr, *q = nullptr;
+  double w_x = 0.0, w_s = 0.0;
+  double *Y[3] = {nullptr, nullptr, nullptr};
+  double *U = nullptr, *X = nullptr, *Ua = nullptr, *Xa = nullptr;
+  double *Uc = nullptr, *Xc = nullptr, *Uf = nullptr, *Xf = nullptr, *U0 = nullptr, *X0 = nullptr;
+  double *wbar = nullptr, *lin = nullptr;
+  double *ys = nullptr, *gv = nullptr, *vv = nullptr, *zbuf = nullptr;
+  double *dk_cur = nullptr, *dk_pc = nullptr, *dk_qc = nullptr, *dk_aff = nullptr;
+  double *theta = nullptr, *beta = nullptr;
+  int max_iter = 0;
+  int *iter = nullptr, *bad_nu = nullptr, *bad_row = nullptr, *dk_done = nullptr;
+  double *part = nullptr, *scal = nullptr;
+  int part_blocks = 0;
+  double gamma = 0.0;
+  int it_host = 0;
+  int64_t launches = 0;
+  double graph_gamma = -1.0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  std::string err;
+};
+
+namespace {
+
+struct Fail {};
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      ctx->err = std::string("CUDA error ") + cudaGetErrorString(e_) + " at " #call;    \
+      throw Fail{};                                                                     \
+    }                                                                                   \
+  } while (0)
+
+#define ARG(cond, msg)        \
+  do {                        \
+    if (!(cond)) {            \
+      ctx->err = (msg);       \
+      return WMPC_E_ARG;      \
+    }                         \
+  } while (0)
+
+template <class T>
+void dalloc(wmpc_ctx* ctx, T** p, size_t count) {
+  CK(cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T)));
+  CK(cudaMemsetAsync(*p, 0, std::max<size_t>(count, 1) * sizeof(T), ctx->stream));
+}
+
+void h2d(wmpc_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+}
+void d2h(wmpc_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+}
+void sync(wmpc_ctx* ctx) { CK(cudaStreamSynchronize(ctx->stream)); }
+void check_launch(wmpc_ctx* ctx) { CK(cudaGetLastError()); }
+
+DevView view(const wmpc_ctx* c) {
+  DevView d;
+  d.n = c->n; d.H = c->H; d.nt = c->nt; d.nu = c->nu; d.nd = c->nd; d.ns = c->ns;
+  d.W = c->W; d.P = c->P;
+  d.a_identity = c->a_identity; d.w_scalar = c->w_scalar; d.w_c = c->w_c;
+  d.stage_of = c->stage_of; d.anc = c->anc; d.cptr = c->cptr; d.cidx = c->cidx; d.prob = c->prob;
+  d.A = c->A; d.At = c->At; d.Bt = c->Bt; d.Wu = c->Wu; d.T = c->T; d.Lam = c->Lam;
+  d.Mb = c->Mb; d.Mf = c->Mf; d.E = c->E; d.e_pinv = c->e_pinv;
+  d.np = c->d_np;
+  d.econ = c->econ;
+  d.xmin = c->xmin; d.xmax = c->xmax; d.xsafe = c->xsafe; d.umin = c->umin; d.umax = c->umax;
+  d.p = c->p; d.q = c->q; d.w_x = c->w_x; d.w_s = c->w_s;
+  d.Y0 = c->Y[0]; d.Y1 = c->Y[1]; d.Y2 = c->Y[2];
+  d.U = c->U; d.X = c->X; d.Ua = c->Ua; d.Xa = c->Xa; d.wbar = c->wbar; d.lin = c->lin;
+  d.theta = c->theta; d.beta = c->beta; d.iter = c->iter; d.bad_nu = c->bad_nu;
+  d.gamma = c->gamma;
+  return d;
+}
+
+int grid_for(size_t len, int threads = 256) {
+  size_t b = (len + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 1184) b = 1184;
+  return (int)b;
+}
+
+size_t smem_bwd(const wmpc_ctx* c, int s) {
+  int K = c->nt + (s < c->H - 1 ? c->nu : 0);
+  return sizeof(double) * (size_t)TM * (K + c->nu + c->nt);
+}
+size_t smem_fwd(const wmpc_ctx* c) {
+  return sizeof(double) * ((size_t)TM * (2 * c->nu + c->nu + 2 * c->nt + c->W) + 2 * TM);
+}
+
+// Dual gradient over all stages: backward H..1 then forward 1..H.
+void launch_dg(wmpc_ctx* ctx, const DevView& d, const double* ysrc, int mode) {
+  for (int s = ctx->H - 1; s >= 0; --s) {
+    int cnt = ctx->off[s + 1] - ctx->off[s];
+    if (cnt <= 0) continue;
+    k_bwd_stage<<<(cnt + TM - 1) / TM, NTHR, smem_bwd(ctx, s), ctx->stream>>>(d, s, ctx->off[s], cnt, ysrc);
+  }
+  for (int s = 0; s < ctx->H; ++s) {
+    int cnt = ctx->off[s + 1] - ctx->off[s];
+    if (cnt <= 0) continue;
+    k_fwd_stage<<<(cnt + TM - 1) / TM, NTHR, smem_fwd(ctx), ctx->stream>>>(d, s, ctx->off[s], cnt, mode);
+  }
+  check_launch(ctx);
+  ctx->launches += 2 * ctx->H;
+}
+
+// Sum-reduce the 4 cost terms of (Uin, Xin[, y]) -> host[4].
+void cost_terms(wmpc_ctx* ctx, const DevView& d, const double* Uin, const double* Xin, const double* y,
+                int pen, double out[4]) {
+  int nb = std::min(ctx->part_blocks, std::max(1, (ctx->n + 7) / 8));
+  ctx->launches++;
+  k_cost_partial<<<nb, 256, 0, ctx->stream>>>(d, Uin, Xin, y, pen, ctx->part);
+  ctx->launches++;
+  k_finish<0><<<1, 256, 0, ctx->stream>>>(ctx->part, nb, 4, 0, 4, ctx->scal);
+  check_launch(ctx);
+  d2h(ctx, out, ctx->scal, 4 * sizeof(double));
+  sync(ctx);
+}
+
+double gconj_value(wmpc_ctx* ctx, const DevView& d, const double* y) {
+  int nb = std::min(ctx->part_blocks, std::max(1, (ctx->n + 7) / 8));
+  ctx->launches++;
+  k_gconj_partial<<<nb, 256, 0, ctx->stream>>>(d, y, 1e-9, ctx->part);
+  ctx->launches++;
+  k_finish<0><<<1, 256, 0, ctx->stream>>>(ctx->part, nb, 2, 0, 1, ctx->scal);
+  ctx->launches++;
+  k_finish<1><<<1, 256, 0, ctx->stream>>>(ctx->part, nb, 2, 1, 1, ctx->scal);
+  check_launch(ctx);
+  double h[2];
+  d2h(ctx, h, ctx->scal, 2 * sizeof(double));
+  sync(ctx);
+  return h[1] > 0.0 ? INFINITY : h[0];
+}
+
+void point_nodes(wmpc_ctx* ctx, wmpc_nodes* nd) {
+  NodePtrs h{nd->e_off, nd->R, nd->g, nd->shift};
+  CK(cudaMemcpyAsync(ctx->d_np, &h, sizeof(NodePtrs), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->nodes = nd;
+}
+
+template <class F>
+int run(wmpc_ctx* ctx, F&& f) {
+  if (!ctx) {
+    g_global_err = "null context";
+    return WMPC_E_ARG;
+  }
+  try {
+    return f();
+  } catch (Fail&) {
+    return WMPC_E_CUDA;
+  }
+}
+
+void free_all(wmpc_ctx* c) {
+  void* ptrs[] = {c->stage_of, c->anc, c->cptr, c->cidx, c->prob, c->A, c->At, c->Bt, c->Wu, c->T,
+                  c->Lam, c->Mb, c->Mf, c->E, c->e_pinv, c->econ, c->tmp, c->demand, c->Ed, c->xmin, c->xmax, c->xsafe, c->umin, c->umax,
+                  c->p, c->q, c->Y[0], c->Y[1], c->Y[2], c->U, c->X, c->Ua, c->Xa, c->Uc, c->Xc,
+                  c->Uf, c->Xf, c->U0, c->X0, c->wbar, c->lin, c->ys, c->gv, c->vv, c->zbuf,
+                  c->dk_cur, c->dk_pc, c->dk_qc, c->dk_aff, c->theta, c->beta, c->iter, c->bad_nu,
+                  c->bad_row, c->dk_done, c->part, c->scal, c->d_np};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->ev2) cudaEventDestroy(c->ev2);
+  if (c->ev3) cudaEventDestroy(c->ev3);
+  if (c->stream) cudaStreamDestroy(c->stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* wmpc_global_error(void) { return g_global_err.c_str(); }
+
+const char* wmpc_last_error(const wmpc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int wmpc_create(const wmpc_dims* dims, wmpc_ctx** out) {
+  if (!dims || !out) {
+    g_global_err = "null argument";
+    return WMPC_E_ARG;
+  }
+  if (dims->n_nodes < 1 || dims->horizon < 1 || dims->n_tanks < 1 || dims->n_inputs < 1 ||
+      dims->n_demands < 0 || dims->n_mixing < 0 || dims->n_mixing > 32 || dims->n_nodes > (1LL << 30)) {
+    g_global_err = "invalid dimensions (need n>=1, H>=1, nt>=1, nu>=1, 0<=ns<=32)";
+    return WMPC_E_ARG;
+  }
+  wmpc_ctx* ctx = new wmpc_ctx();
+  try {
+    ctx->dev = dims->device;
+    CK(cudaSetDevice(ctx->dev));
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ctx->ev0));
+    CK(cudaEventCreate(&ctx->ev1));
+    CK(cudaEventCreate(&ctx->ev2));
+    CK(cudaEventCreate(&ctx->ev3));
+    ctx->n = (int)dims->n_nodes; ctx->H = dims->horizon; ctx->nt = dims->n_tanks;
+    ctx->nu = dims->n_inputs; ctx->nd = dims->n_demands; ctx->ns = dims->n_mixing;
+    ctx->W = 2 * ctx->nt + ctx->nu; ctx->P = ctx->nu + ctx->nt;
+    const size_t n = ctx->n, nt = ctx->nt, nu = ctx->nu, H = ctx->H, W = ctx->W;
+    dalloc(ctx, &ctx->stage_of, n); dalloc(ctx, &ctx->anc, n); dalloc(ctx, &ctx->cptr, n + 1);
+    dalloc(ctx, &ctx->cidx, n); dalloc(ctx, &ctx->prob, n);
+    dalloc(ctx, &ctx->A, nt * nt); dalloc(ctx, &ctx->At, nt * nt); dalloc(ctx, &ctx->Bt, nu * nt);
+    dalloc(ctx, &ctx->Wu, nu * nu); dalloc(ctx, &ctx->T, H * nu * nu); dalloc(ctx, &ctx->Lam, H * nu * nu);
+    dalloc(ctx, &ctx->Mb, H * (nt + nu) * nu); dalloc(ctx, &ctx->Mf, H * 2 * nu * nu);
+    dalloc(ctx, &ctx->E, (size_t)ctx->ns * nu); dalloc(ctx, &ctx->e_pinv, nu * ctx->ns);
+    dalloc(ctx, &ctx->econ, n * nu); dalloc(ctx, &ctx->tmp, n * nu);
+    dalloc(ctx, &ctx->demand, n * ctx->nd); dalloc(ctx, &ctx->Ed, (size_t)ctx->ns * ctx->nd);
+    dalloc(ctx, &ctx->xmin, nt); dalloc(ctx, &ctx->xmax, nt); dalloc(ctx, &ctx->xsafe, nt);
+    dalloc(ctx, &ctx->umin, nu); dalloc(ctx, &ctx->umax, nu); dalloc(ctx, &ctx->p, nt); dalloc(ctx, &ctx->q, nu);
+    for (int k = 0; k < 3; ++k) dalloc(ctx, &ctx->Y[k], n * W);
+    dalloc(ctx, &ctx->U, n * nu); dalloc(ctx, &ctx->X, n * nt); dalloc(ctx, &ctx->Ua, n * nu);
+    dalloc(ctx, &ctx->Xa, n * nt); dalloc(ctx, &ctx->Uc, n * nu); dalloc(ctx, &ctx->Xc, n * nt);
+    dalloc(ctx, &ctx->Uf, n * nu); dalloc(ctx, &ctx->Xf, n * nt); dalloc(ctx, &ctx->U0, n * nu);
+    dalloc(ctx, &ctx->X0, n * nt); dalloc(ctx, &ctx->wbar, n * nt); dalloc(ctx, &ctx->lin, n * nu);
+    dalloc(ctx, &ctx->ys, n * W); dalloc(ctx, &ctx->gv, n * W); dalloc(ctx, &ctx->vv, n * W);
+    dalloc(ctx, &ctx->zbuf, n * std::max(W, (size_t)ctx->P));
+    dalloc(ctx, &ctx->dk_cur, n * nu); dalloc(ctx, &ctx->dk_pc, n * nu); dalloc(ctx, &ctx->dk_qc, n * nu);
+    dalloc(ctx, &ctx->dk_aff, n * nu);
+    dalloc(ctx, &ctx->iter, 1); dalloc(ctx, &ctx->bad_nu, 1); dalloc(ctx, &ctx->bad_row, 1);
+    dalloc(ctx, &ctx->dk_done, 1);
+    dalloc(ctx, &ctx->d_np, 1);
+    ctx->part_blocks = 1184;
+    dalloc(ctx, &ctx->part, (size_t)ctx->part_blocks * 4);
+    dalloc(ctx, &ctx->scal, 16);
+    size_t smax = std::max(smem_fwd(ctx), smem_bwd(ctx, 0));
+    if (smax > 48 * 1024) {
+      CK(cudaFuncSetAttribute(k_fwd_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+      CK(cudaFuncSetAttribute(k_bwd_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+    }
+    sync(ctx);
+  } catch (Fail&) {
+    g_global_err = ctx->err;
+    free_all(ctx);
+    delete ctx;
+    return WMPC_E_CUDA;
+  }
+  *out = ctx;
+  return WMPC_OK;
+}
+
+void wmpc_destroy(wmpc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->dev);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  free_all(ctx);
+  delete ctx;
+}
+
+int wmpc_set_structure(wmpc_ctx* ctx, const double* A, const double* B, const double* Wu,
+                       const double* T, const double* D, const double* Lam, const int64_t* anc_row,
+                       const int64_t* stage_off, const double* prob, const double* E,
+                       const double* e_pinv) {
+  return run(ctx, [&]() -> int {
+    ARG(A && B && Wu && T && D && Lam && anc_row && stage_off && prob, "null structure argument");
+    const int n = ctx->n, H = ctx->H, nt = ctx->nt, nu = ctx->nu, ns = ctx->ns;
+    ARG(stage_off[0] == 0 && stage_off[H] == n, "stage offsets must span all rows");
+    ctx->off.assign(H + 1, 0);
+    std::vector<int> stg(n), anc(n);
+    for (int s = 0; s < H; ++s) {
+      ARG(stage_off[s + 1] >= stage_off[s], "stage offsets must be nondecreasing");
+      ctx->off[s + 1] = (int)stage_off[s + 1];
+      for (int64_t r = stage_off[s]; r < stage_off[s + 1]; ++r) stg[r] = s;
+    }
+    for (int r = 0; r < n; ++r) {
+      int64_t a = anc_row[r];
+      if (stg[r] == 0) {
+        ARG(a == -1, "stage-1 rows must have ancestor row -1");
+      } else {
+        ARG(a >= ctx->off[stg[r] - 1] && a < ctx->off[stg[r]], "ancestor must sit one stage up");
+      }
+      anc[r] = (int)a;
+    }
+    // CSR children, ascending child row (np.add.at order, solver.py:269-274).
+    std::vector<int> cnt(n + 1, 0), cptr(n + 1, 0), cidx(n, 0);
+    for (int r = 0; r < n; ++r)
+      if (anc[r] >= 0) cnt[anc[r]]++;
+    for (int r = 0; r < n; ++r) cptr[r + 1] = cptr[r] + cnt[r];
+    std::vector<int> fill(cptr.begin(), cptr.end() - 1);
+    for (int r = 0; r < n; ++r)
+      if (anc[r] >= 0) cidx[fill[anc[r]]++] = r;
+    // flags
+    bool aid = true;
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j < nt; ++j) aid &= A[i * nt + j] == (i == j ? 1.0 : 0.0);
+    bool wsc = true;
+    for (int i = 0; i < nu; ++i)
+      for (int j = 0; j < nu; ++j) wsc &= (i == j) ? Wu[i * nu + j] == Wu[0] : Wu[i * nu + j] == 0.0;
+    ctx->a_identity = aid;
+    ctx->w_scalar = wsc;
+    ctx->w_c = Wu[0];
+    std::vector<double> At(nt * nt), Bt((size_t)nu * nt);
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j < nt; ++j) At[j * nt + i] = A[i * nt + j];
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j < nu; ++j) Bt[(size_t)j * nt + i] = B[(size_t)i * nu + j];
+    // Mb_s = [[B],[D_{s+1}]] ; Mf_s = [[D_s^T],[-T_s]]
+    std::vector<double> Mb((size_t)H * (nt + nu) * nu, 0.0), Mf((size_t)H * 2 * nu * nu);
+    for (int s = 0; s < H; ++s) {
+      double* mb = Mb.data() + (size_t)s * (nt + nu) * nu;
+      std::memcpy(mb, B, sizeof(double) * nt * nu);
+      if (s + 1 < H) std::memcpy(mb + (size_t)nt * nu, D + (size_t)(s + 1) * nu * nu, sizeof(double) * nu * nu);
+      double* mf = Mf.data() + (size_t)s * 2 * nu * nu;
+      const double* Ds = D + (size_t)s * nu * nu;
+      const double* Ts = T + (size_t)s * nu * nu;
+      for (int k = 0; k < nu; ++k)
+        for (int c = 0; c < nu; ++c) {
+          mf[(size_t)k * nu + c] = Ds[(size_t)c * nu + k];
+          mf[(size_t)(nu + k) * nu + c] = -Ts[(size_t)k * nu + c];
+        }
+    }
+    h2d(ctx, ctx->stage_of, stg.data(), sizeof(int) * n);
+    h2d(ctx, ctx->anc, anc.data(), sizeof(int) * n);
+    h2d(ctx, ctx->cptr, cptr.data(), sizeof(int) * (n + 1));
+    h2d(ctx, ctx->cidx, cidx.data(), sizeof(int) * n);
+    h2d(ctx, ctx->prob, prob, sizeof(double) * n);
+    h2d(ctx, ctx->A, A, sizeof(double) * nt * nt);
+    h2d(ctx, ctx->At, At.data(), sizeof(double) * nt * nt);
+    h2d(ctx, ctx->Bt, Bt.data(), sizeof(double) * nu * nt);
+    h2d(ctx, ctx->Wu, Wu, sizeof(double) * nu * nu);
+    h2d(ctx, ctx->T, T, sizeof(double) * H * nu * nu);
+    h2d(ctx, ctx->Lam, Lam, sizeof(double) * H * nu * nu);
+    h2d(ctx, ctx->Mb, Mb.data(), sizeof(double) * Mb.size());
+    h2d(ctx, ctx->Mf, Mf.data(), sizeof(double) * Mf.size());
+    if (ns > 0) {
+      ARG(E && e_pinv, "E and e_pinv required when n_mixing > 0");
+      h2d(ctx, ctx->E, E, sizeof(double) * ns * nu);
+      h2d(ctx, ctx->e_pinv, e_pinv, sizeof(double) * nu * ns);
+    }
+    sync(ctx);
+    ctx->have_structure = true;
+    return WMPC_OK;
+  });
+}
+
+int wmpc_nodes_create(wmpc_ctx* ctx, wmpc_nodes** out) {
+  return run(ctx, [&]() -> int {
+    ARG(out, "null argument");
+    wmpc_nodes* nd = new wmpc_nodes();
+    nd->dev = ctx->dev;
+    nd->n = ctx->n;
+    const size_t n = ctx->n;
+    try {
+      dalloc(ctx, &nd->u_part, n * ctx->nu);
+      dalloc(ctx, &nd->e_off, n * ctx->nu);
+      dalloc(ctx, &nd->R, n * ctx->nu);
+      dalloc(ctx, &nd->shift, n * ctx->ns);
+      dalloc(ctx, &nd->g, n * ctx->nt);
+    } catch (Fail&) {
+      wmpc_nodes_destroy(nd);
+      throw;
+    }
+    *out = nd;
+    return WMPC_OK;
+  });
+}
+
+void wmpc_nodes_destroy(wmpc_nodes* nd) {
+  if (!nd) return;
+  cudaSetDevice(nd->dev);
+  void* ptrs[] = {nd->u_part, nd->e_off, nd->R, nd->shift, nd->g};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete nd;
+}
+
+int wmpc_bind_nodes(wmpc_ctx* ctx, wmpc_nodes* nodes) {
+  return run(ctx, [&]() -> int {
+    ARG(nodes && nodes->n == (size_t)ctx->n, "node state does not match this context");
+    if (!nodes->ready) {
+      ctx->err = "node state has not been computed";
+      return WMPC_E_STATE;
+    }
+    if (ctx->nodes != nodes) point_nodes(ctx, nodes);
+    ctx->have_nodes = true;
+    return WMPC_OK;
+  });
+}
+
+int wmpc_set_node_data(wmpc_ctx* ctx, wmpc_nodes* nodes, const double* demand, const double* Ed,
+                       const double* demand_gd, const double* econ, int64_t* bad_row) {
+  return run(ctx, [&]() -> int {
+    if (!ctx->have_structure) {
+      ctx->err = "set_structure must precede set_node_data";
+      return WMPC_E_STATE;
+    }
+    ARG(nodes && nodes->n == (size_t)ctx->n, "node state does not match this context");
+    ARG(demand_gd && econ, "null node data");
+    const size_t n = ctx->n;
+    if (ctx->ns > 0) {
+      ARG(demand && Ed, "demand and Ed required when n_mixing > 0");
+      h2d(ctx, ctx->demand, demand, sizeof(double) * n * ctx->nd);
+      h2d(ctx, ctx->Ed, Ed, sizeof(double) * ctx->ns * ctx->nd);
+    }
+    h2d(ctx, nodes->g, demand_gd, sizeof(double) * n * ctx->nt);
+    h2d(ctx, ctx->econ, econ, sizeof(double) * n * ctx->nu);
+    int big = INT_MAX;
+    h2d(ctx, ctx->bad_row, &big, sizeof(int));
+    point_nodes(ctx, nodes);
+    DevView d = view(ctx);
+    int blocks = (int)((n * 32 + 255) / 256);
+    ctx->launches++;
+    k_node_offsets<<<blocks, 256, 0, ctx->stream>>>(d, ctx->demand, ctx->Ed, nodes->shift, nodes->u_part,
+                                                     nodes->e_off, ctx->tmp, ctx->bad_row);
+    ctx->launches++;
+    k_node_R<<<blocks, 256, 0, ctx->stream>>>(d, nodes->e_off, nodes->R);
+    check_launch(ctx);
+    int bad = INT_MAX;
+    d2h(ctx, &bad, ctx->bad_row, sizeof(int));
+    sync(ctx);
+    if (bad != INT_MAX) {
+      ctx->nodes = nullptr;
+      ctx->have_nodes = false;
+      if (bad_row) *bad_row = bad;
+      ctx->err = "coupling E u = -Ed d is infeasible at tree node " + std::to_string(bad + 1);
+      return WMPC_E_INFEASIBLE;
+    }
+    nodes->ready = true;
+    ctx->have_nodes = true;
+    return WMPC_OK;
+  });
+}
+
+int wmpc_get_offsets(wmpc_ctx* ctx, wmpc_nodes* nodes, double* u_part, double* e_offset) {
+  return run(ctx, [&]() -> int {
+    ARG(nodes && nodes->n == (size_t)ctx->n, "node state does not match this context");
+    const size_t bytes = sizeof(double) * (size_t)ctx->n * ctx->nu;
+    if (u_part) d2h(ctx, u_part, nodes->u_part, bytes);
+    if (e_offset) d2h(ctx, e_offset, nodes->e_off, bytes);
+    sync(ctx);
+    return WMPC_OK;
+  });
+}
+
+int wmpc_kernel_launches_per_iteration(const wmpc_ctx* ctx) { return ctx ? 2 * ctx->H + 1 : -1; }
+
+int wmpc_set_bounds(wmpc_ctx* ctx, const double* x_min, const double* x_max, const double* x_safe,
+                    const double* u_min, const double* u_max, double w_x, double w_s, const double* p,
+                    const double* q, const double* econ) {
+  return run(ctx, [&]() -> int {
+    ARG(x_min && x_max && x_safe && u_min && u_max && p && q, "null bound argument");
+    const size_t nt = ctx->nt, nu = ctx->nu;
+    h2d(ctx, ctx->xmin, x_min, sizeof(double) * nt);
+    h2d(ctx, ctx->xmax, x_max, sizeof(double) * nt);
+    h2d(ctx, ctx->xsafe, x_safe, sizeof(double) * nt);
+    h2d(ctx, ctx->umin, u_min, sizeof(double) * nu);
+    h2d(ctx, ctx->umax, u_max, sizeof(double) * nu);
+    h2d(ctx, ctx->p, p, sizeof(double) * nt);
+    h2d(ctx, ctx->q, q, sizeof(double) * nu);
+    if (econ) h2d(ctx, ctx->econ, econ, sizeof(double) * (size_t)ctx->n * nu);
+    ctx->w_x = w_x;
+    ctx->w_s = w_s;
+    sync(ctx);
+    ctx->have_bounds = true;
+    return WMPC_OK;
+  });
+}
+
+static int need_ready(wmpc_ctx* ctx) {
+  if (!ctx->have_structure || !ctx->have_nodes || !ctx->have_bounds) {
+    ctx->err = "structure, node data and bounds must be set first";
+    return WMPC_E_STATE;
+  }
+  return WMPC_OK;
+}
+
+int wmpc_dual_gradient(wmpc_ctx* ctx, const double* y, double* z, double* value) {
+  return run(ctx, [&]() -> int {
+    int st = need_ready(ctx);
+    if (st) return st;
+    ARG(y && z, "null argument");
+    const size_t n = ctx->n;
+    h2d(ctx, ctx->ys, y, sizeof(double) * n * ctx->W);
+    DevView d = view(ctx);
+    d.U = ctx->Uc;
+    d.X = ctx->Xc;
+    launch_dg(ctx, d, ctx->ys, 0);
+    ctx->launches++;
+    k_join_primal<<<grid_for(n * ctx->P), 256, 0, ctx->stream>>>(ctx->n, ctx->nu, ctx->nt, ctx->Uc, ctx->Xc,
+                                                                   ctx->zbuf);
+    check_launch(ctx);
+    d2h(ctx, z, ctx->zbuf, sizeof(double) * n * ctx->P);
+    if (value) {
+      double t[4];
+      cost_terms(ctx, d, ctx->Uc, ctx->Xc, ctx->ys, 0, t);
+      *value = t[0] + t[1];
+    }
+    sync(ctx);
+    return WMPC_OK;
+  });
+}
+
+int wmpc_prox(wmpc_ctx* ctx, const double* v, double gamma, int conjugate, double* out) {
+  return run(ctx, [&]() -> int {
+    if (!ctx->have_bounds) {
+      ctx->err = "bounds must be set first";
+      return WMPC_E_STATE;
+    }
+    ARG(v && out, "null argument");
+    ARG(gamma > 0.0, "gamma must be positive");
+    const size_t len = (size_t)ctx->n * ctx->W;
+    h2d(ctx, ctx->ys, v, sizeof(double) * len);
+    DevView d = view(ctx);
+    int blocks = (int)(((size_t)ctx->n * 32 + 255) / 256);
+    ctx->launches++;
+    k_prox_rows<<<blocks, 256, 0, ctx->stream>>>(d, ctx->ys, ctx->zbuf, gamma, conjugate);
+    check_launch(ctx);
+    d2h(ctx, out, ctx->zbuf, sizeof(double) * len);
+    sync(ctx);
+    return WMPC_OK;
+  });
+}
+
+// gv = Op(vsrc) = H(x*(0) - x*(v)); returns (v.gv, ||gv||^2).
+static void apply_operator(wmpc_ctx* ctx, const double* vsrc, double out[2]) {
+  DevView d = view(ctx);
+  d.U = ctx->Uc;
+  d.X = ctx->Xc;
+  launch_dg(ctx, d, vsrc, 0);
+  size_t len = (size_t)ctx->n * ctx->W;
+  int nb = std::min(ctx->part_blocks, grid_for(len));
+  ctx->launches++;
+  k_op_rows<<<nb, 256, 0, ctx->stream>>>(d, ctx->U0, ctx->X0, ctx->Uc, ctx->Xc, vsrc, ctx->gv, ctx->part);
+  ctx->launches++;
+  k_finish<0><<<1, 256, 0, ctx->stream>>>(ctx->part, nb, 2, 0, 2, ctx->scal);
+  check_launch(ctx);
+  d2h(ctx, out, ctx->scal, 2 * sizeof(double));
+  sync(ctx);
+}
+
+static void zero_dual_solution(wmpc_ctx* ctx) {
+  CK(cudaMemsetAsync(ctx->ys, 0, sizeof(double) * (size_t)ctx->n * ctx->W, ctx->stream));
+  DevView d = view(ctx);
+  d.U = ctx->U0;
+  d.X = ctx->X0;
+  launch_dg(ctx, d, ctx->ys, 0);
+}
+
+int wmpc_power_iteration(wmpc_ctx* ctx, const double* v0, double rel_tol, int max_iter, double* lam,
+                         int* settled, int* iters) {
+  return run(ctx, [&]() -> int {
+    int st = need_ready(ctx);
+    if (st) return st;
+    ARG(v0 && lam && settled, "null argument");
+    const size_t len = (size_t)ctx->n * ctx->W;
+    zero_dual_solution(ctx);
+    h2d(ctx, ctx->vv, v0, sizeof(double) * len);
+    double l = 0.0, lprev = 0.0;
+    int ok = 0, k = 0;
+    for (k = 0; k < max_iter; ++k) {
+      double r[2];
+      apply_operator(ctx, ctx->vv, r);
+      l = r[0];
+      double nrm = std::sqrt(r[1]);
+      if (nrm == 0.0) break;
+      ctx->launches++;
+      k_scale_into<<<grid_for(len), 256, 0, ctx->stream>>>(ctx->gv, len, ctx->scal + 1, ctx->vv);
+      check_launch(ctx);
+      if (std::fabs(l - lprev) <= rel_tol * std::max(std::fabs(l), 1e-300)) {
+        ok = 1;
+        break;
+      }
+      lprev = l;
+    }
+    sync(ctx);
+    *lam = l;
+    *settled = ok;
+    if (iters) *iters = k;
+    return WMPC_OK;
+  });
+}
+
+int wmpc_operator_trace(wmpc_ctx* ctx, double* trace) {
+  return run(ctx, [&]() -> int {
+    int st = need_ready(ctx);
+    if (st) return st;
+    const size_t len = (size_t)ctx->n * ctx->W;
+    zero_dual_solution(ctx);
+    double total = 0.0;
+    const double one = 1.0, zero = 0.0;
+    CK(cudaMemsetAsync(ctx->vv, 0, sizeof(double) * len, ctx->stream));
+    for (size_t i = 0; i < len; ++i) {
+      h2d(ctx, ctx->vv + i, &one, sizeof(double));
+      double r[2];
+      apply_operator(ctx, ctx->vv, r);
+      double gi;
+      d2h(ctx, &gi, ctx->gv + i, sizeof(double));
+      h2d(ctx, ctx->vv + i, &zero, sizeof(double));
+      sync(ctx);
+      total += gi;
+    }
+    *trace = total;
+    return WMPC_OK;
+  });
+}
+
+int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* theta, const double* beta) {
+  return run(ctx, [&]() -> int {
+    int st = need_ready(ctx);
+    if (st) return st;
+    ARG(gamma > 0.0 && max_iter >= 1 && theta && beta, "invalid APG parameters");
+    if (max_iter > ctx->max_iter) {
+      if (ctx->theta) cudaFree(ctx->theta);
+      if (ctx->beta) cudaFree(ctx->beta);
+      ctx->theta = ctx->beta = nullptr;
+      ctx->graph_gamma = -1.0;  // table pointers change: recapture
+      dalloc(ctx, &ctx->theta, max_iter);
+      dalloc(ctx, &ctx->beta, max_iter);
+      ctx->max_iter = max_iter;
+    }
+    h2d(ctx, ctx->theta, theta, sizeof(double) * max_iter);
+    h2d(ctx, ctx->beta, beta, sizeof(double) * max_iter);
+    const size_t len = (size_t)ctx->n * ctx->W;
+    for (int k = 0; k < 3; ++k) CK(cudaMemsetAsync(ctx->Y[k], 0, sizeof(double) * len, ctx->stream));
+    CK(cudaMemsetAsync(ctx->U, 0, sizeof(double) * (size_t)ctx->n * ctx->nu, ctx->stream));
+    CK(cudaMemsetAsync(ctx->X, 0, sizeof(double) * (size_t)ctx->n * ctx->nt, ctx->stream));
+    CK(cudaMemsetAsync(ctx->Ua, 0, sizeof(double) * (size_t)ctx->n * ctx->nu, ctx->stream));
+    CK(cudaMemsetAsync(ctx->Xa, 0, sizeof(double) * (size_t)ctx->n * ctx->nt, ctx->stream));
+    CK(cudaMemsetAsync(ctx->iter, 0, sizeof(int), ctx->stream));
+    int big = INT_MAX;
+    h2d(ctx, ctx->bad_nu, &big, sizeof(int));
+    ctx->gamma = gamma;
+    ctx->it_host = 0;
+    sync(ctx);
+    if (ctx->gexec && ctx->graph_gamma == gamma) return WMPC_OK;  // captured iteration still valid
+    if (ctx->gexec) {
+      cudaGraphExecDestroy(ctx->gexec);
+      ctx->gexec = nullptr;
+    }
+    if (ctx->graph) {
+      cudaGraphDestroy(ctx->graph);
+      ctx->graph = nullptr;
+    }
+    DevView d = view(ctx);
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+    launch_dg(ctx, d, nullptr, 1);
+    k_advance<<<1, 32, 0, ctx->stream>>>(ctx->iter);
+    CK(cudaStreamEndCapture(ctx->stream, &ctx->graph));
+    CK(cudaGraphInstantiate(&ctx->gexec, ctx->graph, 0));
+    ctx->launches -= 2 * ctx->H;  // captured, not launched
+    ctx->graph_gamma = gamma;
+    return WMPC_OK;
+  });
+}
+
+int wmpc_apg_run(wmpc_ctx* ctx, int count) {
+  return run(ctx, [&]() -> int {
+    if (!ctx->gexec) {
+      ctx->err = "wmpc_apg_begin must precede wmpc_apg_run";
+      return WMPC_E_STATE;
+    }
+    ARG(count >= 0 && ctx->it_host + count <= ctx->max_iter, "iteration count exceeds the theta table");
+    for (int i = 0; i < count; ++i) CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+    ctx->it_host += count;
+    ctx->launches += (int64_t)count * (2 * ctx->H + 1);
+    return WMPC_OK;
+  });
+}
+
+int wmpc_apg_run_timed(wmpc_ctx* ctx, int count, float* ms) {
+  return run(ctx, [&]() -> int {
+    if (!ctx->gexec) {
+      ctx->err = "wmpc_apg_begin must precede wmpc_apg_run_timed";
+      return WMPC_E_STATE;
+    }
+    ARG(count >= 0 && ctx->it_host + count <= ctx->max_iter, "iteration count exceeds the theta table");
+    CK(cudaEventRecord(ctx->ev2, ctx->stream));
+    for (int i = 0; i < count; ++i) CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+    CK(cudaEventRecord(ctx->ev3, ctx->stream));
+    CK(cudaEventSynchronize(ctx->ev3));
+    CK(cudaEventElapsedTime(ms, ctx->ev2, ctx->ev3));
+    ctx->it_host += count;
+    ctx->launches += (int64_t)count * (2 * ctx->H + 1);
+    return WMPC_OK;
+  });
+}
+
+int wmpc_apg_iterations(const wmpc_ctx* ctx) { return ctx ? ctx->it_host : -1; }
+
+int wmpc_apg_check(wmpc_ctx* ctx, double* primal_residual, double* image_scale, double* dual_change,
+                   int* first_nonfinite_nu) {
+  return run(ctx, [&]() -> int {
+    if (ctx->it_host < 1) {
+      ctx->err = "no APG iteration has run";
+      return WMPC_E_STATE;
+    }
+    DevView d = view(ctx);
+    const int it = ctx->it_host;
+    size_t len = (size_t)ctx->n * ctx->W;
+    int nb = std::min(ctx->part_blocks, grid_for(len));
+    ctx->launches++;
+    k_check_partial<<<nb, 256, 0, ctx->stream>>>(d, ctx->Y[it % 3], ctx->Y[(it + 2) % 3], ctx->part);
+    ctx->launches++;
+    k_finish<1><<<1, 256, 0, ctx->stream>>>(ctx->part, nb, 3, 0, 3, ctx->scal);
+    check_launch(ctx);
+    double h[3];
+    int bad = INT_MAX;
+    d2h(ctx, h, ctx->scal, 3 * sizeof(double));
+    d2h(ctx, &bad, ctx->bad_nu, sizeof(int));
+    sync(ctx);
+    if (primal_residual) *primal_residual = h[0];
+    if (image_scale) *image_scale = h[1];
+    if (dual_change) *dual_change = h[2];
+    if (first_nonfinite_nu) *first_nonfinite_nu = bad == INT_MAX ? -1 : bad;
+    return WMPC_OK;
+  });
+}
+
+int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
+  return run(ctx, [&]() -> int {
+    int st = need_ready(ctx);
+    if (st) return st;
+    DevView d = view(ctx);
+    const size_t nU = (size_t)ctx->n * ctx->nu;
+    // 1. feasibility restoration of the averaged inputs (problem.py:221-250)
+    if (ctx->ns == 0) {
+      ctx->launches++;
+      k_clip_inputs<<<grid_for(nU), 256, 0, ctx->stream>>>(d, ctx->Ua, ctx->Uf);
+    } else {
+      CK(cudaMemcpyAsync(ctx->dk_cur, ctx->Ua, sizeof(double) * nU, cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(cudaMemsetAsync(ctx->dk_pc, 0, sizeof(double) * nU, ctx->stream));
+      CK(cudaMemsetAsync(ctx->dk_qc, 0, sizeof(double) * nU, ctx->stream));
+      CK(cudaMemsetAsync(ctx->dk_done, 0, sizeof(int), ctx->stream));
+      int nb0 = grid_for(nU);
+      ctx->launches++;
+      k_absmax_partial<<<nb0, 256, 0, ctx->stream>>>(ctx->Ua, nU, ctx->part);
+      ctx->launches++;
+      k_dyk_tol<<<1, 256, 0, ctx->stream>>>(ctx->part, nb0, ctx->scal + 8);
+      int nb = std::min(ctx->part_blocks, std::max(1, (ctx->n + 7) / 8));
+      for (int sweep = 0; sweep < 500; ++sweep) {
+        ctx->launches++;
+        k_dyk_sweep<<<nb, 256, 0, ctx->stream>>>(d, ctx->dk_cur, ctx->dk_pc, ctx->dk_qc, ctx->dk_aff,
+                                                  ctx->dk_done, ctx->part);
+        ctx->launches++;
+        k_dyk_finish<<<1, 256, 0, ctx->stream>>>(ctx->part, nb, ctx->scal + 8, ctx->dk_done);
+        if (sweep % 16 == 15) {
+          int done = 0;
+          d2h(ctx, &done, ctx->dk_done, sizeof(int));
+          sync(ctx);
+          if (done) break;
+        }
+      }
+      CK(cudaMemcpyAsync(ctx->Uf, ctx->dk_cur, sizeof(double) * nU, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    // 2. rollout (problem.py:207-218)
+    for (int s = 0; s < ctx->H; ++s) {
+      int cnt = ctx->off[s + 1] - ctx->off[s];
+      ctx->launches++;
+      k_rollout_stage<<<grid_for((size_t)cnt * ctx->nt), 256, 0, ctx->stream>>>(d, ctx->off[s], cnt, ctx->Uf,
+                                                                                 ctx->Xf);
+    }
+    check_launch(ctx);
+    // 3. primal value (solver.py:453)
+    double tp[4];
+    cost_terms(ctx, d, ctx->Uf, ctx->Xf, nullptr, 1, tp);
+    double primal = tp[0] + (ctx->w_x * tp[2] + ctx->w_s * tp[3]);
+    // 4. dual value at the current iterate (solver.py:454-456)
+    const double* y = ctx->Y[ctx->it_host % 3];
+    DevView dc = d;
+    dc.U = ctx->Uc;
+    dc.X = ctx->Xc;
+    launch_dg(ctx, dc, y, 0);
+    double td[4];
+    cost_terms(ctx, dc, ctx->Uc, ctx->Xc, y, 0, td);
+    double inner = td[0] + td[1];
+    double gc = gconj_value(ctx, d, y);
+    double dual = inner - gc;
+    if (gap) *gap = primal - dual;
+    if (objective) *objective = primal;
+    return WMPC_OK;
+  });
+}
+
+int wmpc_apg_read(wmpc_ctx* ctx, int averaged, double* u0, double* primal, double* primal_avg, double* dual) {
+  return run(ctx, [&]() -> int {
+    DevView d = view(ctx);
+    const size_t n = ctx->n;
+    if (u0) {
+      ctx->launches++;
+      k_u0<<<1, 128, 0, ctx->stream>>>(d, averaged ? ctx->Ua : ctx->U, ctx->off[1], ctx->zbuf);
+      check_launch(ctx);
+      d2h(ctx, u0, ctx->zbuf, sizeof(double) * ctx->nu);
+      sync(ctx);
+    }
+    if (primal) {
+      ctx->launches++;
+      k_join_primal<<<grid_for(n * ctx->P), 256, 0, ctx->stream>>>(ctx->n, ctx->nu, ctx->nt, ctx->U, ctx->X,
+                                                                     ctx->zbuf);
+      d2h(ctx, primal, ctx->zbuf, sizeof(double) * n * ctx->P);
+      sync(ctx);
+    }
+    if (primal_avg) {
+      ctx->launches++;
+      k_join_primal<<<grid_for(n * ctx->P), 256, 0, ctx->stream>>>(ctx->n, ctx->nu, ctx->nt, ctx->Ua, ctx->Xa,
+                                                                     ctx->zbuf);
+      d2h(ctx, primal_avg, ctx->zbuf, sizeof(double) * n * ctx->P);
+      sync(ctx);
+    }
+    if (dual) d2h(ctx, dual, ctx->Y[ctx->it_host % 3], sizeof(double) * n * ctx->W);
+    check_launch(ctx);
+    sync(ctx);
+    return WMPC_OK;
+  });
+}
+
+int wmpc_timer_start(wmpc_ctx* ctx) {
+  return run(ctx, [&]() -> int {
+    CK(cudaEventRecord(ctx->ev0, ctx->stream));
+    return WMPC_OK;
+  });
+}
+
+int wmpc_timer_stop(wmpc_ctx* ctx, float* ms) {
+  return run(ctx, [&]() -> int {
+    CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    CK(cudaEventSynchronize(ctx->ev1));
+    CK(cudaEventElapsedTime(ms, ctx->ev0, ctx->ev1));
+    return WMPC_OK;
+  });
+}
+
+int64_t wmpc_launch_count(const wmpc_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int wmpc_host_alloc(uint64_t bytes, void** out) {
+  if (!out) return WMPC_E_ARG;
+  cudaError_t e = cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault);
+  if (e != cudaSuccess) {
+    g_global_err = std::string("cudaHostAlloc: ") + cudaGetErrorString(e);
+    return WMPC_E_CUDA;
+  }
+  return WMPC_OK;
+}
+
+void wmpc_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,690 @@
+// wmpc_kernels.cuh — v1 kernels: stage-tiled dual gradient, fused prox/averaging,
+// reductions, certificate and factor-step per-node part. General dimensions.
+//
+// Reference mapping (paths relative to /root/reference/pkg/src/watermpc):
+//   k_bwd_stage   solver.py:261-274  backward cost-to-go (one launch per stage)
+//   k_fwd_stage   solver.py:276-287  forward rollout, + solver.py:461-484 fused
+//                 (extrapolation, w + gamma Hz, Moreau prox, ergodic average)
+//   k_prox_rows   problem.py:290-327 / solver.py:546-583
+//   k_node_*      solver.py:206-225  factor step per-node part
+//   k_dyk_*       problem.py:221-250 Dykstra restoration
+//   k_cost_*      problem.py:269-275, solver.py:390-395, problem.py:342-374
+#pragma once
+#include "wmpc_common.cuh"
+
+namespace wmpc {
+
+constexpr int TM = 8;        // nodes per CTA tile in the stage kernels
+constexpr int NTHR = 128;
+
+// ---------------------------------------------------------------------------
+// Backward stage: for every node r of stage s (rows r0..r0+cnt):
+//   wbar_r = Yx_r + (sum_c wbar_c) A          (children ascending)
+//   lin_r  = Yu_r + R_r + [wbar_r | sum_c lin_c] [[B],[D_{s+1}]]
+// Yx/Yu come from the extrapolated dual w = y + beta (y - y_prev) (APG) or
+// directly from ysrc (plain mode).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHR) k_bwd_stage(DevView d, int s, int r0, int cnt,
+                                                    const double* __restrict__ ysrc) {
+  extern __shared__ double sm[];
+  const int nt = d.nt, nu = d.nu, W = d.W;
+  const int tile = blockIdx.x * TM;
+  const int rows = min(TM, cnt - tile);
+  const bool kids = s < d.H - 1;
+  const int K = nt + (kids ? nu : 0);
+  double* in = sm;                 // TM*K
+  double* add = in + TM * K;       // TM*nu
+  double* sw = add + TM * nu;      // TM*nt (child wbar sums when A != I)
+
+  const double *yc, *yp = nullptr;
+  double beta = 0.0;
+  if (ysrc) {
+    yc = ysrc;
+  } else {
+    int it = *d.iter;
+    yc = ybuf(d, it);
+    yp = ybuf(d, it + 2);
+    beta = d.beta[it];
+  }
+  for (int idx = threadIdx.x; idx < rows * nt; idx += blockDim.x) {
+    int m = idx / nt, j = idx - m * nt;
+    int r = r0 + tile + m;
+    const double* yr = yc + (size_t)r * W;
+    double w1 = yr[j], w2 = yr[nt + j];
+    if (yp) {
+      const double* pr = yp + (size_t)r * W;
+      w1 = dadd(w1, dmul(beta, dsub(w1, pr[j])));
+      w2 = dadd(w2, dmul(beta, dsub(w2, pr[nt + j])));
+    }
+    double yx = dadd(w1, w2);
+    double cs = 0.0;
+    if (kids)
+      for (int e = d.cptr[r]; e < d.cptr[r + 1]; ++e) cs += d.wbar[(size_t)d.cidx[e] * nt + j];
+    if (d.a_identity) {
+      in[m * K + j] = yx + cs;
+    } else {
+      in[m * K + j] = yx;
+      sw[m * nt + j] = cs;
+    }
+  }
+  for (int idx = threadIdx.x; idx < rows * nu; idx += blockDim.x) {
+    int m = idx / nu, j = idx - m * nu;
+    int r = r0 + tile + m;
+    double w3 = yc[(size_t)r * W + 2 * nt + j];
+    if (yp) w3 = dadd(w3, dmul(beta, dsub(w3, yp[(size_t)r * W + 2 * nt + j])));
+    double a = w3;
+    if (kids) {
+      a = w3 + d.np->R[(size_t)r * nu + j];
+      double ls = 0.0;
+      for (int e = d.cptr[r]; e < d.cptr[r + 1]; ++e) ls += d.lin[(size_t)d.cidx[e] * nu + j];
+      in[m * K + nt + j] = ls;
+    }
+    add[m * nu + j] = a;
+  }
+  __syncthreads();
+  if (!d.a_identity && kids) {
+    for (int idx = threadIdx.x; idx < rows * nt; idx += blockDim.x) {
+      int m = idx / nt, j = idx - m * nt;
+      double acc = 0.0;
+      for (int k = 0; k < nt; ++k) acc = fma(sw[m * nt + k], d.A[k * nt + j], acc);
+      in[m * K + j] += acc;
+    }
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < rows * nt; idx += blockDim.x) {
+    int m = idx / nt, j = idx - m * nt;
+    d.wbar[(size_t)(r0 + tile + m) * nt + j] = in[m * K + j];
+  }
+  const double* M = d.Mb + (size_t)s * (nt + nu) * nu;
+  for (int c = threadIdx.x; c < nu; c += blockDim.x) {
+    double acc[TM];
+#pragma unroll
+    for (int m = 0; m < TM; ++m) acc[m] = 0.0;
+    for (int k = 0; k < K; ++k) {
+      double b = __ldg(M + (size_t)k * nu + c);
+#pragma unroll
+      for (int m = 0; m < TM; ++m) acc[m] = fma(in[m * K + k], b, acc[m]);
+    }
+    for (int m = 0; m < rows; ++m)
+      d.lin[(size_t)(r0 + tile + m) * nu + c] = add[m * nu + c] + acc[m];
+  }
+}
+
+// Prox of the three slots for one node row held in shared memory.
+// v: the row w + gamma Hz (conj=1) or the prox argument (conj=0).
+// Writes the result row to out (global). Exact numpy expression order.
+struct ProxParams {
+  double gamma;  // conj: Moreau gamma; plain: prox gamma
+  int conj;
+};
+
+__device__ __forceinline__ double prox_arg(const double v, const ProxParams& pp) {
+  return pp.conj ? ddiv(v, pp.gamma) : v;
+}
+
+// step factors for slots 1 and 2 of a row (one warp).
+__device__ void prox_steps(const DevView& d, const double* v, const ProxParams& pp,
+                           double& st1, double& st2) {
+  const int nt = d.nt;
+  const double g = pp.conj ? ddiv(1.0, pp.gamma) : pp.gamma;
+  auto f1 = [&](int j) {
+    double V = prox_arg(v[j], pp);
+    double df = dsub(V, np_clip(V, d.xmin[j], d.xmax[j]));
+    return dmul(df, df);
+  };
+  auto f2 = [&](int j) {
+    double V = prox_arg(v[nt + j], pp);
+    double df = dsub(V, np_max(V, d.xsafe[j]));
+    return dmul(df, df);
+  };
+  double dist1 = __dsqrt_rn(pw_warp(f1, nt));
+  double dist2 = __dsqrt_rn(pw_warp(f2, nt));
+  double thr1 = dmul(g, d.w_x), thr2 = dmul(g, d.w_s);
+  st1 = dist1 > 0.0 ? np_min(1.0, ddiv(thr1, dist1)) : 0.0;
+  st2 = dist2 > 0.0 ? np_min(1.0, ddiv(thr2, dist2)) : 0.0;
+}
+
+__device__ __forceinline__ double prox_elem(const DevView& d, int c, double v, double st1,
+                                            double st2, const ProxParams& pp) {
+  const int nt = d.nt;
+  double V = prox_arg(v, pp);
+  double O;
+  if (c < nt) {
+    double df = dsub(V, np_clip(V, d.xmin[c], d.xmax[c]));
+    O = dsub(V, dmul(st1, df));
+  } else if (c < 2 * nt) {
+    double df = dsub(V, np_max(V, d.xsafe[c - nt]));
+    O = dsub(V, dmul(st2, df));
+  } else {
+    O = np_clip(V, d.umin[c - 2 * nt], d.umax[c - 2 * nt]);
+  }
+  return pp.conj ? dsub(v, dmul(pp.gamma, O)) : O;
+}
+
+// ---------------------------------------------------------------------------
+// Forward stage: u_r = e_off_r + [u_anc | lin_r/p_r] [[D_s^T],[-T_s]];
+//                x_r = x_anc A^T + u_r B^T + g_r.
+// mode 0: plain (store U, X). mode 1: APG — additionally y+ = prox_{gamma g*}(
+// w + gamma (x, x, u)) with w re-extrapolated, non-finite flag, ergodic average.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTHR) k_fwd_stage(DevView d, int s, int r0, int cnt, int mode) {
+  extern __shared__ double sm[];
+  const int nt = d.nt, nu = d.nu, W = d.W;
+  const int tile = blockIdx.x * TM;
+  const int rows = min(TM, cnt - tile);
+  double* inF = sm;                // TM*2nu
+  double* us = inF + TM * 2 * nu;  // TM*nu
+  double* xa = us + TM * nu;       // TM*nt
+  double* xs = xa + TM * nt;       // TM*nt
+  double* vrow = xs + TM * nt;     // TM*W (mode 1)
+  double* stp = vrow + TM * W;     // TM*2
+
+  for (int idx = threadIdx.x; idx < rows * nu; idx += blockDim.x) {
+    int m = idx / nu, j = idx - m * nu;
+    int r = r0 + tile + m;
+    int a = d.anc[r];
+    inF[m * 2 * nu + j] = a < 0 ? d.q[j] : d.U[(size_t)a * nu + j];
+    inF[m * 2 * nu + nu + j] = d.lin[(size_t)r * nu + j] / d.prob[r];
+  }
+  for (int idx = threadIdx.x; idx < rows * nt; idx += blockDim.x) {
+    int m = idx / nt, j = idx - m * nt;
+    int r = r0 + tile + m;
+    int a = d.anc[r];
+    xa[m * nt + j] = a < 0 ? d.p[j] : d.X[(size_t)a * nt + j];
+  }
+  __syncthreads();
+  const double* M = d.Mf + (size_t)s * 2 * nu * nu;
+  for (int c = threadIdx.x; c < nu; c += blockDim.x) {
+    double acc[TM];
+#pragma unroll
+    for (int m = 0; m < TM; ++m) acc[m] = 0.0;
+    for (int k = 0; k < 2 * nu; ++k) {
+      double b = __ldg(M + (size_t)k * nu + c);
+#pragma unroll
+      for (int m = 0; m < TM; ++m) acc[m] = fma(inF[m * 2 * nu + k], b, acc[m]);
+    }
+    for (int m = 0; m < rows; ++m) {
+      int r = r0 + tile + m;
+      double u = d.np->e_off[(size_t)r * nu + c] + acc[m];
+      us[m * nu + c] = u;
+      d.U[(size_t)r * nu + c] = u;
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < nt; c += blockDim.x) {
+    double acc[TM], acx[TM];
+#pragma unroll
+    for (int m = 0; m < TM; ++m) acc[m] = acx[m] = 0.0;
+    for (int k = 0; k < nu; ++k) {
+      double b = __ldg(d.Bt + (size_t)k * nt + c);
+#pragma unroll
+      for (int m = 0; m < TM; ++m) acc[m] = fma(us[m * nu + k], b, acc[m]);
+    }
+    if (!d.a_identity) {
+      for (int k = 0; k < nt; ++k) {
+        double b = __ldg(d.At + (size_t)k * nt + c);
+#pragma unroll
+        for (int m = 0; m < TM; ++m) acx[m] = fma(xa[m * nt + k], b, acx[m]);
+      }
+    }
+    for (int m = 0; m < rows; ++m) {
+      int r = r0 + tile + m;
+      double xprev = d.a_identity ? xa[m * nt + c] : acx[m];
+      double x = (xprev + acc[m]) + d.np->g[(size_t)r * nt + c];
+      xs[m * nt + c] = x;
+      d.X[(size_t)r * nt + c] = x;
+    }
+  }
+  if (mode == 0) return;
+  __syncthreads();
+
+  const int it = *d.iter;
+  const double* yc = ybuf(d, it);
+  const double* yp = ybuf(d, it + 2);
+  double* yn = ybuf_w(d, it + 1);
+  const double beta = d.beta[it], theta = d.theta[it], gamma = d.gamma;
+  for (int idx = threadIdx.x; idx < rows * W; idx += blockDim.x) {
+    int m = idx / W, c = idx - m * W;
+    int r = r0 + tile + m;
+    double y0 = yc[(size_t)r * W + c];
+    double w = dadd(y0, dmul(beta, dsub(y0, yp[(size_t)r * W + c])));
+    double hz = c < nt ? xs[m * nt + c] : (c < 2 * nt ? xs[m * nt + c - nt] : us[m * nu + c - 2 * nt]);
+    vrow[m * W + c] = dadd(w, dmul(gamma, hz));
+  }
+  __syncthreads();
+  ProxParams pp{gamma, 1};
+  const int warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (int m = warp; m < rows; m += nwarp) {
+    double s1, s2;
+    prox_steps(d, vrow + m * W, pp, s1, s2);
+    if ((threadIdx.x & 31) == 0) {
+      stp[2 * m] = s1;
+      stp[2 * m + 1] = s2;
+    }
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int idx = threadIdx.x; idx < rows * W; idx += blockDim.x) {
+    int m = idx / W, c = idx - m * W;
+    int r = r0 + tile + m;
+    double out = prox_elem(d, c, vrow[m * W + c], stp[2 * m], stp[2 * m + 1], pp);
+    yn[(size_t)r * W + c] = out;
+    bad |= !isfinite(out);
+  }
+  if (bad) atomicMin(d.bad_nu, it);
+  const double om = dsub(1.0, theta);
+  for (int idx = threadIdx.x; idx < rows * nu; idx += blockDim.x) {
+    int m = idx / nu, j = idx - m * nu;
+    size_t o = (size_t)(r0 + tile + m) * nu + j;
+    double u = us[m * nu + j];
+    d.Ua[o] = it == 0 ? u : dadd(dmul(d.Ua[o], om), dmul(theta, u));
+  }
+  for (int idx = threadIdx.x; idx < rows * nt; idx += blockDim.x) {
+    int m = idx / nt, j = idx - m * nt;
+    size_t o = (size_t)(r0 + tile + m) * nt + j;
+    double x = xs[m * nt + j];
+    d.Xa[o] = it == 0 ? x : dadd(dmul(d.Xa[o], om), dmul(theta, x));
+  }
+}
+
+__global__ void k_advance(int* iter) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *iter += 1;
+}
+
+// ---------------------------------------------------------------------------
+// Standalone prox (public prox_g / prox_g_conjugate). One warp per row.
+// ---------------------------------------------------------------------------
+__global__ void k_prox_rows(DevView d, const double* __restrict__ vin, double* __restrict__ out,
+                            double gamma, int conj) {
+  const int W = d.W;
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (warp >= d.n) return;
+  const double* v = vin + (size_t)warp * W;
+  ProxParams pp{gamma, conj};
+  double s1, s2;
+  prox_steps(d, v, pp, s1, s2);
+  for (int c = lane; c < W; c += 32) out[(size_t)warp * W + c] = prox_elem(d, c, v[c], s1, s2, pp);
+}
+
+// ---------------------------------------------------------------------------
+// Check-iteration reductions: per-block partials then a one-block finisher.
+// part layout: [resid, scale, dchange] per block.
+// ---------------------------------------------------------------------------
+__global__ void k_check_partial(DevView d, const double* __restrict__ ynew,
+                                const double* __restrict__ yold, double* part) {
+  __shared__ double sh[32];
+  double over = 0.0, scale = 0.0, dch = 0.0;
+  const size_t nU = (size_t)d.n * d.nu, nX = (size_t)d.n * d.nt, nY = (size_t)d.n * d.W;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nU; i += (size_t)gridDim.x * blockDim.x) {
+    int j = (int)(i % d.nu);
+    double u = d.Ua[i];
+    over = np_max(over, np_max(u - d.umax[j], 0.0));
+    over = np_max(over, np_max(d.umin[j] - u, 0.0));
+    scale = np_max(scale, fabs(u));
+  }
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nX; i += (size_t)gridDim.x * blockDim.x)
+    scale = np_max(scale, fabs(d.Xa[i]));
+  if (ynew)
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nY; i += (size_t)gridDim.x * blockDim.x)
+      dch = np_max(dch, fabs(ynew[i] - yold[i]));
+  over = block_reduce<1>(over, sh);
+  if (threadIdx.x == 0) part[3 * blockIdx.x] = over;
+  scale = block_reduce<1>(scale, sh);
+  if (threadIdx.x == 0) part[3 * blockIdx.x + 1] = scale;
+  dch = block_reduce<1>(dch, sh);
+  if (threadIdx.x == 0) part[3 * blockIdx.x + 2] = dch;
+}
+
+// Generic finisher: out[k] = OP over part[b*stride + k], b < nb.
+template <int OP>
+__global__ void k_finish(const double* part, int nb, int stride, int k0, int nk, double* out) {
+  __shared__ double sh[32];
+  for (int k = k0; k < k0 + nk; ++k) {
+    double v = OP == 0 ? 0.0 : -INFINITY;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) v = comb<OP>(v, part[(size_t)b * stride + k]);
+    v = block_reduce<OP>(v, sh);
+    if (threadIdx.x == 0) out[k] = v;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Per-node cost terms (one warp per node), summed per block:
+//   part[b*4+0] = sum p_r (c_r.u_r + du' W du)      smooth cost   (problem.py:269-275)
+//   part[b*4+1] = sum Yx.x + Yu.u  (if y given)     <H'y, z>       (solver.py:289)
+//   part[b*4+2] = sum ||x - clip(x)||               box distance   (solver.py:393)
+//   part[b*4+3] = sum ||x - max(x, xs)||            safety distance(solver.py:394)
+// ---------------------------------------------------------------------------
+__global__ void k_cost_partial(DevView d, const double* __restrict__ Uin, const double* __restrict__ Xin,
+                               const double* __restrict__ y, int want_pen, double* part) {
+  __shared__ double sh[32];
+  const int nt = d.nt, nu = d.nu, W = d.W;
+  int lane = threadIdx.x & 31;
+  int wpb = blockDim.x >> 5;
+  double acc_cost = 0.0, acc_dot = 0.0, acc_box = 0.0, acc_safe = 0.0;
+  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < d.n; r += gridDim.x * wpb) {
+    const double* u = Uin + (size_t)r * nu;
+    int a = d.anc[r];
+    const double* ua = a < 0 ? d.q : Uin + (size_t)a * nu;
+    double lin = 0.0, quad = 0.0;
+    for (int j = lane; j < nu; j += 32) {
+      lin += d.econ[(size_t)r * nu + j] * u[j];
+      double wd;
+      if (d.w_scalar) {
+        wd = d.w_c * (u[j] - ua[j]);
+      } else {
+        wd = 0.0;
+        for (int k = 0; k < nu; ++k) wd = fma(d.Wu[(size_t)j * nu + k], u[k] - ua[k], wd);
+      }
+      quad += (u[j] - ua[j]) * wd;
+    }
+    double dot = 0.0;
+    if (y) {
+      const double* yr = y + (size_t)r * W;
+      const double* x = Xin + (size_t)r * nt;
+      for (int j = lane; j < nt; j += 32) dot += (yr[j] + yr[nt + j]) * x[j];
+      for (int j = lane; j < nu; j += 32) dot += yr[2 * nt + j] * u[j];
+    }
+    double box = 0.0, safe = 0.0;
+    if (want_pen) {
+      const double* x = Xin + (size_t)r * nt;
+      for (int j = lane; j < nt; j += 32) {
+        double b = x[j] - np_clip(x[j], d.xmin[j], d.xmax[j]);
+        double sf = x[j] - np_max(x[j], d.xsafe[j]);
+        box += b * b;
+        safe += sf * sf;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lin += __shfl_down_sync(0xffffffffu, lin, o);
+      quad += __shfl_down_sync(0xffffffffu, quad, o);
+      dot += __shfl_down_sync(0xffffffffu, dot, o);
+      box += __shfl_down_sync(0xffffffffu, box, o);
+      safe += __shfl_down_sync(0xffffffffu, safe, o);
+    }
+    if (lane == 0) {
+      acc_cost += d.prob[r] * (lin + quad);
+      acc_dot += dot;
+      acc_box += sqrt(box);
+      acc_safe += sqrt(safe);
+    }
+  }
+  double v;
+  v = block_reduce<0>(acc_cost, sh);
+  if (threadIdx.x == 0) part[4 * blockIdx.x] = v;
+  v = block_reduce<0>(acc_dot, sh);
+  if (threadIdx.x == 0) part[4 * blockIdx.x + 1] = v;
+  v = block_reduce<0>(acc_box, sh);
+  if (threadIdx.x == 0) part[4 * blockIdx.x + 2] = v;
+  v = block_reduce<0>(acc_safe, sh);
+  if (threadIdx.x == 0) part[4 * blockIdx.x + 3] = v;
+}
+
+// g*(y) (problem.py:342-374): part[b*2] = support sums, part[b*2+1] = domain
+// violation flag (max).
+__device__ __forceinline__ double box_support(double lo, double hi, double y) {
+  double v = hi * (y > 0.0 ? y : 0.0) + lo * (y < 0.0 ? y : 0.0);
+  return isnan(v) ? 0.0 : v;
+}
+__global__ void k_gconj_partial(DevView d, const double* __restrict__ y, double tol, double* part) {
+  __shared__ double sh[32];
+  const int nt = d.nt, nu = d.nu, W = d.W;
+  int lane = threadIdx.x & 31;
+  int wpb = blockDim.x >> 5;
+  double acc = 0.0, viol = 0.0;
+  const double slack = 1.0 + tol;
+  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < d.n; r += gridDim.x * wpb) {
+    const double* yr = y + (size_t)r * W;
+    double n1 = 0.0, n2 = 0.0, sup = 0.0, v = 0.0;
+    for (int j = lane; j < nt; j += 32) {
+      double a = yr[j], b = yr[nt + j];
+      n1 += a * a;
+      n2 += b * b;
+      if (b > tol * (1.0 + fabs(d.xsafe[j]))) v = 1.0;
+      sup += box_support(d.xmin[j], d.xmax[j], a) + d.xsafe[j] * (b < 0.0 ? b : 0.0);
+    }
+    for (int j = lane; j < nu; j += 32) sup += box_support(d.umin[j], d.umax[j], yr[2 * nt + j]);
+    for (int o = 16; o > 0; o >>= 1) {
+      n1 += __shfl_down_sync(0xffffffffu, n1, o);
+      n2 += __shfl_down_sync(0xffffffffu, n2, o);
+      sup += __shfl_down_sync(0xffffffffu, sup, o);
+      v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+    }
+    if (lane == 0) {
+      if (sqrt(n1) > d.w_x * slack + tol) v = 1.0;
+      if (sqrt(n2) > d.w_s * slack + tol) v = 1.0;
+      acc += sup;
+      viol = fmax(viol, v);
+    }
+  }
+  double t = block_reduce<0>(acc, sh);
+  if (threadIdx.x == 0) part[2 * blockIdx.x] = t;
+  t = block_reduce<1>(viol, sh);
+  if (threadIdx.x == 0) part[2 * blockIdx.x + 1] = t;
+}
+
+// ---------------------------------------------------------------------------
+// Dykstra restoration sweep (problem.py:239-249), one warp per node; the
+// global stopping test is evaluated by k_dyk_finish between sweeps.
+// ---------------------------------------------------------------------------
+__global__ void k_dyk_sweep(DevView d, double* cur, double* pc, double* qc, double* aff,
+                            const int* done, double* part) {
+  __shared__ double sh[32];
+  if (*done) return;
+  const int nu = d.nu, ns = d.ns;
+  int lane = threadIdx.x & 31;
+  int wpb = blockDim.x >> 5;
+  double moved = 0.0;
+  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < d.n; r += gridDim.x * wpb) {
+    double* c = cur + (size_t)r * nu;
+    double* P = pc + (size_t)r * nu;
+    double* Q = qc + (size_t)r * nu;
+    double* A = aff + (size_t)r * nu;
+    for (int j = lane; j < nu; j += 32) A[j] = c[j] + P[j];
+    __syncwarp();
+    // t_i = A.E_i + shift_i ;  A_j -= sum_i t_i pinv[j][i]
+    double tl[32];  // ns <= 32 (checked at wmpc_create)
+    for (int i = 0; i < ns; ++i) {
+      double t = 0.0;
+      for (int j = lane; j < nu; j += 32) t += A[j] * d.E[(size_t)i * nu + j];
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      tl[i] = t + d.np->shift[(size_t)r * ns + i];
+    }
+    __syncwarp();
+    for (int j = lane; j < nu; j += 32) {
+      double corr = 0.0;
+      for (int i = 0; i < ns; ++i) corr += tl[i] * d.e_pinv[(size_t)j * ns + i];
+      double a = A[j] - corr;
+      double pn = c[j] + P[j] - a;
+      double nx = np_clip(a + Q[j], d.umin[j], d.umax[j]);
+      Q[j] = a + Q[j] - nx;
+      P[j] = pn;
+      moved = np_max(moved, fabs(nx - c[j]));
+      c[j] = nx;
+    }
+    __syncwarp();
+  }
+  moved = block_reduce<1>(moved, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = moved;
+}
+
+__global__ void k_dyk_finish(const double* part, int nb, const double* tol, int* done) {
+  __shared__ double sh[32];
+  if (*done) return;
+  double v = -INFINITY;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) v = np_max(v, part[b]);
+  v = block_reduce<1>(v, sh);
+  if (threadIdx.x == 0 && v <= *tol) *done = 1;
+}
+
+__global__ void k_absmax_partial(const double* __restrict__ a, size_t len, double* part) {
+  __shared__ double sh[32];
+  double m = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x)
+    m = np_max(m, fabs(a[i]));
+  m = block_reduce<1>(m, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = m;
+}
+
+__global__ void k_dyk_tol(const double* part, int nb, double* tol) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) v = np_max(v, part[b]);
+  v = block_reduce<1>(v, sh);
+  if (threadIdx.x == 0) *tol = 1e-13 * (1.0 + v);
+}
+
+__global__ void k_clip_inputs(DevView d, const double* __restrict__ src, double* dst) {
+  size_t len = (size_t)d.n * d.nu;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x) {
+    int j = (int)(i % d.nu);
+    dst[i] = np_clip(src[i], d.umin[j], d.umax[j]);
+  }
+}
+
+// Rollout x_r = x_anc A^T + u_r B^T + g_r for one stage (problem.py:207-218).
+__global__ void k_rollout_stage(DevView d, int r0, int cnt, const double* __restrict__ Uin, double* Xout) {
+  const int nt = d.nt, nu = d.nu;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < cnt * nt; idx += gridDim.x * blockDim.x) {
+    int m = idx / nt, j = idx - m * nt;
+    int r = r0 + m;
+    int a = d.anc[r];
+    const double* xa = a < 0 ? d.p : Xout + (size_t)a * nt;
+    double xp = 0.0;
+    if (d.a_identity) {
+      xp = xa[j];
+    } else {
+      for (int k = 0; k < nt; ++k) xp = fma(xa[k], d.A[(size_t)j * nt + k], xp);
+    }
+    double bu = 0.0;
+    for (int k = 0; k < nu; ++k) bu = fma(Uin[(size_t)r * nu + k], d.Bt[(size_t)k * nt + j], bu);
+    Xout[(size_t)r * nt + j] = (xp + bu) + d.np->g[(size_t)r * nt + j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Factor step per-node part (solver.py:206-225), one warp per node.
+// ---------------------------------------------------------------------------
+__global__ void k_node_offsets(DevView d, const double* __restrict__ demand, const double* __restrict__ Ed,
+                               double* shift, double* u_part, double* e_off, double* tmp, int* bad_row) {
+  const int nu = d.nu, ns = d.ns, nd = d.nd;
+  int lane = threadIdx.x & 31;
+  int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= d.n) return;
+  double* up = u_part + (size_t)r * nu;
+  double* t = tmp + (size_t)r * nu;
+  if (ns > 0) {
+    for (int i = lane; i < ns; i += 32) {
+      double s = 0.0;
+      for (int k = 0; k < nd; ++k) s = fma(demand[(size_t)r * nd + k], Ed[(size_t)i * nd + k], s);
+      shift[(size_t)r * ns + i] = s;
+    }
+    __syncwarp();
+    for (int j = lane; j < nu; j += 32) {
+      double s = 0.0;
+      for (int i = 0; i < ns; ++i) s = fma(shift[(size_t)r * ns + i], d.e_pinv[(size_t)j * ns + i], s);
+      up[j] = -s;
+    }
+    __syncwarp();
+    bool bad = false;
+    for (int i = lane; i < ns; i += 32) {
+      double s = 0.0;
+      for (int j = 0; j < nu; ++j) s = fma(up[j], d.E[(size_t)i * nu + j], s);
+      double rhs = shift[(size_t)r * ns + i];
+      if (fabs(s + rhs) > 1e-9 * (1.0 + fabs(rhs))) bad = true;
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(bad_row, r);
+  } else {
+    for (int j = lane; j < nu; j += 32) up[j] = 0.0;
+  }
+  __syncwarp();
+  const int s = d.stage_of[r];
+  const double* L = d.Lam + (size_t)s * nu * nu;
+  const double* T = d.T + (size_t)s * nu * nu;
+  for (int j = lane; j < nu; j += 32) {
+    double a = 0.0;
+    for (int k = 0; k < nu; ++k) a = fma(up[k], L[(size_t)k * nu + j], a);
+    t[j] = a + d.econ[(size_t)r * nu + j];
+  }
+  __syncwarp();
+  for (int j = lane; j < nu; j += 32) {
+    double a = 0.0;
+    for (int k = 0; k < nu; ++k) a = fma(t[k], T[(size_t)k * nu + j], a);
+    e_off[(size_t)r * nu + j] = up[j] - a;
+  }
+}
+
+// R_a = sum_c -2 p_c (e_off_c W), children ascending.
+__global__ void k_node_R(DevView d, const double* __restrict__ e_off, double* Rout) {
+  const int nu = d.nu;
+  int lane = threadIdx.x & 31;
+  int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= d.n) return;
+  for (int j = lane; j < nu; j += 32) {
+    double acc = 0.0;
+    for (int e = d.cptr[r]; e < d.cptr[r + 1]; ++e) {
+      int c = d.cidx[e];
+      double ew = 0.0;
+      if (d.w_scalar) {
+        ew = e_off[(size_t)c * nu + j] * d.w_c;
+      } else {
+        for (int k = 0; k < nu; ++k) ew = fma(e_off[(size_t)c * nu + k], d.Wu[(size_t)k * nu + j], ew);
+      }
+      acc += (-2.0 * d.prob[c]) * ew;
+    }
+    Rout[(size_t)r * nu + j] = acc;
+  }
+}
+
+// Power iteration helpers (solver.py:348-366).
+__global__ void k_op_rows(DevView d, const double* __restrict__ U0, const double* __restrict__ X0,
+                          const double* __restrict__ Uv, const double* __restrict__ Xv,
+                          const double* __restrict__ v, double* gv, double* part) {
+  __shared__ double sh[32];
+  const int nt = d.nt, nu = d.nu, W = d.W;
+  double dot = 0.0, nn = 0.0;
+  size_t len = (size_t)d.n * W;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x) {
+    size_t r = i / W;
+    int c = (int)(i - r * W);
+    double gval = c < 2 * nt ? X0[r * nt + (c < nt ? c : c - nt)] - Xv[r * nt + (c < nt ? c : c - nt)]
+                             : U0[r * nu + c - 2 * nt] - Uv[r * nu + c - 2 * nt];
+    gv[i] = gval;
+    dot += v[i] * gval;
+    nn += gval * gval;
+  }
+  dot = block_reduce<0>(dot, sh);
+  if (threadIdx.x == 0) part[2 * blockIdx.x] = dot;
+  nn = block_reduce<0>(nn, sh);
+  if (threadIdx.x == 0) part[2 * blockIdx.x + 1] = nn;
+}
+
+__global__ void k_scale_into(const double* __restrict__ src, size_t len, const double* nrm2, double* dst) {
+  double nrm = sqrt(*nrm2);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i] / nrm;
+}
+
+// u0 = sum_{stage 1} p_r U_r, clipped (solver.py:525-528).
+__global__ void k_u0(DevView d, const double* __restrict__ Uin, int cnt1, double* out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d.nu; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < cnt1; ++r) s = fma(d.prob[r], Uin[(size_t)r * d.nu + j], s);
+    out[j] = np_clip(s, d.umin[j], d.umax[j]);
+  }
+}
+
+// join (U, X) rows into primal rows [u | x].
+__global__ void k_join_primal(int n, int nu, int nt, const double* __restrict__ U,
+                              const double* __restrict__ X, double* z) {
+  const int P = nu + nt;
+  size_t len = (size_t)n * P;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x) {
+    size_t r = i / P;
+    int c = (int)(i - r * P);
+    z[i] = c < nu ? U[r * nu + c] : X[r * nt + c - nu];
+  }
+}
+
+}  // namespace wmpc

@@ -1,0 +1,123 @@
+"""Seeded synthetic Barcelona-dimension networks and uniform scenario trees.
+
+The reference ships no Barcelona data; this generator builds a
+network with the paper's dimensions (``PAPER.md`` city study: 63 tanks,
+114 controlled flows = 75 pumps + 39 valves, 88 demand sectors, 17 mixing
+nodes) and the SURVEY §8d conventions:
+
+* A = I, B = +-dt (<= 2 nonzeros per column), Gd = -dt, hourly units (dt = 1);
+* E/Ed are mixing-node conservation rows; each mixing node owns one source
+  pump so E has full row rank and every node's coupling is feasible;
+* x in [0, 5000] m^3, x_safe = 1200, u in [0, q_max], q_max ~ U(300, 900),
+  alpha0 ~ U(0.001, 0.031);
+* forecasts d_hat ~ 5 + 5U, alpha_hat ~ 0.02 + 0.01U; per-node errors are
+  N(0, 0.05^2) relative to the stage forecast;
+* weights (W_alpha, W_u, W_s, W_x) = (1, 1e-2, 1, 100); p = 2500, q = 0.
+
+Named configs: C1 [2,2,2] 182 nodes, C2 [2]*7 2,430,
+C3 [4,4,4,2,2,2] 10,196, C4 [4]*6 79,188 — all with horizon 24.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .model import CostWeights, NetworkModel
+from .problem import assemble_problem
+from .tree import attach_forecast, uniform_tree
+
+N_TANKS, N_FLOWS, N_DEMANDS, N_MIXING = 63, 114, 88, 17
+HORIZON = 24
+
+CONFIGS = {
+    "C1": [2, 2, 2],
+    "C2": [2] * 7,
+    "C3": [4, 4, 4, 2, 2, 2],
+    "C4": [4] * 6,
+}
+
+WEIGHTS = dict(w_alpha=1.0, w_u=1e-2, w_s=1.0, w_x=100.0)
+
+
+def barcelona_network(seed: int = 0) -> NetworkModel:
+    """Deterministic 63/114/88/17 flow network (A = I, dt = 1 h)."""
+    rng = np.random.default_rng(seed)
+    nt, nu, nd, ns = N_TANKS, N_FLOWS, N_DEMANDS, N_MIXING
+    B = np.zeros((nt, nu))
+    Gd = np.zeros((nt, nd))
+    E = np.zeros((ns, nu))
+    Ed = np.zeros((ns, nd))
+    col = 0
+    # 39 valves: mixing node k -> tanks (first 5 nodes feed 3 tanks, others 2).
+    tank = 0
+    for k in range(ns):
+        for _ in range(3 if k < 5 else 2):
+            E[k, col] -= 1.0
+            B[tank, col] += 1.0
+            tank += 1
+            col += 1
+    assert col == 39 and tank == 39
+    # 17 source pumps, one into each mixing node (full row rank of E).
+    for k in range(ns):
+        E[k, col] += 1.0
+        col += 1
+    # 24 source pumps into tanks 39..62.
+    for t in range(39, nt):
+        B[t, col] += 1.0
+        col += 1
+    # 34 transfer pumps tank -> tank.
+    for i in range(34):
+        src = 39 + (i % 24)
+        dst = (7 * i + 3) % 39
+        B[src, col] -= 1.0
+        B[dst, col] += 1.0
+        col += 1
+    assert col == nu
+    # 71 tank demands (every tank once, tanks 0..7 twice), 17 mixing demands.
+    d = 0
+    for t in range(nt):
+        Gd[t, d] -= 1.0
+        d += 1
+    for t in range(8):
+        Gd[t, d] -= 1.0
+        d += 1
+    for k in range(ns):
+        Ed[k, d] -= 1.0
+        d += 1
+    assert d == nd
+    q_max = rng.uniform(300.0, 900.0, nu)
+    alpha0 = rng.uniform(0.001, 0.031, nu)
+    model = NetworkModel(
+        A=np.eye(nt), B=B, Gd=Gd, E=E, Ed=Ed,
+        x_min=np.zeros(nt), x_max=np.full(nt, 5000.0), x_safe=np.full(nt, 1200.0),
+        u_min=np.zeros(nu), u_max=q_max, alpha0=alpha0, dt=1.0,
+    )
+    model.validate()
+    return model
+
+
+def barcelona_instance(branching, seed: int = 0, horizon: int = HORIZON,
+                       weights: dict | None = None):
+    """Assembled instance on a uniform tree with seeded forecasts and errors."""
+    model = barcelona_network(seed)
+    rng = np.random.default_rng(1000 + seed)
+    nd, nu = model.n_demands, model.n_inputs
+    d_hat = 5.0 + 5.0 * rng.random((horizon, nd))
+    a_hat = 0.02 + 0.01 * rng.random((horizon, nu))
+    tree = uniform_tree(branching, horizon, nd, nu)
+    n = tree.n_nodes
+    z = rng.standard_normal((n, nd + nu))
+    st = np.maximum(tree.stage - 1, 0)
+    scale = np.concatenate([d_hat[st], a_hat[st]], axis=1)
+    eps = 0.05 * z * scale
+    eps[0] = 0.0
+    tree.eps = eps
+    tree = attach_forecast(tree, d_hat, a_hat)
+    w = CostWeights(**(weights or WEIGHTS))
+    p = np.full(model.n_tanks, 2500.0)
+    q = np.zeros(nu)
+    return assemble_problem(model, tree, w, p, q)
+
+
+def config_instance(name: str, seed: int = 0):
+    return barcelona_instance(CONFIGS[name], seed=seed)
