@@ -118,12 +118,28 @@ int wmpc_apg_read(wmpc_ctx* ctx, int averaged, double* u0, double* primal,
 /* Iterations completed since wmpc_apg_begin. */
 int wmpc_apg_iterations(const wmpc_ctx* ctx);
 
-/* Kernels launched per APG iteration (bench accounting). */
+/* Kernels launched per APG iteration (bench accounting; 0 = one persistent
+ * launch per wmpc_apg_run call). */
 int wmpc_kernel_launches_per_iteration(const wmpc_ctx* ctx);
+/* Row-tile size of the persistent structured kernel (A = I, W = cI), or 0 when
+ * the general per-stage kernels run. */
+int wmpc_fast_path(const wmpc_ctx* ctx);
 
 /* Timing helpers for bench.py: run `count` iterations between CUDA events on
  * the context's stream; *ms = elapsed device time. */
 int wmpc_apg_run_timed(wmpc_ctx* ctx, int count, float* ms);
+
+/* Test hook: number of v[i] / g64[i % 64] (n samples) where the kernels'
+ * reciprocal-based exact division differs from IEEE division. */
+int wmpc_debug_div(const double* v, const double* g64, int n, uint64_t* mismatches);
+
+/* Diagnostics: run `count` APG iterations of the persistent kernel with
+ * per-CTA clock64 counters (grid*12 values: total, phases A-D, projector,
+ * prox, row wait, grid sync, chain steps) copied to `counters`. */
+int wmpc_profile_fast(wmpc_ctx* ctx, int count, uint64_t* counters, int cap);
+
+/* Device time (ms) of the last debug/test-hook launch. */
+float wmpc_last_debug_ms(const wmpc_ctx* ctx);
 
 /* Device-time bracket on the context's stream (bench.py): start records an
  * event; stop records a second one, waits for it and returns the elapsed ms. */

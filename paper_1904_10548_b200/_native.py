@@ -64,6 +64,10 @@ SIGNATURES = {
     "wmpc_apg_read": (C.c_int, [_vp, C.c_int, _dp, _dp, _dp, _dp]),
     "wmpc_apg_iterations": (C.c_int, [_vp]),
     "wmpc_kernel_launches_per_iteration": (C.c_int, [_vp]),
+    "wmpc_fast_path": (C.c_int, [_vp]),
+    "wmpc_profile_fast": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_int]),
+    "wmpc_last_debug_ms": (C.c_float, [_vp]),
+    "wmpc_debug_div": (C.c_int, [_dp, _dp, C.c_int, C.POINTER(C.c_uint64)]),
     "wmpc_timer_start": (C.c_int, [_vp]),
     "wmpc_timer_stop": (C.c_int, [_vp, C.POINTER(C.c_float)]),
     "wmpc_launch_count": (C.c_int64, [_vp]),

@@ -15,7 +15,7 @@
 #include <vector>
 
 #include "wmpc.h"
-#include "wmpc_kernels.cuh"
+#include "wmpc_fast.cuh"
 
 using namespace wmpc;
 
@@ -31,7 +31,7 @@ struct wmpc_nodes {
 struct wmpc_ctx {
   int dev = 0;
   cudaStream_t stream = nullptr;
-  int n = 0, H = 0, nt = 0, nu = 0, nd = 0, ns = 0, W = 0, P = 0;
+  int n = 0, H = 0, nt = 0, nu = 0, nd = 0, ns = 0, W = 0, P = 0, lx = 0, ly = 0;
   int a_identity = 0, w_scalar = 0;
   double w_c = 0.0;
   std::vector<int> off;  // H+1
@@ -49,7 +49,7 @@ struct wmpc_ctx {
   double *Y[3] = {nullptr, nullptr, nullptr};
   double *U = nullptr, *X = nullptr, *Ua = nullptr, *Xa = nullptr;
   double *Uc = nullptr, *Xc = nullptr, *Uf = nullptr, *Xf = nullptr, *U0 = nullptr, *X0 = nullptr;
-  double *wbar = nullptr, *lin = nullptr;
+  double *wbar = nullptr, *lin = nullptr, *Yc = nullptr;
   double *ys = nullptr, *gv = nullptr, *vv = nullptr, *zbuf = nullptr;
   double *dk_cur = nullptr, *dk_pc = nullptr, *dk_qc = nullptr, *dk_aff = nullptr;
   double *theta = nullptr, *beta = nullptr;
@@ -61,6 +61,21 @@ struct wmpc_ctx {
   int it_host = 0;
   int64_t launches = 0;
   double graph_gamma = -1.0;
+  // structured fast path (wmpc_fast.cuh)
+  bool fast = false;
+  int kstar = 0, nchain = 0, fast_mc = 1, fast_cpc = 1, fast_gs = 1, fast_grid = 0;
+  int fast_nrow = 2, fast_rec = 0, fast_enz = 0, fast_bnz = 0;
+  unsigned long long* prof = nullptr;
+  float last_debug_ms = 0.f;
+  int prof_on = 0;
+  size_t fast_smem = 0;
+  int *chain_node = nullptr, *bc_ptr = nullptr, *bc_row = nullptr, *br_ptr = nullptr, *br_col = nullptr;
+  int *e_ptr = nullptr, *e_col = nullptr;
+  double *e_val = nullptr, *aux = nullptr;
+  std::vector<double> prob_host;
+  int* off_dev = nullptr;
+  double *bc_val = nullptr, *br_val = nullptr;
+  int sms = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
@@ -106,7 +121,7 @@ void check_launch(wmpc_ctx* ctx) { CK(cudaGetLastError()); }
 DevView view(const wmpc_ctx* c) {
   DevView d;
   d.n = c->n; d.H = c->H; d.nt = c->nt; d.nu = c->nu; d.nd = c->nd; d.ns = c->ns;
-  d.W = c->W; d.P = c->P;
+  d.W = c->W; d.P = c->P; d.lx = c->lx; d.ly = c->ly; d.Yc = c->Yc;
   d.a_identity = c->a_identity; d.w_scalar = c->w_scalar; d.w_c = c->w_c;
   d.stage_of = c->stage_of; d.anc = c->anc; d.cptr = c->cptr; d.cidx = c->cidx; d.prob = c->prob;
   d.A = c->A; d.At = c->At; d.Bt = c->Bt; d.Wu = c->Wu; d.T = c->T; d.Lam = c->Lam;
@@ -181,6 +196,206 @@ double gconj_value(wmpc_ctx* ctx, const DevView& d, const double* y) {
   return h[1] > 0.0 ? INFINITY : h[0];
 }
 
+template <class T>
+void upload_vec(wmpc_ctx* ctx, T** dst, const std::vector<T>& v) {
+  if (*dst) cudaFree(*dst);
+  *dst = nullptr;
+  dalloc(ctx, dst, v.size());
+  h2d(ctx, *dst, v.data(), sizeof(T) * v.size());
+}
+
+template <int MC>
+void fast_attr(wmpc_ctx* ctx, size_t smem) {
+  CK(cudaFuncSetAttribute(k_apg_fast<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+size_t fast_smem_bytes(const wmpc_ctx* c, int MC, int nrow, int rec, int cpc, int enz, int bnz) {
+  const int nst = c->H - c->kstar, nu = c->nu, nt = c->nt, lx = c->lx, ns = c->ns;
+  size_t dbl = (size_t)nrow * MC * rec + 2 * (size_t)MC * nu + (size_t)MC * FAST_MAXNS + (size_t)MC * lx +
+               (size_t)MC * nu + (size_t)MC * lx + (size_t)MC * 2 * nt + 2 * MC + (3 * nt + 2 * nu) +
+               (size_t)nu * ns + enz + 2 * (size_t)bnz;
+  size_t ints = (ns + 1) + enz + (nu + 1) + bnz + (nt + 1) + bnz + (size_t)nrow * MC + c->H + 1 +
+                (size_t)cpc * nst;
+  return dbl * sizeof(double) + ints * sizeof(int) + 64;
+}
+
+// Decide whether the structured persistent kernel applies and lay out its data:
+// A = I, W = cI, n_u even, n_s <= 32, and every stage factor equal to the
+// null(E) projector (T_s = P/(2c), D_s = P up to 1e-12 relative).
+void configure_fast(wmpc_ctx* ctx, const double* B, const double* E, const double* e_pinv, const double* T,
+                    const double* D, const std::vector<int>& cptr, const std::vector<int>& cidx) {
+  ctx->fast = false;
+  const char* env = getenv("WMPC_DISABLE_FAST");
+  if (env && env[0] == '1') return;
+  const int H = ctx->H, nt = ctx->nt, nu = ctx->nu, ns = ctx->ns;
+  if (!ctx->a_identity || !ctx->w_scalar || (nu % 2) || ns > FAST_MAXNS || ctx->w_c <= 0.0) return;
+  if (nt > 64 || nu > 128 || ctx->W > 256 || (ctx->ly / 2) > 128) return;  // division-free layouts
+  // projector check against the host recursion's factors
+  std::vector<double> P((size_t)nu * nu);
+  for (int i = 0; i < nu; ++i)
+    for (int j = 0; j < nu; ++j) {
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int k = 0; k < ns; ++k) s -= e_pinv[(size_t)i * ns + k] * E[(size_t)k * nu + j];
+      P[(size_t)i * nu + j] = s;
+    }
+  const double c2 = 2.0 * ctx->w_c;
+  for (int s = 0; s < H; ++s) {
+    double tmax = 0.0, terr = 0.0, derr = 0.0;
+    for (size_t k = 0; k < (size_t)nu * nu; ++k) {
+      const double t = T[(size_t)s * nu * nu + k], dv = D[(size_t)s * nu * nu + k];
+      tmax = std::max(tmax, std::fabs(t));
+      terr = std::max(terr, std::fabs(t - P[k] / c2));
+      derr = std::max(derr, std::fabs(dv - P[k]));
+    }
+    if (terr > 1e-12 * std::max(tmax, 1e-300) || derr > 1e-12) return;
+  }
+  // first chain stage: from the leaves up, stages whose nodes all have one child and equal counts
+  const std::vector<int>& off = ctx->off;
+  int kstar = H - 1;
+  while (kstar > 0) {
+    int s = kstar - 1;
+    if (off[s + 1] - off[s] != off[s + 2] - off[s + 1]) break;
+    bool ok = true;
+    for (int r = off[s]; r < off[s + 1] && ok; ++r) ok = (cptr[r + 1] - cptr[r]) == 1;
+    if (!ok) break;
+    kstar = s;
+  }
+  const int nchain = off[kstar + 1] - off[kstar];
+  std::vector<int> chain((size_t)(H - kstar) * nchain);
+  for (int i = 0; i < nchain; ++i) {
+    int r = off[kstar] + i;
+    for (int s = kstar; s < H; ++s) {
+      chain[(size_t)(s - kstar) * nchain + i] = r;
+      if (s + 1 < H) r = cidx[cptr[r]];
+    }
+  }
+  // sparse B (both orientations) and E (rows)
+  std::vector<int> bcp(nu + 1, 0), bcr, brp(nt + 1, 0), brc, ep(ns + 1, 0), ec;
+  std::vector<double> bcv, brv, ev;
+  for (int j = 0; j < nu; ++j) {
+    for (int i = 0; i < nt; ++i)
+      if (B[(size_t)i * nu + j] != 0.0) {
+        bcr.push_back(i);
+        bcv.push_back(B[(size_t)i * nu + j]);
+      }
+    bcp[j + 1] = (int)bcr.size();
+  }
+  for (int i = 0; i < nt; ++i) {
+    for (int j = 0; j < nu; ++j)
+      if (B[(size_t)i * nu + j] != 0.0) {
+        brc.push_back(j);
+        brv.push_back(B[(size_t)i * nu + j]);
+      }
+    brp[i + 1] = (int)brc.size();
+  }
+  for (int i = 0; i < ns; ++i) {
+    for (int j = 0; j < nu; ++j)
+      if (E[(size_t)i * nu + j] != 0.0) {
+        ec.push_back(j);
+        ev.push_back(E[(size_t)i * nu + j]);
+      }
+    ep[i + 1] = (int)ec.size();
+  }
+  const int bnz = (int)bcr.size(), enz = (int)ec.size();
+  if (bcr.empty()) {
+    bcr.push_back(0); bcv.push_back(0.0); brc.push_back(0); brv.push_back(0.0);
+  }
+  if (ec.empty()) {
+    ec.push_back(0); ev.push_back(0.0);
+  }
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev));
+  ctx->sms = sms;
+  int cpc = (nchain + sms - 1) / sms;
+  if (const char* e = getenv("WMPC_CPC")) cpc = std::max(cpc, atoi(e));
+  int MC = 1;
+  while (MC < 8 && MC < cpc) MC *= 2;
+  if (const char* e = getenv("WMPC_MC")) MC = std::min(8, std::max(MC, atoi(e)));
+  int ngroups = (cpc + MC - 1) / MC;
+  int gs = (cpc + ngroups - 1) / ngroups;
+  ctx->kstar = kstar;  // fast_smem_bytes reads it
+  const int W = ctx->W, lx = ctx->lx, ly = ctx->ly;
+  const int rec = std::max(ly + nu, 2 * W + 3 * nu + 2 * lx + 2);
+  const size_t cap = 227 * 1024;
+  int nrow = 0;
+  for (int nr = 2; nr <= 8; ++nr)
+    if (fast_smem_bytes(ctx, MC, nr, rec, cpc, enz, bnz) <= cap) nrow = nr;
+  if (const char* e = getenv("WMPC_NROW")) nrow = std::min(nrow, std::max(2, atoi(e)));
+  if (nrow < 2) return;
+  size_t smem = fast_smem_bytes(ctx, MC, nrow, rec, cpc, enz, bnz);
+  switch (MC) {
+    case 1: fast_attr<1>(ctx, smem); break;
+    case 2: fast_attr<2>(ctx, smem); break;
+    case 4: fast_attr<4>(ctx, smem); break;
+    default: fast_attr<8>(ctx, smem); break;
+  }
+  upload_vec(ctx, &ctx->chain_node, chain);
+  upload_vec(ctx, &ctx->bc_ptr, bcp);
+  upload_vec(ctx, &ctx->bc_row, bcr);
+  upload_vec(ctx, &ctx->bc_val, bcv);
+  upload_vec(ctx, &ctx->br_ptr, brp);
+  upload_vec(ctx, &ctx->br_col, brc);
+  upload_vec(ctx, &ctx->br_val, brv);
+  upload_vec(ctx, &ctx->e_ptr, ep);
+  upload_vec(ctx, &ctx->e_col, ec);
+  upload_vec(ctx, &ctx->e_val, ev);
+  upload_vec(ctx, &ctx->off_dev, off);
+  {
+    std::vector<double> aux((size_t)2 * ctx->n, 0.0);
+    for (int r = 0; r < ctx->n; ++r) aux[2 * r] = 1.0 / (2.0 * ctx->w_c * ctx->prob_host[r]);
+    upload_vec(ctx, &ctx->aux, aux);
+  }
+  ctx->nchain = nchain;
+  ctx->fast_mc = MC;
+  ctx->fast_cpc = cpc;
+  ctx->fast_gs = gs;
+  ctx->fast_grid = sms;  // one persistent CTA per SM
+  ctx->fast_smem = smem;
+  ctx->fast_nrow = nrow;
+  ctx->fast_rec = rec;
+  ctx->fast_enz = enz;
+  ctx->fast_bnz = bnz;
+  ctx->fast = true;
+}
+
+template <int MC>
+void launch_fast_mc(wmpc_ctx* ctx, FastView& f) {
+  void* args[] = {(void*)&f, (void*)&ctx->off_dev};
+  CK(cudaLaunchCooperativeKernel((void*)k_apg_fast<MC>, dim3(ctx->fast_grid), dim3(FAST_THREADS), args,
+                                 ctx->fast_smem, ctx->stream));
+}
+
+void launch_fast(wmpc_ctx* ctx, int count) {
+  FastView f;
+  f.d = view(ctx);
+  f.kstar = ctx->kstar;
+  f.nchain = ctx->nchain;
+  f.chain_node = ctx->chain_node;
+  f.bc_ptr = ctx->bc_ptr; f.bc_row = ctx->bc_row; f.bc_val = ctx->bc_val;
+  f.br_ptr = ctx->br_ptr; f.br_col = ctx->br_col; f.br_val = ctx->br_val;
+  f.e_ptr = ctx->e_ptr; f.e_col = ctx->e_col; f.e_val = ctx->e_val;
+  f.aux = ctx->aux;
+  f.e_nnz = ctx->fast_enz;
+  f.b_nnz = ctx->fast_bnz;
+  f.inv_2c = 1.0 / (2.0 * ctx->w_c);
+  f.inv_gamma = 1.0 / ctx->gamma;
+  f.cpc = ctx->fast_cpc;
+  f.gs = ctx->fast_gs;
+  f.nrow = ctx->fast_nrow;
+  f.rec = ctx->fast_rec;
+  f.max_iter = ctx->max_iter;
+  f.count = count;
+  f.store_uv = 1;
+  f.prof = ctx->prof_on ? ctx->prof : nullptr;
+  switch (ctx->fast_mc) {
+    case 1: launch_fast_mc<1>(ctx, f); break;
+    case 2: launch_fast_mc<2>(ctx, f); break;
+    case 4: launch_fast_mc<4>(ctx, f); break;
+    default: launch_fast_mc<8>(ctx, f); break;
+  }
+  ctx->launches += 1;
+}
+
 void point_nodes(wmpc_ctx* ctx, wmpc_nodes* nd) {
   NodePtrs h{nd->e_off, nd->R, nd->g, nd->shift};
   CK(cudaMemcpyAsync(ctx->d_np, &h, sizeof(NodePtrs), cudaMemcpyHostToDevice, ctx->stream));
@@ -205,9 +420,12 @@ void free_all(wmpc_ctx* c) {
   void* ptrs[] = {c->stage_of, c->anc, c->cptr, c->cidx, c->prob, c->A, c->At, c->Bt, c->Wu, c->T,
                   c->Lam, c->Mb, c->Mf, c->E, c->e_pinv, c->econ, c->tmp, c->demand, c->Ed, c->xmin, c->xmax, c->xsafe, c->umin, c->umax,
                   c->p, c->q, c->Y[0], c->Y[1], c->Y[2], c->U, c->X, c->Ua, c->Xa, c->Uc, c->Xc,
-                  c->Uf, c->Xf, c->U0, c->X0, c->wbar, c->lin, c->ys, c->gv, c->vv, c->zbuf,
+                  c->Uf, c->Xf, c->U0, c->X0, c->wbar, c->lin, c->Yc, c->ys, c->gv, c->vv, c->zbuf,
                   c->dk_cur, c->dk_pc, c->dk_qc, c->dk_aff, c->theta, c->beta, c->iter, c->bad_nu,
-                  c->bad_row, c->dk_done, c->part, c->scal, c->d_np};
+                  c->bad_row, c->dk_done, c->part, c->scal, c->d_np, c->chain_node,
+                  c->bc_ptr, c->bc_row, c->br_ptr, c->br_col, c->off_dev, c->bc_val, c->br_val,
+                  c->e_ptr, c->e_col, c->e_val, c->aux,
+                  c->prof};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -249,7 +467,8 @@ int wmpc_create(const wmpc_dims* dims, wmpc_ctx** out) {
     ctx->n = (int)dims->n_nodes; ctx->H = dims->horizon; ctx->nt = dims->n_tanks;
     ctx->nu = dims->n_inputs; ctx->nd = dims->n_demands; ctx->ns = dims->n_mixing;
     ctx->W = 2 * ctx->nt + ctx->nu; ctx->P = ctx->nu + ctx->nt;
-    const size_t n = ctx->n, nt = ctx->nt, nu = ctx->nu, H = ctx->H, W = ctx->W;
+    ctx->lx = ctx->nt + (ctx->nt & 1); ctx->ly = ctx->lx + ctx->nu;
+    const size_t n = ctx->n, nt = ctx->nt, nu = ctx->nu, H = ctx->H, W = ctx->W, lx = ctx->lx;
     dalloc(ctx, &ctx->stage_of, n); dalloc(ctx, &ctx->anc, n); dalloc(ctx, &ctx->cptr, n + 1);
     dalloc(ctx, &ctx->cidx, n); dalloc(ctx, &ctx->prob, n);
     dalloc(ctx, &ctx->A, nt * nt); dalloc(ctx, &ctx->At, nt * nt); dalloc(ctx, &ctx->Bt, nu * nt);
@@ -261,10 +480,11 @@ int wmpc_create(const wmpc_dims* dims, wmpc_ctx** out) {
     dalloc(ctx, &ctx->xmin, nt); dalloc(ctx, &ctx->xmax, nt); dalloc(ctx, &ctx->xsafe, nt);
     dalloc(ctx, &ctx->umin, nu); dalloc(ctx, &ctx->umax, nu); dalloc(ctx, &ctx->p, nt); dalloc(ctx, &ctx->q, nu);
     for (int k = 0; k < 3; ++k) dalloc(ctx, &ctx->Y[k], n * W);
-    dalloc(ctx, &ctx->U, n * nu); dalloc(ctx, &ctx->X, n * nt); dalloc(ctx, &ctx->Ua, n * nu);
-    dalloc(ctx, &ctx->Xa, n * nt); dalloc(ctx, &ctx->Uc, n * nu); dalloc(ctx, &ctx->Xc, n * nt);
-    dalloc(ctx, &ctx->Uf, n * nu); dalloc(ctx, &ctx->Xf, n * nt); dalloc(ctx, &ctx->U0, n * nu);
-    dalloc(ctx, &ctx->X0, n * nt); dalloc(ctx, &ctx->wbar, n * nt); dalloc(ctx, &ctx->lin, n * nu);
+    dalloc(ctx, &ctx->U, n * nu); dalloc(ctx, &ctx->X, n * lx); dalloc(ctx, &ctx->Ua, n * nu);
+    dalloc(ctx, &ctx->Xa, n * lx); dalloc(ctx, &ctx->Uc, n * nu); dalloc(ctx, &ctx->Xc, n * lx);
+    dalloc(ctx, &ctx->Uf, n * nu); dalloc(ctx, &ctx->Xf, n * lx); dalloc(ctx, &ctx->U0, n * nu);
+    dalloc(ctx, &ctx->X0, n * lx); dalloc(ctx, &ctx->wbar, n * lx); dalloc(ctx, &ctx->lin, n * nu);
+    dalloc(ctx, &ctx->Yc, n * ctx->ly);
     dalloc(ctx, &ctx->ys, n * W); dalloc(ctx, &ctx->gv, n * W); dalloc(ctx, &ctx->vv, n * W);
     dalloc(ctx, &ctx->zbuf, n * std::max(W, (size_t)ctx->P));
     dalloc(ctx, &ctx->dk_cur, n * nu); dalloc(ctx, &ctx->dk_pc, n * nu); dalloc(ctx, &ctx->dk_qc, n * nu);
@@ -366,6 +586,7 @@ int wmpc_set_structure(wmpc_ctx* ctx, const double* A, const double* B, const do
     h2d(ctx, ctx->cptr, cptr.data(), sizeof(int) * (n + 1));
     h2d(ctx, ctx->cidx, cidx.data(), sizeof(int) * n);
     h2d(ctx, ctx->prob, prob, sizeof(double) * n);
+    ctx->prob_host.assign(prob, prob + n);
     h2d(ctx, ctx->A, A, sizeof(double) * nt * nt);
     h2d(ctx, ctx->At, At.data(), sizeof(double) * nt * nt);
     h2d(ctx, ctx->Bt, Bt.data(), sizeof(double) * nu * nt);
@@ -379,6 +600,9 @@ int wmpc_set_structure(wmpc_ctx* ctx, const double* A, const double* B, const do
       h2d(ctx, ctx->E, E, sizeof(double) * ns * nu);
       h2d(ctx, ctx->e_pinv, e_pinv, sizeof(double) * nu * ns);
     }
+    sync(ctx);
+    configure_fast(ctx, B, E, e_pinv, T, D, cptr, cidx);
+    ctx->graph_gamma = -1.0;
     sync(ctx);
     ctx->have_structure = true;
     return WMPC_OK;
@@ -397,7 +621,7 @@ int wmpc_nodes_create(wmpc_ctx* ctx, wmpc_nodes** out) {
       dalloc(ctx, &nd->e_off, n * ctx->nu);
       dalloc(ctx, &nd->R, n * ctx->nu);
       dalloc(ctx, &nd->shift, n * ctx->ns);
-      dalloc(ctx, &nd->g, n * ctx->nt);
+      dalloc(ctx, &nd->g, n * ctx->lx);
     } catch (Fail&) {
       wmpc_nodes_destroy(nd);
       throw;
@@ -444,7 +668,8 @@ int wmpc_set_node_data(wmpc_ctx* ctx, wmpc_nodes* nodes, const double* demand, c
       h2d(ctx, ctx->demand, demand, sizeof(double) * n * ctx->nd);
       h2d(ctx, ctx->Ed, Ed, sizeof(double) * ctx->ns * ctx->nd);
     }
-    h2d(ctx, nodes->g, demand_gd, sizeof(double) * n * ctx->nt);
+    CK(cudaMemcpy2DAsync(nodes->g, sizeof(double) * ctx->lx, demand_gd, sizeof(double) * ctx->nt,
+                         sizeof(double) * ctx->nt, n, cudaMemcpyHostToDevice, ctx->stream));
     h2d(ctx, ctx->econ, econ, sizeof(double) * n * ctx->nu);
     int big = INT_MAX;
     h2d(ctx, ctx->bad_row, &big, sizeof(int));
@@ -484,7 +709,11 @@ int wmpc_get_offsets(wmpc_ctx* ctx, wmpc_nodes* nodes, double* u_part, double* e
   });
 }
 
-int wmpc_kernel_launches_per_iteration(const wmpc_ctx* ctx) { return ctx ? 2 * ctx->H + 1 : -1; }
+int wmpc_kernel_launches_per_iteration(const wmpc_ctx* ctx) {
+  return ctx ? (ctx->fast ? 0 : 2 * ctx->H + 1) : -1;  // fast: one persistent launch per chunk
+}
+
+int wmpc_fast_path(const wmpc_ctx* ctx) { return ctx && ctx->fast ? ctx->fast_mc : 0; }
 
 int wmpc_set_bounds(wmpc_ctx* ctx, const double* x_min, const double* x_max, const double* x_safe,
                     const double* u_min, const double* u_max, double w_x, double w_s, const double* p,
@@ -528,7 +757,7 @@ int wmpc_dual_gradient(wmpc_ctx* ctx, const double* y, double* z, double* value)
     d.X = ctx->Xc;
     launch_dg(ctx, d, ctx->ys, 0);
     ctx->launches++;
-    k_join_primal<<<grid_for(n * ctx->P), 256, 0, ctx->stream>>>(ctx->n, ctx->nu, ctx->nt, ctx->Uc, ctx->Xc,
+    k_join_primal<<<grid_for(n * ctx->P), 256, 0, ctx->stream>>>(ctx->n, ctx->nu, ctx->nt, ctx->lx, ctx->Uc, ctx->Xc,
                                                                    ctx->zbuf);
     check_launch(ctx);
     d2h(ctx, z, ctx->zbuf, sizeof(double) * n * ctx->P);
@@ -665,15 +894,17 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
     const size_t len = (size_t)ctx->n * ctx->W;
     for (int k = 0; k < 3; ++k) CK(cudaMemsetAsync(ctx->Y[k], 0, sizeof(double) * len, ctx->stream));
     CK(cudaMemsetAsync(ctx->U, 0, sizeof(double) * (size_t)ctx->n * ctx->nu, ctx->stream));
-    CK(cudaMemsetAsync(ctx->X, 0, sizeof(double) * (size_t)ctx->n * ctx->nt, ctx->stream));
+    CK(cudaMemsetAsync(ctx->X, 0, sizeof(double) * (size_t)ctx->n * ctx->lx, ctx->stream));
+    CK(cudaMemsetAsync(ctx->Yc, 0, sizeof(double) * (size_t)ctx->n * ctx->ly, ctx->stream));
     CK(cudaMemsetAsync(ctx->Ua, 0, sizeof(double) * (size_t)ctx->n * ctx->nu, ctx->stream));
-    CK(cudaMemsetAsync(ctx->Xa, 0, sizeof(double) * (size_t)ctx->n * ctx->nt, ctx->stream));
+    CK(cudaMemsetAsync(ctx->Xa, 0, sizeof(double) * (size_t)ctx->n * ctx->lx, ctx->stream));
     CK(cudaMemsetAsync(ctx->iter, 0, sizeof(int), ctx->stream));
     int big = INT_MAX;
     h2d(ctx, ctx->bad_nu, &big, sizeof(int));
     ctx->gamma = gamma;
     ctx->it_host = 0;
     sync(ctx);
+    if (ctx->fast) return WMPC_OK;  // persistent kernel: no graph
     if (ctx->gexec && ctx->graph_gamma == gamma) return WMPC_OK;  // captured iteration still valid
     if (ctx->gexec) {
       cudaGraphExecDestroy(ctx->gexec);
@@ -697,6 +928,13 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
 
 int wmpc_apg_run(wmpc_ctx* ctx, int count) {
   return run(ctx, [&]() -> int {
+    if (ctx->fast && ctx->max_iter > 0) {
+      ARG(count >= 0 && ctx->it_host + count <= ctx->max_iter, "iteration count exceeds the theta table");
+      if (count > 0) launch_fast(ctx, count);
+      check_launch(ctx);
+      ctx->it_host += count;
+      return WMPC_OK;
+    }
     if (!ctx->gexec) {
       ctx->err = "wmpc_apg_begin must precede wmpc_apg_run";
       return WMPC_E_STATE;
@@ -711,6 +949,16 @@ int wmpc_apg_run(wmpc_ctx* ctx, int count) {
 
 int wmpc_apg_run_timed(wmpc_ctx* ctx, int count, float* ms) {
   return run(ctx, [&]() -> int {
+    if (ctx->fast && ctx->max_iter > 0) {
+      ARG(count >= 0 && ctx->it_host + count <= ctx->max_iter, "iteration count exceeds the theta table");
+      CK(cudaEventRecord(ctx->ev2, ctx->stream));
+      if (count > 0) launch_fast(ctx, count);
+      CK(cudaEventRecord(ctx->ev3, ctx->stream));
+      CK(cudaEventSynchronize(ctx->ev3));
+      CK(cudaEventElapsedTime(ms, ctx->ev2, ctx->ev3));
+      ctx->it_host += count;
+      return WMPC_OK;
+    }
     if (!ctx->gexec) {
       ctx->err = "wmpc_apg_begin must precede wmpc_apg_run_timed";
       return WMPC_E_STATE;
@@ -836,14 +1084,14 @@ int wmpc_apg_read(wmpc_ctx* ctx, int averaged, double* u0, double* primal, doubl
     }
     if (primal) {
       ctx->launches++;
-      k_join_primal<<<grid_for(n * ctx->P), 256, 0, ctx->stream>>>(ctx->n, ctx->nu, ctx->nt, ctx->U, ctx->X,
+      k_join_primal<<<grid_for(n * ctx->P), 256, 0, ctx->stream>>>(ctx->n, ctx->nu, ctx->nt, ctx->lx, ctx->U, ctx->X,
                                                                      ctx->zbuf);
       d2h(ctx, primal, ctx->zbuf, sizeof(double) * n * ctx->P);
       sync(ctx);
     }
     if (primal_avg) {
       ctx->launches++;
-      k_join_primal<<<grid_for(n * ctx->P), 256, 0, ctx->stream>>>(ctx->n, ctx->nu, ctx->nt, ctx->Ua, ctx->Xa,
+      k_join_primal<<<grid_for(n * ctx->P), 256, 0, ctx->stream>>>(ctx->n, ctx->nu, ctx->nt, ctx->lx, ctx->Ua, ctx->Xa,
                                                                      ctx->zbuf);
       d2h(ctx, primal_avg, ctx->zbuf, sizeof(double) * n * ctx->P);
       sync(ctx);
@@ -885,6 +1133,53 @@ int wmpc_host_alloc(uint64_t bytes, void** out) {
 
 void wmpc_host_free(void* p) {
   if (p) cudaFreeHost(p);
+}
+
+int wmpc_debug_div(const double* v, const double* g64, int n, uint64_t* mismatches) {
+  double *dv = nullptr, *dg = nullptr;
+  unsigned long long* dbad = nullptr;
+  if (cudaMalloc(&dv, sizeof(double) * n) || cudaMalloc(&dg, sizeof(double) * 64) ||
+      cudaMalloc(&dbad, sizeof(unsigned long long))) {
+    g_global_err = "cudaMalloc failed";
+    return WMPC_E_CUDA;
+  }
+  cudaMemcpy(dv, v, sizeof(double) * n, cudaMemcpyHostToDevice);
+  cudaMemcpy(dg, g64, sizeof(double) * 64, cudaMemcpyHostToDevice);
+  cudaMemset(dbad, 0, sizeof(unsigned long long));
+  k_debug_div<<<1184, 256>>>(dv, dg, n, dbad);
+  unsigned long long bad = 0;
+  cudaError_t e = cudaMemcpy(&bad, dbad, sizeof(bad), cudaMemcpyDeviceToHost);
+  cudaFree(dv);
+  cudaFree(dg);
+  cudaFree(dbad);
+  if (e != cudaSuccess) {
+    g_global_err = cudaGetErrorString(e);
+    return WMPC_E_CUDA;
+  }
+  *mismatches = bad;
+  return WMPC_OK;
+}
+
+float wmpc_last_debug_ms(const wmpc_ctx* ctx) { return ctx ? ctx->last_debug_ms : -1.f; }
+
+int wmpc_profile_fast(wmpc_ctx* ctx, int count, uint64_t* counters, int cap) {
+  return run(ctx, [&]() -> int {
+    if (!ctx->fast || !ctx->max_iter) {
+      ctx->err = "fast path not configured or no APG begun";
+      return WMPC_E_STATE;
+    }
+    ARG(count >= 1 && ctx->it_host + count <= ctx->max_iter, "bad count");
+    if (!ctx->prof) dalloc(ctx, &ctx->prof, (size_t)ctx->fast_grid * P_N);
+    ctx->prof_on = 1;
+    launch_fast(ctx, count);
+    ctx->prof_on = 0;
+    ctx->it_host += count;
+    check_launch(ctx);
+    size_t nvals = std::min((size_t)cap, (size_t)ctx->fast_grid * P_N);
+    d2h(ctx, counters, ctx->prof, sizeof(uint64_t) * nvals);
+    sync(ctx);
+    return WMPC_OK;
+  });
 }
 
 }  // extern "C"

@@ -17,6 +17,8 @@ struct NodePtrs {
 // Everything a kernel needs, passed by value (plain device pointers + dims).
 struct DevView {
   int n, H, nt, nu, nd, ns, W, P;  // W = 2nt+nu (dual row), P = nu+nt (primal row)
+  int lx;                          // row stride of state-sized arrays (nt rounded up to even)
+  int ly;                          // row stride of the collapsed dual Yc = [Yx (lx) | Yu (nu)]
   int a_identity;                  // A == I exactly
   int w_scalar;                    // Wu == c I exactly
   double w_c;                      // c when w_scalar
@@ -47,6 +49,7 @@ struct DevView {
   double *Y0, *Y1, *Y2;
   double *U, *X, *Ua, *Xa;
   double *wbar, *lin;
+  double* Yc;                      // collapsed extrapolated dual of the next iteration (fast path)
   const double *theta, *beta;
   int* iter;
   int* bad_nu;

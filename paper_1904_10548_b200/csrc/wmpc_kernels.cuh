@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(NTHR) k_bwd_stage(DevView d, int s, int r0, in
     double yx = dadd(w1, w2);
     double cs = 0.0;
     if (kids)
-      for (int e = d.cptr[r]; e < d.cptr[r + 1]; ++e) cs += d.wbar[(size_t)d.cidx[e] * nt + j];
+      for (int e = d.cptr[r]; e < d.cptr[r + 1]; ++e) cs += d.wbar[(size_t)d.cidx[e] * d.lx + j];
     if (d.a_identity) {
       in[m * K + j] = yx + cs;
     } else {
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(NTHR) k_bwd_stage(DevView d, int s, int r0, in
   }
   for (int idx = threadIdx.x; idx < rows * nt; idx += blockDim.x) {
     int m = idx / nt, j = idx - m * nt;
-    d.wbar[(size_t)(r0 + tile + m) * nt + j] = in[m * K + j];
+    d.wbar[(size_t)(r0 + tile + m) * d.lx + j] = in[m * K + j];
   }
   const double* M = d.Mb + (size_t)s * (nt + nu) * nu;
   for (int c = threadIdx.x; c < nu; c += blockDim.x) {
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(NTHR) k_fwd_stage(DevView d, int s, int r0, in
     int m = idx / nt, j = idx - m * nt;
     int r = r0 + tile + m;
     int a = d.anc[r];
-    xa[m * nt + j] = a < 0 ? d.p[j] : d.X[(size_t)a * nt + j];
+    xa[m * nt + j] = a < 0 ? d.p[j] : d.X[(size_t)a * d.lx + j];
   }
   __syncthreads();
   const double* M = d.Mf + (size_t)s * 2 * nu * nu;
@@ -230,9 +230,9 @@ __global__ void __launch_bounds__(NTHR) k_fwd_stage(DevView d, int s, int r0, in
     for (int m = 0; m < rows; ++m) {
       int r = r0 + tile + m;
       double xprev = d.a_identity ? xa[m * nt + c] : acx[m];
-      double x = (xprev + acc[m]) + d.np->g[(size_t)r * nt + c];
+      double x = (xprev + acc[m]) + d.np->g[(size_t)r * d.lx + c];
       xs[m * nt + c] = x;
-      d.X[(size_t)r * nt + c] = x;
+      d.X[(size_t)r * d.lx + c] = x;
     }
   }
   if (mode == 0) return;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(NTHR) k_fwd_stage(DevView d, int s, int r0, in
   }
   for (int idx = threadIdx.x; idx < rows * nt; idx += blockDim.x) {
     int m = idx / nt, j = idx - m * nt;
-    size_t o = (size_t)(r0 + tile + m) * nt + j;
+    size_t o = (size_t)(r0 + tile + m) * d.lx + j;
     double x = xs[m * nt + j];
     d.Xa[o] = it == 0 ? x : dadd(dmul(d.Xa[o], om), dmul(theta, x));
   }
@@ -315,7 +315,7 @@ __global__ void k_check_partial(DevView d, const double* __restrict__ ynew,
                                 const double* __restrict__ yold, double* part) {
   __shared__ double sh[32];
   double over = 0.0, scale = 0.0, dch = 0.0;
-  const size_t nU = (size_t)d.n * d.nu, nX = (size_t)d.n * d.nt, nY = (size_t)d.n * d.W;
+  const size_t nU = (size_t)d.n * d.nu, nX = (size_t)d.n * d.lx, nY = (size_t)d.n * d.W;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nU; i += (size_t)gridDim.x * blockDim.x) {
     int j = (int)(i % d.nu);
     double u = d.Ua[i];
@@ -382,13 +382,13 @@ __global__ void k_cost_partial(DevView d, const double* __restrict__ Uin, const 
     double dot = 0.0;
     if (y) {
       const double* yr = y + (size_t)r * W;
-      const double* x = Xin + (size_t)r * nt;
+      const double* x = Xin + (size_t)r * d.lx;
       for (int j = lane; j < nt; j += 32) dot += (yr[j] + yr[nt + j]) * x[j];
       for (int j = lane; j < nu; j += 32) dot += yr[2 * nt + j] * u[j];
     }
     double box = 0.0, safe = 0.0;
     if (want_pen) {
-      const double* x = Xin + (size_t)r * nt;
+      const double* x = Xin + (size_t)r * d.lx;
       for (int j = lane; j < nt; j += 32) {
         double b = x[j] - np_clip(x[j], d.xmin[j], d.xmax[j]);
         double sf = x[j] - np_max(x[j], d.xsafe[j]);
@@ -550,7 +550,7 @@ __global__ void k_rollout_stage(DevView d, int r0, int cnt, const double* __rest
     int m = idx / nt, j = idx - m * nt;
     int r = r0 + m;
     int a = d.anc[r];
-    const double* xa = a < 0 ? d.p : Xout + (size_t)a * nt;
+    const double* xa = a < 0 ? d.p : Xout + (size_t)a * d.lx;
     double xp = 0.0;
     if (d.a_identity) {
       xp = xa[j];
@@ -559,7 +559,7 @@ __global__ void k_rollout_stage(DevView d, int r0, int cnt, const double* __rest
     }
     double bu = 0.0;
     for (int k = 0; k < nu; ++k) bu = fma(Uin[(size_t)r * nu + k], d.Bt[(size_t)k * nt + j], bu);
-    Xout[(size_t)r * nt + j] = (xp + bu) + d.np->g[(size_t)r * nt + j];
+    Xout[(size_t)r * d.lx + j] = (xp + bu) + d.np->g[(size_t)r * d.lx + j];
   }
 }
 
@@ -648,7 +648,7 @@ __global__ void k_op_rows(DevView d, const double* __restrict__ U0, const double
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x) {
     size_t r = i / W;
     int c = (int)(i - r * W);
-    double gval = c < 2 * nt ? X0[r * nt + (c < nt ? c : c - nt)] - Xv[r * nt + (c < nt ? c : c - nt)]
+    double gval = c < 2 * nt ? X0[r * d.lx + (c < nt ? c : c - nt)] - Xv[r * d.lx + (c < nt ? c : c - nt)]
                              : U0[r * nu + c - 2 * nt] - Uv[r * nu + c - 2 * nt];
     gv[i] = gval;
     dot += v[i] * gval;
@@ -676,14 +676,14 @@ __global__ void k_u0(DevView d, const double* __restrict__ Uin, int cnt1, double
 }
 
 // join (U, X) rows into primal rows [u | x].
-__global__ void k_join_primal(int n, int nu, int nt, const double* __restrict__ U,
+__global__ void k_join_primal(int n, int nu, int nt, int lx, const double* __restrict__ U,
                               const double* __restrict__ X, double* z) {
   const int P = nu + nt;
   size_t len = (size_t)n * P;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x) {
     size_t r = i / P;
     int c = (int)(i - r * P);
-    z[i] = c < nu ? U[r * nu + c] : X[r * nt + c - nu];
+    z[i] = c < nu ? U[r * nu + c] : X[r * lx + c - nu];
   }
 }
 

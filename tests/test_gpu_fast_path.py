@@ -1,0 +1,114 @@
+"""The persistent structured kernel (wmpc_fast.cuh) against the general
+per-stage kernels and the oracle. The fast path applies when A = I,
+W_u = c I and n_u is even; WMPC_DISABLE_FAST=1 forces the general path."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import make_model, rel_err
+from oracle import port
+from paper_1904_10548_b200 import (CostWeights, SolverConfig, assemble_problem, attach_forecast,
+                                   factor_step, solve, uniform_tree)
+from paper_1904_10548_b200 import _native as nat
+from paper_1904_10548_b200.synthetic import barcelona_instance, config_instance
+
+pytestmark = pytest.mark.gpu
+
+
+def _solve(inst, iters, gamma, fast: bool, gce=None):
+    old = os.environ.get("WMPC_DISABLE_FAST")
+    os.environ["WMPC_DISABLE_FAST"] = "0" if fast else "1"
+    try:
+        cache = factor_step(inst)
+        ctx = cache._bind()
+        mode = nat.load().wmpc_fast_path(ctx.h)
+        res = solve(inst, SolverConfig(max_iter=iters, tol=1e-30, gamma=gamma,
+                                       gap_check_every=gce or iters + 1), cache=cache)
+    finally:
+        if old is None:
+            del os.environ["WMPC_DISABLE_FAST"]
+        else:
+            os.environ["WMPC_DISABLE_FAST"] = old
+    return res, mode
+
+
+def _scalar_w_instance(seed, branching, horizon, n_tanks=3, n_inputs=4, n_mixing=1):
+    rng = np.random.default_rng(seed)
+    model = make_model(rng, n_tanks, n_inputs, 2, n_mixing)
+    tree = uniform_tree(branching, horizon, 2, n_inputs)
+    tree.eps = 0.1 * rng.standard_normal((tree.n_nodes, 2 + n_inputs))
+    tree.eps[0] = 0.0
+    tree = attach_forecast(tree, 0.3 + 0.2 * rng.random((horizon, 2)), 0.5 + rng.random((horizon, n_inputs)))
+    w = CostWeights(w_alpha=1.0, w_u=0.7, w_s=2.0, w_x=5.0)
+    p = model.x_safe * (1.2 + 0.5 * rng.random(n_tanks))
+    return assemble_problem(model, tree, w, p, 0.3 * rng.random(n_inputs))
+
+
+@pytest.mark.parametrize("branching,horizon", [([2, 3], 5), ([3], 1), ([1, 2, 2], 4), ([2, 2, 2, 2], 4)])
+def test_fast_matches_general_small_scalar_w(branching, horizon):
+    inst = _scalar_w_instance(5, branching, horizon)
+    fac, e_off = port.factor(inst)
+    gamma = 1.0 / port.power_lipschitz(inst, fac, e_off)
+    rf, mf = _solve(inst, 120, gamma, True, gce=40)
+    rg, mg = _solve(inst, 120, gamma, False, gce=40)
+    assert mf > 0 and mg == 0
+    ro = port.apg_solve(inst, gamma, max_iter=120, tol=1e-30, gap_check_every=40, fac=fac, e_off=e_off,
+                        reference_cost_accounting=False)
+    for k in ("u0", "primal", "primal_avg", "dual"):
+        assert rel_err(getattr(rf, k), getattr(rg, k)) <= 1e-11, k
+        assert rel_err(getattr(rf, k), getattr(ro, k)) <= 1e-9, k
+    assert abs(rf.objective - ro.objective) <= 1e-9 * (1 + abs(ro.objective))
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_fast_matches_general_barcelona(cfg):
+    inst = config_instance(cfg)
+    gamma = 1.0 / 5e9
+    rf, mf = _solve(inst, 60, gamma, True)
+    rg, mg = _solve(inst, 60, gamma, False)
+    assert mf > 0 and mg == 0
+    for k in ("u0", "primal", "primal_avg", "dual"):
+        assert rel_err(getattr(rf, k), getattr(rg, k)) <= 1e-11, k
+    assert abs(rf.duality_gap - rg.duality_gap) <= 1e-10 * (1 + abs(rg.duality_gap))
+
+
+def test_fast_path_chunked_equals_single_launch():
+    inst = config_instance("C1")
+    gamma = 1.0 / 1.1e8
+    a, _ = _solve(inst, 100, gamma, True)            # one launch of 100 iterations
+    b, _ = _solve(inst, 100, gamma, True, gce=7)     # launches of 7 iterations
+    np.testing.assert_array_equal(a.dual, b.dual)
+    np.testing.assert_array_equal(a.primal_avg, b.primal_avg)
+    np.testing.assert_array_equal(a.primal, b.primal)
+
+
+def test_fast_path_pure_chain_tree():
+    inst = barcelona_instance([], seed=3, horizon=24)  # a single scenario: 24 chain nodes
+    gamma = 1.0 / 1e8
+    rf, mf = _solve(inst, 50, gamma, True)
+    rg, _ = _solve(inst, 50, gamma, False)
+    assert mf > 0
+    assert rel_err(rf.dual, rg.dual) <= 1e-11
+
+
+def test_reciprocal_division_is_exact():
+    """The kernels divide by gamma through RN(1/gamma) + one fma correction;
+    it must agree bit for bit with IEEE division (incl. edge magnitudes)."""
+    rng = np.random.default_rng(0)
+    n = 1 << 22
+    v = rng.standard_normal(n) * np.exp2(rng.integers(-60, 60, n))
+    v[: 1 << 12] = rng.standard_normal(1 << 12) * np.exp2(rng.integers(-1070, 1023, 1 << 12))
+    v[5] = 0.0
+    v[6] = np.inf
+    v[7] = -np.inf
+    v[8] = np.nan
+    g = np.exp2(rng.uniform(-40, 20, 64)) * (1 + rng.random(64))
+    g[:4] = [1.0 / 1.731949602497e9, 1.0 / 1.0888e8, 0.37, 3.0]
+    bad = nat.C.c_uint64(0)
+    rc = nat.load().wmpc_debug_div(nat.ptr(v), nat.ptr(g), n, nat.C.byref(bad))
+    assert rc == 0
+    assert bad.value == 0
