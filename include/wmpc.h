@@ -121,8 +121,10 @@ int wmpc_apg_iterations(const wmpc_ctx* ctx);
 /* Kernels launched per APG iteration (bench accounting; 0 = one persistent
  * launch per wmpc_apg_run call). */
 int wmpc_kernel_launches_per_iteration(const wmpc_ctx* ctx);
-/* Row-tile size of the persistent structured kernel (A = I, W = cI), or 0 when
- * the general per-stage kernels run. */
+/* Structured persistent kernel in use (A = I, W = cI): 200 + tile size for the
+ * scan-form kernel (default), 100 + row slots for the warp-per-chain kernel,
+ * the row-tile size for the step-recursive CTA kernel, 0 when the general
+ * per-stage kernels run. */
 int wmpc_fast_path(const wmpc_ctx* ctx);
 
 /* Timing helpers for bench.py: run `count` iterations between CUDA events on

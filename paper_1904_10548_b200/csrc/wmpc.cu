@@ -15,7 +15,8 @@
 #include <vector>
 
 #include "wmpc.h"
-#include "wmpc_fast.cuh"
+#include "wmpc_warp.cuh"
+#include "wmpc_scan.cuh"
 
 using namespace wmpc;
 
@@ -24,7 +25,7 @@ static thread_local std::string g_global_err;
 struct wmpc_nodes {
   int dev = 0;
   size_t n = 0;
-  double *u_part = nullptr, *e_off = nullptr, *R = nullptr, *shift = nullptr, *g = nullptr;
+  double *u_part = nullptr, *e_off = nullptr, *R = nullptr, *shift = nullptr, *g = nullptr, *ebar = nullptr;
   bool ready = false;
 };
 
@@ -65,6 +66,18 @@ struct wmpc_ctx {
   bool fast = false;
   int kstar = 0, nchain = 0, fast_mc = 1, fast_cpc = 1, fast_gs = 1, fast_grid = 0;
   int fast_nrow = 2, fast_rec = 0, fast_enz = 0, fast_bnz = 0;
+  int use_warp = 0, warp_nrow = 2;
+  size_t warp_smem = 0;
+  int use_scan = 0, scan_work = 0;
+  size_t scan_smem = 0;
+  // graph-of-kernels scan path (wmpc_scan.cuh)
+  int use_graphk = 0, n_branch = 0;
+  double *Lb = nullptr, *Atop = nullptr, *delta = nullptr;
+  int *bd_ptr = nullptr, *bd_idx = nullptr, *bd_w = nullptr, *bt_ptr = nullptr, *bt_idx = nullptr, *bt_w = nullptr;
+  size_t sm_up = 0, sm_bu = 0, sm_bru = 0, sm_down = 0, sm_prox = 0;
+  cudaGraphExec_t gk_exec1 = nullptr, gk_exec8 = nullptr;
+  double gk_gamma = -1.0;
+  int gk_maxit = -1;
   unsigned long long* prof = nullptr;
   float last_debug_ms = 0.f;
   int prof_on = 0;
@@ -211,9 +224,8 @@ void fast_attr(wmpc_ctx* ctx, size_t smem) {
 
 size_t fast_smem_bytes(const wmpc_ctx* c, int MC, int nrow, int rec, int cpc, int enz, int bnz) {
   const int nst = c->H - c->kstar, nu = c->nu, nt = c->nt, lx = c->lx, ns = c->ns;
-  size_t dbl = (size_t)nrow * MC * rec + 2 * (size_t)MC * nu + (size_t)MC * FAST_MAXNS + (size_t)MC * lx +
-               (size_t)MC * nu + (size_t)MC * lx + (size_t)MC * 2 * nt + 2 * MC + (3 * nt + 2 * nu) +
-               (size_t)nu * ns + enz + 2 * (size_t)bnz;
+  size_t dbl = (size_t)nrow * MC * rec + 2 * (size_t)MC * nu + 3 * (size_t)MC * lx + (size_t)MC * FAST_MAXNS +
+               (size_t)MC * 2 * nt + 2 * MC + (3 * nt + 2 * nu) + (size_t)nu * ns + enz + 2 * (size_t)bnz;
   size_t ints = (ns + 1) + enz + (nu + 1) + bnz + (nt + 1) + bnz + (size_t)nrow * MC + c->H + 1 +
                 (size_t)cpc * nst;
   return dbl * sizeof(double) + ints * sizeof(int) + 64;
@@ -222,6 +234,78 @@ size_t fast_smem_bytes(const wmpc_ctx* c, int MC, int nrow, int rec, int cpc, in
 // Decide whether the structured persistent kernel applies and lay out its data:
 // A = I, W = cI, n_u even, n_s <= 32, and every stage factor equal to the
 // null(E) projector (T_s = P/(2c), D_s = P up to 1e-12 relative).
+// Graph-of-kernels scan path: per-branching-node descendant lists with depth
+// weights, buffers, shared-memory sizes. Default when the chains fit.
+void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::vector<int>& cidx, int enz,
+                      int bnz) {
+  ctx->use_graphk = 0;
+  if (ctx->gk_exec1) cudaGraphExecDestroy(ctx->gk_exec1);
+  if (ctx->gk_exec8) cudaGraphExecDestroy(ctx->gk_exec8);
+  ctx->gk_exec1 = ctx->gk_exec8 = nullptr;
+  ctx->gk_gamma = -1.0;
+  const char* ek = getenv("WMPC_KERNEL");
+  if (ek && std::string(ek) != "graph") return;
+  const int H = ctx->H, kstar = ctx->kstar, nst = H - kstar, nt = ctx->nt, nu = ctx->nu, ns = ctx->ns;
+  const int lx = ctx->lx, ly = ctx->ly;
+  if (nst > SC_THREADS || kstar > 30) return;
+  const std::vector<int>& off = ctx->off;
+  const int nb = off[kstar], nchain = off[kstar + 1] - off[kstar];
+  const size_t ops = ops_bytes(nt, nu, ns, enz, bnz);
+  const size_t rows_b = sizeof(int) * (size_t)((nst + 3) & ~3);
+  const size_t up = sizeof(double) * (size_t)nst * (ly + nu + lx + nu + FAST_MAXNS) + rows_b + ops;
+  const size_t down = sizeof(double) * ((size_t)nst * (3 * nu + lx + 2 + nu + FAST_MAXNS) + nu + lx) + rows_b + ops;
+  const size_t bu = sizeof(double) * (4 * (size_t)(2 * lx + nu) + 2 * lx + 3 * nu + FAST_MAXNS) + ops;
+  const size_t bru = sizeof(double) * (2 * (size_t)nu + FAST_MAXNS) + ops;
+  const size_t prox = sizeof(double) * ((size_t)SC_NPB * (ctx->fast_rec + nu + lx + 2) + 3 * nt + 2 * nu) +
+                      sizeof(int) * SC_NPB + 16;
+  const size_t cap = 227 * 1024;
+  if (std::max(std::max(up, down), std::max(std::max(bu, bru), prox)) > cap) return;
+  // branching descendants / chain tops of every branching row, with depth weights
+  std::vector<int> stage(ctx->n);
+  for (int s = 0; s < H; ++s)
+    for (int r = off[s]; r < off[s + 1]; ++r) stage[r] = s;
+  std::vector<int> bdp(nb + 1, 0), bdi, bdw, btp(nb + 1, 0), bti, btw;
+  std::vector<int> stack;
+  for (int r = 0; r < nb; ++r) {
+    stack.assign(cidx.begin() + cptr[r], cidx.begin() + cptr[r + 1]);
+    while (!stack.empty()) {
+      const int e = stack.back();
+      stack.pop_back();
+      if (e < nb) {
+        bdi.push_back(e);
+        bdw.push_back(stage[e] - stage[r]);
+        for (int c = cptr[e]; c < cptr[e + 1]; ++c) stack.push_back(cidx[c]);
+      } else {
+        bti.push_back(e - off[kstar]);
+        btw.push_back(kstar - stage[r] - 1);
+      }
+    }
+    bdp[r + 1] = (int)bdi.size();
+    btp[r + 1] = (int)bti.size();
+  }
+  if (bdi.empty()) { bdi.push_back(0); bdw.push_back(0); }
+  if (bti.empty()) { bti.push_back(0); btw.push_back(0); }
+  upload_vec(ctx, &ctx->bd_ptr, bdp);
+  upload_vec(ctx, &ctx->bd_idx, bdi);
+  upload_vec(ctx, &ctx->bd_w, bdw);
+  upload_vec(ctx, &ctx->bt_ptr, btp);
+  upload_vec(ctx, &ctx->bt_idx, bti);
+  upload_vec(ctx, &ctx->bt_w, btw);
+  std::vector<double> zl((size_t)ctx->n * nu, 0.0), za((size_t)nchain * nu, 0.0),
+      zd((size_t)std::max(nb, 1) * lx, 0.0);
+  upload_vec(ctx, &ctx->Lb, zl);
+  upload_vec(ctx, &ctx->Atop, za);
+  upload_vec(ctx, &ctx->delta, zd);
+  CK(cudaFuncSetAttribute(k_chain_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
+  CK(cudaFuncSetAttribute(k_chain_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
+  CK(cudaFuncSetAttribute(k_branch_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bu));
+  CK(cudaFuncSetAttribute(k_branch_u, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bru));
+  CK(cudaFuncSetAttribute(k_prox_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox));
+  ctx->sm_up = up; ctx->sm_down = down; ctx->sm_bu = bu; ctx->sm_bru = bru; ctx->sm_prox = prox;
+  ctx->n_branch = nb;
+  ctx->use_graphk = 1;
+}
+
 void configure_fast(wmpc_ctx* ctx, const double* B, const double* E, const double* e_pinv, const double* T,
                     const double* D, const std::vector<int>& cptr, const std::vector<int>& cidx) {
   ctx->fast = false;
@@ -355,7 +439,65 @@ void configure_fast(wmpc_ctx* ctx, const double* B, const double* E, const doubl
   ctx->fast_rec = rec;
   ctx->fast_enz = enz;
   ctx->fast_bnz = bnz;
+  // warp-per-chain variant (default when it fits)
+  {
+    auto wsm = [&](int nr) {
+      size_t dbl = (size_t)FW_WARPS * nr * rec + (size_t)FW_WARPS * FW_SCR + (3 * nt + 2 * nu) + (size_t)nu * ns +
+                   enz + 2 * (size_t)bnz;
+      size_t ints = (ns + 1) + enz + (nu + 1) + bnz + (nt + 1) + bnz + (H + 1);
+      return dbl * sizeof(double) + ints * sizeof(int) + 64;
+    };
+    int wn = 0;
+    for (int nr = 2; nr <= 8; ++nr)
+      if (wsm(nr) <= cap) wn = nr;
+    if (const char* e = getenv("WMPC_WARP_NROW")) wn = std::min(wn, std::max(2, atoi(e)));
+    const char* ek = getenv("WMPC_KERNEL");
+    bool want = ek && std::string(ek) == "warp";  // scan kernel is the default
+    if (wn >= 2 && want) {
+      ctx->warp_nrow = wn;
+      ctx->warp_smem = wsm(wn);
+      CK(cudaFuncSetAttribute(k_apg_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->warp_smem));
+      ctx->use_warp = 1;
+    } else {
+      ctx->use_warp = 0;
+    }
+  }
+  // scan-form kernel (default when the chain fits in shared memory)
+  {
+    const int nst = H - kstar;
+    const size_t dA = (size_t)nst * (ly + nu + lx + nu + FAST_MAXNS);
+    const size_t dD = (size_t)nst * (rec + nu + nu + lx + FAST_MAXNS) + nu + lx + 2 * nst;
+    const size_t dB = (size_t)MC * rec + 2 * (size_t)MC * nu + 3 * (size_t)MC * lx + (size_t)MC * FAST_MAXNS +
+                      (size_t)MC * 2 * nt + 2 * MC;
+    const size_t work = std::max(dA, std::max(dD, dB));
+    const size_t shared = (3 * nt + 2 * nu) + (size_t)nu * ns + enz + 2 * (size_t)bnz;
+    const size_t ints = (ns + 1) + enz + (nu + 1) + bnz + (nt + 1) + bnz + std::max(MC, nst) + H + 1 +
+                        (size_t)cpc * nst;
+    const size_t bytes = (work + shared) * sizeof(double) + ints * sizeof(int) + 64;
+    const char* ek = getenv("WMPC_KERNEL");
+    const bool want = !(ek && (std::string(ek) == "cta" || std::string(ek) == "warp"));
+    ctx->use_scan = 0;
+    if (want && bytes <= cap && nst <= FAST_THREADS) {
+      ctx->scan_work = (int)work;
+      ctx->scan_smem = bytes;
+      switch (MC) {
+        case 1: CK(cudaFuncSetAttribute(k_apg_scan<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)); break;
+        case 2: CK(cudaFuncSetAttribute(k_apg_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)); break;
+        case 4: CK(cudaFuncSetAttribute(k_apg_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)); break;
+        default: CK(cudaFuncSetAttribute(k_apg_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)); break;
+      }
+      ctx->use_scan = 1;
+    }
+  }
+  configure_graphk(ctx, cptr, cidx, enz, bnz);
   ctx->fast = true;
+}
+
+template <int MC>
+void launch_scan_mc(wmpc_ctx* ctx, FastView& f) {
+  void* args[] = {(void*)&f, (void*)&ctx->off_dev};
+  CK(cudaLaunchCooperativeKernel((void*)k_apg_scan<MC>, dim3(ctx->fast_grid), dim3(FAST_THREADS), args,
+                                 ctx->scan_smem, ctx->stream));
 }
 
 template <int MC>
@@ -365,7 +507,50 @@ void launch_fast_mc(wmpc_ctx* ctx, FastView& f) {
                                  ctx->fast_smem, ctx->stream));
 }
 
-void launch_fast(wmpc_ctx* ctx, int count) {
+FastView make_fastview(wmpc_ctx* ctx, int count);
+
+int graphk_kernels(const wmpc_ctx* ctx) { return ctx->n_branch > 0 ? 6 : 4; }
+
+// One APG iteration of the graph-of-kernels path, enqueued on ctx->stream.
+void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
+  cudaStream_t st = ctx->stream;
+  const int nb = ctx->n_branch, nc = ctx->nchain;
+  k_chain_up<<<nc, SC_THREADS, ctx->sm_up, st>>>(f);
+  if (nb > 0) {
+    k_branch_up<<<nb, SC_THREADS, ctx->sm_bu, st>>>(f);
+    k_branch_u<<<nb, SC_THREADS, ctx->sm_bru, st>>>(f);
+  }
+  k_chain_down<<<nc, SC_THREADS, ctx->sm_down, st>>>(f);
+  k_prox_nodes<<<(ctx->n + SC_NPB - 1) / SC_NPB, SC_THREADS, ctx->sm_prox, st>>>(f);
+  k_advance<<<1, 32, 0, st>>>(ctx->iter);
+}
+
+void capture_graphk(wmpc_ctx* ctx) {
+  if (ctx->gk_exec1 && ctx->gk_gamma == ctx->gamma && ctx->gk_maxit == ctx->max_iter) return;
+  if (ctx->gk_exec1) cudaGraphExecDestroy(ctx->gk_exec1);
+  if (ctx->gk_exec8) cudaGraphExecDestroy(ctx->gk_exec8);
+  ctx->gk_exec1 = ctx->gk_exec8 = nullptr;
+  FastView f = make_fastview(ctx, 1);
+  for (int reps : {1, 8}) {
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+    for (int i = 0; i < reps; ++i) enqueue_graphk_iteration(ctx, f);
+    CK(cudaStreamEndCapture(ctx->stream, &g));
+    CK(cudaGraphInstantiate(reps == 1 ? &ctx->gk_exec1 : &ctx->gk_exec8, g, 0));
+    cudaGraphDestroy(g);
+  }
+  ctx->gk_gamma = ctx->gamma;
+  ctx->gk_maxit = ctx->max_iter;
+}
+
+void launch_graphk(wmpc_ctx* ctx, int count) {
+  int i = 0;
+  for (; i + 8 <= count; i += 8) CK(cudaGraphLaunch(ctx->gk_exec8, ctx->stream));
+  for (; i < count; ++i) CK(cudaGraphLaunch(ctx->gk_exec1, ctx->stream));
+  ctx->launches += (int64_t)count * graphk_kernels(ctx);
+}
+
+FastView make_fastview(wmpc_ctx* ctx, int count) {
   FastView f;
   f.d = view(ctx);
   f.kstar = ctx->kstar;
@@ -387,6 +572,41 @@ void launch_fast(wmpc_ctx* ctx, int count) {
   f.count = count;
   f.store_uv = 1;
   f.prof = ctx->prof_on ? ctx->prof : nullptr;
+  f.n_branch = ctx->n_branch;
+  f.Lb = ctx->Lb;
+  f.Atop = ctx->Atop;
+  f.delta = ctx->delta;
+  f.bd_ptr = ctx->bd_ptr; f.bd_idx = ctx->bd_idx; f.bd_w = ctx->bd_w;
+  f.bt_ptr = ctx->bt_ptr; f.bt_idx = ctx->bt_idx; f.bt_w = ctx->bt_w;
+  f.work_doubles = ctx->scan_work;
+  return f;
+}
+
+void launch_fast(wmpc_ctx* ctx, int count) {
+  if (ctx->use_graphk) {
+    launch_graphk(ctx, count);
+    return;
+  }
+  FastView f = make_fastview(ctx, count);
+  if (ctx->use_scan) {
+    f.work_doubles = ctx->scan_work;
+    switch (ctx->fast_mc) {
+      case 1: launch_scan_mc<1>(ctx, f); break;
+      case 2: launch_scan_mc<2>(ctx, f); break;
+      case 4: launch_scan_mc<4>(ctx, f); break;
+      default: launch_scan_mc<8>(ctx, f); break;
+    }
+    ctx->launches += 1;
+    return;
+  }
+  if (ctx->use_warp) {
+    f.nrow = ctx->warp_nrow;
+    void* args[] = {(void*)&f, (void*)&ctx->off_dev};
+    CK(cudaLaunchCooperativeKernel((void*)k_apg_warp, dim3(ctx->fast_grid), dim3(FW_THREADS), args, ctx->warp_smem,
+                                   ctx->stream));
+    ctx->launches += 1;
+    return;
+  }
   switch (ctx->fast_mc) {
     case 1: launch_fast_mc<1>(ctx, f); break;
     case 2: launch_fast_mc<2>(ctx, f); break;
@@ -397,7 +617,7 @@ void launch_fast(wmpc_ctx* ctx, int count) {
 }
 
 void point_nodes(wmpc_ctx* ctx, wmpc_nodes* nd) {
-  NodePtrs h{nd->e_off, nd->R, nd->g, nd->shift};
+  NodePtrs h{nd->e_off, nd->R, nd->g, nd->shift, nd->ebar};
   CK(cudaMemcpyAsync(ctx->d_np, &h, sizeof(NodePtrs), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->nodes = nd;
@@ -425,11 +645,14 @@ void free_all(wmpc_ctx* c) {
                   c->bad_row, c->dk_done, c->part, c->scal, c->d_np, c->chain_node,
                   c->bc_ptr, c->bc_row, c->br_ptr, c->br_col, c->off_dev, c->bc_val, c->br_val,
                   c->e_ptr, c->e_col, c->e_val, c->aux,
+                  c->Lb, c->Atop, c->delta, c->bd_ptr, c->bd_idx, c->bd_w, c->bt_ptr, c->bt_idx, c->bt_w,
                   c->prof};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->gk_exec1) cudaGraphExecDestroy(c->gk_exec1);
+  if (c->gk_exec8) cudaGraphExecDestroy(c->gk_exec8);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->ev2) cudaEventDestroy(c->ev2);
@@ -622,6 +845,7 @@ int wmpc_nodes_create(wmpc_ctx* ctx, wmpc_nodes** out) {
       dalloc(ctx, &nd->R, n * ctx->nu);
       dalloc(ctx, &nd->shift, n * ctx->ns);
       dalloc(ctx, &nd->g, n * ctx->lx);
+      dalloc(ctx, &nd->ebar, n * ctx->nu);
     } catch (Fail&) {
       wmpc_nodes_destroy(nd);
       throw;
@@ -634,7 +858,7 @@ int wmpc_nodes_create(wmpc_ctx* ctx, wmpc_nodes** out) {
 void wmpc_nodes_destroy(wmpc_nodes* nd) {
   if (!nd) return;
   cudaSetDevice(nd->dev);
-  void* ptrs[] = {nd->u_part, nd->e_off, nd->R, nd->shift, nd->g};
+  void* ptrs[] = {nd->u_part, nd->e_off, nd->R, nd->shift, nd->g, nd->ebar};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete nd;
@@ -681,6 +905,18 @@ int wmpc_set_node_data(wmpc_ctx* ctx, wmpc_nodes* nodes, const double* demand, c
                                                      nodes->e_off, ctx->tmp, ctx->bad_row);
     ctx->launches++;
     k_node_R<<<blocks, 256, 0, ctx->stream>>>(d, nodes->e_off, nodes->R);
+    if (ctx->fast) {
+      ctx->launches++;
+      const int tot = ctx->nchain * ctx->nu;
+      k_chain_ebar<<<(tot + 255) / 256, 256, 0, ctx->stream>>>(ctx->chain_node, ctx->nchain, ctx->H - ctx->kstar,
+                                                               ctx->nu, nodes->e_off, nodes->ebar);
+      if (ctx->use_graphk && ctx->n_branch > 0) {
+        ctx->launches++;
+        const int tb = ctx->n_branch * ctx->nu;
+        k_branch_ebar<<<(tb + 255) / 256, 256, 0, ctx->stream>>>(ctx->anc, ctx->n_branch, ctx->nu, nodes->e_off,
+                                                                 nodes->ebar);
+      }
+    }
     check_launch(ctx);
     int bad = INT_MAX;
     d2h(ctx, &bad, ctx->bad_row, sizeof(int));
@@ -710,10 +946,17 @@ int wmpc_get_offsets(wmpc_ctx* ctx, wmpc_nodes* nodes, double* u_part, double* e
 }
 
 int wmpc_kernel_launches_per_iteration(const wmpc_ctx* ctx) {
-  return ctx ? (ctx->fast ? 0 : 2 * ctx->H + 1) : -1;  // fast: one persistent launch per chunk
+  if (!ctx) return -1;
+  if (ctx->fast && ctx->use_graphk) return graphk_kernels(ctx);
+  return ctx->fast ? 0 : 2 * ctx->H + 1;  // fast: one persistent launch per chunk
 }
 
-int wmpc_fast_path(const wmpc_ctx* ctx) { return ctx && ctx->fast ? ctx->fast_mc : 0; }
+int wmpc_fast_path(const wmpc_ctx* ctx) {
+  if (!ctx || !ctx->fast) return 0;
+  if (ctx->use_graphk) return 300;
+  if (ctx->use_scan) return 200 + ctx->fast_mc;
+  return ctx->use_warp ? 100 + ctx->warp_nrow : ctx->fast_mc;
+}
 
 int wmpc_set_bounds(wmpc_ctx* ctx, const double* x_min, const double* x_max, const double* x_safe,
                     const double* u_min, const double* u_max, double w_x, double w_s, const double* p,
@@ -904,7 +1147,10 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
     ctx->gamma = gamma;
     ctx->it_host = 0;
     sync(ctx);
-    if (ctx->fast) return WMPC_OK;  // persistent kernel: no graph
+    if (ctx->fast) {
+      if (ctx->use_graphk) capture_graphk(ctx);
+      return WMPC_OK;  // persistent kernel: no graph
+    }
     if (ctx->gexec && ctx->graph_gamma == gamma) return WMPC_OK;  // captured iteration still valid
     if (ctx->gexec) {
       cudaGraphExecDestroy(ctx->gexec);

@@ -12,6 +12,7 @@ struct NodePtrs {
   const double* R;      // n*nu   sum_c -2 p_c e_off_c W
   const double* g;      // n*nt   demand_gd
   const double* shift;  // n*ns   demand Ed^T
+  const double* ebar;   // n*nu   chain-local prefix of e_off (fast path; 0 off chains)
 };
 
 // Everything a kernel needs, passed by value (plain device pointers + dims).

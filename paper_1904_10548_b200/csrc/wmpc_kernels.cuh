@@ -637,6 +637,21 @@ __global__ void k_node_R(DevView d, const double* __restrict__ e_off, double* Ro
   }
 }
 
+// Chain-local prefix of e_off for the scan-form kernel: for the node at chain
+// position t, sum_{t' < t} e_off[chain node t'] (sequential, top to leaf).
+__global__ void k_chain_ebar(const int* __restrict__ chain_node, int nchain, int nst, int nu,
+                             const double* __restrict__ e_off, double* ebar) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nchain * nu) return;
+  const int ci = idx / nu, k = idx - ci * nu;
+  double acc = 0.0;
+  for (int t = 0; t < nst; ++t) {
+    const size_t r = (size_t)chain_node[(size_t)t * nchain + ci];
+    ebar[r * nu + k] = acc;
+    acc = acc + e_off[r * nu + k];
+  }
+}
+
 // Power iteration helpers (solver.py:348-366).
 __global__ void k_op_rows(DevView d, const double* __restrict__ U0, const double* __restrict__ X0,
                           const double* __restrict__ Uv, const double* __restrict__ Xv,

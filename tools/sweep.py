@@ -22,9 +22,10 @@ def loop_time(cfg, iters, env):
     for k in env: del os.environ[k]
     return ms.value * 1e3 / iters, mode, inst.n_nonroot
 
-cases = [("C1", {}), ("C2", {}), ("C2", {"WMPC_CPC": "2"}), ("C2", {"WMPC_CPC": "4"}), ("C2", {"WMPC_CPC": "8"}),
-         ("C2", {"WMPC_DISABLE_FAST": "1"}), ("C3", {}), ("C3", {"WMPC_CPC": "8"}), ("C4", {}),
-         ("C4", {"WMPC_DISABLE_FAST": "1"})]
+import ast
+cases = ast.literal_eval(sys.argv[1]) if len(sys.argv) > 1 else [
+    ("C1", {}), ("C1", {"WMPC_KERNEL": "cta"}), ("C2", {}), ("C2", {"WMPC_KERNEL": "cta"}),
+    ("C3", {}), ("C3", {"WMPC_KERNEL": "cta"}), ("C4", {}), ("C4", {"WMPC_KERNEL": "cta"})]
 for cfg, env in cases:
     iters = 50 if cfg != "C4" else 10
     us, mode, n = loop_time(cfg, iters, env)
