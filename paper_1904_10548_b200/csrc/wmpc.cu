@@ -72,9 +72,13 @@ struct wmpc_ctx {
   size_t scan_smem = 0;
   // graph-of-kernels scan path (wmpc_scan.cuh)
   int use_graphk = 0, n_branch = 0;
-  double *Lb = nullptr, *Atop = nullptr, *delta = nullptr;
-  int *bd_ptr = nullptr, *bd_idx = nullptr, *bd_w = nullptr, *bt_ptr = nullptr, *bt_idx = nullptr, *bt_w = nullptr;
-  size_t sm_up = 0, sm_bu = 0, sm_bru = 0, sm_down = 0, sm_prox = 0;
+  double *Lb = nullptr, *Asub = nullptr;
+  unsigned char* blob = nullptr;
+  int blob16 = 0;
+  int *gi_ptr = nullptr, *gi_item = nullptr, *gi_w = nullptr, *cpath = nullptr;
+  unsigned* cown = nullptr;
+  std::vector<std::pair<int, int>> gk_groups;  // (first row, rows) per stage group, bottom-up
+  size_t sm_up = 0, sm_grp = 0, sm_down = 0, sm_prox = 0;
   cudaGraphExec_t gk_exec1 = nullptr, gk_exec8 = nullptr;
   double gk_gamma = -1.0;
   int gk_maxit = -1;
@@ -234,10 +238,13 @@ size_t fast_smem_bytes(const wmpc_ctx* c, int MC, int nrow, int rec, int cpc, in
 // Decide whether the structured persistent kernel applies and lay out its data:
 // A = I, W = cI, n_u even, n_s <= 32, and every stage factor equal to the
 // null(E) projector (T_s = P/(2c), D_s = P up to 1e-12 relative).
-// Graph-of-kernels scan path: per-branching-node descendant lists with depth
-// weights, buffers, shared-memory sizes. Default when the chains fit.
-void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::vector<int>& cidx, int enz,
-                      int bnz) {
+// Graph-of-kernels scan path: operator blob, stage groups of the branching
+// region with per-row item lists, chain root paths. Default when it fits.
+void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::vector<int>& cidx,
+                      const std::vector<double>& ept, const std::vector<int>& ep, const std::vector<int>& ec,
+                      const std::vector<double>& ev, const std::vector<int>& bcp, const std::vector<int>& bcr,
+                      const std::vector<double>& bcv, const std::vector<int>& brp, const std::vector<int>& brc,
+                      const std::vector<double>& brv, int enz, int bnz) {
   ctx->use_graphk = 0;
   if (ctx->gk_exec1) cudaGraphExecDestroy(ctx->gk_exec1);
   if (ctx->gk_exec8) cudaGraphExecDestroy(ctx->gk_exec8);
@@ -247,61 +254,128 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   if (ek && std::string(ek) != "graph") return;
   const int H = ctx->H, kstar = ctx->kstar, nst = H - kstar, nt = ctx->nt, nu = ctx->nu, ns = ctx->ns;
   const int lx = ctx->lx, ly = ctx->ly;
-  if (nst > SC_THREADS || kstar > 30) return;
+  if (H > SC_THREADS || kstar > SC_MAXK) return;
   const std::vector<int>& off = ctx->off;
   const int nb = off[kstar], nchain = off[kstar + 1] - off[kstar];
-  const size_t ops = ops_bytes(nt, nu, ns, enz, bnz);
-  const size_t rows_b = sizeof(int) * (size_t)((nst + 3) & ~3);
-  const size_t up = sizeof(double) * (size_t)nst * (ly + nu + lx + nu + FAST_MAXNS) + rows_b + ops;
-  const size_t down = sizeof(double) * ((size_t)nst * (3 * nu + lx + 2 + nu + FAST_MAXNS) + nu + lx) + rows_b + ops;
-  const size_t bu = sizeof(double) * (4 * (size_t)(2 * lx + nu) + 2 * lx + 3 * nu + FAST_MAXNS) + ops;
-  const size_t bru = sizeof(double) * (2 * (size_t)nu + FAST_MAXNS) + ops;
+  // chains must be stage-major contiguous: row = nb + t * nchain + chain
+  for (int i = 0; i < nchain; ++i) {
+    int r = nb + i;
+    for (int t = 1; t < nst; ++t) {
+      if (cptr[r + 1] - cptr[r] != 1 || cidx[cptr[r]] != nb + t * nchain + i) return;
+      r = cidx[cptr[r]];
+    }
+  }
+  const BlobLayout bl = blob_layout(nt, nu, ns, enz, bnz);
+  const size_t cap = 227 * 1024;
+  const size_t up = sizeof(double) * (size_t)nst * (ly + nu + 2 + lx + nu + FAST_MAXNS) + bl.bytes;
+  const size_t grp = sizeof(double) * ((size_t)(SC_THREADS / 32) * 256 + 2 * lx + 2 * nu + FAST_MAXNS) + bl.bytes;
+  const size_t down = sizeof(double) * (size_t)H * (2 * nu + lx + FAST_MAXNS) + sizeof(int) * ((H + 3) & ~3) + bl.bytes;
   const size_t prox = sizeof(double) * ((size_t)SC_NPB * (ctx->fast_rec + nu + lx + 2) + 3 * nt + 2 * nu) +
                       sizeof(int) * SC_NPB + 16;
-  const size_t cap = 227 * 1024;
-  if (std::max(std::max(up, down), std::max(std::max(bu, bru), prox)) > cap) return;
-  // branching descendants / chain tops of every branching row, with depth weights
-  std::vector<int> stage(ctx->n);
-  for (int s = 0; s < H; ++s)
+  if (std::max(std::max(up, down), std::max(grp, prox)) > cap) return;
+  // operator blob
+  std::vector<unsigned char> blob(bl.bytes, 0);
+  {
+    double* dp = reinterpret_cast<double*>(blob.data());
+    int* ip = reinterpret_cast<int*>(blob.data());
+    for (int j = 0; j < nu; ++j)
+      for (int k = 0; k < ns; ++k) dp[bl.ept + k * nu + j] = ept[(size_t)j * ns + k];
+    for (int e = 0; e < enz; ++e) { dp[bl.ev + e] = ev[e]; ip[bl.ecol + e] = ec[e]; }
+    for (int i = 0; i <= ns; ++i) ip[bl.eptr + i] = ep[i];
+    for (int e = 0; e < bnz; ++e) {
+      dp[bl.bcv + e] = bcv[e]; ip[bl.bcr + e] = bcr[e];
+      dp[bl.brv + e] = brv[e]; ip[bl.brc + e] = brc[e];
+    }
+    for (int j = 0; j <= nu; ++j) ip[bl.bcp + j] = bcp[j];
+    for (int i = 0; i <= nt; ++i) ip[bl.brp + i] = brp[i];
+  }
+  upload_vec(ctx, &ctx->blob, blob);
+  // stage of every branching row; stage groups bottom-up with <= 32 items per row
+  std::vector<int> stage(std::max(nb, 1), 0);
+  for (int s = 0; s < kstar; ++s)
     for (int r = off[s]; r < off[s + 1]; ++r) stage[r] = s;
-  std::vector<int> bdp(nb + 1, 0), bdi, bdw, btp(nb + 1, 0), bti, btw;
-  std::vector<int> stack;
-  for (int r = 0; r < nb; ++r) {
-    stack.assign(cidx.begin() + cptr[r], cidx.begin() + cptr[r + 1]);
-    while (!stack.empty()) {
-      const int e = stack.back();
-      stack.pop_back();
-      if (e < nb) {
-        bdi.push_back(e);
-        bdw.push_back(stage[e] - stage[r]);
-        for (int c = cptr[e]; c < cptr[e + 1]; ++c) stack.push_back(cidx[c]);
-      } else {
-        bti.push_back(e - off[kstar]);
-        btw.push_back(kstar - stage[r] - 1);
+  auto items_of = [&](int r, int s_hi, std::vector<int>* it, std::vector<int>* wt) {
+    int cnt = 0;
+    std::vector<int> st(cidx.begin() + cptr[r], cidx.begin() + cptr[r + 1]);
+    std::vector<int> dep(st.size(), 1);
+    while (!st.empty()) {
+      const int e = st.back(), de = dep.back();
+      st.pop_back();
+      dep.pop_back();
+      const bool frontier = e >= off[s_hi + 1];
+      ++cnt;
+      if (it) {
+        it->push_back(e * 2 + (frontier ? 1 : 0));
+        wt->push_back(frontier ? de - 1 : de);
+      }
+      if (!frontier)
+        for (int c = cptr[e]; c < cptr[e + 1]; ++c) {
+          st.push_back(cidx[c]);
+          dep.push_back(de + 1);
+        }
+    }
+    return cnt;
+  };
+  ctx->gk_groups.clear();
+  std::vector<int> gip(nb + 1, 0), gii, giw;
+  {
+    std::vector<std::pair<int, int>> groups;  // (s_lo, s_hi), bottom-up
+    int s_hi = kstar - 1;
+    while (s_hi >= 0) {
+      int s_lo = s_hi;
+      while (s_lo > 0) {
+        int mx = 0;
+        for (int r = off[s_lo - 1]; r < off[s_lo]; ++r) mx = std::max(mx, items_of(r, s_hi, nullptr, nullptr));
+        if (mx > 32) break;
+        --s_lo;
+      }
+      groups.push_back({s_lo, s_hi});
+      s_hi = s_lo - 1;
+    }
+    std::vector<int> ghi(std::max(kstar, 1), 0);
+    for (auto& g : groups)
+      for (int s = g.first; s <= g.second; ++s) ghi[s] = g.second;
+    for (int r = 0; r < nb; ++r) {
+      items_of(r, ghi[stage[r]], &gii, &giw);
+      gip[r + 1] = (int)gii.size();
+    }
+    for (auto& g : groups) ctx->gk_groups.push_back({off[g.first], off[g.second + 1] - off[g.first]});
+  }
+  if (gii.empty()) { gii.push_back(0); giw.push_back(0); }
+  upload_vec(ctx, &ctx->gi_ptr, gip);
+  upload_vec(ctx, &ctx->gi_item, gii);
+  upload_vec(ctx, &ctx->gi_w, giw);
+  // chain root paths and ancestor ownership (first chain below a row writes it)
+  std::vector<int> cpath((size_t)std::max(nchain * kstar, 1), 0);
+  std::vector<unsigned> cown(nchain, 0u);
+  if (kstar > 0) {
+    std::vector<int> anc(ctx->n, -1);
+    for (int r = 0; r < ctx->n; ++r)
+      for (int c = cptr[r]; c < cptr[r + 1]; ++c) anc[cidx[c]] = r;
+    std::vector<int> first(nb, -1);
+    for (int i = 0; i < nchain; ++i) {
+      int a = anc[nb + i];
+      for (int m = kstar - 1; m >= 0; --m) {
+        cpath[(size_t)i * kstar + m] = a;
+        if (first[a] < 0) {
+          first[a] = i;
+          cown[i] |= 1u << m;
+        }
+        a = anc[a];
       }
     }
-    bdp[r + 1] = (int)bdi.size();
-    btp[r + 1] = (int)bti.size();
   }
-  if (bdi.empty()) { bdi.push_back(0); bdw.push_back(0); }
-  if (bti.empty()) { bti.push_back(0); btw.push_back(0); }
-  upload_vec(ctx, &ctx->bd_ptr, bdp);
-  upload_vec(ctx, &ctx->bd_idx, bdi);
-  upload_vec(ctx, &ctx->bd_w, bdw);
-  upload_vec(ctx, &ctx->bt_ptr, btp);
-  upload_vec(ctx, &ctx->bt_idx, bti);
-  upload_vec(ctx, &ctx->bt_w, btw);
-  std::vector<double> zl((size_t)ctx->n * nu, 0.0), za((size_t)nchain * nu, 0.0),
-      zd((size_t)std::max(nb, 1) * lx, 0.0);
+  upload_vec(ctx, &ctx->cpath, cpath);
+  upload_vec(ctx, &ctx->cown, cown);
+  std::vector<double> zl((size_t)ctx->n * nu, 0.0), za((size_t)(nb + nchain) * nu, 0.0);
   upload_vec(ctx, &ctx->Lb, zl);
-  upload_vec(ctx, &ctx->Atop, za);
-  upload_vec(ctx, &ctx->delta, zd);
+  upload_vec(ctx, &ctx->Asub, za);
   CK(cudaFuncSetAttribute(k_chain_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
   CK(cudaFuncSetAttribute(k_chain_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
-  CK(cudaFuncSetAttribute(k_branch_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bu));
-  CK(cudaFuncSetAttribute(k_branch_u, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bru));
+  CK(cudaFuncSetAttribute(k_branch_grp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grp));
   CK(cudaFuncSetAttribute(k_prox_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox));
-  ctx->sm_up = up; ctx->sm_down = down; ctx->sm_bu = bu; ctx->sm_bru = bru; ctx->sm_prox = prox;
+  ctx->sm_up = up; ctx->sm_down = down; ctx->sm_grp = grp; ctx->sm_prox = prox;
+  ctx->blob16 = bl.bytes / 16;
   ctx->n_branch = nb;
   ctx->use_graphk = 1;
 }
@@ -489,7 +563,8 @@ void configure_fast(wmpc_ctx* ctx, const double* B, const double* E, const doubl
       ctx->use_scan = 1;
     }
   }
-  configure_graphk(ctx, cptr, cidx, enz, bnz);
+  configure_graphk(ctx, cptr, cidx, std::vector<double>(e_pinv, e_pinv + (size_t)nu * ns), ep, ec, ev, bcp, bcr,
+                   bcv, brp, brc, brv, enz, bnz);
   ctx->fast = true;
 }
 
@@ -509,20 +584,16 @@ void launch_fast_mc(wmpc_ctx* ctx, FastView& f) {
 
 FastView make_fastview(wmpc_ctx* ctx, int count);
 
-int graphk_kernels(const wmpc_ctx* ctx) { return ctx->n_branch > 0 ? 6 : 4; }
+int graphk_kernels(const wmpc_ctx* ctx) { return 3 + (int)ctx->gk_groups.size(); }
 
 // One APG iteration of the graph-of-kernels path, enqueued on ctx->stream.
 void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
   cudaStream_t st = ctx->stream;
-  const int nb = ctx->n_branch, nc = ctx->nchain;
+  const int nc = ctx->nchain;
   k_chain_up<<<nc, SC_THREADS, ctx->sm_up, st>>>(f);
-  if (nb > 0) {
-    k_branch_up<<<nb, SC_THREADS, ctx->sm_bu, st>>>(f);
-    k_branch_u<<<nb, SC_THREADS, ctx->sm_bru, st>>>(f);
-  }
+  for (const auto& g : ctx->gk_groups) k_branch_grp<<<g.second, SC_THREADS, ctx->sm_grp, st>>>(f, g.first);
   k_chain_down<<<nc, SC_THREADS, ctx->sm_down, st>>>(f);
   k_prox_nodes<<<(ctx->n + SC_NPB - 1) / SC_NPB, SC_THREADS, ctx->sm_prox, st>>>(f);
-  k_advance<<<1, 32, 0, st>>>(ctx->iter);
 }
 
 void capture_graphk(wmpc_ctx* ctx) {
@@ -574,10 +645,12 @@ FastView make_fastview(wmpc_ctx* ctx, int count) {
   f.prof = ctx->prof_on ? ctx->prof : nullptr;
   f.n_branch = ctx->n_branch;
   f.Lb = ctx->Lb;
-  f.Atop = ctx->Atop;
-  f.delta = ctx->delta;
-  f.bd_ptr = ctx->bd_ptr; f.bd_idx = ctx->bd_idx; f.bd_w = ctx->bd_w;
-  f.bt_ptr = ctx->bt_ptr; f.bt_idx = ctx->bt_idx; f.bt_w = ctx->bt_w;
+  f.Asub = ctx->Asub;
+  f.blob = reinterpret_cast<const double*>(ctx->blob);
+  f.blob16 = ctx->blob16;
+  f.gi_ptr = ctx->gi_ptr; f.gi_item = ctx->gi_item; f.gi_w = ctx->gi_w;
+  f.cpath = ctx->cpath;
+  f.cown = ctx->cown;
   f.work_doubles = ctx->scan_work;
   return f;
 }
@@ -645,7 +718,7 @@ void free_all(wmpc_ctx* c) {
                   c->bad_row, c->dk_done, c->part, c->scal, c->d_np, c->chain_node,
                   c->bc_ptr, c->bc_row, c->br_ptr, c->br_col, c->off_dev, c->bc_val, c->br_val,
                   c->e_ptr, c->e_col, c->e_val, c->aux,
-                  c->Lb, c->Atop, c->delta, c->bd_ptr, c->bd_idx, c->bd_w, c->bt_ptr, c->bt_idx, c->bt_w,
+                  c->Lb, c->Asub, c->blob, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
                   c->prof};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -910,12 +983,6 @@ int wmpc_set_node_data(wmpc_ctx* ctx, wmpc_nodes* nodes, const double* demand, c
       const int tot = ctx->nchain * ctx->nu;
       k_chain_ebar<<<(tot + 255) / 256, 256, 0, ctx->stream>>>(ctx->chain_node, ctx->nchain, ctx->H - ctx->kstar,
                                                                ctx->nu, nodes->e_off, nodes->ebar);
-      if (ctx->use_graphk && ctx->n_branch > 0) {
-        ctx->launches++;
-        const int tb = ctx->n_branch * ctx->nu;
-        k_branch_ebar<<<(tb + 255) / 256, 256, 0, ctx->stream>>>(ctx->anc, ctx->n_branch, ctx->nu, nodes->e_off,
-                                                                 nodes->ebar);
-      }
     }
     check_launch(ctx);
     int bad = INT_MAX;

@@ -6,77 +6,81 @@
 // idempotent (P(a + P b) = P(a + b)):
 //   wbar_r = sum_{sub(r)} Yx,     a_r = (Yu_r + wbar_r B) + R_r,
 //   lin_r  = a_r + P sum_{desc(r)} a,           L_r = lin_r / (2c p_r),
-//   u_r    = e_off_r + P(q + Ebar_r - sum_{path(r)} L),
+//   u_r    = e_off_r + P(q + sum_{anc(r)} e_off - sum_{path(r)} L),
 //   x_r    = (x_anc + u_r B^T) + g_r.
-// One APG iteration (solver.py:460-506) is six graph nodes:
-//   k_chain_up    one CTA per chain: suffix scans, projector   -> L, chain totals
-//   k_branch_up   one CTA per branching node: depth-weighted sums over its
-//                 subtree (chain totals stand in for whole chains) -> L
-//   k_branch_u    one CTA per branching node: walk-up sum of L, projector -> U, B u + g
-//   k_chain_down  one CTA per chain: prefix scans, projector   -> U, X
-//   k_prox_nodes  node-parallel Moreau prox, averages, next collapsed dual
-//   k_advance     iteration counter
-// Graph edges replace grid barriers (measured 0.7 us per dependent kernel
-// vs 1.25 us per cooperative grid.sync on B200).
+// Rows at stages >= kstar form nchain chains laid out stage-major
+// (row = n_branch + t*nchain + chain). One APG iteration (solver.py:460-506)
+// is the graph
+//   k_chain_up       one CTA per chain: suffix scans + projector -> L, subtree totals
+//   k_branch_grp x G one CTA per branching row of a stage group: depth-weighted
+//                    sums over the group's rows and the frontier totals below -> L
+//   k_chain_down     one CTA per chain: the whole root path (ancestors + chain):
+//                    prefix scans + projector -> U, X
+//   k_prox_nodes     node-parallel Moreau prox, ergodic averages, next collapsed dual
+// Graph edges replace grid barriers (measured 0.7 us per dependent kernel vs
+// 1.25 us per cooperative grid.sync on B200). The iteration counter is bumped
+// by k_chain_up; k_prox_nodes uses it - 1.
 #pragma once
 #include "wmpc_fast.cuh"
 
 namespace wmpc {
 
 constexpr int SC_THREADS = 256;
-constexpr int SC_NPB = 4;  // nodes per CTA in k_prox_nodes
+constexpr int SC_NPB = 4;    // nodes per CTA in k_prox_nodes
+constexpr int SC_MAXK = 30;  // max branching depth (bits of cown)
 
-// E^+ (transposed), E rows, B both ways, into shared memory; returns the Ops view.
-__device__ Ops load_ops(const FastView& f, double* sp) {
+// ---------------------------------------------------------------- operators
+// Blob layout (doubles, then ints): [E^+ transposed ns x nu | E vals | B CSC vals
+// | B CSR vals | pad | E ptr | E cols | B CSC ptr | B CSC rows | B CSR ptr | B CSR cols]
+struct BlobLayout {
+  int ept, ev, bcv, brv, dbl_end, eptr, ecol, bcp, bcr, brp, brc, bytes;
+};
+__host__ __device__ inline BlobLayout blob_layout(int nt, int nu, int ns, int enz, int bnz) {
+  BlobLayout b;
+  b.ept = 0;
+  b.ev = b.ept + nu * ns;
+  b.bcv = b.ev + enz;
+  b.brv = b.bcv + bnz;
+  b.dbl_end = b.brv + bnz;
+  b.dbl_end += b.dbl_end & 1;
+  int ib = 2 * b.dbl_end;  // int offsets
+  b.eptr = ib;
+  b.ecol = b.eptr + ns + 1;
+  b.bcp = b.ecol + enz;
+  b.bcr = b.bcp + nu + 1;
+  b.brp = b.bcr + bnz;
+  b.brc = b.brp + nt + 1;
+  const int iend = b.brc + bnz;
+  b.bytes = ((iend * 4 + 15) / 16) * 16;
+  return b;
+}
+
+__device__ __forceinline__ void issue_blob(const FastView& f, void* dst) {
+  const int4* src = reinterpret_cast<const int4*>(f.blob);
+  int4* d = reinterpret_cast<int4*>(dst);
+  for (int i = threadIdx.x; i < f.blob16; i += blockDim.x) cp16(d + i, src + i);
+}
+__device__ __forceinline__ Ops blob_ops(const FastView& f, const void* sp) {
   const DevView& d = f.d;
-  const int nt = d.nt, nu = d.nu, ns = d.ns, bnnz = f.b_nnz;
-  double* s_bnd = sp;             sp += 3 * nt + 2 * nu;
-  double* s_ept = sp;             sp += nu * ns;
-  double* s_ev = sp;              sp += f.e_nnz;
-  double* s_bcv = sp;             sp += bnnz;
-  double* s_brv = sp;             sp += bnnz;
-  int* ip = reinterpret_cast<int*>(sp);
-  int* s_eptr = ip;               ip += ns + 1;
-  int* s_ecol = ip;               ip += f.e_nnz;
-  int* s_bcp = ip;                ip += nu + 1;
-  int* s_bcr = ip;                ip += bnnz;
-  int* s_brp = ip;                ip += nt + 1;
-  int* s_brc = ip;
-  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
-    s_bnd[i] = d.xmin[i];
-    s_bnd[nt + i] = d.xmax[i];
-    s_bnd[2 * nt + i] = d.xsafe[i];
-  }
-  for (int i = threadIdx.x; i < nu; i += blockDim.x) {
-    s_bnd[3 * nt + i] = d.umin[i];
-    s_bnd[3 * nt + nu + i] = d.umax[i];
-  }
-  for (int i = threadIdx.x; i < nu * ns; i += blockDim.x) {
-    int j = i / ns, k = i - j * ns;
-    s_ept[k * nu + j] = d.e_pinv[i];
-  }
-  for (int i = threadIdx.x; i < f.e_nnz; i += blockDim.x) {
-    s_ev[i] = f.e_val[i];
-    s_ecol[i] = f.e_col[i];
-  }
-  for (int i = threadIdx.x; i <= ns; i += blockDim.x) s_eptr[i] = f.e_ptr[i];
-  for (int i = threadIdx.x; i < bnnz; i += blockDim.x) {
-    s_bcv[i] = f.bc_val[i];
-    s_bcr[i] = f.bc_row[i];
-    s_brv[i] = f.br_val[i];
-    s_brc[i] = f.br_col[i];
-  }
-  for (int i = threadIdx.x; i <= nu; i += blockDim.x) s_bcp[i] = f.bc_ptr[i];
-  for (int i = threadIdx.x; i <= nt; i += blockDim.x) s_brp[i] = f.br_ptr[i];
-  return Ops{s_ept, s_eptr, s_ecol, s_ev, s_bcp, s_bcr, s_bcv, s_brp, s_brc, s_brv,
-             s_bnd, s_bnd + nt, s_bnd + 2 * nt, s_bnd + 3 * nt, s_bnd + 3 * nt + nu};
-}
-__host__ __device__ inline size_t ops_bytes(int nt, int nu, int ns, int enz, int bnz) {
-  return sizeof(double) * ((size_t)3 * nt + 2 * nu + (size_t)nu * ns + enz + 2 * (size_t)bnz) +
-         sizeof(int) * ((size_t)ns + 1 + enz + nu + 1 + bnz + nt + 1 + bnz) + 16;
+  const BlobLayout b = blob_layout(d.nt, d.nu, d.ns, f.e_nnz, f.b_nnz);
+  const double* dp = reinterpret_cast<const double*>(sp);
+  const int* ip = reinterpret_cast<const int*>(sp);
+  Ops op{};
+  op.ep = dp + b.ept;
+  op.eval = dp + b.ev;
+  op.bcv = dp + b.bcv;
+  op.brv = dp + b.brv;
+  op.eptr = ip + b.eptr;
+  op.ecol = ip + b.ecol;
+  op.bcp = ip + b.bcp;
+  op.bcr = ip + b.bcr;
+  op.brp = ip + b.brp;
+  op.brc = ip + b.brc;
+  return op;
 }
 
-// out[m] = P in[m] for m < rows (stride nu); T scratch rows x FAST_MAXNS. 2 barriers.
+// out[m] = P in[m] for m < rows (stride nu; in place allowed); T scratch
+// rows x FAST_MAXNS. 2 barriers.
 __device__ __forceinline__ void proj_rows(const DevView& d, const Ops& op, const double* in, double* out,
                                           double* T, int rows) {
   const int nu = d.nu, ns = d.ns;
@@ -102,28 +106,33 @@ __device__ __forceinline__ void proj_rows(const DevView& d, const Ops& op, const
   __syncthreads();
 }
 
+__device__ __forceinline__ int chain_row(const FastView& f, int t, int ci) { return f.n_branch + t * f.nchain + ci; }
+
 // ---------------------------------------------------------------- k_chain_up
+// Shared: rec nst x (ly + nu + 2) [Yx | Yu->a | R | aux], WB nst x lx,
+// S nst x nu, T nst x FAST_MAXNS, blob.
 __global__ void __launch_bounds__(SC_THREADS) k_chain_up(FastView f) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly;
   const int nst = d.H - f.kstar, ci = blockIdx.x;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int ra = ly + nu;                                   // [Yx | Yu | R]
-  double* rec = reinterpret_cast<double*>(smem_raw);        // nst * ra
-  double* WB = rec + (size_t)nst * ra;                      // nst * lx
-  double* S = WB + (size_t)nst * lx;                        // nst * nu (projected in place)
-  double* T = S + (size_t)nst * nu;                         // nst * FAST_MAXNS
-  int* rows = reinterpret_cast<int*>(T + (size_t)nst * FAST_MAXNS);
-  double* opsp = reinterpret_cast<double*>(rows + ((nst + 3) & ~3));
+  const int ra = ly + nu + 2;
+  double* rec = reinterpret_cast<double*>(smem_raw);
+  double* WB = rec + (size_t)nst * ra;
+  double* S = WB + (size_t)nst * lx;
+  double* T = S + (size_t)nst * nu;
+  void* bl = T + (size_t)nst * FAST_MAXNS;
+  if (ci == 0 && threadIdx.x == 0) *d.iter += 1;  // this iteration's number + 1 (read by k_prox_nodes)
   const NodePtrs np = *d.np;
-  if (threadIdx.x < nst) rows[threadIdx.x] = f.chain_node[(size_t)threadIdx.x * f.nchain + ci];
-  __syncthreads();
-  FOR_RC(nst, 7, (ly >> 1), t, k) cp16(rec + (size_t)t * ra + 2 * k, d.Yc + (size_t)rows[t] * ly + 2 * k);
-  FOR_RC(nst - 1, 6, (nu >> 1), t, k) cp16(rec + (size_t)t * ra + ly + 2 * k, np.R + (size_t)rows[t] * nu + 2 * k);
+  issue_blob(f, bl);
+  FOR_RC(nst, 7, (ly >> 1), t, k) cp16(rec + (size_t)t * ra + 2 * k, d.Yc + (size_t)chain_row(f, t, ci) * ly + 2 * k);
+  FOR_RC(nst - 1, 6, (nu >> 1), t, k)
+    cp16(rec + (size_t)t * ra + ly + 2 * k, np.R + (size_t)chain_row(f, t, ci) * nu + 2 * k);
+  if (threadIdx.x < nst) cp16(rec + (size_t)threadIdx.x * ra + ly + nu, f.aux + (size_t)chain_row(f, threadIdx.x, ci) * 2);
   cp_commit();
-  const Ops op = load_ops(f, opsp);
   cp_wait<0>();
   __syncthreads();
+  const Ops op = blob_ops(f, bl);
   if (threadIdx.x < nt) {  // wbar suffix scan: wbar_t = Yx_t + wbar_{t+1}
     const int j = threadIdx.x;
     double acc = 0.0;
@@ -132,10 +141,10 @@ __global__ void __launch_bounds__(SC_THREADS) k_chain_up(FastView f) {
       acc = t == nst - 1 ? yx : yx + acc;
       WB[t * lx + j] = acc;
     }
-    d.wbar[(size_t)rows[0] * lx + j] = acc;
+    d.wbar[(size_t)chain_row(f, 0, ci) * lx + j] = acc;
   }
   __syncthreads();
-  FOR_NU(nst, t, k) {  // a = (Yu + wbar B) + R over Yu
+  FOR_NU(nst, t, k) {  // a = (Yu + wbar B) + R, over Yu
     double* R = rec + (size_t)t * ra;
     double bw = 0.0;
     for (int e = op.bcp[k]; e < op.bcp[k + 1]; ++e) bw = fma(WB[t * lx + op.bcr[e]], op.bcv[e], bw);
@@ -152,207 +161,198 @@ __global__ void __launch_bounds__(SC_THREADS) k_chain_up(FastView f) {
       const double a = rec[(size_t)t * ra + lx + k];
       acc = t == nst - 1 ? a : a + acc;
     }
-    f.Atop[(size_t)ci * nu + k] = acc;
+    f.Asub[(size_t)chain_row(f, 0, ci) * nu + k] = acc;
   }
   __syncthreads();
   proj_rows(d, op, S, S, T, nst - 1);
   FOR_NU(nst, t, k) {
-    const double a = rec[(size_t)t * ra + lx + k];
+    const double* R = rec + (size_t)t * ra;
+    const double a = R[lx + k];
     const double l = t < nst - 1 ? a + S[t * nu + k] : a;
-    f.Lb[(size_t)rows[t] * nu + k] = l * f.aux[(size_t)rows[t] * 2];
+    f.Lb[(size_t)chain_row(f, t, ci) * nu + k] = l * R[ly + nu];
   }
 }
 
-// ---------------------------------------------------------------- k_branch_up
-// One CTA per branching node r: depth-weighted sums over its subtree.
-//   W1 = wbar_r = Yx_r + sum_{e in desc_B} Yx_e + sum_{tops} wbar_t
-//   W2 = sum_{d in desc_B(r)} wbar_d = sum_e w_e Yx_e + sum_t w_t wbar_t
-//   Su = sum_e (Yu_e + R_e) + sum_t Atop_t
+// ---------------------------------------------------------------- k_branch_grp
+// One CTA per branching row r of a stage group. Items: the group's rows below
+// r (kind 0, weight depth(e)-depth(r)) and the frontier rows right below the
+// group (kind 1, weight depth(f)-depth(r)-1; chain tops or the top rows of the
+// group below, whose wbar / subtree totals are already final):
+//   W1 = wbar_r = Yx_r + sum_0 Yx_e + sum_1 wbar_f
+//   W2 = sum_{d in desc_B(r)} wbar_d = sum_0 w Yx_e + sum_1 w wbar_f
+//   Su = sum_0 (Yu_e + R_e) + sum_1 Asub_f
 //   a_r = (Yu_r + W1 B) + R_r,  S_r = Su + W2 B,  lin_r = a_r + P S_r.
-__global__ void __launch_bounds__(SC_THREADS) k_branch_up(FastView f) {
+__global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly;
-  const int r = blockIdx.x;
+  const int r = r0 + blockIdx.x;
+  constexpr int NW = SC_THREADS / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* part = reinterpret_cast<double*>(smem_raw);  // 4 * (2 lx + nu) partials
-  const int pw = 2 * lx + nu;
-  double* W1 = part + 4 * pw;   // lx
-  double* W2 = W1 + lx;         // lx
-  double* Sv = W2 + lx;         // nu
-  double* av = Sv + nu;         // nu
-  double* PS = av + nu;         // nu
-  double* T = PS + nu;          // FAST_MAXNS
-  double* opsp = T + FAST_MAXNS;
+  double* part = reinterpret_cast<double*>(smem_raw);  // NW x 256: [s1 64 | s2 64 | su 128]
+  double* W1 = part + NW * 256;  // lx
+  double* W2 = W1 + lx;          // lx
+  double* av = W2 + lx;          // nu
+  double* Sv = av + nu;          // nu
+  double* T = Sv + nu;           // FAST_MAXNS
+  void* bl = T + FAST_MAXNS;
   const NodePtrs np = *d.np;
-  const Ops op = load_ops(f, opsp);
-  const int grp = threadIdx.x >> 6, c = threadIdx.x & 63;  // 4 groups x 64 lanes
-  const int e0 = f.bd_ptr[r], e1 = f.bd_ptr[r + 1], t0 = f.bt_ptr[r], t1 = f.bt_ptr[r + 1];
-  // Yx part (c < nt)
-  if (c < nt) {
-    double s1 = 0.0, s2 = 0.0;
-#pragma unroll 4
-    for (int e = e0 + grp; e < e1; e += 4) {
-      const double v = d.Yc[(size_t)f.bd_idx[e] * ly + c];
-      s1 += v;
-      s2 = fma((double)f.bd_w[e], v, s2);
+  issue_blob(f, bl);
+  cp_commit();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double s1[2] = {0.0, 0.0}, s2[2] = {0.0, 0.0}, su[4] = {0.0, 0.0, 0.0, 0.0};
+  const int e0 = f.gi_ptr[r], e1 = f.gi_ptr[r + 1];
+  for (int e = e0 + warp; e < e1; e += NW) {
+    const int item = f.gi_item[e];
+    const size_t row = (size_t)(item >> 1);
+    const bool fr = item & 1;
+    const double w = (double)f.gi_w[e];
+    const double* px = fr ? d.wbar + row * lx : d.Yc + row * ly;
+    double vx[2], vu[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int c = lane + 32 * i;
+      vx[i] = c < nt ? px[c] : 0.0;
     }
-    for (int e = t0 + grp; e < t1; e += 4) {
-      const int tr = f.chain_node[f.bt_idx[e]];  // chain top row (stage kstar, t = 0)
-      const double v = d.wbar[(size_t)tr * lx + c];
-      s1 += v;
-      s2 = fma((double)f.bt_w[e], v, s2);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = lane + 32 * i;
+      vu[i] = c < nu ? (fr ? f.Asub[row * nu + c] : d.Yc[row * ly + lx + c] + np.R[row * nu + c]) : 0.0;
     }
-    part[grp * pw + c] = s1;
-    part[grp * pw + lx + c] = s2;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      s1[i] += vx[i];
+      s2[i] = fma(w, vx[i], s2[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) su[i] += vu[i];
   }
-  // Yu + R part (two passes of 64 lanes over nu <= 128)
-  for (int k = c; k < nu; k += 64) {
-    double s = 0.0;
-    for (int e = e0 + grp; e < e1; e += 4) {
-      const size_t er = (size_t)f.bd_idx[e];
-      s += d.Yc[er * ly + lx + k] + np.R[er * nu + k];
-    }
-    for (int e = t0 + grp; e < t1; e += 4) s += f.Atop[(size_t)f.bt_idx[e] * nu + k];
-    part[grp * pw + 2 * lx + k] = s;
+  double* pw = part + warp * 256;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    pw[lane + 32 * i] = s1[i];
+    pw[64 + lane + 32 * i] = s2[i];
   }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) pw[128 + lane + 32 * i] = su[i];
   __syncthreads();
   if (threadIdx.x < nt) {
     const int j = threadIdx.x;
-    const double* yc = d.Yc + (size_t)r * ly;
-    W1[j] = yc[j] + (((part[j] + part[pw + j]) + part[2 * pw + j]) + part[3 * pw + j]);
-    W2[j] = ((part[lx + j] + part[pw + lx + j]) + part[2 * pw + lx + j]) + part[3 * pw + lx + j];
+    double a1 = part[j], a2 = part[64 + j];
+    for (int w = 1; w < NW; ++w) {
+      a1 += part[w * 256 + j];
+      a2 += part[w * 256 + 64 + j];
+    }
+    W1[j] = d.Yc[(size_t)r * ly + j] + a1;
+    W2[j] = a2;
   }
+  cp_wait<0>();
   __syncthreads();
+  const Ops op = blob_ops(f, bl);
   if (threadIdx.x < nu) {
     const int k = threadIdx.x;
-    const double su = ((part[2 * lx + k] + part[pw + 2 * lx + k]) + part[2 * pw + 2 * lx + k]) +
-                      part[3 * pw + 2 * lx + k];
+    double s = part[128 + k];
+    for (int w = 1; w < NW; ++w) s += part[w * 256 + 128 + k];
     double b1 = 0.0, b2 = 0.0;
     for (int e = op.bcp[k]; e < op.bcp[k + 1]; ++e) {
       b1 = fma(W1[op.bcr[e]], op.bcv[e], b1);
       b2 = fma(W2[op.bcr[e]], op.bcv[e], b2);
     }
     av[k] = (d.Yc[(size_t)r * ly + lx + k] + b1) + np.R[(size_t)r * nu + k];
-    Sv[k] = su + b2;
+    Sv[k] = s + b2;
   }
+  if (threadIdx.x < nt) d.wbar[(size_t)r * lx + threadIdx.x] = W1[threadIdx.x];
   __syncthreads();
-  proj_rows(d, op, Sv, PS, T, 1);
+  if (threadIdx.x < nu) f.Asub[(size_t)r * nu + threadIdx.x] = av[threadIdx.x] + Sv[threadIdx.x];
+  proj_rows(d, op, Sv, Sv, T, 1);
   if (threadIdx.x < nu) {
     const int k = threadIdx.x;
-    f.Lb[(size_t)r * nu + k] = (av[k] + PS[k]) * f.aux[(size_t)r * 2];
+    f.Lb[(size_t)r * nu + k] = (av[k] + Sv[k]) * f.aux[(size_t)r * 2];
   }
-}
-
-// ---------------------------------------------------------------- k_branch_u
-// One CTA per branching node: u_r = e_off_r + P(q + Ebar_r - sum_{path} L), delta = B u + g.
-__global__ void __launch_bounds__(SC_THREADS) k_branch_u(FastView f) {
-  const DevView& d = f.d;
-  const int nt = d.nt, nu = d.nu, lx = d.lx;
-  const int r = blockIdx.x;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* z = reinterpret_cast<double*>(smem_raw);  // nu
-  double* pz = z + nu;                               // nu
-  double* T = pz + nu;                               // FAST_MAXNS
-  double* opsp = T + FAST_MAXNS;
-  const NodePtrs np = *d.np;
-  const Ops op = load_ops(f, opsp);
-  if (threadIdx.x < nu) {
-    const int k = threadIdx.x;
-    double ls = 0.0;  // sum over the path, root side first
-    int path[32];
-    int depth = 0;
-    for (int a = r; a >= 0 && depth < 32; a = d.anc[a]) path[depth++] = a;
-    for (int i = depth - 1; i >= 0; --i) ls = ls + f.Lb[(size_t)path[i] * nu + k];
-    z[k] = (d.q[k] + np.ebar[(size_t)r * nu + k]) - ls;
-  }
-  __syncthreads();
-  proj_rows(d, op, z, pz, T, 1);
-  if (threadIdx.x < nu) {
-    const int k = threadIdx.x;
-    const double u = np.e_off[(size_t)r * nu + k] + pz[k];
-    pz[k] = u;
-    d.U[(size_t)r * nu + k] = u;
-  }
-  __syncthreads();
-  if (threadIdx.x < nt) {
-    const int j = threadIdx.x;
-    double bu = 0.0;
-    for (int e = op.brp[j]; e < op.brp[j + 1]; ++e) bu = fma(pz[op.brc[e]], op.brv[e], bu);
-    f.delta[(size_t)r * lx + j] = bu;  // B u; g added by the x walk-up
-  }
-}
-
-// x of a branching row by the walk-up sum x = (x_anc + B u) + g (reference association).
-__device__ __forceinline__ double branch_x(const FastView& f, const NodePtrs& np, int r, int j) {
-  const DevView& d = f.d;
-  int path[32];
-  int depth = 0;
-  for (int a = r; a >= 0 && depth < 32; a = d.anc[a]) path[depth++] = a;
-  double x = d.p[j];
-  for (int i = depth - 1; i >= 0; --i) x = (x + f.delta[(size_t)path[i] * d.lx + j]) + np.g[(size_t)path[i] * d.lx + j];
-  return x;
 }
 
 // ---------------------------------------------------------------- k_chain_down
+// One CTA per chain over its whole root path: the kstar ancestors (root
+// first) then the nst chain rows, H rows in all.
+//   z_m = (q + sum_{m' < m} e_off_m') - sum_{m' <= m} L_m',  u_m = e_off_m + P z_m,
+//   x_m = (x_{m-1} + u_m B^T) + g_m,  x_{-1} = p.
+// Ancestor rows are written by the chain that owns them (cown).
+// Shared: rec H x (2nu + lx) [L->z | e_off | g], T H x FAST_MAXNS, rows H, blob.
 __global__ void __launch_bounds__(SC_THREADS) k_chain_down(FastView f) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx;
-  const int nst = d.H - f.kstar, ci = blockIdx.x;
+  const int kb = f.kstar, nr = d.H, ci = blockIdx.x;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int rd = 3 * nu + lx + 2;                           // [L | e_off | ebar | g | aux]
-  double* rec = reinterpret_cast<double*>(smem_raw);        // nst * rd
-  double* Z = rec + (size_t)nst * rd;                       // nst * nu: z, then u
-  double* T = Z + (size_t)nst * nu;                         // nst * FAST_MAXNS
-  double* ua = T + (size_t)nst * FAST_MAXNS;                // nu
-  double* xa = ua + nu;                                     // lx
-  int* rows = reinterpret_cast<int*>(xa + lx);
-  double* opsp = reinterpret_cast<double*>(rows + ((nst + 3) & ~3));
+  const int rd = 2 * nu + lx;
+  double* rec = reinterpret_cast<double*>(smem_raw);
+  double* T = rec + (size_t)nr * rd;
+  int* rows = reinterpret_cast<int*>(T + (size_t)nr * FAST_MAXNS);
+  void* bl = rows + ((nr + 3) & ~3);
   const NodePtrs np = *d.np;
-  if (threadIdx.x < nst) rows[threadIdx.x] = f.chain_node[(size_t)threadIdx.x * f.nchain + ci];
-  __syncthreads();
-  FOR_RC(nst, 6, (nu >> 1), t, k) cp16(rec + (size_t)t * rd + 2 * k, f.Lb + (size_t)rows[t] * nu + 2 * k);
-  FOR_RC(nst, 6, (nu >> 1), t, k) cp16(rec + (size_t)t * rd + nu + 2 * k, np.e_off + (size_t)rows[t] * nu + 2 * k);
-  FOR_RC(nst, 6, (nu >> 1), t, k) cp16(rec + (size_t)t * rd + 2 * nu + 2 * k, np.ebar + (size_t)rows[t] * nu + 2 * k);
-  FOR_RC(nst, 5, (lx >> 1), t, k) cp16(rec + (size_t)t * rd + 3 * nu + 2 * k, np.g + (size_t)rows[t] * lx + 2 * k);
-  cp_commit();
-  const Ops op = load_ops(f, opsp);
-  {
-    const int a = d.anc[rows[0]];
-    for (int k = threadIdx.x; k < nu; k += blockDim.x) ua[k] = a < 0 ? d.q[k] : d.U[(size_t)a * nu + k];
-    for (int j = threadIdx.x; j < nt; j += blockDim.x) xa[j] = a < 0 ? d.p[j] : branch_x(f, np, a, j);
+  issue_blob(f, bl);
+  if (threadIdx.x < nr) {
+    const int m = threadIdx.x;
+    rows[m] = m < kb ? f.cpath[(size_t)ci * kb + m] : chain_row(f, m - kb, ci);
   }
+  __syncthreads();
+  FOR_RC(nr, 6, (nu >> 1), m, k) cp16(rec + (size_t)m * rd + 2 * k, f.Lb + (size_t)rows[m] * nu + 2 * k);
+  FOR_RC(nr, 6, (nu >> 1), m, k) cp16(rec + (size_t)m * rd + nu + 2 * k, np.e_off + (size_t)rows[m] * nu + 2 * k);
+  FOR_RC(nr, 5, (lx >> 1), m, k) cp16(rec + (size_t)m * rd + 2 * nu + 2 * k, np.g + (size_t)rows[m] * lx + 2 * k);
+  cp_commit();
   cp_wait<0>();
   __syncthreads();
-  if (threadIdx.x < nu) {  // z_t = (u_anc + Ebar_t) - sum_{t' <= t} L_t'
+  const Ops op = blob_ops(f, bl);
+  if (threadIdx.x < nu) {
     const int k = threadIdx.x;
-    const double u0 = ua[k];
-    double acc = 0.0;
-    for (int t = 0; t < nst; ++t) {
-      const double* R = rec + (size_t)t * rd;
-      acc = acc + R[k];
-      Z[t * nu + k] = (u0 + R[2 * nu + k]) - acc;
+    double ls = 0.0, es = d.q[k];
+    for (int m = 0; m < nr; ++m) {
+      double* R = rec + (size_t)m * rd;
+      ls = m == 0 ? R[k] : ls + R[k];
+      R[k] = es - ls;  // z over L
+      es = es + R[nu + k];
     }
   }
   __syncthreads();
-  proj_rows(d, op, Z, Z, T, nst);
-  FOR_NU(nst, t, k) {
-    const double u = rec[(size_t)t * rd + nu + k] + Z[t * nu + k];
-    Z[t * nu + k] = u;
-    d.U[(size_t)rows[t] * nu + k] = u;
+  // projector over rows of stride rd: E pass then E^+ pass
+  FOR_RC(nr, 5, d.ns, m, i) {
+    const double* z = rec + (size_t)m * rd;
+    double v = 0.0;
+    for (int e = op.eptr[i]; e < op.eptr[i + 1]; ++e) v = fma(op.eval[e], z[op.ecol[e]], v);
+    T[m * FAST_MAXNS + i] = v;
   }
   __syncthreads();
-  FOR_NT(nst, t, j) {  // u B^T into the dead L slot
+  const unsigned own = kb > 0 ? f.cown[ci] : 0u;
+  FOR_NU(nr, m, k) {
+    double* R = rec + (size_t)m * rd;
+    const double* tm = T + m * FAST_MAXNS;
+    const int ns = d.ns;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int i = 0;
+    for (; i + 3 < ns; i += 4) {
+      a0 = fma(op.ep[i * nu + k], tm[i], a0);
+      a1 = fma(op.ep[(i + 1) * nu + k], tm[i + 1], a1);
+      a2 = fma(op.ep[(i + 2) * nu + k], tm[i + 2], a2);
+      a3 = fma(op.ep[(i + 3) * nu + k], tm[i + 3], a3);
+    }
+    for (; i < ns; ++i) a0 = fma(op.ep[i * nu + k], tm[i], a0);
+    const double u = R[nu + k] + (R[k] - ((a0 + a1) + (a2 + a3)));
+    R[k] = u;
+    if (m >= kb || ((own >> m) & 1u)) d.U[(size_t)rows[m] * nu + k] = u;
+  }
+  __syncthreads();
+  FOR_NT(nr, m, j) {  // u B^T into the dead e_off slot
+    double* R = rec + (size_t)m * rd;
     double bu = 0.0;
-    for (int e = op.brp[j]; e < op.brp[j + 1]; ++e) bu = fma(Z[t * nu + op.brc[e]], op.brv[e], bu);
-    rec[(size_t)t * rd + j] = bu;
+    for (int e = op.brp[j]; e < op.brp[j + 1]; ++e) bu = fma(R[op.brc[e]], op.brv[e], bu);
+    R[nu + j] = bu;
   }
   __syncthreads();
   if (threadIdx.x < nt) {
     const int j = threadIdx.x;
-    double x = xa[j];
-    for (int t = 0; t < nst; ++t) {
-      x = (x + rec[(size_t)t * rd + j]) + rec[(size_t)t * rd + 3 * nu + j];
-      d.X[(size_t)rows[t] * lx + j] = x;
+    double x = d.p[j];
+    for (int m = 0; m < nr; ++m) {
+      const double* R = rec + (size_t)m * rd;
+      x = (x + R[nu + j]) + R[2 * nu + j];
+      if (m >= kb || ((own >> m) & 1u)) d.X[(size_t)rows[m] * lx + j] = x;
     }
   }
 }
@@ -372,19 +372,16 @@ __global__ void __launch_bounds__(SC_THREADS) k_prox_nodes(FastView f) {
   int* rows = reinterpret_cast<int*>(s_bnd + 3 * nt + 2 * nu);
   const int r0 = blockIdx.x * SC_NPB;
   const int nrow = min(SC_NPB, d.n - r0);
-  const int it = *d.iter;
+  const int it = *d.iter - 1;
   if (threadIdx.x < nrow) rows[threadIdx.x] = r0 + threadIdx.x;
-  __syncthreads();
-  FOR_RC(nrow, 7, (W >> 1), m, k) cp16(rec + (size_t)m * f.rec + o.y + 2 * k, ybuf(d, it) + (size_t)rows[m] * W + 2 * k);
+  FOR_RC(nrow, 7, (W >> 1), m, k) cp16(rec + (size_t)m * f.rec + o.y + 2 * k, ybuf(d, it) + (size_t)(r0 + m) * W + 2 * k);
   FOR_RC(nrow, 7, (W >> 1), m, k)
-    cp16(rec + (size_t)m * f.rec + o.ym + 2 * k, ybuf(d, it + 2) + (size_t)rows[m] * W + 2 * k);
-  FOR_RC(nrow, 6, (nu >> 1), m, k) cp16(U + m * nu + 2 * k, d.U + (size_t)rows[m] * nu + 2 * k);
+    cp16(rec + (size_t)m * f.rec + o.ym + 2 * k, ybuf(d, it + 2) + (size_t)(r0 + m) * W + 2 * k);
+  FOR_RC(nrow, 6, (nu >> 1), m, k) cp16(U + m * nu + 2 * k, d.U + (size_t)(r0 + m) * nu + 2 * k);
+  FOR_RC(nrow, 5, (lx >> 1), m, k) cp16(X + m * lx + 2 * k, d.X + (size_t)(r0 + m) * lx + 2 * k);
   if (it > 0) {
-    FOR_RC(nrow, 6, (nu >> 1), m, k) cp16(rec + (size_t)m * f.rec + o.ua + 2 * k, d.Ua + (size_t)rows[m] * nu + 2 * k);
-    FOR_RC(nrow, 5, (lx >> 1), m, k) cp16(rec + (size_t)m * f.rec + o.xa + 2 * k, d.Xa + (size_t)rows[m] * lx + 2 * k);
-  }
-  FOR_RC(nrow, 5, (lx >> 1), m, k) {
-    if (rows[m] >= f.n_branch) cp16(X + m * lx + 2 * k, d.X + (size_t)rows[m] * lx + 2 * k);
+    FOR_RC(nrow, 6, (nu >> 1), m, k) cp16(rec + (size_t)m * f.rec + o.ua + 2 * k, d.Ua + (size_t)(r0 + m) * nu + 2 * k);
+    FOR_RC(nrow, 5, (lx >> 1), m, k) cp16(rec + (size_t)m * f.rec + o.xa + 2 * k, d.Xa + (size_t)(r0 + m) * lx + 2 * k);
   }
   cp_commit();
   for (int i = threadIdx.x; i < nt; i += blockDim.x) {
@@ -395,14 +392,6 @@ __global__ void __launch_bounds__(SC_THREADS) k_prox_nodes(FastView f) {
   for (int i = threadIdx.x; i < nu; i += blockDim.x) {
     s_bnd[3 * nt + i] = d.umin[i];
     s_bnd[3 * nt + nu + i] = d.umax[i];
-  }
-  const NodePtrs np = *d.np;
-  FOR_NT(nrow, m, j) {  // branching rows: x by walk-up; store X
-    if (rows[m] < f.n_branch) {
-      const double x = branch_x(f, np, rows[m], j);
-      X[m * lx + j] = x;
-      d.X[(size_t)rows[m] * lx + j] = x;
-    }
   }
   cp_wait<0>();
   __syncthreads();
@@ -417,20 +406,4 @@ __global__ void __launch_bounds__(SC_THREADS) k_prox_nodes(FastView f) {
             has_next ? d.beta[it + 1] : 0.0, has_next);
 }
 
-}  // namespace wmpc
-
-namespace wmpc {
-// Ebar of branching rows: sum of e_off over the strict ancestors, root first.
-__global__ void k_branch_ebar(const int* __restrict__ anc, int nb, int nu, const double* __restrict__ e_off,
-                              double* ebar) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= nb * nu) return;
-  const int r = idx / nu, k = idx - r * nu;
-  int path[32];
-  int depth = 0;
-  for (int a = anc[r]; a >= 0 && depth < 32; a = anc[a]) path[depth++] = a;
-  double acc = 0.0;
-  for (int i = depth - 1; i >= 0; --i) acc = acc + e_off[(size_t)path[i] * nu + k];
-  ebar[(size_t)r * nu + k] = acc;
-}
 }  // namespace wmpc
