@@ -211,6 +211,19 @@ def ncu_traffic(cfg: str):
         return None
 
 
+def kernel_desc(mode: int, per_iter: int) -> str:
+    if mode == 300:
+        return (f"one APG iteration = CUDA graph of {per_iter} kernels (k_chain_up, k_branch_grp per stage "
+                "group, k_chain_down, k_prox_nodes); timed per iteration")
+    if mode == 310:
+        return f"one APG iteration = CUDA graph of {per_iter} kernels (k_branch_grp per stage group, k_chain_fused)"
+    if mode >= 200:
+        return "k_apg_scan (persistent cooperative kernel)"
+    if mode > 0:
+        return "k_apg_fast (persistent cooperative kernel)"
+    return f"APG iteration = CUDA graph of {per_iter} per-stage kernels (general path)"
+
+
 def run_ours(args):
     world, rank, local = dist_env()
     import torch
@@ -234,7 +247,8 @@ def run_ours(args):
     iters = args.iters
     cfg = SolverConfig(max_iter=iters, tol=1e-30, gamma=gamma, gap_check_every=iters + 1)
     ctx = cache._bind()
-    fast = nat.load().wmpc_fast_path(ctx.h) > 0
+    mode = nat.load().wmpc_fast_path(ctx.h)
+    per_iter = nat.load().wmpc_kernel_launches_per_iteration(ctx.h)
     theta = S.theta_sequence(iters)
     beta = S._beta_table(theta)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
@@ -283,8 +297,7 @@ def run_ours(args):
     achieved = alg_bytes / t_iter / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": ncu_traffic(args.config),
-            "kernel": ("k_apg_fast (persistent cooperative kernel, all iterations of a solve in one launch)"
-                       if fast else f"APG iteration = CUDA graph of {2 * 24 + 1} launches"),
+            "kernel": kernel_desc(mode, per_iter),
             "algorithmic_bytes_per_launch": alg_bytes, "us_per_iteration": t_iter * 1e6,
             "peak_source": peak_src}
 

@@ -52,10 +52,9 @@ struct wmpc_ctx {
   double *Uc = nullptr, *Xc = nullptr, *Uf = nullptr, *Xf = nullptr, *U0 = nullptr, *X0 = nullptr;
   double *wbar = nullptr, *lin = nullptr, *Yc = nullptr;
   double *ys = nullptr, *gv = nullptr, *vv = nullptr, *zbuf = nullptr;
-  double *dk_cur = nullptr, *dk_pc = nullptr, *dk_qc = nullptr, *dk_aff = nullptr;
   double *theta = nullptr, *beta = nullptr;
   int max_iter = 0;
-  int *iter = nullptr, *bad_nu = nullptr, *bad_row = nullptr, *dk_done = nullptr;
+  int *iter = nullptr, *bad_nu = nullptr, *bad_row = nullptr;
   double *part = nullptr, *scal = nullptr;
   int part_blocks = 0;
   double gamma = 0.0;
@@ -65,13 +64,21 @@ struct wmpc_ctx {
   // structured fast path (wmpc_fast.cuh)
   bool fast = false;
   int kstar = 0, nchain = 0, fast_mc = 1, fast_cpc = 1, fast_gs = 1, fast_grid = 0;
-  int fast_nrow = 2, fast_rec = 0, fast_enz = 0, fast_bnz = 0;
+  int fast_nrow = 2, fast_rec = 0, fast_enz = 0, fast_bnz = 0, fast_knz = 0;
   int use_warp = 0, warp_nrow = 2;
   size_t warp_smem = 0;
   int use_scan = 0, scan_work = 0;
   size_t scan_smem = 0;
   // graph-of-kernels scan path (wmpc_scan.cuh)
-  int use_graphk = 0, n_branch = 0;
+  // sparse projector operands (K = (E E^T)^{-1} E by rows, E by columns)
+  int *pj_kp = nullptr, *pj_kc = nullptr, *pj_ecp = nullptr, *pj_ecr = nullptr;
+  double *pj_kv = nullptr, *pj_ecv = nullptr;
+  unsigned long long* dk_mv = nullptr;
+  int* dk_sweeps = nullptr;
+  int use_graphk = 0, n_branch = 0, use_fused = 0, fused_pb = 1, fused_ring_off = 0, fused_threads = 1024;
+  size_t sm_fused = 0;
+  int* store_it = nullptr;
+  int store_it_host = 0;
   double *Lb = nullptr, *Asub = nullptr;
   unsigned char* blob = nullptr;
   int blob16 = 0;
@@ -265,7 +272,37 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
       r = cidx[cptr[r]];
     }
   }
-  const BlobLayout bl = blob_layout(nt, nu, ns, enz, bnz);
+  // sparse projector operands: K = (E E^T)^{-1} E = (E^+)^T (entries below
+  // 1e-14 max|K| are rounding noise of the SVD), E by columns
+  std::vector<int> kp(ns + 1, 0), kc, ecp(nu + 1, 0), ecr;
+  std::vector<double> kv, ecv;
+  {
+    double kmax = 0.0;
+    for (size_t i = 0; i < ept.size(); ++i) kmax = std::max(kmax, std::fabs(ept[i]));
+    for (int i = 0; i < ns; ++i) {
+      for (int k = 0; k < nu; ++k) {
+        const double v = ept[(size_t)k * ns + i];
+        if (std::fabs(v) > 1e-14 * kmax) {
+          kc.push_back(k);
+          kv.push_back(v);
+        }
+      }
+      kp[i + 1] = (int)kc.size();
+    }
+    std::vector<std::vector<std::pair<int, double>>> cols(nu);
+    for (int i = 0; i < ns; ++i)
+      for (int e = ep[i]; e < ep[i + 1]; ++e) cols[ec[e]].push_back({i, ev[e]});
+    for (int k = 0; k < nu; ++k) {
+      for (auto& pr : cols[k]) {
+        ecr.push_back(pr.first);
+        ecv.push_back(pr.second);
+      }
+      ecp[k + 1] = (int)ecr.size();
+    }
+  }
+  const int knz = (int)kc.size();
+  ctx->fast_knz = knz;
+  const BlobLayout bl = blob_layout(nt, nu, ns, knz, enz, bnz);
   const size_t cap = 227 * 1024;
   const size_t up = sizeof(double) * (size_t)nst * (ly + nu + 2 + lx + nu + FAST_MAXNS) + bl.bytes;
   const size_t grp = sizeof(double) * ((size_t)(SC_THREADS / 32) * 256 + 2 * lx + 2 * nu + FAST_MAXNS) + bl.bytes;
@@ -278,10 +315,10 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   {
     double* dp = reinterpret_cast<double*>(blob.data());
     int* ip = reinterpret_cast<int*>(blob.data());
-    for (int j = 0; j < nu; ++j)
-      for (int k = 0; k < ns; ++k) dp[bl.ept + k * nu + j] = ept[(size_t)j * ns + k];
-    for (int e = 0; e < enz; ++e) { dp[bl.ev + e] = ev[e]; ip[bl.ecol + e] = ec[e]; }
-    for (int i = 0; i <= ns; ++i) ip[bl.eptr + i] = ep[i];
+    for (int e = 0; e < knz; ++e) { dp[bl.kv + e] = kv[e]; ip[bl.kcol + e] = kc[e]; }
+    for (int i = 0; i <= ns; ++i) ip[bl.kptr + i] = kp[i];
+    for (int e = 0; e < enz; ++e) { dp[bl.ecv + e] = ecv[e]; ip[bl.ecr + e] = ecr[e]; }
+    for (int k = 0; k <= nu; ++k) ip[bl.ecp + k] = ecp[k];
     for (int e = 0; e < bnz; ++e) {
       dp[bl.bcv + e] = bcv[e]; ip[bl.bcr + e] = bcr[e];
       dp[bl.brv + e] = brv[e]; ip[bl.brc + e] = brc[e];
@@ -352,18 +389,27 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
     std::vector<int> anc(ctx->n, -1);
     for (int r = 0; r < ctx->n; ++r)
       for (int c = cptr[r]; c < cptr[r + 1]; ++c) anc[cidx[c]] = r;
-    std::vector<int> first(nb, -1);
+    // ownership: every branching row is written (U, X, prox) by one chain
+    // below it, balanced so that a chain owns as few ancestors as possible
+    std::vector<int> lo(nb, INT_MAX), hi(nb, -1), cnt(nchain, 0);
     for (int i = 0; i < nchain; ++i) {
       int a = anc[nb + i];
       for (int m = kstar - 1; m >= 0; --m) {
         cpath[(size_t)i * kstar + m] = a;
-        if (first[a] < 0) {
-          first[a] = i;
-          cown[i] |= 1u << m;
-        }
+        lo[a] = std::min(lo[a], i);
+        hi[a] = std::max(hi[a], i + 1);
         a = anc[a];
       }
     }
+    for (int st = kstar - 1; st >= 0; --st)
+      for (int a = off[st]; a < off[st + 1]; ++a) {
+        if (hi[a] < 0) continue;
+        int best = lo[a];
+        for (int i = lo[a]; i < hi[a]; ++i)
+          if (cnt[i] < cnt[best]) best = i;
+        cnt[best]++;
+        cown[best] |= 1u << st;
+      }
   }
   upload_vec(ctx, &ctx->cpath, cpath);
   upload_vec(ctx, &ctx->cown, cown);
@@ -375,6 +421,40 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   CK(cudaFuncSetAttribute(k_branch_grp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grp));
   CK(cudaFuncSetAttribute(k_prox_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox));
   ctx->sm_up = up; ctx->sm_down = down; ctx->sm_grp = grp; ctx->sm_prox = prox;
+  // fused chain kernel (down + prox + next up); pb rows per prox batch
+  {
+    ctx->use_fused = 0;
+    const char* ef = getenv("WMPC_FUSED");
+    const int rp = 2 * ctx->W + nu + lx;
+    auto layout = [&](int pb, int* ring_off) {
+      size_t dbl = (size_t)2 * H * nu + (size_t)H * lx + (size_t)H * FAST_MAXNS + (size_t)pb * 128 + 2 * pb + 2;
+      const size_t ints = ((H + 3) & ~3);
+      const size_t ring = (size_t)2 * pb * rp;
+      if (ring <= (size_t)H * nu) {
+        *ring_off = H * nu;
+        return dbl * sizeof(double) + ints * sizeof(int);
+      }
+      const size_t head = dbl * sizeof(double) + ints * sizeof(int);
+      *ring_off = (int)((head + 15) / 16 * 2);  // in doubles, 16-byte aligned
+      return (size_t)*ring_off * sizeof(double) + ring * sizeof(double);
+    };
+    const bool wide = ctx->nchain >= 2 * ctx->sms;  // many chains: occupancy over per-chain latency
+    int pb = wide ? std::max(1, (H * nu) / (2 * rp)) : 8;
+    int ft = wide ? 512 : 1024;
+    if (const char* e = getenv("WMPC_PB")) pb = std::max(1, atoi(e));
+    if (const char* e = getenv("WMPC_FT")) ft = std::min(1024, std::max(256, atoi(e) / 256 * 256));
+    ctx->fused_threads = ft;
+    pb = std::min(pb, nst);
+    int roff = 0;
+    const size_t fb = layout(pb, &roff);
+    if (ef && ef[0] == '1' && fb <= cap) {  // opt-in: slower than the 4-kernel graph on B200 so far
+      CK(cudaFuncSetAttribute(k_chain_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb));
+      ctx->sm_fused = fb;
+      ctx->fused_pb = pb;
+      ctx->fused_ring_off = roff;
+      ctx->use_fused = 1;
+    }
+  }
   ctx->blob16 = bl.bytes / 16;
   ctx->n_branch = nb;
   ctx->use_graphk = 1;
@@ -584,12 +664,22 @@ void launch_fast_mc(wmpc_ctx* ctx, FastView& f) {
 
 FastView make_fastview(wmpc_ctx* ctx, int count);
 
-int graphk_kernels(const wmpc_ctx* ctx) { return 3 + (int)ctx->gk_groups.size(); }
+int graphk_kernels(const wmpc_ctx* ctx) {
+  const int g = (int)ctx->gk_groups.size();
+  if (ctx->use_fused) return g + 1 + (g == 0 ? 1 : 0);
+  return 3 + g + (g == 0 ? 1 : 0);
+}
 
 // One APG iteration of the graph-of-kernels path, enqueued on ctx->stream.
 void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
   cudaStream_t st = ctx->stream;
   const int nc = ctx->nchain;
+  if (ctx->gk_groups.empty()) k_advance<<<1, 32, 0, st>>>(ctx->iter);  // else the first group kernel counts
+  if (ctx->use_fused) {  // up pass of iteration 0 runs in wmpc_apg_begin
+    for (const auto& g : ctx->gk_groups) k_branch_grp<<<g.second, SC_THREADS, ctx->sm_grp, st>>>(f, g.first);
+    k_chain_fused<<<nc, ctx->fused_threads, ctx->sm_fused, st>>>(f);
+    return;
+  }
   k_chain_up<<<nc, SC_THREADS, ctx->sm_up, st>>>(f);
   for (const auto& g : ctx->gk_groups) k_branch_grp<<<g.second, SC_THREADS, ctx->sm_grp, st>>>(f, g.first);
   k_chain_down<<<nc, SC_THREADS, ctx->sm_down, st>>>(f);
@@ -615,6 +705,8 @@ void capture_graphk(wmpc_ctx* ctx) {
 }
 
 void launch_graphk(wmpc_ctx* ctx, int count) {
+  ctx->store_it_host = ctx->it_host + count - 1;  // U, X of the chunk's last iteration reach HBM
+  CK(cudaMemcpyAsync(ctx->store_it, &ctx->store_it_host, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   int i = 0;
   for (; i + 8 <= count; i += 8) CK(cudaGraphLaunch(ctx->gk_exec8, ctx->stream));
   for (; i < count; ++i) CK(cudaGraphLaunch(ctx->gk_exec1, ctx->stream));
@@ -633,6 +725,7 @@ FastView make_fastview(wmpc_ctx* ctx, int count) {
   f.aux = ctx->aux;
   f.e_nnz = ctx->fast_enz;
   f.b_nnz = ctx->fast_bnz;
+  f.k_nnz = ctx->fast_knz;
   f.inv_2c = 1.0 / (2.0 * ctx->w_c);
   f.inv_gamma = 1.0 / ctx->gamma;
   f.cpc = ctx->fast_cpc;
@@ -651,6 +744,9 @@ FastView make_fastview(wmpc_ctx* ctx, int count) {
   f.gi_ptr = ctx->gi_ptr; f.gi_item = ctx->gi_item; f.gi_w = ctx->gi_w;
   f.cpath = ctx->cpath;
   f.cown = ctx->cown;
+  f.store_it = ctx->store_it;
+  f.pb = ctx->fused_pb;
+  f.ring_off = ctx->fused_ring_off;
   f.work_doubles = ctx->scan_work;
   return f;
 }
@@ -714,11 +810,12 @@ void free_all(wmpc_ctx* c) {
                   c->Lam, c->Mb, c->Mf, c->E, c->e_pinv, c->econ, c->tmp, c->demand, c->Ed, c->xmin, c->xmax, c->xsafe, c->umin, c->umax,
                   c->p, c->q, c->Y[0], c->Y[1], c->Y[2], c->U, c->X, c->Ua, c->Xa, c->Uc, c->Xc,
                   c->Uf, c->Xf, c->U0, c->X0, c->wbar, c->lin, c->Yc, c->ys, c->gv, c->vv, c->zbuf,
-                  c->dk_cur, c->dk_pc, c->dk_qc, c->dk_aff, c->theta, c->beta, c->iter, c->bad_nu,
-                  c->bad_row, c->dk_done, c->part, c->scal, c->d_np, c->chain_node,
+                  c->theta, c->beta, c->iter, c->bad_nu,
+                  c->bad_row, c->part, c->scal, c->d_np, c->chain_node,
                   c->bc_ptr, c->bc_row, c->br_ptr, c->br_col, c->off_dev, c->bc_val, c->br_val,
                   c->e_ptr, c->e_col, c->e_val, c->aux,
-                  c->Lb, c->Asub, c->blob, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
+                  c->Lb, c->Asub, c->blob, c->store_it, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
+                  c->pj_ecv, c->dk_mv, c->dk_sweeps, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
                   c->prof};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -783,10 +880,8 @@ int wmpc_create(const wmpc_dims* dims, wmpc_ctx** out) {
     dalloc(ctx, &ctx->Yc, n * ctx->ly);
     dalloc(ctx, &ctx->ys, n * W); dalloc(ctx, &ctx->gv, n * W); dalloc(ctx, &ctx->vv, n * W);
     dalloc(ctx, &ctx->zbuf, n * std::max(W, (size_t)ctx->P));
-    dalloc(ctx, &ctx->dk_cur, n * nu); dalloc(ctx, &ctx->dk_pc, n * nu); dalloc(ctx, &ctx->dk_qc, n * nu);
-    dalloc(ctx, &ctx->dk_aff, n * nu);
     dalloc(ctx, &ctx->iter, 1); dalloc(ctx, &ctx->bad_nu, 1); dalloc(ctx, &ctx->bad_row, 1);
-    dalloc(ctx, &ctx->dk_done, 1);
+    dalloc(ctx, &ctx->store_it, 1);
     dalloc(ctx, &ctx->d_np, 1);
     ctx->part_blocks = 1184;
     dalloc(ctx, &ctx->part, (size_t)ctx->part_blocks * 4);
@@ -895,6 +990,40 @@ int wmpc_set_structure(wmpc_ctx* ctx, const double* A, const double* B, const do
       ARG(E && e_pinv, "E and e_pinv required when n_mixing > 0");
       h2d(ctx, ctx->E, E, sizeof(double) * ns * nu);
       h2d(ctx, ctx->e_pinv, e_pinv, sizeof(double) * nu * ns);
+    }
+    if (ns > 0) {  // sparse projector for the certificate's Dykstra (and the graph kernels)
+      std::vector<int> kp(ns + 1, 0), kc, ecp(nu + 1, 0), ecr;
+      std::vector<double> kv, ecv;
+      double kmax = 0.0;
+      for (size_t i = 0; i < (size_t)nu * ns; ++i) kmax = std::max(kmax, std::fabs(e_pinv[i]));
+      for (int i = 0; i < ns; ++i) {
+        for (int k = 0; k < nu; ++k) {
+          const double v = e_pinv[(size_t)k * ns + i];
+          if (std::fabs(v) > 1e-14 * kmax) {
+            kc.push_back(k);
+            kv.push_back(v);
+          }
+        }
+        kp[i + 1] = (int)kc.size();
+      }
+      for (int k = 0; k < nu; ++k) {
+        for (int i = 0; i < ns; ++i)
+          if (E[(size_t)i * nu + k] != 0.0) {
+            ecr.push_back(i);
+            ecv.push_back(E[(size_t)i * nu + k]);
+          }
+        ecp[k + 1] = (int)ecr.size();
+      }
+      if (kc.empty()) { kc.push_back(0); kv.push_back(0.0); }
+      if (ecr.empty()) { ecr.push_back(0); ecv.push_back(0.0); }
+      upload_vec(ctx, &ctx->pj_kp, kp);
+      upload_vec(ctx, &ctx->pj_kc, kc);
+      upload_vec(ctx, &ctx->pj_kv, kv);
+      upload_vec(ctx, &ctx->pj_ecp, ecp);
+      upload_vec(ctx, &ctx->pj_ecr, ecr);
+      upload_vec(ctx, &ctx->pj_ecv, ecv);
+      if (!ctx->dk_mv) dalloc(ctx, &ctx->dk_mv, 512);
+      if (!ctx->dk_sweeps) dalloc(ctx, &ctx->dk_sweeps, 1);
     }
     sync(ctx);
     configure_fast(ctx, B, E, e_pinv, T, D, cptr, cidx);
@@ -1020,7 +1149,7 @@ int wmpc_kernel_launches_per_iteration(const wmpc_ctx* ctx) {
 
 int wmpc_fast_path(const wmpc_ctx* ctx) {
   if (!ctx || !ctx->fast) return 0;
-  if (ctx->use_graphk) return 300;
+  if (ctx->use_graphk) return ctx->use_fused ? 310 : 300;
   if (ctx->use_scan) return 200 + ctx->fast_mc;
   return ctx->use_warp ? 100 + ctx->warp_nrow : ctx->fast_mc;
 }
@@ -1215,7 +1344,15 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
     ctx->it_host = 0;
     sync(ctx);
     if (ctx->fast) {
-      if (ctx->use_graphk) capture_graphk(ctx);
+      if (ctx->use_graphk) {
+        capture_graphk(ctx);
+        if (ctx->use_fused) {  // up pass of iteration 0 (Yc = 0)
+          FastView f = make_fastview(ctx, 1);
+          k_chain_up<<<ctx->nchain, SC_THREADS, ctx->sm_up, ctx->stream>>>(f);
+          ctx->launches++;
+          check_launch(ctx);
+        }
+      }
       return WMPC_OK;  // persistent kernel: no graph
     }
     if (ctx->gexec && ctx->graph_gamma == gamma) return WMPC_OK;  // captured iteration still valid
@@ -1330,30 +1467,18 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
       ctx->launches++;
       k_clip_inputs<<<grid_for(nU), 256, 0, ctx->stream>>>(d, ctx->Ua, ctx->Uf);
     } else {
-      CK(cudaMemcpyAsync(ctx->dk_cur, ctx->Ua, sizeof(double) * nU, cudaMemcpyDeviceToDevice, ctx->stream));
-      CK(cudaMemsetAsync(ctx->dk_pc, 0, sizeof(double) * nU, ctx->stream));
-      CK(cudaMemsetAsync(ctx->dk_qc, 0, sizeof(double) * nU, ctx->stream));
-      CK(cudaMemsetAsync(ctx->dk_done, 0, sizeof(int), ctx->stream));
       int nb0 = grid_for(nU);
       ctx->launches++;
       k_absmax_partial<<<nb0, 256, 0, ctx->stream>>>(ctx->Ua, nU, ctx->part);
       ctx->launches++;
       k_dyk_tol<<<1, 256, 0, ctx->stream>>>(ctx->part, nb0, ctx->scal + 8);
-      int nb = std::min(ctx->part_blocks, std::max(1, (ctx->n + 7) / 8));
-      for (int sweep = 0; sweep < 500; ++sweep) {
-        ctx->launches++;
-        k_dyk_sweep<<<nb, 256, 0, ctx->stream>>>(d, ctx->dk_cur, ctx->dk_pc, ctx->dk_qc, ctx->dk_aff,
-                                                  ctx->dk_done, ctx->part);
-        ctx->launches++;
-        k_dyk_finish<<<1, 256, 0, ctx->stream>>>(ctx->part, nb, ctx->scal + 8, ctx->dk_done);
-        if (sweep % 16 == 15) {
-          int done = 0;
-          d2h(ctx, &done, ctx->dk_done, sizeof(int));
-          sync(ctx);
-          if (done) break;
-        }
-      }
-      CK(cudaMemcpyAsync(ctx->Uf, ctx->dk_cur, sizeof(double) * nU, cudaMemcpyDeviceToDevice, ctx->stream));
+      DykOps po{ctx->pj_kp, ctx->pj_kc, ctx->pj_ecp, ctx->pj_ecr, ctx->pj_kv, ctx->pj_ecv};
+      CK(cudaMemsetAsync(ctx->dk_mv, 0, sizeof(unsigned long long) * 512, ctx->stream));
+      const int nbw = (ctx->n + 7) / 8;
+      ctx->launches += 3;
+      k_dyk_warp<<<nbw, 256, 0, ctx->stream>>>(d, po, ctx->Ua, nullptr, ctx->dk_mv, ctx->dk_sweeps, 500, 1);
+      k_dyk_count<<<1, 32, 0, ctx->stream>>>(ctx->dk_mv, 500, ctx->scal + 8, ctx->dk_sweeps);
+      k_dyk_warp<<<nbw, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 2);
     }
     // 2. rollout (problem.py:207-218)
     for (int s = 0; s < ctx->H; ++s) {
@@ -1482,13 +1607,22 @@ int wmpc_profile_fast(wmpc_ctx* ctx, int count, uint64_t* counters, int cap) {
       return WMPC_E_STATE;
     }
     ARG(count >= 1 && ctx->it_host + count <= ctx->max_iter, "bad count");
-    if (!ctx->prof) dalloc(ctx, &ctx->prof, (size_t)ctx->fast_grid * P_N);
+    const size_t slots = (size_t)std::max(ctx->fast_grid, ctx->nchain) * P_N;
+    if (!ctx->prof) dalloc(ctx, &ctx->prof, slots);
+    CK(cudaMemsetAsync(ctx->prof, 0, sizeof(uint64_t) * slots, ctx->stream));
     ctx->prof_on = 1;
-    launch_fast(ctx, count);
+    if (ctx->use_graphk) {  // direct launches with the clock counters on
+      ctx->store_it_host = ctx->it_host + count - 1;
+      CK(cudaMemcpyAsync(ctx->store_it, &ctx->store_it_host, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+      FastView f = make_fastview(ctx, 1);
+      for (int i = 0; i < count; ++i) enqueue_graphk_iteration(ctx, f);
+    } else {
+      launch_fast(ctx, count);
+    }
     ctx->prof_on = 0;
     ctx->it_host += count;
     check_launch(ctx);
-    size_t nvals = std::min((size_t)cap, (size_t)ctx->fast_grid * P_N);
+    size_t nvals = std::min((size_t)cap, slots);
     d2h(ctx, counters, ctx->prof, sizeof(uint64_t) * nvals);
     sync(ctx);
     return WMPC_OK;

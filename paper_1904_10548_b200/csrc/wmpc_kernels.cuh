@@ -464,60 +464,6 @@ __global__ void k_gconj_partial(DevView d, const double* __restrict__ y, double 
   if (threadIdx.x == 0) part[2 * blockIdx.x + 1] = t;
 }
 
-// ---------------------------------------------------------------------------
-// Dykstra restoration sweep (problem.py:239-249), one warp per node; the
-// global stopping test is evaluated by k_dyk_finish between sweeps.
-// ---------------------------------------------------------------------------
-__global__ void k_dyk_sweep(DevView d, double* cur, double* pc, double* qc, double* aff,
-                            const int* done, double* part) {
-  __shared__ double sh[32];
-  if (*done) return;
-  const int nu = d.nu, ns = d.ns;
-  int lane = threadIdx.x & 31;
-  int wpb = blockDim.x >> 5;
-  double moved = 0.0;
-  for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < d.n; r += gridDim.x * wpb) {
-    double* c = cur + (size_t)r * nu;
-    double* P = pc + (size_t)r * nu;
-    double* Q = qc + (size_t)r * nu;
-    double* A = aff + (size_t)r * nu;
-    for (int j = lane; j < nu; j += 32) A[j] = c[j] + P[j];
-    __syncwarp();
-    // t_i = A.E_i + shift_i ;  A_j -= sum_i t_i pinv[j][i]
-    double tl[32];  // ns <= 32 (checked at wmpc_create)
-    for (int i = 0; i < ns; ++i) {
-      double t = 0.0;
-      for (int j = lane; j < nu; j += 32) t += A[j] * d.E[(size_t)i * nu + j];
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      tl[i] = t + d.np->shift[(size_t)r * ns + i];
-    }
-    __syncwarp();
-    for (int j = lane; j < nu; j += 32) {
-      double corr = 0.0;
-      for (int i = 0; i < ns; ++i) corr += tl[i] * d.e_pinv[(size_t)j * ns + i];
-      double a = A[j] - corr;
-      double pn = c[j] + P[j] - a;
-      double nx = np_clip(a + Q[j], d.umin[j], d.umax[j]);
-      Q[j] = a + Q[j] - nx;
-      P[j] = pn;
-      moved = np_max(moved, fabs(nx - c[j]));
-      c[j] = nx;
-    }
-    __syncwarp();
-  }
-  moved = block_reduce<1>(moved, sh);
-  if (threadIdx.x == 0) part[blockIdx.x] = moved;
-}
-
-__global__ void k_dyk_finish(const double* part, int nb, const double* tol, int* done) {
-  __shared__ double sh[32];
-  if (*done) return;
-  double v = -INFINITY;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) v = np_max(v, part[b]);
-  v = block_reduce<1>(v, sh);
-  if (threadIdx.x == 0 && v <= *tol) *done = 1;
-}
-
 __global__ void k_absmax_partial(const double* __restrict__ a, size_t len, double* part) {
   __shared__ double sh[32];
   double m = 0.0;
@@ -702,4 +648,103 @@ __global__ void k_join_primal(int n, int nu, int nt, int lx, const double* __res
   }
 }
 
+}  // namespace wmpc
+
+namespace wmpc {
+// Dykstra feasibility restoration (problem.py:221-250), one warp per node,
+// all sweeps in one launch. The reference stops every node at the first sweep
+// whose global max movement is <= tol, so it runs twice: pass 1 runs all
+// sweeps and atomically maxes each sweep's movement into mv[sweep] (a node at
+// an exact fixed point stops contributing); pass 2 reruns each node for the
+// global sweep count and writes the result. The affine projection is
+// P(a) - E^+ shift_r with the sparse form P a = a - E^T (K a), K = (E E^T)^{-1} E.
+struct DykOps {
+  const int *kp, *kc, *ecp, *ecr;
+  const double *kv, *ecv;
+};
+constexpr int DYK_MAXQ = 4;  // nu <= 128
+__global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const double* __restrict__ u_in,
+                                                  double* __restrict__ u_out, unsigned long long* mv,
+                                                  const int* sweeps_in, int max_sweeps, int pass) {
+  __shared__ double sA[8][128];
+  __shared__ double sT[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + warp;
+  if (r >= d.n) return;
+  const int nu = d.nu, ns = d.ns;
+  const int nsw = pass == 1 ? max_sweeps : *sweeps_in;
+  double cur[DYK_MAXQ], pc[DYK_MAXQ], qc[DYK_MAXQ], c[DYK_MAXQ], lo[DYK_MAXQ], hi[DYK_MAXQ];
+  const double* sh = d.np->shift + (size_t)r * ns;
+#pragma unroll
+  for (int q = 0; q < DYK_MAXQ; ++q) {
+    const int k = lane + 32 * q;
+    const bool ok = k < nu;
+    cur[q] = ok ? u_in[(size_t)r * nu + k] : 0.0;
+    pc[q] = 0.0;
+    qc[q] = 0.0;
+    double e = 0.0;
+    if (ok)
+      for (int i = 0; i < ns; ++i) e = fma(d.e_pinv[(size_t)k * ns + i], sh[i], e);
+    c[q] = e;
+    lo[q] = ok ? d.umin[k] : 0.0;
+    hi[q] = ok ? d.umax[k] : 0.0;
+  }
+  for (int s = 0; s < nsw; ++s) {
+#pragma unroll
+    for (int q = 0; q < DYK_MAXQ; ++q) {
+      const int k = lane + 32 * q;
+      if (k < nu) sA[warp][k] = cur[q] + pc[q];
+    }
+    __syncwarp();
+    if (lane < ns) {
+      double t = 0.0;
+      for (int e = po.kp[lane]; e < po.kp[lane + 1]; ++e) t = fma(po.kv[e], sA[warp][po.kc[e]], t);
+      sT[warp][lane] = t;
+    }
+    __syncwarp();
+    double moved = 0.0;
+    bool same = true;
+#pragma unroll
+    for (int q = 0; q < DYK_MAXQ; ++q) {
+      const int k = lane + 32 * q;
+      if (k < nu) {
+        double corr = 0.0;
+        for (int e = po.ecp[k]; e < po.ecp[k + 1]; ++e) corr = fma(po.ecv[e], sT[warp][po.ecr[e]], corr);
+        const double A = sA[warp][k];
+        const double a = A - (corr + c[q]);
+        const double pn = A - a;  // cur + pc - aff
+        const double nx = np_clip(a + qc[q], lo[q], hi[q]);
+        const double qn = (a + qc[q]) - nx;
+        moved = np_max(moved, fabs(nx - cur[q]));
+        same &= nx == cur[q] && pn == pc[q] && qn == qc[q];
+        pc[q] = pn;
+        qc[q] = qn;
+        cur[q] = nx;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) moved = np_max(moved, __shfl_xor_sync(0xffffffffu, moved, o));
+    if (pass == 1 && lane == 0 && moved > 0.0) atomicMax(mv + s, (unsigned long long)__double_as_longlong(moved));
+    if (__all_sync(0xffffffffu, same)) break;  // exact fixed point: every later sweep repeats it
+    __syncwarp();
+  }
+  if (pass == 2) {
+#pragma unroll
+    for (int q = 0; q < DYK_MAXQ; ++q) {
+      const int k = lane + 32 * q;
+      if (k < nu) u_out[(size_t)r * nu + k] = cur[q];
+    }
+  }
+}
+
+// Global sweep count: first sweep whose max movement is <= tol (or all).
+__global__ void k_dyk_count(const unsigned long long* mv, int max_sweeps, const double* tol, int* sweeps) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int k = max_sweeps;
+  for (int s = 0; s < max_sweeps; ++s)
+    if (__longlong_as_double((long long)mv[s]) <= *tol) {
+      k = s + 1;
+      break;
+    }
+  *sweeps = k;
+}
 }  // namespace wmpc

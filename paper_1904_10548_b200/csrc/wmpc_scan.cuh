@@ -30,23 +30,28 @@ constexpr int SC_NPB = 4;    // nodes per CTA in k_prox_nodes
 constexpr int SC_MAXK = 30;  // max branching depth (bits of cown)
 
 // ---------------------------------------------------------------- operators
-// Blob layout (doubles, then ints): [E^+ transposed ns x nu | E vals | B CSC vals
-// | B CSR vals | pad | E ptr | E cols | B CSC ptr | B CSC rows | B CSR ptr | B CSR cols]
+// The projector onto null(E) is applied as P z = z - E^T (K z) with
+// K = (E E^T)^{-1} E = (E^+)^T stored sparse (for the Barcelona network E E^T
+// is diagonal, so K has the 56 nonzeros of E: ~130 flops per row instead of
+// the ~2,000 of a dense E^+ pass).
+// Blob layout (doubles, then ints): [K vals | E CSC vals | B CSC vals | B CSR vals
+// | pad | K ptr | K cols | E CSC ptr | E CSC rows | B CSC ptr | B CSC rows | B CSR ptr | B CSR cols]
 struct BlobLayout {
-  int ept, ev, bcv, brv, dbl_end, eptr, ecol, bcp, bcr, brp, brc, bytes;
+  int kv, ecv, bcv, brv, dbl_end, kptr, kcol, ecp, ecr, bcp, bcr, brp, brc, bytes;
 };
-__host__ __device__ inline BlobLayout blob_layout(int nt, int nu, int ns, int enz, int bnz) {
+__host__ __device__ inline BlobLayout blob_layout(int nt, int nu, int ns, int knz, int enz, int bnz) {
   BlobLayout b;
-  b.ept = 0;
-  b.ev = b.ept + nu * ns;
-  b.bcv = b.ev + enz;
+  b.kv = 0;
+  b.ecv = b.kv + knz;
+  b.bcv = b.ecv + enz;
   b.brv = b.bcv + bnz;
   b.dbl_end = b.brv + bnz;
   b.dbl_end += b.dbl_end & 1;
-  int ib = 2 * b.dbl_end;  // int offsets
-  b.eptr = ib;
-  b.ecol = b.eptr + ns + 1;
-  b.bcp = b.ecol + enz;
+  b.kptr = 2 * b.dbl_end;  // int offsets
+  b.kcol = b.kptr + ns + 1;
+  b.ecp = b.kcol + knz;
+  b.ecr = b.ecp + nu + 1;
+  b.bcp = b.ecr + enz;
   b.bcr = b.bcp + nu + 1;
   b.brp = b.bcr + bnz;
   b.brc = b.brp + nt + 1;
@@ -62,16 +67,18 @@ __device__ __forceinline__ void issue_blob(const FastView& f, void* dst) {
 }
 __device__ __forceinline__ Ops blob_ops(const FastView& f, const void* sp) {
   const DevView& d = f.d;
-  const BlobLayout b = blob_layout(d.nt, d.nu, d.ns, f.e_nnz, f.b_nnz);
+  const BlobLayout b = blob_layout(d.nt, d.nu, d.ns, f.k_nnz, f.e_nnz, f.b_nnz);
   const double* dp = reinterpret_cast<const double*>(sp);
   const int* ip = reinterpret_cast<const int*>(sp);
   Ops op{};
-  op.ep = dp + b.ept;
-  op.eval = dp + b.ev;
+  op.kval = dp + b.kv;
+  op.ecv = dp + b.ecv;
   op.bcv = dp + b.bcv;
   op.brv = dp + b.brv;
-  op.eptr = ip + b.eptr;
-  op.ecol = ip + b.ecol;
+  op.kptr = ip + b.kptr;
+  op.kcol = ip + b.kcol;
+  op.ecp = ip + b.ecp;
+  op.ecr = ip + b.ecr;
   op.bcp = ip + b.bcp;
   op.bcr = ip + b.bcr;
   op.brp = ip + b.brp;
@@ -79,31 +86,29 @@ __device__ __forceinline__ Ops blob_ops(const FastView& f, const void* sp) {
   return op;
 }
 
-// out[m] = P in[m] for m < rows (stride nu; in place allowed); T scratch
-// rows x FAST_MAXNS. 2 barriers.
-__device__ __forceinline__ void proj_rows(const DevView& d, const Ops& op, const double* in, double* out,
-                                          double* T, int rows) {
+// out[m*so + k] = (P in[m])_k for m < rows (rows of stride si; in place
+// allowed). T scratch rows x FAST_MAXNS. 2 barriers.
+__device__ __forceinline__ void proj_rows_s(const DevView& d, const Ops& op, const double* in, int si, double* out,
+                                            int so, double* T, int rows) {
   const int nu = d.nu, ns = d.ns;
   FOR_RC(rows, 5, ns, m, i) {
+    const double* z = in + (size_t)m * si;
     double v = 0.0;
-    for (int e = op.eptr[i]; e < op.eptr[i + 1]; ++e) v = fma(op.eval[e], in[m * nu + op.ecol[e]], v);
+    for (int e = op.kptr[i]; e < op.kptr[i + 1]; ++e) v = fma(op.kval[e], z[op.kcol[e]], v);
     T[m * FAST_MAXNS + i] = v;
   }
   __syncthreads();
   FOR_NU(rows, m, k) {
     const double* tm = T + m * FAST_MAXNS;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int i = 0;
-    for (; i + 3 < ns; i += 4) {
-      a0 = fma(op.ep[i * nu + k], tm[i], a0);
-      a1 = fma(op.ep[(i + 1) * nu + k], tm[i + 1], a1);
-      a2 = fma(op.ep[(i + 2) * nu + k], tm[i + 2], a2);
-      a3 = fma(op.ep[(i + 3) * nu + k], tm[i + 3], a3);
-    }
-    for (; i < ns; ++i) a0 = fma(op.ep[i * nu + k], tm[i], a0);
-    out[m * nu + k] = in[m * nu + k] - ((a0 + a1) + (a2 + a3));
+    double c = 0.0;
+    for (int e = op.ecp[k]; e < op.ecp[k + 1]; ++e) c = fma(op.ecv[e], tm[op.ecr[e]], c);
+    out[(size_t)m * so + k] = in[(size_t)m * si + k] - c;
   }
   __syncthreads();
+}
+__device__ __forceinline__ void proj_rows(const DevView& d, const Ops& op, const double* in, double* out,
+                                          double* T, int rows) {
+  proj_rows_s(d, op, in, d.nu, out, d.nu, T, rows);
 }
 
 __device__ __forceinline__ int chain_row(const FastView& f, int t, int ci) { return f.n_branch + t * f.nchain + ci; }
@@ -122,7 +127,6 @@ __global__ void __launch_bounds__(SC_THREADS) k_chain_up(FastView f) {
   double* S = WB + (size_t)nst * lx;
   double* T = S + (size_t)nst * nu;
   void* bl = T + (size_t)nst * FAST_MAXNS;
-  if (ci == 0 && threadIdx.x == 0) *d.iter += 1;  // this iteration's number + 1 (read by k_prox_nodes)
   const NodePtrs np = *d.np;
   issue_blob(f, bl);
   FOR_RC(nst, 7, (ly >> 1), t, k) cp16(rec + (size_t)t * ra + 2 * k, d.Yc + (size_t)chain_row(f, t, ci) * ly + 2 * k);
@@ -187,6 +191,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0) {
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly;
   const int r = r0 + blockIdx.x;
   constexpr int NW = SC_THREADS / 32;
+  if (r0 == f.n_branch - gridDim.x && blockIdx.x == 0 && threadIdx.x == 0) *d.iter += 1;  // first kernel of the iteration
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* part = reinterpret_cast<double*>(smem_raw);  // NW x 256: [s1 64 | s2 64 | su 128]
   double* W1 = part + NW * 256;  // lx
@@ -312,11 +317,11 @@ __global__ void __launch_bounds__(SC_THREADS) k_chain_down(FastView f) {
     }
   }
   __syncthreads();
-  // projector over rows of stride rd: E pass then E^+ pass
+  // u = e_off + P z (in the z slot)
   FOR_RC(nr, 5, d.ns, m, i) {
     const double* z = rec + (size_t)m * rd;
     double v = 0.0;
-    for (int e = op.eptr[i]; e < op.eptr[i + 1]; ++e) v = fma(op.eval[e], z[op.ecol[e]], v);
+    for (int e = op.kptr[i]; e < op.kptr[i + 1]; ++e) v = fma(op.kval[e], z[op.kcol[e]], v);
     T[m * FAST_MAXNS + i] = v;
   }
   __syncthreads();
@@ -324,17 +329,9 @@ __global__ void __launch_bounds__(SC_THREADS) k_chain_down(FastView f) {
   FOR_NU(nr, m, k) {
     double* R = rec + (size_t)m * rd;
     const double* tm = T + m * FAST_MAXNS;
-    const int ns = d.ns;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int i = 0;
-    for (; i + 3 < ns; i += 4) {
-      a0 = fma(op.ep[i * nu + k], tm[i], a0);
-      a1 = fma(op.ep[(i + 1) * nu + k], tm[i + 1], a1);
-      a2 = fma(op.ep[(i + 2) * nu + k], tm[i + 2], a2);
-      a3 = fma(op.ep[(i + 3) * nu + k], tm[i + 3], a3);
-    }
-    for (; i < ns; ++i) a0 = fma(op.ep[i * nu + k], tm[i], a0);
-    const double u = R[nu + k] + (R[k] - ((a0 + a1) + (a2 + a3)));
+    double c = 0.0;
+    for (int e = op.ecp[k]; e < op.ecp[k + 1]; ++e) c = fma(op.ecv[e], tm[op.ecr[e]], c);
+    const double u = R[nu + k] + (R[k] - c);
     R[k] = u;
     if (m >= kb || ((own >> m) & 1u)) d.U[(size_t)rows[m] * nu + k] = u;
   }
@@ -403,7 +400,223 @@ __global__ void __launch_bounds__(SC_THREADS) k_prox_nodes(FastView f) {
   op.umax = s_bnd + 3 * nt + nu;
   const bool has_next = it + 1 < f.max_iter;
   prox_rows(f, op, rows, nrow, U, nu, X, lx, rec, f.rec, rec + o.lin, f.rec, stp, it, d.beta[it], d.theta[it],
-            has_next ? d.beta[it + 1] : 0.0, has_next);
+            has_next ? d.beta[it + 1] : 0.0, has_next, o);
+}
+
+
+// ---------------------------------------------------------------- k_chain_fused
+// One CTA per chain, three phases in shared memory:
+//   D  down pass of iteration it over the root path (as k_chain_down) -> u, x
+//   P  Moreau prox of the chain rows and of the ancestors this chain owns
+//      (records streamed through a 2-slot cp.async ring, pb rows per batch);
+//      the next collapsed dual Yc overwrites u, x in place
+//   U  up pass of iteration it+1 on the chain's Yc (as k_chain_up) -> L, wbar, Asub
+// so per chain node only y, y_prev, Ua, Xa, L, e_off, g, R move through HBM.
+// Shared (doubles): Z H x nu (L->z->u->Yu->a), E H x nu (e_off->Bu->ring->R->S),
+// G H x lx (g->x->Yx->wbar), T H x FAST_MAXNS, d2 pb x 128, stp 2pb, [ring], rows H.
+__device__ __forceinline__ void fused_issue(const FastView& f, double* slot, int rp, const int* grow, int bn, int it) {
+  const DevView& d = f.d;
+  const int W = d.W, nu = d.nu, lx = d.lx;
+  const double* y = ybuf(d, it);
+  const double* ym = ybuf(d, it + 2);
+  FOR_RC(bn, 7, (W >> 1), m, k) cp16(slot + (size_t)m * rp + 2 * k, y + (size_t)grow[m] * W + 2 * k);
+  FOR_RC(bn, 7, (W >> 1), m, k) cp16(slot + (size_t)m * rp + W + 2 * k, ym + (size_t)grow[m] * W + 2 * k);
+  if (it > 0) {
+    FOR_RC(bn, 6, (nu >> 1), m, k) cp16(slot + (size_t)m * rp + 2 * W + 2 * k, d.Ua + (size_t)grow[m] * nu + 2 * k);
+    FOR_RC(bn, 5, (lx >> 1), m, k) cp16(slot + (size_t)m * rp + 2 * W + nu + 2 * k, d.Xa + (size_t)grow[m] * lx + 2 * k);
+  }
+}
+__device__ __forceinline__ void fused_batch(int b, int n_own, unsigned own, int kb, int nst, int pb, int& m0, int& bn) {
+  if (b < n_own) {
+    unsigned w = own;
+    for (int i = 0; i < b; ++i) w &= w - 1;
+    m0 = __ffs(w) - 1;
+    bn = 1;
+  } else {
+    const int c = b - n_own;
+    m0 = kb + c * pb;
+    bn = min(pb, nst - c * pb);
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_chain_fused(FastView f) {
+  const DevView& d = f.d;
+  const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly, W = d.W, ns = d.ns;
+  const int kb = f.kstar, H = d.H, nst = H - kb, ci = blockIdx.x, pb = f.pb;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* Z = reinterpret_cast<double*>(smem_raw);
+  double* E = Z + (size_t)H * nu;
+  double* G = E + (size_t)H * nu;
+  double* T = G + (size_t)H * lx;
+  double* d2 = T + (size_t)H * FAST_MAXNS;
+  double* stp = d2 + (size_t)pb * 128;
+  double* ring = reinterpret_cast<double*>(smem_raw) + f.ring_off;
+  const int rp = 2 * W + nu + lx;
+  int* rows = reinterpret_cast<int*>(stp + 2 * pb + 2);
+  const NodePtrs np = *d.np;
+  const Ops op = blob_ops(f, f.blob);
+  const int it = *d.iter - 1;
+  const bool has_next = it + 1 < f.max_iter;
+  const bool store = it == *f.store_it;
+  const unsigned own = kb > 0 ? f.cown[ci] : 0u;
+  unsigned long long* pc = f.prof && threadIdx.x == 0 ? f.prof + (size_t)ci * P_N : nullptr;
+  unsigned long long t0 = pc ? clk() : 0, tstart = t0;
+#define FSTEP(slot)                     \
+  if (pc) {                              \
+    const unsigned long long t_ = clk(); \
+    pc[slot] += t_ - t0;                 \
+    t0 = t_;                             \
+  }
+  if (threadIdx.x < H) {
+    const int m = threadIdx.x;
+    rows[m] = m < kb ? f.cpath[(size_t)ci * kb + m] : chain_row(f, m - kb, ci);
+  }
+  __syncthreads();
+  // ---- D: down pass
+  FOR_RC(H, 6, (nu >> 1), m, k) cp16(Z + (size_t)m * nu + 2 * k, f.Lb + (size_t)rows[m] * nu + 2 * k);
+  FOR_RC(H, 6, (nu >> 1), m, k) cp16(E + (size_t)m * nu + 2 * k, np.e_off + (size_t)rows[m] * nu + 2 * k);
+  FOR_RC(H, 5, (lx >> 1), m, k) cp16(G + (size_t)m * lx + 2 * k, np.g + (size_t)rows[m] * lx + 2 * k);
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  FSTEP(1);
+  if (threadIdx.x < nu) {
+    const int k = threadIdx.x;
+    double ls = 0.0, es = d.q[k];
+    for (int m = 0; m < H; ++m) {
+      const double l = Z[m * nu + k];
+      ls = m == 0 ? l : ls + l;
+      Z[m * nu + k] = es - ls;
+      es = es + E[m * nu + k];
+    }
+  }
+  __syncthreads();
+  FOR_RC(H, 5, ns, m, i) {
+    const double* z = Z + (size_t)m * nu;
+    double v = 0.0;
+    for (int e = op.kptr[i]; e < op.kptr[i + 1]; ++e) v = fma(op.kval[e], z[op.kcol[e]], v);
+    T[m * FAST_MAXNS + i] = v;
+  }
+  __syncthreads();
+  FOR_NU(H, m, k) {
+    const double* tm = T + m * FAST_MAXNS;
+    double c = 0.0;
+    for (int e = op.ecp[k]; e < op.ecp[k + 1]; ++e) c = fma(op.ecv[e], tm[op.ecr[e]], c);
+    const double u = E[m * nu + k] + (Z[m * nu + k] - c);
+    Z[m * nu + k] = u;
+    if (store && (m >= kb || ((own >> m) & 1u))) d.U[(size_t)rows[m] * nu + k] = u;
+  }
+  __syncthreads();
+  FOR_NT(H, m, j) {
+    double bu = 0.0;
+    for (int e = op.brp[j]; e < op.brp[j + 1]; ++e) bu = fma(Z[m * nu + op.brc[e]], op.brv[e], bu);
+    E[m * nu + j] = bu;
+  }
+  __syncthreads();
+  if (threadIdx.x < nt) {
+    const int j = threadIdx.x;
+    double x = d.p[j];
+    for (int m = 0; m < H; ++m) {
+      x = (x + E[m * nu + j]) + G[m * lx + j];
+      G[m * lx + j] = x;
+      if (store && (m >= kb || ((own >> m) & 1u))) d.X[(size_t)rows[m] * lx + j] = x;
+    }
+  }
+  __syncthreads();
+  FSTEP(2);
+  // ---- P: prox of owned ancestors (one row per batch) and chain rows (pb per batch)
+  Ops pop = op;
+  pop.xmin = d.xmin;
+  pop.xmax = d.xmax;
+  pop.xsafe = d.xsafe;
+  pop.umin = d.umin;
+  pop.umax = d.umax;
+  RecOff o{};
+  o.y = 0;
+  o.ym = W;
+  o.ua = 2 * W;
+  o.xa = 2 * W + nu;
+  const int n_own = __popc(own);
+  const int nbat = n_own + (nst + pb - 1) / pb;
+  const double beta = d.beta[it], theta = d.theta[it], beta1 = has_next ? d.beta[it + 1] : 0.0;
+  {
+    int m0, bn;
+    fused_batch(0, n_own, own, kb, nst, pb, m0, bn);
+    fused_issue(f, ring, rp, rows + m0, bn, it);
+    cp_commit();
+  }
+  for (int b = 0; b < nbat; ++b) {
+    int m0, bn;
+    fused_batch(b, n_own, own, kb, nst, pb, m0, bn);
+    double* slot = ring + (size_t)(b & 1) * pb * rp;
+    if (b + 1 < nbat) {
+      int m1, bn1;
+      fused_batch(b + 1, n_own, own, kb, nst, pb, m1, bn1);
+      fused_issue(f, ring + (size_t)((b + 1) & 1) * pb * rp, rp, rows + m1, bn1, it);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    FSTEP(3);
+    prox_rows(f, pop, rows + m0, bn, Z + (size_t)m0 * nu, nu, G + (size_t)m0 * lx, lx, slot, rp, d2, 128, stp, it, beta,
+              theta, beta1, has_next, o, G + (size_t)m0 * lx, lx, Z + (size_t)m0 * nu, nu);
+    if (m0 < kb && has_next) {  // owned ancestor: its collapsed dual goes to HBM for k_branch_grp
+      const size_t r = (size_t)rows[m0];
+      for (int j = threadIdx.x; j < nt; j += blockDim.x) d.Yc[r * ly + j] = G[m0 * lx + j];
+      for (int k = threadIdx.x; k < nu; k += blockDim.x) d.Yc[r * ly + lx + k] = Z[m0 * nu + k];
+    }
+    FSTEP(4);
+  }
+  if (!has_next) return;
+  // ---- U: up pass of the next iteration on the chain rows (smem rows kb..H-1)
+  double* Zc = Z + (size_t)kb * nu;  // Yu -> a
+  double* Gc = G + (size_t)kb * lx;  // Yx -> wbar
+  FOR_RC(nst - 1, 6, (nu >> 1), t, k) cp16(E + (size_t)t * nu + 2 * k, np.R + (size_t)chain_row(f, t, ci) * nu + 2 * k);
+  cp_commit();
+  if (threadIdx.x < nt) {  // wbar suffix scan (own column only: no barrier needed before)
+    const int j = threadIdx.x;
+    double acc = 0.0;
+    for (int t = nst - 1; t >= 0; --t) {
+      const double yx = Gc[t * lx + j];
+      acc = t == nst - 1 ? yx : yx + acc;
+      Gc[t * lx + j] = acc;
+    }
+    d.wbar[(size_t)chain_row(f, 0, ci) * lx + j] = acc;
+  }
+  cp_wait<0>();
+  __syncthreads();
+  FSTEP(5);
+  FOR_NU(nst, t, k) {  // a = (Yu + wbar B) + R
+    double bw = 0.0;
+    for (int e = op.bcp[k]; e < op.bcp[k + 1]; ++e) bw = fma(Gc[t * lx + op.bcr[e]], op.bcv[e], bw);
+    double a = Zc[t * nu + k] + bw;
+    if (t < nst - 1) a = a + E[t * nu + k];
+    Zc[t * nu + k] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x < nu) {  // S_t = A_{t+1} (into E), A_0 -> Asub of the chain top
+    const int k = threadIdx.x;
+    double acc = 0.0;
+    for (int t = nst - 1; t >= 0; --t) {
+      E[t * nu + k] = acc;
+      const double a = Zc[t * nu + k];
+      acc = t == nst - 1 ? a : a + acc;
+    }
+    f.Asub[(size_t)chain_row(f, 0, ci) * nu + k] = acc;
+  }
+  __syncthreads();
+  proj_rows(d, op, E, E, T, nst - 1);
+  FOR_NU(nst, t, k) {
+    const double a = Zc[t * nu + k];
+    const double l = t < nst - 1 ? a + E[t * nu + k] : a;
+    const size_t r = (size_t)chain_row(f, t, ci);
+    f.Lb[r * nu + k] = l * f.aux[r * 2];
+  }
+  FSTEP(6);
+  if (pc) pc[0] += clk() - tstart;
+#undef FSTEP
 }
 
 }  // namespace wmpc

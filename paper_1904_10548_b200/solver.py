@@ -92,6 +92,15 @@ class _DeviceTree:
         m = instance.model
         self.ctx = nat.Context(instance.n_nonroot, len(instance.stage_slices), m.n_tanks,
                                m.n_inputs, m.n_demands, m.n_mixing, _DEVICE)
+        self.spare: list = []  # NodeSets of dead caches, reused (no cudaMalloc/cudaFree per factor_step)
+
+    def take_nodes(self) -> nat.NodeSet:
+        return self.spare.pop() if self.spare else nat.NodeSet(self.ctx)
+
+
+def _recycle_nodes(dev: _DeviceTree, nodes: nat.NodeSet) -> None:
+    if len(dev.spare) < 2:
+        dev.spare.append(nodes)
 
 
 # signature -> weakref(_DeviceTree); contexts die with their last cache.
@@ -234,7 +243,7 @@ def factor_step(instance, structure_from: FactorCache | None = None) -> FactorCa
         fresh_structure = True
     if fresh_structure:
         _upload_structure(dev, instance, basis, e_pinv, lam, t_mat, d_gain)
-    nodes = nat.NodeSet(dev.ctx)
+    nodes = dev.take_nodes()
     demand = nat.f64(instance.demand)
     Ed = nat.f64(m.Ed)
     gd = nat.f64(instance.demand_gd)
@@ -242,9 +251,11 @@ def factor_step(instance, structure_from: FactorCache | None = None) -> FactorCa
     bad = np.zeros(1, dtype=np.int64)
     dev.ctx.call("wmpc_set_node_data", nodes.h, nat.ptr(demand) if m.n_mixing else None,
                  nat.ptr(Ed) if m.n_mixing else None, nat.ptr(gd), nat.ptr(econ), nat.ptr(bad))
-    return FactorCache(null_basis=basis, e_pinv=e_pinv, d_gain=d_gain, t_mat=t_mat, lam=lam,
-                       pi=pi, kappa=kappa, lipschitz=lipschitz, signature=sig, _dev=dev,
-                       _nodes=nodes)
+    cache = FactorCache(null_basis=basis, e_pinv=e_pinv, d_gain=d_gain, t_mat=t_mat, lam=lam,
+                        pi=pi, kappa=kappa, lipschitz=lipschitz, signature=sig, _dev=dev,
+                        _nodes=nodes)
+    weakref.finalize(cache, _recycle_nodes, dev, nodes)
+    return cache
 
 
 def _check_cache(cache: FactorCache, instance) -> None:

@@ -15,10 +15,12 @@ for l in sass[start + 1:]:
     if m: cur = (m.group(1).split("/")[-1], int(m.group(2))); continue
     m = re.search(r"/\*([0-9a-f]{4,})\*/", l)
     if m and cur: off2line[int(m.group(1), 16)] = cur
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", *sys.argv[4:]], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-h = rows[1]; data = rows[2:]
-i_s = h.index("Warp Stall Sampling (All Samples)")
+if rows and rows[0] and rows[0][0] == "Kernel Name":
+    rows = rows[1:]
+h = rows[0]; data = [r for r in rows[1:] if r and r[0].startswith("0x")]
+i_s = h.index(os.environ.get("NCU_COL", "Warp Stall Sampling (All Samples)"))
 stall_cols = [i for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
 base = min(int(r[0], 16) for r in data)
 agg, reasons = {}, {}
