@@ -86,6 +86,7 @@ struct wmpc_ctx {
   unsigned* cown = nullptr;
   std::vector<std::pair<int, int>> gk_groups;  // (first row, rows) per stage group, bottom-up
   size_t sm_up = 0, sm_grp = 0, sm_down = 0, sm_prox = 0;
+  int up_threads = 512, down_threads = 512;
   cudaGraphExec_t gk_exec1 = nullptr, gk_exec8 = nullptr;
   double gk_gamma = -1.0;
   int gk_maxit = -1;
@@ -304,7 +305,7 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   ctx->fast_knz = knz;
   const BlobLayout bl = blob_layout(nt, nu, ns, knz, enz, bnz);
   const size_t cap = 227 * 1024;
-  const size_t up = sizeof(double) * (size_t)nst * (ly + nu + 2 + lx + nu + FAST_MAXNS) + bl.bytes;
+  const size_t up = sizeof(double) * (size_t)nst * (ly + nu + 2 + FAST_MAXNS) + bl.bytes;
   const size_t grp = sizeof(double) * ((size_t)(SC_THREADS / 32) * 256 + 2 * lx + 2 * nu + FAST_MAXNS) + bl.bytes;
   const size_t down = sizeof(double) * (size_t)H * (2 * nu + lx + FAST_MAXNS) + sizeof(int) * ((H + 3) & ~3) + bl.bytes;
   const size_t prox = sizeof(double) * ((size_t)SC_NPB * (ctx->fast_rec + nu + lx + 2) + 3 * nt + 2 * nu) +
@@ -421,6 +422,9 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   CK(cudaFuncSetAttribute(k_branch_grp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grp));
   CK(cudaFuncSetAttribute(k_prox_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox));
   ctx->sm_up = up; ctx->sm_down = down; ctx->sm_grp = grp; ctx->sm_prox = prox;
+  ctx->up_threads = ctx->down_threads = 512;  // measured: 512 beats 256 on C2 and C4
+  if (const char* e = getenv("WMPC_UPT")) ctx->up_threads = atoi(e) >= 512 ? 512 : 256;
+  if (const char* e = getenv("WMPC_DNT")) ctx->down_threads = atoi(e) >= 512 ? 512 : 256;
   // fused chain kernel (down + prox + next up); pb rows per prox batch
   {
     ctx->use_fused = 0;
@@ -680,9 +684,9 @@ void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
     k_chain_fused<<<nc, ctx->fused_threads, ctx->sm_fused, st>>>(f);
     return;
   }
-  k_chain_up<<<nc, SC_THREADS, ctx->sm_up, st>>>(f);
+  k_chain_up<<<nc, ctx->up_threads, ctx->sm_up, st>>>(f);
   for (const auto& g : ctx->gk_groups) k_branch_grp<<<g.second, SC_THREADS, ctx->sm_grp, st>>>(f, g.first);
-  k_chain_down<<<nc, SC_THREADS, ctx->sm_down, st>>>(f);
+  k_chain_down<<<nc, ctx->down_threads, ctx->sm_down, st>>>(f);
   k_prox_nodes<<<(ctx->n + SC_NPB - 1) / SC_NPB, SC_THREADS, ctx->sm_prox, st>>>(f);
 }
 
@@ -1348,7 +1352,7 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
         capture_graphk(ctx);
         if (ctx->use_fused) {  // up pass of iteration 0 (Yc = 0)
           FastView f = make_fastview(ctx, 1);
-          k_chain_up<<<ctx->nchain, SC_THREADS, ctx->sm_up, ctx->stream>>>(f);
+          k_chain_up<<<ctx->nchain, ctx->up_threads, ctx->sm_up, ctx->stream>>>(f);
           ctx->launches++;
           check_launch(ctx);
         }

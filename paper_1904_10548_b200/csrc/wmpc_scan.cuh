@@ -114,18 +114,16 @@ __device__ __forceinline__ void proj_rows(const DevView& d, const Ops& op, const
 __device__ __forceinline__ int chain_row(const FastView& f, int t, int ci) { return f.n_branch + t * f.nchain + ci; }
 
 // ---------------------------------------------------------------- k_chain_up
-// Shared: rec nst x (ly + nu + 2) [Yx | Yu->a | R | aux], WB nst x lx,
-// S nst x nu, T nst x FAST_MAXNS, blob.
-__global__ void __launch_bounds__(SC_THREADS) k_chain_up(FastView f) {
+// Shared: rec nst x (ly + nu + 2) [Yx->wbar | Yu->a | R->S->PS | aux],
+// T nst x FAST_MAXNS, blob (in-place phases keep 4 CTAs per SM at H = 24).
+__global__ void __launch_bounds__(512) k_chain_up(FastView f) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly;
   const int nst = d.H - f.kstar, ci = blockIdx.x;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int ra = ly + nu + 2;
   double* rec = reinterpret_cast<double*>(smem_raw);
-  double* WB = rec + (size_t)nst * ra;
-  double* S = WB + (size_t)nst * lx;
-  double* T = S + (size_t)nst * nu;
+  double* T = rec + (size_t)nst * ra;
   void* bl = T + (size_t)nst * FAST_MAXNS;
   const NodePtrs np = *d.np;
   issue_blob(f, bl);
@@ -137,13 +135,13 @@ __global__ void __launch_bounds__(SC_THREADS) k_chain_up(FastView f) {
   cp_wait<0>();
   __syncthreads();
   const Ops op = blob_ops(f, bl);
-  if (threadIdx.x < nt) {  // wbar suffix scan: wbar_t = Yx_t + wbar_{t+1}
+  if (threadIdx.x < nt) {  // wbar suffix scan in place: wbar_t = Yx_t + wbar_{t+1}
     const int j = threadIdx.x;
     double acc = 0.0;
     for (int t = nst - 1; t >= 0; --t) {
       const double yx = rec[(size_t)t * ra + j];
       acc = t == nst - 1 ? yx : yx + acc;
-      WB[t * lx + j] = acc;
+      rec[(size_t)t * ra + j] = acc;
     }
     d.wbar[(size_t)chain_row(f, 0, ci) * lx + j] = acc;
   }
@@ -151,28 +149,29 @@ __global__ void __launch_bounds__(SC_THREADS) k_chain_up(FastView f) {
   FOR_NU(nst, t, k) {  // a = (Yu + wbar B) + R, over Yu
     double* R = rec + (size_t)t * ra;
     double bw = 0.0;
-    for (int e = op.bcp[k]; e < op.bcp[k + 1]; ++e) bw = fma(WB[t * lx + op.bcr[e]], op.bcv[e], bw);
+    for (int e = op.bcp[k]; e < op.bcp[k + 1]; ++e) bw = fma(R[op.bcr[e]], op.bcv[e], bw);
     double a = R[lx + k] + bw;
     if (t < nst - 1) a = a + R[ly + k];
     R[lx + k] = a;
   }
   __syncthreads();
-  if (threadIdx.x < nu) {  // S_t = A_{t+1}, A_t = a_t + S_t
+  if (threadIdx.x < nu) {  // S_t = A_{t+1} over R, A_t = a_t + S_t
     const int k = threadIdx.x;
     double acc = 0.0;
     for (int t = nst - 1; t >= 0; --t) {
-      S[t * nu + k] = acc;
-      const double a = rec[(size_t)t * ra + lx + k];
+      double* R = rec + (size_t)t * ra;
+      R[ly + k] = acc;
+      const double a = R[lx + k];
       acc = t == nst - 1 ? a : a + acc;
     }
     f.Asub[(size_t)chain_row(f, 0, ci) * nu + k] = acc;
   }
   __syncthreads();
-  proj_rows(d, op, S, S, T, nst - 1);
+  proj_rows_s(d, op, rec + ly, ra, rec + ly, ra, T, nst - 1);
   FOR_NU(nst, t, k) {
     const double* R = rec + (size_t)t * ra;
     const double a = R[lx + k];
-    const double l = t < nst - 1 ? a + S[t * nu + k] : a;
+    const double l = t < nst - 1 ? a + R[ly + k] : a;
     f.Lb[(size_t)chain_row(f, t, ci) * nu + k] = l * R[ly + nu];
   }
 }
@@ -282,7 +281,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0) {
 //   x_m = (x_{m-1} + u_m B^T) + g_m,  x_{-1} = p.
 // Ancestor rows are written by the chain that owns them (cown).
 // Shared: rec H x (2nu + lx) [L->z | e_off | g], T H x FAST_MAXNS, rows H, blob.
-__global__ void __launch_bounds__(SC_THREADS) k_chain_down(FastView f) {
+__global__ void __launch_bounds__(512) k_chain_down(FastView f) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx;
   const int kb = f.kstar, nr = d.H, ci = blockIdx.x;
