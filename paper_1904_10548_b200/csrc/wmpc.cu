@@ -86,7 +86,7 @@ struct wmpc_ctx {
   unsigned* cown = nullptr;
   std::vector<std::pair<int, int>> gk_groups;  // (first row, rows) per stage group, bottom-up
   size_t sm_up = 0, sm_grp = 0, sm_down = 0, sm_prox = 0;
-  int up_threads = 512, down_threads = 512;
+  int up_threads = 512, down_threads = 512, prox_warp = 1;
   cudaGraphExec_t gk_exec1 = nullptr, gk_exec8 = nullptr;
   double gk_gamma = -1.0;
   int gk_maxit = -1;
@@ -425,6 +425,8 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   ctx->up_threads = ctx->down_threads = 512;  // measured: 512 beats 256 on C2 and C4
   if (const char* e = getenv("WMPC_UPT")) ctx->up_threads = atoi(e) >= 512 ? 512 : 256;
   if (const char* e = getenv("WMPC_DNT")) ctx->down_threads = atoi(e) >= 512 ? 512 : 256;
+  ctx->prox_warp = nt <= 64 && nu <= 128 ? 1 : 0;
+  if (const char* e = getenv("WMPC_PROX")) ctx->prox_warp = std::string(e) == "warp" ? ctx->prox_warp : 0;
   // fused chain kernel (down + prox + next up); pb rows per prox batch
   {
     ctx->use_fused = 0;
@@ -687,7 +689,10 @@ void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
   k_chain_up<<<nc, ctx->up_threads, ctx->sm_up, st>>>(f);
   for (const auto& g : ctx->gk_groups) k_branch_grp<<<g.second, SC_THREADS, ctx->sm_grp, st>>>(f, g.first);
   k_chain_down<<<nc, ctx->down_threads, ctx->sm_down, st>>>(f);
-  k_prox_nodes<<<(ctx->n + SC_NPB - 1) / SC_NPB, SC_THREADS, ctx->sm_prox, st>>>(f);
+  if (ctx->prox_warp)
+    k_prox_warp<<<(ctx->n + PW_ROWS - 1) / PW_ROWS, 256, 0, st>>>(f);
+  else
+    k_prox_nodes<<<(ctx->n + SC_NPB - 1) / SC_NPB, SC_THREADS, ctx->sm_prox, st>>>(f);
 }
 
 void capture_graphk(wmpc_ctx* ctx) {

@@ -403,6 +403,125 @@ __global__ void __launch_bounds__(SC_THREADS) k_prox_nodes(FastView f) {
 }
 
 
+// ---------------------------------------------------------------- k_prox_warp
+// Node-parallel Moreau prox without CTA barriers: two warps per node, operands
+// straight from global memory into registers (every load issued up front).
+//   warp 2m   : the tank part, lanes own columns j and j+32 of both tank slots;
+//               the two slot norms use numpy's pairwise order through an
+//               8-lane group each (pw_group8) on a per-warp shared array
+//   warp 2m+1 : the input part (plain box projection), columns k + 32q
+// Same expression order as prox_rows (bit-exact with numpy), V kept in registers.
+constexpr int PW_ROWS = 4;  // nodes per 256-thread CTA
+__global__ void __launch_bounds__(256) k_prox_warp(FastView f) {
+  const DevView& d = f.d;
+  const int nt = d.nt, nu = d.nu, W = d.W, lx = d.lx, ly = d.ly;
+  __shared__ double sd2[PW_ROWS][2][64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = warp >> 1;
+  const int r = blockIdx.x * PW_ROWS + m;
+  if (r >= d.n) return;
+  const int it = *d.iter - 1;
+  const bool next = it + 1 < f.max_iter;
+  const double gamma = d.gamma, ig = f.inv_gamma;
+  const double beta = d.beta[it], theta = d.theta[it], beta1 = next ? d.beta[it + 1] : 0.0;
+  const double om = dsub(1.0, theta);
+  const size_t rw = (size_t)r * W;
+  const double* y = ybuf(d, it) + rw;
+  const double* ym = ybuf(d, it + 2) + rw;
+  double* yn = ybuf_w(d, it + 1) + rw;
+  bool bad = false;
+  if ((warp & 1) == 0) {
+    double xv[2], xa[2], y1[2], y2[2], m1[2], m2[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = lane + 32 * q;
+      const bool ok = j < nt;
+      xv[q] = ok ? d.X[(size_t)r * lx + j] : 0.0;
+      xa[q] = ok && it > 0 ? d.Xa[(size_t)r * lx + j] : 0.0;
+      y1[q] = ok ? y[j] : 0.0;
+      y2[q] = ok ? y[nt + j] : 0.0;
+      m1[q] = ok ? ym[j] : 0.0;
+      m2[q] = ok ? ym[nt + j] : 0.0;
+    }
+    double v1[2], v2[2], V1[2], V2[2], c1[2], c2[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = lane + 32 * q;
+      const bool ok = j < nt;
+      const double x = xv[q];
+      if (ok) d.Xa[(size_t)r * lx + j] = it == 0 ? x : dadd(dmul(xa[q], om), dmul(theta, x));
+      const double gx = dmul(gamma, x);
+      v1[q] = dadd(dadd(y1[q], dmul(beta, dsub(y1[q], m1[q]))), gx);
+      v2[q] = dadd(dadd(y2[q], dmul(beta, dsub(y2[q], m2[q]))), gx);
+      V1[q] = div_by(v1[q], gamma, ig);
+      V2[q] = div_by(v2[q], gamma, ig);
+      c1[q] = ok ? np_clip(V1[q], d.xmin[j], d.xmax[j]) : 0.0;
+      c2[q] = ok ? np_max(V2[q], d.xsafe[j]) : 0.0;
+      if (ok) {
+        const double df1 = dsub(V1[q], c1[q]), df2 = dsub(V2[q], c2[q]);
+        sd2[m][0][j] = dmul(df1, df1);
+        sd2[m][1][j] = dmul(df2, df2);
+      }
+    }
+    __syncwarp();
+    double st = 0.0;
+    if (lane < 16) {
+      const int slot = lane >> 3;
+      const double ssum = pw_group8(sd2[m][slot], nt, lane & 7, 0xffu << (lane & 8));
+      if ((lane & 7) == 0) {
+        const double dist = __dsqrt_rn(ssum);
+        const double thr = dmul(ig, slot ? d.w_s : d.w_x);  // prox parameter RN(1/gamma) (solver.py:571)
+        st = dist > 0.0 ? np_min(1.0, div_exact(thr, dist)) : 0.0;
+      }
+    }
+    const double st1 = __shfl_sync(0xffffffffu, st, 0), st2 = __shfl_sync(0xffffffffu, st, 8);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = lane + 32 * q;
+      if (j < nt) {
+        const double O1 = dsub(V1[q], dmul(st1, dsub(V1[q], c1[q])));
+        const double O2 = dsub(V2[q], dmul(st2, dsub(V2[q], c2[q])));
+        const double p1 = dsub(v1[q], dmul(gamma, O1)), p2 = dsub(v2[q], dmul(gamma, O2));
+        yn[j] = p1;
+        yn[nt + j] = p2;
+        bad |= !isfinite(p1) || !isfinite(p2);
+        if (next) {
+          const double w1 = dadd(p1, dmul(beta1, dsub(p1, y1[q])));
+          const double w2 = dadd(p2, dmul(beta1, dsub(p2, y2[q])));
+          d.Yc[(size_t)r * ly + j] = dadd(w1, w2);
+        }
+      }
+    }
+  } else {
+    constexpr int Q = 4;  // nu <= 128
+    double uv[Q], ua[Q], y3[Q], m3[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int k = lane + 32 * q;
+      const bool ok = k < nu;
+      uv[q] = ok ? d.U[(size_t)r * nu + k] : 0.0;
+      ua[q] = ok && it > 0 ? d.Ua[(size_t)r * nu + k] : 0.0;
+      y3[q] = ok ? y[2 * nt + k] : 0.0;
+      m3[q] = ok ? ym[2 * nt + k] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int k = lane + 32 * q;
+      if (k < nu) {
+        const double u = uv[q];
+        d.Ua[(size_t)r * nu + k] = it == 0 ? u : dadd(dmul(ua[q], om), dmul(theta, u));
+        const double v3 = dadd(dadd(y3[q], dmul(beta, dsub(y3[q], m3[q]))), dmul(gamma, u));
+        const double V3 = div_by(v3, gamma, ig);
+        const double p3 = dsub(v3, dmul(gamma, np_clip(V3, d.umin[k], d.umax[k])));
+        yn[2 * nt + k] = p3;
+        bad |= !isfinite(p3);
+        if (next) d.Yc[(size_t)r * ly + lx + k] = dadd(p3, dmul(beta1, dsub(p3, y3[q])));
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(d.bad_nu, it);
+}
+
 // ---------------------------------------------------------------- k_chain_fused
 // One CTA per chain, three phases in shared memory:
 //   D  down pass of iteration it over the root path (as k_chain_down) -> u, x
