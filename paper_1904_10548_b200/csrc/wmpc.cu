@@ -87,6 +87,9 @@ struct wmpc_ctx {
   std::vector<std::pair<int, int>> gk_groups;  // (first row, rows) per stage group, bottom-up
   size_t sm_up = 0, sm_grp = 0, sm_down = 0, sm_prox = 0;
   int up_threads = 512, down_threads = 512, prox_warp = 1;
+  int *ell_cnt = nullptr, *ell_idx = nullptr;
+  double* ell_val = nullptr;
+  int ell_w = 4;
   cudaGraphExec_t gk_exec1 = nullptr, gk_exec8 = nullptr;
   double gk_gamma = -1.0;
   int gk_maxit = -1;
@@ -246,6 +249,25 @@ size_t fast_smem_bytes(const wmpc_ctx* c, int MC, int nrow, int rec, int cpc, in
 // Decide whether the structured persistent kernel applies and lay out its data:
 // A = I, W = cI, n_u even, n_s <= 32, and every stage factor equal to the
 // null(E) projector (T_s = P/(2c), D_s = P up to 1e-12 relative).
+template <int WE>
+void gk_attrs(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
+  CK(cudaFuncSetAttribute(k_chain_up<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
+  CK(cudaFuncSetAttribute(k_chain_down<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
+  CK(cudaFuncSetAttribute(k_branch_grp<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grp));
+}
+template <int WE>
+void gk_up(wmpc_ctx* ctx, const FastView& f) {
+  k_chain_up<WE><<<ctx->nchain, ctx->up_threads, ctx->sm_up, ctx->stream>>>(f);
+}
+template <int WE>
+void gk_grp(wmpc_ctx* ctx, const FastView& f) {
+  for (const auto& g : ctx->gk_groups) k_branch_grp<WE><<<g.second, SC_THREADS, ctx->sm_grp, ctx->stream>>>(f, g.first);
+}
+template <int WE>
+void gk_down(wmpc_ctx* ctx, const FastView& f) {
+  k_chain_down<WE><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);
+}
+
 // Graph-of-kernels scan path: operator blob, stage groups of the branching
 // region with per-row item lists, chain root paths. Default when it fits.
 void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::vector<int>& cidx,
@@ -305,9 +327,9 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   ctx->fast_knz = knz;
   const BlobLayout bl = blob_layout(nt, nu, ns, knz, enz, bnz);
   const size_t cap = 227 * 1024;
-  const size_t up = sizeof(double) * (size_t)nst * (ly + nu + 2 + FAST_MAXNS) + bl.bytes;
-  const size_t grp = sizeof(double) * ((size_t)(SC_THREADS / 32) * 256 + 2 * lx + 2 * nu + FAST_MAXNS) + bl.bytes;
-  const size_t down = sizeof(double) * (size_t)H * (2 * nu + lx + FAST_MAXNS) + sizeof(int) * ((H + 3) & ~3) + bl.bytes;
+  const size_t up = sizeof(double) * (size_t)nst * (ly + nu + 2 + FAST_MAXNS);
+  const size_t grp = sizeof(double) * ((size_t)(SC_THREADS / 32) * 256 + 2 * lx + 2 * nu + FAST_MAXNS);
+  const size_t down = sizeof(double) * (size_t)H * (2 * nu + lx + FAST_MAXNS) + sizeof(int) * ((H + 3) & ~3);
   const size_t prox = sizeof(double) * ((size_t)SC_NPB * (ctx->fast_rec + nu + lx + 2) + 3 * nt + 2 * nu) +
                       sizeof(int) * SC_NPB + 16;
   if (std::max(std::max(up, down), std::max(grp, prox)) > cap) return;
@@ -328,6 +350,35 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
     for (int i = 0; i <= nt; ++i) ip[bl.brp + i] = brp[i];
   }
   upload_vec(ctx, &ctx->blob, blob);
+  // ELL operators, owners [B cols | B rows | E cols | K rows], width = max entries per owner
+  {
+    std::vector<std::vector<std::pair<int, double>>> owners((size_t)2 * nu + nt + ns);
+    for (int k = 0; k < nu; ++k)
+      for (int e = bcp[k]; e < bcp[k + 1]; ++e) owners[k].push_back({bcr[e], bcv[e]});
+    for (int j = 0; j < nt; ++j)
+      for (int e = brp[j]; e < brp[j + 1]; ++e) owners[nu + j].push_back({brc[e], brv[e]});
+    for (int k = 0; k < nu; ++k)
+      for (int e = ecp[k]; e < ecp[k + 1]; ++e) owners[nu + nt + k].push_back({ecr[e], ecv[e]});
+    for (int i = 0; i < ns; ++i)
+      for (int e = kp[i]; e < kp[i + 1]; ++e) owners[2 * nu + nt + i].push_back({kc[e], kv[e]});
+    size_t w = 1;
+    for (auto& o : owners) w = std::max(w, o.size());
+    if (w > 8) return;  // wide operators: the persistent kernels handle them
+    const int we = w <= 4 ? 4 : 8;
+    std::vector<int> cnt(owners.size()), idx(owners.size() * we, 0);
+    std::vector<double> val(owners.size() * we, 0.0);
+    for (size_t o = 0; o < owners.size(); ++o) {
+      cnt[o] = (int)owners[o].size();
+      for (size_t e = 0; e < owners[o].size(); ++e) {
+        idx[o * we + e] = owners[o][e].first;
+        val[o * we + e] = owners[o][e].second;
+      }
+    }
+    upload_vec(ctx, &ctx->ell_cnt, cnt);
+    upload_vec(ctx, &ctx->ell_idx, idx);
+    upload_vec(ctx, &ctx->ell_val, val);
+    ctx->ell_w = we;
+  }
   // stage of every branching row; stage groups bottom-up with <= 32 items per row
   std::vector<int> stage(std::max(nb, 1), 0);
   for (int s = 0; s < kstar; ++s)
@@ -417,9 +468,8 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   std::vector<double> zl((size_t)ctx->n * nu, 0.0), za((size_t)(nb + nchain) * nu, 0.0);
   upload_vec(ctx, &ctx->Lb, zl);
   upload_vec(ctx, &ctx->Asub, za);
-  CK(cudaFuncSetAttribute(k_chain_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
-  CK(cudaFuncSetAttribute(k_chain_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
-  CK(cudaFuncSetAttribute(k_branch_grp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grp));
+  if (ctx->ell_w == 4) gk_attrs<4>(ctx, up, down, grp);
+  else gk_attrs<8>(ctx, up, down, grp);
   CK(cudaFuncSetAttribute(k_prox_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox));
   ctx->sm_up = up; ctx->sm_down = down; ctx->sm_grp = grp; ctx->sm_prox = prox;
   ctx->up_threads = ctx->down_threads = 512;  // measured: 512 beats 256 on C2 and C4
@@ -682,13 +732,19 @@ void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
   const int nc = ctx->nchain;
   if (ctx->gk_groups.empty()) k_advance<<<1, 32, 0, st>>>(ctx->iter);  // else the first group kernel counts
   if (ctx->use_fused) {  // up pass of iteration 0 runs in wmpc_apg_begin
-    for (const auto& g : ctx->gk_groups) k_branch_grp<<<g.second, SC_THREADS, ctx->sm_grp, st>>>(f, g.first);
+    if (ctx->ell_w == 4) gk_grp<4>(ctx, f); else gk_grp<8>(ctx, f);
     k_chain_fused<<<nc, ctx->fused_threads, ctx->sm_fused, st>>>(f);
     return;
   }
-  k_chain_up<<<nc, ctx->up_threads, ctx->sm_up, st>>>(f);
-  for (const auto& g : ctx->gk_groups) k_branch_grp<<<g.second, SC_THREADS, ctx->sm_grp, st>>>(f, g.first);
-  k_chain_down<<<nc, ctx->down_threads, ctx->sm_down, st>>>(f);
+  if (ctx->ell_w == 4) {
+    gk_up<4>(ctx, f);
+    gk_grp<4>(ctx, f);
+    gk_down<4>(ctx, f);
+  } else {
+    gk_up<8>(ctx, f);
+    gk_grp<8>(ctx, f);
+    gk_down<8>(ctx, f);
+  }
   if (ctx->prox_warp)
     k_prox_warp<<<(ctx->n + PW_ROWS - 1) / PW_ROWS, 256, 0, st>>>(f);
   else
@@ -754,6 +810,10 @@ FastView make_fastview(wmpc_ctx* ctx, int count) {
   f.cpath = ctx->cpath;
   f.cown = ctx->cown;
   f.store_it = ctx->store_it;
+  f.ell_cnt = ctx->ell_cnt;
+  f.ell_idx = ctx->ell_idx;
+  f.ell_val = ctx->ell_val;
+  f.ell_w = ctx->ell_w;
   f.pb = ctx->fused_pb;
   f.ring_off = ctx->fused_ring_off;
   f.work_doubles = ctx->scan_work;
@@ -823,7 +883,7 @@ void free_all(wmpc_ctx* c) {
                   c->bad_row, c->part, c->scal, c->d_np, c->chain_node,
                   c->bc_ptr, c->bc_row, c->br_ptr, c->br_col, c->off_dev, c->bc_val, c->br_val,
                   c->e_ptr, c->e_col, c->e_val, c->aux,
-                  c->Lb, c->Asub, c->blob, c->store_it, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
+                  c->Lb, c->Asub, c->blob, c->store_it, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
                   c->pj_ecv, c->dk_mv, c->dk_sweeps, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
                   c->prof};
   for (void* p : ptrs)
@@ -1357,7 +1417,7 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
         capture_graphk(ctx);
         if (ctx->use_fused) {  // up pass of iteration 0 (Yc = 0)
           FastView f = make_fastview(ctx, 1);
-          k_chain_up<<<ctx->nchain, ctx->up_threads, ctx->sm_up, ctx->stream>>>(f);
+          if (ctx->ell_w == 4) gk_up<4>(ctx, f); else gk_up<8>(ctx, f);
           ctx->launches++;
           check_launch(ctx);
         }

@@ -113,28 +113,65 @@ __device__ __forceinline__ void proj_rows(const DevView& d, const Ops& op, const
 
 __device__ __forceinline__ int chain_row(const FastView& f, int t, int ci) { return f.n_branch + t * f.nchain + ci; }
 
+// Register-resident sparse operators (ELL, width WE): a thread owns one column
+// (or row) for a whole phase and loops over tree rows, so the operator entries
+// are loaded once (from L1) instead of walked through shared memory per row.
+enum { ELL_BC = 0 };  // owner offsets: B by column [0,nu), B by row [nu,nu+nt), E by column, K by row
+template <int WE>
+struct Ell {
+  int n;
+  int idx[WE];
+  double val[WE];
+};
+template <int WE>
+__device__ __forceinline__ Ell<WE> ell_load(const FastView& f, int owner) {
+  Ell<WE> o;
+  o.n = f.ell_cnt[owner];
+  const int* ip = f.ell_idx + (size_t)owner * f.ell_w;
+  const double* vp = f.ell_val + (size_t)owner * f.ell_w;
+#pragma unroll
+  for (int e = 0; e < WE; ++e) {
+    o.idx[e] = e < o.n ? ip[e] : 0;
+    o.val[e] = e < o.n ? vp[e] : 0.0;
+  }
+  return o;
+}
+template <int WE>
+__device__ __forceinline__ double ell_dot(const Ell<WE>& o, const double* x) {
+  double s = 0.0;
+#pragma unroll
+  for (int e = 0; e < WE; ++e)
+    if (e < o.n) s = fma(o.val[e], x[o.idx[e]], s);
+  return s;
+}
+__device__ __forceinline__ int own_bc(const DevView& d, int k) { return k; }
+__device__ __forceinline__ int own_br(const DevView& d, int j) { return d.nu + j; }
+__device__ __forceinline__ int own_ec(const DevView& d, int k) { return d.nu + d.nt + k; }
+__device__ __forceinline__ int own_kr(const DevView& d, int i) { return 2 * d.nu + d.nt + i; }
+
 // ---------------------------------------------------------------- k_chain_up
 // Shared: rec nst x (ly + nu + 2) [Yx->wbar | Yu->a | R->S->PS | aux],
-// T nst x FAST_MAXNS, blob (in-place phases keep 4 CTAs per SM at H = 24).
+// T nst x FAST_MAXNS (in-place phases keep 4 CTAs per SM at H = 24).
+template <int WE>
 __global__ void __launch_bounds__(512) k_chain_up(FastView f) {
   const DevView& d = f.d;
-  const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly;
+  const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly, ns = d.ns;
   const int nst = d.H - f.kstar, ci = blockIdx.x;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int ra = ly + nu + 2;
   double* rec = reinterpret_cast<double*>(smem_raw);
   double* T = rec + (size_t)nst * ra;
-  void* bl = T + (size_t)nst * FAST_MAXNS;
   const NodePtrs np = *d.np;
-  issue_blob(f, bl);
   FOR_RC(nst, 7, (ly >> 1), t, k) cp16(rec + (size_t)t * ra + 2 * k, d.Yc + (size_t)chain_row(f, t, ci) * ly + 2 * k);
   FOR_RC(nst - 1, 6, (nu >> 1), t, k)
     cp16(rec + (size_t)t * ra + ly + 2 * k, np.R + (size_t)chain_row(f, t, ci) * nu + 2 * k);
   if (threadIdx.x < nst) cp16(rec + (size_t)threadIdx.x * ra + ly + nu, f.aux + (size_t)chain_row(f, threadIdx.x, ci) * 2);
   cp_commit();
+  const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
+  const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
+  const Ell<WE> bc = ell_load<WE>(f, own_bc(d, k < nu ? k : 0));
   cp_wait<0>();
   __syncthreads();
-  const Ops op = blob_ops(f, bl);
   if (threadIdx.x < nt) {  // wbar suffix scan in place: wbar_t = Yx_t + wbar_{t+1}
     const int j = threadIdx.x;
     double acc = 0.0;
@@ -146,33 +183,38 @@ __global__ void __launch_bounds__(512) k_chain_up(FastView f) {
     d.wbar[(size_t)chain_row(f, 0, ci) * lx + j] = acc;
   }
   __syncthreads();
-  FOR_NU(nst, t, k) {  // a = (Yu + wbar B) + R, over Yu
-    double* R = rec + (size_t)t * ra;
-    double bw = 0.0;
-    for (int e = op.bcp[k]; e < op.bcp[k + 1]; ++e) bw = fma(R[op.bcr[e]], op.bcv[e], bw);
-    double a = R[lx + k] + bw;
-    if (t < nst - 1) a = a + R[ly + k];
-    R[lx + k] = a;
-  }
+  if (k < nu)
+    for (int t = tk; t < nst; t += sk) {  // a = (Yu + wbar B) + R, over Yu
+      double* R = rec + (size_t)t * ra;
+      double a = R[lx + k] + ell_dot(bc, R);
+      if (t < nst - 1) a = a + R[ly + k];
+      R[lx + k] = a;
+    }
   __syncthreads();
   if (threadIdx.x < nu) {  // S_t = A_{t+1} over R, A_t = a_t + S_t
-    const int k = threadIdx.x;
     double acc = 0.0;
     for (int t = nst - 1; t >= 0; --t) {
       double* R = rec + (size_t)t * ra;
-      R[ly + k] = acc;
-      const double a = R[lx + k];
+      R[ly + threadIdx.x] = acc;
+      const double a = R[lx + threadIdx.x];
       acc = t == nst - 1 ? a : a + acc;
     }
-    f.Asub[(size_t)chain_row(f, 0, ci) * nu + k] = acc;
+    f.Asub[(size_t)chain_row(f, 0, ci) * nu + threadIdx.x] = acc;
   }
   __syncthreads();
-  proj_rows_s(d, op, rec + ly, ra, rec + ly, ra, T, nst - 1);
-  FOR_NU(nst, t, k) {
-    const double* R = rec + (size_t)t * ra;
-    const double a = R[lx + k];
-    const double l = t < nst - 1 ? a + R[ly + k] : a;
-    f.Lb[(size_t)chain_row(f, t, ci) * nu + k] = l * R[ly + nu];
+  if (i < ns) {  // T = K S
+    const Ell<WE> kr = ell_load<WE>(f, own_kr(d, i));
+    for (int t = ti; t < nst - 1; t += si) T[t * FAST_MAXNS + i] = ell_dot(kr, rec + (size_t)t * ra + ly);
+  }
+  __syncthreads();
+  if (k < nu) {  // L = (a + (S - E^T T)) / (2c p)
+    const Ell<WE> ec = ell_load<WE>(f, own_ec(d, k));
+    for (int t = tk; t < nst; t += sk) {
+      const double* R = rec + (size_t)t * ra;
+      const double a = R[lx + k];
+      const double l = t < nst - 1 ? a + (R[ly + k] - ell_dot(ec, T + t * FAST_MAXNS)) : a;
+      f.Lb[(size_t)chain_row(f, t, ci) * nu + k] = l * R[ly + nu];
+    }
   }
 }
 
@@ -185,6 +227,7 @@ __global__ void __launch_bounds__(512) k_chain_up(FastView f) {
 //   W2 = sum_{d in desc_B(r)} wbar_d = sum_0 w Yx_e + sum_1 w wbar_f
 //   Su = sum_0 (Yu_e + R_e) + sum_1 Asub_f
 //   a_r = (Yu_r + W1 B) + R_r,  S_r = Su + W2 B,  lin_r = a_r + P S_r.
+template <int WE>
 __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly;
@@ -198,10 +241,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0) {
   double* av = W2 + lx;          // nu
   double* Sv = av + nu;          // nu
   double* T = Sv + nu;           // FAST_MAXNS
-  void* bl = T + FAST_MAXNS;
   const NodePtrs np = *d.np;
-  issue_blob(f, bl);
-  cp_commit();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double s1[2] = {0.0, 0.0}, s2[2] = {0.0, 0.0}, su[4] = {0.0, 0.0, 0.0, 0.0};
   const int e0 = f.gi_ptr[r], e1 = f.gi_ptr[r + 1];
@@ -249,28 +289,30 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0) {
     W1[j] = d.Yc[(size_t)r * ly + j] + a1;
     W2[j] = a2;
   }
-  cp_wait<0>();
   __syncthreads();
-  const Ops op = blob_ops(f, bl);
   if (threadIdx.x < nu) {
     const int k = threadIdx.x;
     double s = part[128 + k];
     for (int w = 1; w < NW; ++w) s += part[w * 256 + 128 + k];
     double b1 = 0.0, b2 = 0.0;
-    for (int e = op.bcp[k]; e < op.bcp[k + 1]; ++e) {
-      b1 = fma(W1[op.bcr[e]], op.bcv[e], b1);
-      b2 = fma(W2[op.bcr[e]], op.bcv[e], b2);
-    }
+    const Ell<WE> bc = ell_load<WE>(f, own_bc(d, k));
+    b1 = ell_dot(bc, W1);
+    b2 = ell_dot(bc, W2);
     av[k] = (d.Yc[(size_t)r * ly + lx + k] + b1) + np.R[(size_t)r * nu + k];
     Sv[k] = s + b2;
   }
   if (threadIdx.x < nt) d.wbar[(size_t)r * lx + threadIdx.x] = W1[threadIdx.x];
   __syncthreads();
   if (threadIdx.x < nu) f.Asub[(size_t)r * nu + threadIdx.x] = av[threadIdx.x] + Sv[threadIdx.x];
-  proj_rows(d, op, Sv, Sv, T, 1);
+  if (threadIdx.x < d.ns) {
+    const Ell<WE> kr = ell_load<WE>(f, own_kr(d, threadIdx.x));
+    T[threadIdx.x] = ell_dot(kr, Sv);
+  }
+  __syncthreads();
   if (threadIdx.x < nu) {
     const int k = threadIdx.x;
-    f.Lb[(size_t)r * nu + k] = (av[k] + Sv[k]) * f.aux[(size_t)r * 2];
+    const Ell<WE> ec = ell_load<WE>(f, own_ec(d, k));
+    f.Lb[(size_t)r * nu + k] = (av[k] + (Sv[k] - ell_dot(ec, T))) * f.aux[(size_t)r * 2];
   }
 }
 
@@ -280,19 +322,18 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0) {
 //   z_m = (q + sum_{m' < m} e_off_m') - sum_{m' <= m} L_m',  u_m = e_off_m + P z_m,
 //   x_m = (x_{m-1} + u_m B^T) + g_m,  x_{-1} = p.
 // Ancestor rows are written by the chain that owns them (cown).
-// Shared: rec H x (2nu + lx) [L->z | e_off | g], T H x FAST_MAXNS, rows H, blob.
+// Shared: rec H x (2nu + lx) [L->z->u | e_off->Bu | g], T H x FAST_MAXNS, rows H.
+template <int WE>
 __global__ void __launch_bounds__(512) k_chain_down(FastView f) {
   const DevView& d = f.d;
-  const int nt = d.nt, nu = d.nu, lx = d.lx;
+  const int nt = d.nt, nu = d.nu, lx = d.lx, ns = d.ns;
   const int kb = f.kstar, nr = d.H, ci = blockIdx.x;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int rd = 2 * nu + lx;
   double* rec = reinterpret_cast<double*>(smem_raw);
   double* T = rec + (size_t)nr * rd;
   int* rows = reinterpret_cast<int*>(T + (size_t)nr * FAST_MAXNS);
-  void* bl = rows + ((nr + 3) & ~3);
   const NodePtrs np = *d.np;
-  issue_blob(f, bl);
   if (threadIdx.x < nr) {
     const int m = threadIdx.x;
     rows[m] = m < kb ? f.cpath[(size_t)ci * kb + m] : chain_row(f, m - kb, ci);
@@ -302,12 +343,15 @@ __global__ void __launch_bounds__(512) k_chain_down(FastView f) {
   FOR_RC(nr, 6, (nu >> 1), m, k) cp16(rec + (size_t)m * rd + nu + 2 * k, np.e_off + (size_t)rows[m] * nu + 2 * k);
   FOR_RC(nr, 5, (lx >> 1), m, k) cp16(rec + (size_t)m * rd + 2 * nu + 2 * k, np.g + (size_t)rows[m] * lx + 2 * k);
   cp_commit();
+  const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
+  const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
+  const int j = threadIdx.x & 63, tj = threadIdx.x >> 6, sj = blockDim.x >> 6;
+  const unsigned own = kb > 0 ? f.cown[ci] : 0u;
+  const double qk = k < nu ? d.q[k] : 0.0;
   cp_wait<0>();
   __syncthreads();
-  const Ops op = blob_ops(f, bl);
   if (threadIdx.x < nu) {
-    const int k = threadIdx.x;
-    double ls = 0.0, es = d.q[k];
+    double ls = 0.0, es = qk;
     for (int m = 0; m < nr; ++m) {
       double* R = rec + (size_t)m * rd;
       ls = m == 0 ? R[k] : ls + R[k];
@@ -316,39 +360,35 @@ __global__ void __launch_bounds__(512) k_chain_down(FastView f) {
     }
   }
   __syncthreads();
-  // u = e_off + P z (in the z slot)
-  FOR_RC(nr, 5, d.ns, m, i) {
-    const double* z = rec + (size_t)m * rd;
-    double v = 0.0;
-    for (int e = op.kptr[i]; e < op.kptr[i + 1]; ++e) v = fma(op.kval[e], z[op.kcol[e]], v);
-    T[m * FAST_MAXNS + i] = v;
+  if (i < ns) {  // T = K z
+    const Ell<WE> kr = ell_load<WE>(f, own_kr(d, i));
+    for (int m = ti; m < nr; m += si) T[m * FAST_MAXNS + i] = ell_dot(kr, rec + (size_t)m * rd);
   }
   __syncthreads();
-  const unsigned own = kb > 0 ? f.cown[ci] : 0u;
-  FOR_NU(nr, m, k) {
-    double* R = rec + (size_t)m * rd;
-    const double* tm = T + m * FAST_MAXNS;
-    double c = 0.0;
-    for (int e = op.ecp[k]; e < op.ecp[k + 1]; ++e) c = fma(op.ecv[e], tm[op.ecr[e]], c);
-    const double u = R[nu + k] + (R[k] - c);
-    R[k] = u;
-    if (m >= kb || ((own >> m) & 1u)) d.U[(size_t)rows[m] * nu + k] = u;
+  if (k < nu) {  // u = e_off + (z - E^T T), in the z slot
+    const Ell<WE> ec = ell_load<WE>(f, own_ec(d, k));
+    for (int m = tk; m < nr; m += sk) {
+      double* R = rec + (size_t)m * rd;
+      const double u = R[nu + k] + (R[k] - ell_dot(ec, T + m * FAST_MAXNS));
+      R[k] = u;
+      if (m >= kb || ((own >> m) & 1u)) d.U[(size_t)rows[m] * nu + k] = u;
+    }
   }
   __syncthreads();
-  FOR_NT(nr, m, j) {  // u B^T into the dead e_off slot
-    double* R = rec + (size_t)m * rd;
-    double bu = 0.0;
-    for (int e = op.brp[j]; e < op.brp[j + 1]; ++e) bu = fma(R[op.brc[e]], op.brv[e], bu);
-    R[nu + j] = bu;
+  if (j < nt) {  // u B^T into the dead e_off slot
+    const Ell<WE> br = ell_load<WE>(f, own_br(d, j));
+    for (int m = tj; m < nr; m += sj) {
+      double* R = rec + (size_t)m * rd;
+      R[nu + j] = ell_dot(br, R);
+    }
   }
   __syncthreads();
   if (threadIdx.x < nt) {
-    const int j = threadIdx.x;
-    double x = d.p[j];
+    double x = d.p[threadIdx.x];
     for (int m = 0; m < nr; ++m) {
       const double* R = rec + (size_t)m * rd;
-      x = (x + R[nu + j]) + R[2 * nu + j];
-      if (m >= kb || ((own >> m) & 1u)) d.X[(size_t)rows[m] * lx + j] = x;
+      x = (x + R[nu + threadIdx.x]) + R[2 * nu + threadIdx.x];
+      if (m >= kb || ((own >> m) & 1u)) d.X[(size_t)rows[m] * lx + threadIdx.x] = x;
     }
   }
 }
@@ -405,121 +445,153 @@ __global__ void __launch_bounds__(SC_THREADS) k_prox_nodes(FastView f) {
 
 // ---------------------------------------------------------------- k_prox_warp
 // Node-parallel Moreau prox without CTA barriers: two warps per node, operands
-// straight from global memory into registers (every load issued up front).
-//   warp 2m   : the tank part, lanes own columns j and j+32 of both tank slots;
-//               the two slot norms use numpy's pairwise order through an
-//               8-lane group each (pw_group8) on a per-warp shared array
-//   warp 2m+1 : the input part (plain box projection), columns k + 32q
+// straight from memory into registers (every load issued up front).
+//   x warp : the tank part, lanes own columns j and j+32 of both tank slots;
+//            the two slot norms use numpy's pairwise order through an 8-lane
+//            group each (pw_group8) on a per-warp shared array sd2 (2 x 64)
+//   u warp : the input part (plain box projection), columns k + 32q
 // Same expression order as prox_rows (bit-exact with numpy), V kept in registers.
+struct ProxIt {
+  int it;
+  bool next;
+  double gamma, ig, beta, theta, beta1, om;
+};
+__device__ __forceinline__ ProxIt prox_it(const FastView& f) {
+  const DevView& d = f.d;
+  ProxIt p;
+  p.it = *d.iter - 1;
+  p.next = p.it + 1 < f.max_iter;
+  p.gamma = d.gamma;
+  p.ig = f.inv_gamma;
+  p.beta = d.beta[p.it];
+  p.theta = d.theta[p.it];
+  p.beta1 = p.next ? d.beta[p.it + 1] : 0.0;
+  p.om = dsub(1.0, p.theta);
+  return p;
+}
+// x: the node's state row (lx stride not needed: x[j]), returns bad.
+__device__ __forceinline__ bool prox_x_warp(const FastView& f, const ProxIt& P, int r, const double* x_row,
+                                            double* sd2) {
+  const DevView& d = f.d;
+  const int nt = d.nt, W = d.W, lx = d.lx, ly = d.ly, lane = threadIdx.x & 31;
+  const size_t rw = (size_t)r * W;
+  const double* y = ybuf(d, P.it) + rw;
+  const double* ym = ybuf(d, P.it + 2) + rw;
+  double* yn = ybuf_w(d, P.it + 1) + rw;
+  const double gamma = P.gamma, ig = P.ig;
+  double xv[2], xa[2], y1[2], y2[2], m1[2], m2[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int j = lane + 32 * q;
+    const bool ok = j < nt;
+    xv[q] = ok ? x_row[j] : 0.0;
+    xa[q] = ok && P.it > 0 ? d.Xa[(size_t)r * lx + j] : 0.0;
+    y1[q] = ok ? y[j] : 0.0;
+    y2[q] = ok ? y[nt + j] : 0.0;
+    m1[q] = ok ? ym[j] : 0.0;
+    m2[q] = ok ? ym[nt + j] : 0.0;
+  }
+  double v1[2], v2[2], V1[2], V2[2], c1[2], c2[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int j = lane + 32 * q;
+    const bool ok = j < nt;
+    const double x = xv[q];
+    if (ok) d.Xa[(size_t)r * lx + j] = P.it == 0 ? x : dadd(dmul(xa[q], P.om), dmul(P.theta, x));
+    const double gx = dmul(gamma, x);
+    v1[q] = dadd(dadd(y1[q], dmul(P.beta, dsub(y1[q], m1[q]))), gx);
+    v2[q] = dadd(dadd(y2[q], dmul(P.beta, dsub(y2[q], m2[q]))), gx);
+    V1[q] = div_by(v1[q], gamma, ig);
+    V2[q] = div_by(v2[q], gamma, ig);
+    c1[q] = ok ? np_clip(V1[q], d.xmin[j], d.xmax[j]) : 0.0;
+    c2[q] = ok ? np_max(V2[q], d.xsafe[j]) : 0.0;
+    if (ok) {
+      const double df1 = dsub(V1[q], c1[q]), df2 = dsub(V2[q], c2[q]);
+      sd2[j] = dmul(df1, df1);
+      sd2[64 + j] = dmul(df2, df2);
+    }
+  }
+  __syncwarp();
+  double st = 0.0;
+  if (lane < 16) {
+    const int slot = lane >> 3;
+    const double ssum = pw_group8(sd2 + 64 * slot, nt, lane & 7, 0xffu << (lane & 8));
+    if ((lane & 7) == 0) {
+      const double dist = __dsqrt_rn(ssum);
+      const double thr = dmul(ig, slot ? d.w_s : d.w_x);  // prox parameter RN(1/gamma) (solver.py:571)
+      st = dist > 0.0 ? np_min(1.0, div_exact(thr, dist)) : 0.0;
+    }
+  }
+  const double st1 = __shfl_sync(0xffffffffu, st, 0), st2 = __shfl_sync(0xffffffffu, st, 8);
+  bool bad = false;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int j = lane + 32 * q;
+    if (j < nt) {
+      const double O1 = dsub(V1[q], dmul(st1, dsub(V1[q], c1[q])));
+      const double O2 = dsub(V2[q], dmul(st2, dsub(V2[q], c2[q])));
+      const double p1 = dsub(v1[q], dmul(gamma, O1)), p2 = dsub(v2[q], dmul(gamma, O2));
+      yn[j] = p1;
+      yn[nt + j] = p2;
+      bad |= !isfinite(p1) || !isfinite(p2);
+      if (P.next) {
+        const double w1 = dadd(p1, dmul(P.beta1, dsub(p1, y1[q])));
+        const double w2 = dadd(p2, dmul(P.beta1, dsub(p2, y2[q])));
+        d.Yc[(size_t)r * ly + j] = dadd(w1, w2);
+      }
+    }
+  }
+  __syncwarp();
+  return bad;
+}
+__device__ __forceinline__ bool prox_u_warp(const FastView& f, const ProxIt& P, int r, const double* u_row) {
+  const DevView& d = f.d;
+  const int nt = d.nt, nu = d.nu, W = d.W, lx = d.lx, ly = d.ly, lane = threadIdx.x & 31;
+  const size_t rw = (size_t)r * W;
+  const double* y = ybuf(d, P.it) + rw + 2 * nt;
+  const double* ym = ybuf(d, P.it + 2) + rw + 2 * nt;
+  double* yn = ybuf_w(d, P.it + 1) + rw + 2 * nt;
+  constexpr int Q = 4;  // nu <= 128
+  double uv[Q], ua[Q], y3[Q], m3[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int k = lane + 32 * q;
+    const bool ok = k < nu;
+    uv[q] = ok ? u_row[k] : 0.0;
+    ua[q] = ok && P.it > 0 ? d.Ua[(size_t)r * nu + k] : 0.0;
+    y3[q] = ok ? y[k] : 0.0;
+    m3[q] = ok ? ym[k] : 0.0;
+  }
+  bool bad = false;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int k = lane + 32 * q;
+    if (k < nu) {
+      const double u = uv[q];
+      d.Ua[(size_t)r * nu + k] = P.it == 0 ? u : dadd(dmul(ua[q], P.om), dmul(P.theta, u));
+      const double v3 = dadd(dadd(y3[q], dmul(P.beta, dsub(y3[q], m3[q]))), dmul(P.gamma, u));
+      const double V3 = div_by(v3, P.gamma, P.ig);
+      const double p3 = dsub(v3, dmul(P.gamma, np_clip(V3, d.umin[k], d.umax[k])));
+      yn[k] = p3;
+      bad |= !isfinite(p3);
+      if (P.next) d.Yc[(size_t)r * ly + lx + k] = dadd(p3, dmul(P.beta1, dsub(p3, y3[q])));
+    }
+  }
+  return bad;
+}
+
 constexpr int PW_ROWS = 4;  // nodes per 256-thread CTA
 __global__ void __launch_bounds__(256) k_prox_warp(FastView f) {
   const DevView& d = f.d;
-  const int nt = d.nt, nu = d.nu, W = d.W, lx = d.lx, ly = d.ly;
-  __shared__ double sd2[PW_ROWS][2][64];
+  __shared__ double sd2[PW_ROWS][128];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = warp >> 1;
   const int r = blockIdx.x * PW_ROWS + m;
   if (r >= d.n) return;
-  const int it = *d.iter - 1;
-  const bool next = it + 1 < f.max_iter;
-  const double gamma = d.gamma, ig = f.inv_gamma;
-  const double beta = d.beta[it], theta = d.theta[it], beta1 = next ? d.beta[it + 1] : 0.0;
-  const double om = dsub(1.0, theta);
-  const size_t rw = (size_t)r * W;
-  const double* y = ybuf(d, it) + rw;
-  const double* ym = ybuf(d, it + 2) + rw;
-  double* yn = ybuf_w(d, it + 1) + rw;
-  bool bad = false;
-  if ((warp & 1) == 0) {
-    double xv[2], xa[2], y1[2], y2[2], m1[2], m2[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int j = lane + 32 * q;
-      const bool ok = j < nt;
-      xv[q] = ok ? d.X[(size_t)r * lx + j] : 0.0;
-      xa[q] = ok && it > 0 ? d.Xa[(size_t)r * lx + j] : 0.0;
-      y1[q] = ok ? y[j] : 0.0;
-      y2[q] = ok ? y[nt + j] : 0.0;
-      m1[q] = ok ? ym[j] : 0.0;
-      m2[q] = ok ? ym[nt + j] : 0.0;
-    }
-    double v1[2], v2[2], V1[2], V2[2], c1[2], c2[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int j = lane + 32 * q;
-      const bool ok = j < nt;
-      const double x = xv[q];
-      if (ok) d.Xa[(size_t)r * lx + j] = it == 0 ? x : dadd(dmul(xa[q], om), dmul(theta, x));
-      const double gx = dmul(gamma, x);
-      v1[q] = dadd(dadd(y1[q], dmul(beta, dsub(y1[q], m1[q]))), gx);
-      v2[q] = dadd(dadd(y2[q], dmul(beta, dsub(y2[q], m2[q]))), gx);
-      V1[q] = div_by(v1[q], gamma, ig);
-      V2[q] = div_by(v2[q], gamma, ig);
-      c1[q] = ok ? np_clip(V1[q], d.xmin[j], d.xmax[j]) : 0.0;
-      c2[q] = ok ? np_max(V2[q], d.xsafe[j]) : 0.0;
-      if (ok) {
-        const double df1 = dsub(V1[q], c1[q]), df2 = dsub(V2[q], c2[q]);
-        sd2[m][0][j] = dmul(df1, df1);
-        sd2[m][1][j] = dmul(df2, df2);
-      }
-    }
-    __syncwarp();
-    double st = 0.0;
-    if (lane < 16) {
-      const int slot = lane >> 3;
-      const double ssum = pw_group8(sd2[m][slot], nt, lane & 7, 0xffu << (lane & 8));
-      if ((lane & 7) == 0) {
-        const double dist = __dsqrt_rn(ssum);
-        const double thr = dmul(ig, slot ? d.w_s : d.w_x);  // prox parameter RN(1/gamma) (solver.py:571)
-        st = dist > 0.0 ? np_min(1.0, div_exact(thr, dist)) : 0.0;
-      }
-    }
-    const double st1 = __shfl_sync(0xffffffffu, st, 0), st2 = __shfl_sync(0xffffffffu, st, 8);
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int j = lane + 32 * q;
-      if (j < nt) {
-        const double O1 = dsub(V1[q], dmul(st1, dsub(V1[q], c1[q])));
-        const double O2 = dsub(V2[q], dmul(st2, dsub(V2[q], c2[q])));
-        const double p1 = dsub(v1[q], dmul(gamma, O1)), p2 = dsub(v2[q], dmul(gamma, O2));
-        yn[j] = p1;
-        yn[nt + j] = p2;
-        bad |= !isfinite(p1) || !isfinite(p2);
-        if (next) {
-          const double w1 = dadd(p1, dmul(beta1, dsub(p1, y1[q])));
-          const double w2 = dadd(p2, dmul(beta1, dsub(p2, y2[q])));
-          d.Yc[(size_t)r * ly + j] = dadd(w1, w2);
-        }
-      }
-    }
-  } else {
-    constexpr int Q = 4;  // nu <= 128
-    double uv[Q], ua[Q], y3[Q], m3[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int k = lane + 32 * q;
-      const bool ok = k < nu;
-      uv[q] = ok ? d.U[(size_t)r * nu + k] : 0.0;
-      ua[q] = ok && it > 0 ? d.Ua[(size_t)r * nu + k] : 0.0;
-      y3[q] = ok ? y[2 * nt + k] : 0.0;
-      m3[q] = ok ? ym[2 * nt + k] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int k = lane + 32 * q;
-      if (k < nu) {
-        const double u = uv[q];
-        d.Ua[(size_t)r * nu + k] = it == 0 ? u : dadd(dmul(ua[q], om), dmul(theta, u));
-        const double v3 = dadd(dadd(y3[q], dmul(beta, dsub(y3[q], m3[q]))), dmul(gamma, u));
-        const double V3 = div_by(v3, gamma, ig);
-        const double p3 = dsub(v3, dmul(gamma, np_clip(V3, d.umin[k], d.umax[k])));
-        yn[2 * nt + k] = p3;
-        bad |= !isfinite(p3);
-        if (next) d.Yc[(size_t)r * ly + lx + k] = dadd(p3, dmul(beta1, dsub(p3, y3[q])));
-      }
-    }
-  }
-  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(d.bad_nu, it);
+  const ProxIt P = prox_it(f);
+  const bool bad = (warp & 1) == 0 ? prox_x_warp(f, P, r, d.X + (size_t)r * d.lx, sd2[m])
+                                   : prox_u_warp(f, P, r, d.U + (size_t)r * d.nu);
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(d.bad_nu, P.it);
 }
 
 // ---------------------------------------------------------------- k_chain_fused
