@@ -85,6 +85,13 @@ struct wmpc_ctx {
   int *gi_ptr = nullptr, *gi_item = nullptr, *gi_w = nullptr, *cpath = nullptr;
   unsigned* cown = nullptr;
   std::vector<std::pair<int, int>> gk_groups;  // (first row, rows) per stage group, bottom-up
+  std::pair<int, int> rep_group{0, 0};         // subtree sharding: replicated rows (first, count)
+  std::vector<int> h_cptr, h_cidx;             // host CSR children
+  double* Yc_save = nullptr;                   // certificate: APG state while Yc holds collapse(y)
+  int* acct = nullptr;                         // subtree sharding: rows counted in global sums
+  int* rep_gidx = nullptr;                     // per local row: global replicated index or -1
+  double* xbuf = nullptr;                      // exchange buffer (caller-owned device memory)
+  int n_rep_global = 0, shard_k = -1;
   size_t sm_up = 0, sm_grp = 0, sm_down = 0, sm_prox = 0;
   int up_threads = 512, down_threads = 512, prox_warp = 1;
   int *ell_cnt = nullptr, *ell_idx = nullptr;
@@ -162,6 +169,7 @@ DevView view(const wmpc_ctx* c) {
   d.U = c->U; d.X = c->X; d.Ua = c->Ua; d.Xa = c->Xa; d.wbar = c->wbar; d.lin = c->lin;
   d.theta = c->theta; d.beta = c->beta; d.iter = c->iter; d.bad_nu = c->bad_nu;
   d.gamma = c->gamma;
+  d.acct = c->acct;
   return d;
 }
 
@@ -260,12 +268,89 @@ void gk_up(wmpc_ctx* ctx, const FastView& f) {
   k_chain_up<WE><<<ctx->nchain, ctx->up_threads, ctx->sm_up, ctx->stream>>>(f);
 }
 template <int WE>
-void gk_grp(wmpc_ctx* ctx, const FastView& f) {
-  for (const auto& g : ctx->gk_groups) k_branch_grp<WE><<<g.second, SC_THREADS, ctx->sm_grp, ctx->stream>>>(f, g.first);
+void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump) {
+  for (const auto& g : ctx->gk_groups) {
+    k_branch_grp<WE><<<g.second, SC_THREADS, ctx->sm_grp, ctx->stream>>>(f, g.first, bump, GRP_FULL);
+    bump = 0;
+  }
+}
+template <int WE>
+void gk_rep(wmpc_ctx* ctx, const FastView& f, int mode, int bump) {
+  if (ctx->rep_group.second > 0)
+    k_branch_grp<WE><<<ctx->rep_group.second, SC_THREADS, ctx->sm_grp, ctx->stream>>>(f, ctx->rep_group.first, bump,
+                                                                                        mode);
 }
 template <int WE>
 void gk_down(wmpc_ctx* ctx, const FastView& f) {
   k_chain_down<WE><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);
+}
+
+// Branching-region stage groups, bottom-up, with <= 32 items per row, and
+// their item lists. Stages < k_rep (subtree sharding) form the replicated
+// group: its in-group items are limited to the rows this rank accounts for
+// (acct), its frontier is this rank's own stage-k_rep rows.
+void build_groups(wmpc_ctx* ctx, int k_rep, const int* acct) {
+  const int kstar = ctx->kstar;
+  const std::vector<int>& off = ctx->off;
+  const std::vector<int>& cptr = ctx->h_cptr;
+  const std::vector<int>& cidx = ctx->h_cidx;
+  const int nb = off[kstar];
+  std::vector<int> stage(std::max(nb, 1), 0);
+  for (int s = 0; s < kstar; ++s)
+    for (int r = off[s]; r < off[s + 1]; ++r) stage[r] = s;
+  auto items_of = [&](int r, int s_hi, std::vector<int>* it, std::vector<int>* wt) {
+    int cnt = 0;
+    std::vector<int> st(cidx.begin() + cptr[r], cidx.begin() + cptr[r + 1]);
+    std::vector<int> dep(st.size(), 1);
+    while (!st.empty()) {
+      const int e = st.back(), de = dep.back();
+      st.pop_back();
+      dep.pop_back();
+      const bool frontier = e >= off[s_hi + 1];
+      const bool counted = frontier || !acct || acct[e];
+      if (counted) ++cnt;
+      if (it && counted) {
+        it->push_back(e * 2 + (frontier ? 1 : 0));
+        wt->push_back(frontier ? de - 1 : de);
+      }
+      if (!frontier)
+        for (int c = cptr[e]; c < cptr[e + 1]; ++c) {
+          st.push_back(cidx[c]);
+          dep.push_back(de + 1);
+        }
+    }
+    return cnt;
+  };
+  ctx->gk_groups.clear();
+  ctx->rep_group = {0, 0};
+  std::vector<int> gip(nb + 1, 0), gii, giw;
+  std::vector<std::pair<int, int>> groups;  // (s_lo, s_hi), bottom-up
+  int s_hi = kstar - 1;
+  while (s_hi >= k_rep) {
+    int s_lo = s_hi;
+    while (s_lo > k_rep) {
+      int mx = 0;
+      for (int r = off[s_lo - 1]; r < off[s_lo]; ++r) mx = std::max(mx, items_of(r, s_hi, nullptr, nullptr));
+      if (mx > 32) break;
+      --s_lo;
+    }
+    groups.push_back({s_lo, s_hi});
+    s_hi = s_lo - 1;
+  }
+  std::vector<int> ghi(std::max(kstar, 1), 0);
+  for (auto& g : groups)
+    for (int st = g.first; st <= g.second; ++st) ghi[st] = g.second;
+  for (int st = 0; st < k_rep; ++st) ghi[st] = k_rep - 1;  // replicated group, frontier = stage k_rep
+  for (int r = 0; r < nb; ++r) {
+    items_of(r, ghi[stage[r]], &gii, &giw);
+    gip[r + 1] = (int)gii.size();
+  }
+  for (auto& g : groups) ctx->gk_groups.push_back({off[g.first], off[g.second + 1] - off[g.first]});
+  if (k_rep > 0) ctx->rep_group = {0, off[k_rep]};
+  if (gii.empty()) { gii.push_back(0); giw.push_back(0); }
+  upload_vec(ctx, &ctx->gi_ptr, gip);
+  upload_vec(ctx, &ctx->gi_item, gii);
+  upload_vec(ctx, &ctx->gi_w, giw);
 }
 
 // Graph-of-kernels scan path: operator blob, stage groups of the branching
@@ -379,61 +464,9 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
     upload_vec(ctx, &ctx->ell_val, val);
     ctx->ell_w = we;
   }
-  // stage of every branching row; stage groups bottom-up with <= 32 items per row
-  std::vector<int> stage(std::max(nb, 1), 0);
-  for (int s = 0; s < kstar; ++s)
-    for (int r = off[s]; r < off[s + 1]; ++r) stage[r] = s;
-  auto items_of = [&](int r, int s_hi, std::vector<int>* it, std::vector<int>* wt) {
-    int cnt = 0;
-    std::vector<int> st(cidx.begin() + cptr[r], cidx.begin() + cptr[r + 1]);
-    std::vector<int> dep(st.size(), 1);
-    while (!st.empty()) {
-      const int e = st.back(), de = dep.back();
-      st.pop_back();
-      dep.pop_back();
-      const bool frontier = e >= off[s_hi + 1];
-      ++cnt;
-      if (it) {
-        it->push_back(e * 2 + (frontier ? 1 : 0));
-        wt->push_back(frontier ? de - 1 : de);
-      }
-      if (!frontier)
-        for (int c = cptr[e]; c < cptr[e + 1]; ++c) {
-          st.push_back(cidx[c]);
-          dep.push_back(de + 1);
-        }
-    }
-    return cnt;
-  };
-  ctx->gk_groups.clear();
-  std::vector<int> gip(nb + 1, 0), gii, giw;
-  {
-    std::vector<std::pair<int, int>> groups;  // (s_lo, s_hi), bottom-up
-    int s_hi = kstar - 1;
-    while (s_hi >= 0) {
-      int s_lo = s_hi;
-      while (s_lo > 0) {
-        int mx = 0;
-        for (int r = off[s_lo - 1]; r < off[s_lo]; ++r) mx = std::max(mx, items_of(r, s_hi, nullptr, nullptr));
-        if (mx > 32) break;
-        --s_lo;
-      }
-      groups.push_back({s_lo, s_hi});
-      s_hi = s_lo - 1;
-    }
-    std::vector<int> ghi(std::max(kstar, 1), 0);
-    for (auto& g : groups)
-      for (int s = g.first; s <= g.second; ++s) ghi[s] = g.second;
-    for (int r = 0; r < nb; ++r) {
-      items_of(r, ghi[stage[r]], &gii, &giw);
-      gip[r + 1] = (int)gii.size();
-    }
-    for (auto& g : groups) ctx->gk_groups.push_back({off[g.first], off[g.second + 1] - off[g.first]});
-  }
-  if (gii.empty()) { gii.push_back(0); giw.push_back(0); }
-  upload_vec(ctx, &ctx->gi_ptr, gip);
-  upload_vec(ctx, &ctx->gi_item, gii);
-  upload_vec(ctx, &ctx->gi_w, giw);
+  ctx->h_cptr = cptr;
+  ctx->h_cidx = cidx;
+  build_groups(ctx, 0, nullptr);
   // chain root paths and ancestor ownership (first chain below a row writes it)
   std::vector<int> cpath((size_t)std::max(nchain * kstar, 1), 0);
   std::vector<unsigned> cown(nchain, 0u);
@@ -468,6 +501,9 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   std::vector<double> zl((size_t)ctx->n * nu, 0.0), za((size_t)(nb + nchain) * nu, 0.0);
   upload_vec(ctx, &ctx->Lb, zl);
   upload_vec(ctx, &ctx->Asub, za);
+  if (ctx->Yc_save) cudaFree(ctx->Yc_save);
+  ctx->Yc_save = nullptr;
+  dalloc(ctx, &ctx->Yc_save, (size_t)ctx->n * ly);
   if (ctx->ell_w == 4) gk_attrs<4>(ctx, up, down, grp);
   else gk_attrs<8>(ctx, up, down, grp);
   CK(cudaFuncSetAttribute(k_prox_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox));
@@ -732,17 +768,17 @@ void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
   const int nc = ctx->nchain;
   if (ctx->gk_groups.empty()) k_advance<<<1, 32, 0, st>>>(ctx->iter);  // else the first group kernel counts
   if (ctx->use_fused) {  // up pass of iteration 0 runs in wmpc_apg_begin
-    if (ctx->ell_w == 4) gk_grp<4>(ctx, f); else gk_grp<8>(ctx, f);
+    if (ctx->ell_w == 4) gk_grp<4>(ctx, f, 1); else gk_grp<8>(ctx, f, 1);
     k_chain_fused<<<nc, ctx->fused_threads, ctx->sm_fused, st>>>(f);
     return;
   }
   if (ctx->ell_w == 4) {
     gk_up<4>(ctx, f);
-    gk_grp<4>(ctx, f);
+    gk_grp<4>(ctx, f, 1);
     gk_down<4>(ctx, f);
   } else {
     gk_up<8>(ctx, f);
-    gk_grp<8>(ctx, f);
+    gk_grp<8>(ctx, f, 1);
     gk_down<8>(ctx, f);
   }
   if (ctx->prox_warp)
@@ -776,6 +812,38 @@ void launch_graphk(wmpc_ctx* ctx, int count) {
   for (; i + 8 <= count; i += 8) CK(cudaGraphLaunch(ctx->gk_exec8, ctx->stream));
   for (; i < count; ++i) CK(cudaGraphLaunch(ctx->gk_exec1, ctx->stream));
   ctx->launches += (int64_t)count * graphk_kernels(ctx);
+}
+
+// Dual-function minimiser z*(y) for the certificate (solver.py:454-456) with
+// the chain/branch kernels: Yc is saved, replaced by collapse(y), and the
+// up/branch/down passes write U, X into Uc, Xc. phase 0: up to the exchange
+// point (sharded: partial sums in xbuf); phase 1: the rest; -1: both.
+template <int WE>
+void dual_eval_graph(wmpc_ctx* ctx, const double* y, int phase) {
+  FastView f = make_fastview(ctx, 1);
+  f.d.U = ctx->Uc;
+  f.d.X = ctx->Xc;
+  const int nthr = 256;
+  if (phase <= 0) {
+    CK(cudaMemcpyAsync(ctx->Yc_save, ctx->Yc, sizeof(double) * (size_t)ctx->n * ctx->ly, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    k_collapse<<<grid_for((size_t)ctx->n * ctx->ly), nthr, 0, ctx->stream>>>(f.d, y, ctx->Yc);
+    gk_up<WE>(ctx, f);
+    gk_grp<WE>(ctx, f, 0);
+    if (ctx->rep_group.second > 0) {
+      CK(cudaMemsetAsync(ctx->xbuf, 0, sizeof(double) * 256 * (size_t)ctx->n_rep_global, ctx->stream));
+      gk_rep<WE>(ctx, f, GRP_PARTIAL, 0);
+    }
+    ctx->launches += 2 + ctx->gk_groups.size() + (ctx->rep_group.second > 0);
+  }
+  if (phase != 0) {
+    if (ctx->rep_group.second > 0) gk_rep<WE>(ctx, f, GRP_FINISH, 0);
+    k_chain_down<WE><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);
+    CK(cudaMemcpyAsync(ctx->Yc, ctx->Yc_save, sizeof(double) * (size_t)ctx->n * ctx->ly, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    ctx->launches += 1 + (ctx->rep_group.second > 0);
+  }
+  check_launch(ctx);
 }
 
 FastView make_fastview(wmpc_ctx* ctx, int count) {
@@ -814,6 +882,8 @@ FastView make_fastview(wmpc_ctx* ctx, int count) {
   f.ell_idx = ctx->ell_idx;
   f.ell_val = ctx->ell_val;
   f.ell_w = ctx->ell_w;
+  f.xbuf = ctx->xbuf;
+  f.rep_gidx = ctx->rep_gidx;
   f.pb = ctx->fused_pb;
   f.ring_off = ctx->fused_ring_off;
   f.work_doubles = ctx->scan_work;
@@ -883,7 +953,7 @@ void free_all(wmpc_ctx* c) {
                   c->bad_row, c->part, c->scal, c->d_np, c->chain_node,
                   c->bc_ptr, c->bc_row, c->br_ptr, c->br_col, c->off_dev, c->bc_val, c->br_val,
                   c->e_ptr, c->e_col, c->e_val, c->aux,
-                  c->Lb, c->Asub, c->blob, c->store_it, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
+                  c->Lb, c->Asub, c->blob, c->store_it, c->Yc_save, c->acct, c->rep_gidx, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
                   c->pj_ecv, c->dk_mv, c->dk_sweeps, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
                   c->prof};
   for (void* p : ptrs)
@@ -1566,7 +1636,12 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
     DevView dc = d;
     dc.U = ctx->Uc;
     dc.X = ctx->Xc;
-    launch_dg(ctx, dc, y, 0);
+    if (ctx->fast && ctx->use_graphk) {
+      if (ctx->ell_w == 4) dual_eval_graph<4>(ctx, y, -1);
+      else dual_eval_graph<8>(ctx, y, -1);
+    } else {
+      launch_dg(ctx, dc, y, 0);
+    }
     double td[4];
     cost_terms(ctx, dc, ctx->Uc, ctx->Xc, y, 0, td);
     double inner = td[0] + td[1];

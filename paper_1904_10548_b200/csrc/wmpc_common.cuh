@@ -55,6 +55,7 @@ struct DevView {
   int* iter;
   int* bad_nu;
   double gamma;
+  const int* acct;  // subtree sharding: rows this rank accounts for in global sums (null: all)
 };
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }

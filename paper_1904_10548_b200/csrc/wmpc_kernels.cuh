@@ -364,6 +364,7 @@ __global__ void k_cost_partial(DevView d, const double* __restrict__ Uin, const 
   int wpb = blockDim.x >> 5;
   double acc_cost = 0.0, acc_dot = 0.0, acc_box = 0.0, acc_safe = 0.0;
   for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < d.n; r += gridDim.x * wpb) {
+    if (d.acct && !d.acct[r]) continue;
     const double* u = Uin + (size_t)r * nu;
     int a = d.anc[r];
     const double* ua = a < 0 ? d.q : Uin + (size_t)a * nu;
@@ -435,6 +436,7 @@ __global__ void k_gconj_partial(DevView d, const double* __restrict__ y, double 
   double acc = 0.0, viol = 0.0;
   const double slack = 1.0 + tol;
   for (int r = blockIdx.x * wpb + (threadIdx.x >> 5); r < d.n; r += gridDim.x * wpb) {
+    if (d.acct && !d.acct[r]) continue;
     const double* yr = y + (size_t)r * W;
     double n1 = 0.0, n2 = 0.0, sup = 0.0, v = 0.0;
     for (int j = lane; j < nt; j += 32) {

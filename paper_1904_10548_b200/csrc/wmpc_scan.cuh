@@ -227,13 +227,20 @@ __global__ void __launch_bounds__(512) k_chain_up(FastView f) {
 //   W2 = sum_{d in desc_B(r)} wbar_d = sum_0 w Yx_e + sum_1 w wbar_f
 //   Su = sum_0 (Yu_e + R_e) + sum_1 Asub_f
 //   a_r = (Yu_r + W1 B) + R_r,  S_r = Su + W2 B,  lin_r = a_r + P S_r.
+//
+// Subtree sharding (shard.py): a row replicated on several ranks runs twice.
+// mode GRP_PARTIAL writes the item sums (without the row's own Yx) into the
+// exchange buffer at the row's global replicated index; after the host-level
+// all-reduce over ranks, mode GRP_FINISH reads them back and finishes the row
+// identically on every rank. bump: first kernel of an APG iteration.
+enum { GRP_FULL = 0, GRP_PARTIAL = 1, GRP_FINISH = 2 };
 template <int WE>
-__global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0) {
+__global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, int bump, int mode) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly;
   const int r = r0 + blockIdx.x;
   constexpr int NW = SC_THREADS / 32;
-  if (r0 == f.n_branch - gridDim.x && blockIdx.x == 0 && threadIdx.x == 0) *d.iter += 1;  // first kernel of the iteration
+  if (bump && blockIdx.x == 0 && threadIdx.x == 0) *d.iter += 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* part = reinterpret_cast<double*>(smem_raw);  // NW x 256: [s1 64 | s2 64 | su 128]
   double* W1 = part + NW * 256;  // lx
@@ -244,7 +251,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0) {
   const NodePtrs np = *d.np;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double s1[2] = {0.0, 0.0}, s2[2] = {0.0, 0.0}, su[4] = {0.0, 0.0, 0.0, 0.0};
-  const int e0 = f.gi_ptr[r], e1 = f.gi_ptr[r + 1];
+  const int e0 = mode == GRP_FINISH ? 0 : f.gi_ptr[r], e1 = mode == GRP_FINISH ? 0 : f.gi_ptr[r + 1];
   for (int e = e0 + warp; e < e1; e += NW) {
     const int item = f.gi_item[e];
     const size_t row = (size_t)(item >> 1);
@@ -279,12 +286,28 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) pw[128 + lane + 32 * i] = su[i];
   __syncthreads();
+  double* xb = mode == GRP_FULL ? nullptr : f.xbuf + (size_t)f.rep_gidx[r] * 256;
+  if (mode == GRP_PARTIAL) {  // item sums to the exchange buffer
+    for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+      double a = part[c];
+      for (int w = 1; w < NW; ++w) a += part[w * 256 + c];
+      xb[c] = a;
+    }
+    return;
+  }
   if (threadIdx.x < nt) {
     const int j = threadIdx.x;
-    double a1 = part[j], a2 = part[64 + j];
-    for (int w = 1; w < NW; ++w) {
-      a1 += part[w * 256 + j];
-      a2 += part[w * 256 + 64 + j];
+    double a1, a2;
+    if (xb) {
+      a1 = xb[j];
+      a2 = xb[64 + j];
+    } else {
+      a1 = part[j];
+      a2 = part[64 + j];
+      for (int w = 1; w < NW; ++w) {
+        a1 += part[w * 256 + j];
+        a2 += part[w * 256 + 64 + j];
+      }
     }
     W1[j] = d.Yc[(size_t)r * ly + j] + a1;
     W2[j] = a2;
@@ -292,8 +315,13 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0) {
   __syncthreads();
   if (threadIdx.x < nu) {
     const int k = threadIdx.x;
-    double s = part[128 + k];
-    for (int w = 1; w < NW; ++w) s += part[w * 256 + 128 + k];
+    double s;
+    if (xb) {
+      s = xb[128 + k];
+    } else {
+      s = part[128 + k];
+      for (int w = 1; w < NW; ++w) s += part[w * 256 + 128 + k];
+    }
     double b1 = 0.0, b2 = 0.0;
     const Ell<WE> bc = ell_load<WE>(f, own_bc(d, k));
     b1 = ell_dot(bc, W1);
@@ -592,6 +620,19 @@ __global__ void __launch_bounds__(256) k_prox_warp(FastView f) {
   const bool bad = (warp & 1) == 0 ? prox_x_warp(f, P, r, d.X + (size_t)r * d.lx, sd2[m])
                                    : prox_u_warp(f, P, r, d.U + (size_t)r * d.nu);
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(d.bad_nu, P.it);
+}
+
+// Collapsed dual of a given y (no extrapolation): Yc = [y1 + y2 | y3], for
+// evaluating the dual function with the chain/branch kernels (certificate).
+__global__ void k_collapse(DevView d, const double* __restrict__ y, double* Yc) {
+  const int nt = d.nt, nu = d.nu, W = d.W, lx = d.lx, ly = d.ly;
+  const size_t len = (size_t)d.n * ly;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / ly;
+    const int c = (int)(i - r * ly);
+    const double* yr = y + r * W;
+    Yc[i] = c < nt ? yr[c] + yr[nt + c] : (c < lx ? 0.0 : (c - lx < nu ? yr[2 * nt + c - lx] : 0.0));
+  }
 }
 
 // ---------------------------------------------------------------- k_chain_fused
