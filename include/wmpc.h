@@ -154,6 +154,49 @@ int64_t wmpc_launch_count(const wmpc_ctx* ctx);
 int wmpc_host_alloc(uint64_t bytes, void** out);
 void wmpc_host_free(void* p);
 
+/* ---- Subtree sharding across GPUs (host side in shard.py).
+ * The context holds one rank's rows: its own stage-k subtrees plus their
+ * ancestors (stages < k), which are replicated on every rank sharing them.
+ * Per APG iteration the replicated rows need the item sums of all ranks'
+ * subtrees: phase 0 writes this rank's partial sums into the exchange buffer
+ * (n_rep_global x 256 doubles, caller-owned device memory, zero except this
+ * rank's rows), the caller all-reduces (sum) it across ranks, phase 1
+ * finishes the replicated rows identically on every rank and runs the down
+ * pass and the prox. With k = 0 there is nothing to exchange.
+ * rep_gidx[r]: global index of local row r among the replicated rows, or -1;
+ * acct[r]: 1 if this rank accounts for row r in global sums (its own rows and
+ * the replicated rows whose lowest holder it is). Replaces the single-process
+ * loop of solve() (solver.py:460-506) for one rank. */
+int wmpc_shard_setup(wmpc_ctx* ctx, int k_stage, int n_rep_global, const int64_t* rep_gidx,
+                     const int64_t* acct);
+/* Before wmpc_set_structure of a shard: rows at stages < stage are treated as
+ * branching rows even where this rank holds a single child (the replicated
+ * rows must go through the exchange, not the chain scans). */
+int wmpc_set_min_branch_stage(wmpc_ctx* ctx, int stage);
+int wmpc_shard_set_exchange(wmpc_ctx* ctx, void* device_buffer);
+int wmpc_shard_step(wmpc_ctx* ctx, int phase);
+/* R of a replicated row (sum over its children, solver.py:269-274) spans
+ * ranks: phase 0 writes this rank's accounted children, the caller sums the
+ * exchange buffer across ranks, phase 1 stores the totals. Once per factor. */
+int wmpc_shard_fix_R(wmpc_ctx* ctx, int phase);
+/* Wait for the context's stream (before the caller touches the exchange buffer). */
+int wmpc_sync(wmpc_ctx* ctx);
+/* Certificate pieces for a sharded solve (solver.py:449-457, problem.py:221-250):
+ * local max|Ua| (the Dykstra tolerance is global), local per-sweep Dykstra
+ * movement maxima (mv[max_sweeps]; the global stop sweep is the first whose
+ * all-rank max is <= tol), the dual minimiser in two phases around the same
+ * exchange as wmpc_shard_step, and the raw accounted sums
+ * terms = [primal cost, <y,Hz> (0), box^2, safe^2 | dual cost, <y,Hz>, -, - |
+ *          g* support sum, g* domain violation]. */
+int wmpc_cert_absmax(wmpc_ctx* ctx, double* absmax);
+int wmpc_cert_dykstra(wmpc_ctx* ctx, int max_sweeps, double* mv);
+int wmpc_shard_dual_eval(wmpc_ctx* ctx, int phase);
+int wmpc_cert_terms(wmpc_ctx* ctx, int sweeps, double* terms);
+/* u0 from the stage-1 rows gathered in global order (k_u0 on the host:
+ * clip(sum_r fma(p_r, u_r)), bit-identical to the device kernel). */
+void wmpc_u0_rows(int nu, int mu1, const double* prob, const double* rows, const double* u_min,
+                  const double* u_max, double* u0);
+
 #ifdef __cplusplus
 }
 #endif

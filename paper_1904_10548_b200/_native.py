@@ -73,6 +73,17 @@ SIGNATURES = {
     "wmpc_launch_count": (C.c_int64, [_vp]),
     "wmpc_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_vp)]),
     "wmpc_host_free": (None, [_vp]),
+    "wmpc_shard_setup": (C.c_int, [_vp, C.c_int, C.c_int, _ip, _ip]),
+    "wmpc_shard_set_exchange": (C.c_int, [_vp, _vp]),
+    "wmpc_shard_step": (C.c_int, [_vp, C.c_int]),
+    "wmpc_sync": (C.c_int, [_vp]),
+    "wmpc_set_min_branch_stage": (C.c_int, [_vp, C.c_int]),
+    "wmpc_shard_fix_R": (C.c_int, [_vp, C.c_int]),
+    "wmpc_cert_absmax": (C.c_int, [_vp, _dp]),
+    "wmpc_cert_dykstra": (C.c_int, [_vp, C.c_int, _dp]),
+    "wmpc_shard_dual_eval": (C.c_int, [_vp, C.c_int]),
+    "wmpc_cert_terms": (C.c_int, [_vp, C.c_int, _dp]),
+    "wmpc_u0_rows": (None, [C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp]),
 }
 
 _LIB = None

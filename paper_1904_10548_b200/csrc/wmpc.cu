@@ -91,7 +91,7 @@ struct wmpc_ctx {
   int* acct = nullptr;                         // subtree sharding: rows counted in global sums
   int* rep_gidx = nullptr;                     // per local row: global replicated index or -1
   double* xbuf = nullptr;                      // exchange buffer (caller-owned device memory)
-  int n_rep_global = 0, shard_k = -1;
+  int n_rep_global = 0, shard_k = -1, kstar_min = 0;
   size_t sm_up = 0, sm_grp = 0, sm_down = 0, sm_prox = 0;
   int up_threads = 512, down_threads = 512, prox_warp = 1;
   int *ell_cnt = nullptr, *ell_idx = nullptr;
@@ -230,6 +230,17 @@ double gconj_value(wmpc_ctx* ctx, const DevView& d, const double* y) {
   d2h(ctx, h, ctx->scal, 2 * sizeof(double));
   sync(ctx);
   return h[1] > 0.0 ? INFINITY : h[0];
+}
+
+void gconj_raw(wmpc_ctx* ctx, const DevView& d, const double* y, double out[2]) {
+  int nb = std::min(ctx->part_blocks, std::max(1, (ctx->n + 7) / 8));
+  ctx->launches += 3;
+  k_gconj_partial<<<nb, 256, 0, ctx->stream>>>(d, y, 1e-9, ctx->part);
+  k_finish<0><<<1, 256, 0, ctx->stream>>>(ctx->part, nb, 2, 0, 1, ctx->scal);
+  k_finish<1><<<1, 256, 0, ctx->stream>>>(ctx->part, nb, 2, 1, 1, ctx->scal);
+  check_launch(ctx);
+  d2h(ctx, out, ctx->scal, 2 * sizeof(double));
+  sync(ctx);
 }
 
 template <class T>
@@ -590,6 +601,7 @@ void configure_fast(wmpc_ctx* ctx, const double* B, const double* E, const doubl
     if (!ok) break;
     kstar = s;
   }
+  kstar = std::max(kstar, std::min(ctx->kstar_min, H - 1));  // shards: replicated rows stay branching rows
   const int nchain = off[kstar + 1] - off[kstar];
   std::vector<int> chain((size_t)(H - kstar) * nchain);
   for (int i = 0; i < nchain; ++i) {
@@ -967,6 +979,35 @@ void free_all(wmpc_ctx* c) {
   if (c->ev2) cudaEventDestroy(c->ev2);
   if (c->ev3) cudaEventDestroy(c->ev3);
   if (c->stream) cudaStreamDestroy(c->stream);
+}
+
+template <int WE>
+void shard_step(wmpc_ctx* ctx, int phase) {
+  FastView f = make_fastview(ctx, 1);
+  const bool rep = ctx->rep_group.second > 0;
+  if (phase == 0) {
+    int bump = 1;
+    if (ctx->gk_groups.empty() && !rep) {
+      k_advance<<<1, 32, 0, ctx->stream>>>(ctx->iter);
+      bump = 0;
+    }
+    gk_up<WE>(ctx, f);
+    gk_grp<WE>(ctx, f, bump);
+    if (rep) {
+      CK(cudaMemsetAsync(ctx->xbuf, 0, sizeof(double) * 256 * (size_t)ctx->n_rep_global, ctx->stream));
+      gk_rep<WE>(ctx, f, GRP_PARTIAL, ctx->gk_groups.empty() ? 1 : 0);
+    }
+    ctx->launches += 1 + ctx->gk_groups.size() + rep;
+  } else {
+    if (rep) gk_rep<WE>(ctx, f, GRP_FINISH, 0);
+    gk_down<WE>(ctx, f);
+    if (ctx->prox_warp)
+      k_prox_warp<<<(ctx->n + PW_ROWS - 1) / PW_ROWS, 256, 0, ctx->stream>>>(f);
+    else
+      k_prox_nodes<<<(ctx->n + SC_NPB - 1) / SC_NPB, SC_THREADS, ctx->sm_prox, ctx->stream>>>(f);
+    ctx->launches += 2 + rep;
+  }
+  check_launch(ctx);
 }
 
 }  // namespace
@@ -1517,6 +1558,10 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
 
 int wmpc_apg_run(wmpc_ctx* ctx, int count) {
   return run(ctx, [&]() -> int {
+    if (ctx->shard_k > 0) {
+      ctx->err = "a shard with replicated rows advances through wmpc_shard_step";
+      return WMPC_E_STATE;
+    }
     if (ctx->fast && ctx->max_iter > 0) {
       ARG(count >= 0 && ctx->it_host + count <= ctx->max_iter, "iteration count exceeds the theta table");
       if (count > 0) launch_fast(ctx, count);
@@ -1538,6 +1583,10 @@ int wmpc_apg_run(wmpc_ctx* ctx, int count) {
 
 int wmpc_apg_run_timed(wmpc_ctx* ctx, int count, float* ms) {
   return run(ctx, [&]() -> int {
+    if (ctx->shard_k > 0) {
+      ctx->err = "a shard with replicated rows advances through wmpc_shard_step";
+      return WMPC_E_STATE;
+    }
     if (ctx->fast && ctx->max_iter > 0) {
       ARG(count >= 0 && ctx->it_host + count <= ctx->max_iter, "iteration count exceeds the theta table");
       CK(cudaEventRecord(ctx->ev2, ctx->stream));
@@ -1597,6 +1646,10 @@ int wmpc_apg_check(wmpc_ctx* ctx, double* primal_residual, double* image_scale, 
 
 int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
   return run(ctx, [&]() -> int {
+    if (ctx->shard_k > 0) {
+      ctx->err = "a shard with replicated rows certifies through wmpc_cert_* and the exchange";
+      return WMPC_E_STATE;
+    }
     int st = need_ready(ctx);
     if (st) return st;
     DevView d = view(ctx);
@@ -1771,6 +1824,197 @@ int wmpc_profile_fast(wmpc_ctx* ctx, int count, uint64_t* counters, int cap) {
     sync(ctx);
     return WMPC_OK;
   });
+}
+
+// ---------------------------------------------------------------- sharding
+int wmpc_shard_setup(wmpc_ctx* ctx, int k_stage, int n_rep_global, const int64_t* rep_gidx, const int64_t* acct) {
+  return run(ctx, [&]() -> int {
+    if (!ctx->have_structure || !ctx->fast || !ctx->use_graphk) {
+      ctx->err = "subtree sharding needs the structured graph path (A = I, W = cI) and a set structure";
+      return WMPC_E_STATE;
+    }
+    ARG(k_stage >= 0 && k_stage <= ctx->kstar, "shard stage must lie in the branching region");
+    ARG(rep_gidx && acct && n_rep_global >= 0, "null shard argument");
+    ARG(k_stage == 0 || n_rep_global >= 1, "replicated rows need an exchange buffer");
+    const int n = ctx->n;
+    std::vector<int> ac(n), rg(n);
+    for (int r = 0; r < n; ++r) {
+      ac[r] = acct[r] ? 1 : 0;
+      rg[r] = (int)rep_gidx[r];
+      ARG(rg[r] < n_rep_global, "replicated index out of range");
+      ARG((r < ctx->off[k_stage]) == (rg[r] >= 0), "rows above the shard stage (and only those) are replicated");
+    }
+    upload_vec(ctx, &ctx->acct, ac);
+    upload_vec(ctx, &ctx->rep_gidx, rg);
+    ctx->n_rep_global = n_rep_global;
+    ctx->shard_k = k_stage;
+    build_groups(ctx, k_stage, ac.data());
+    ctx->gk_gamma = -1.0;  // groups changed: recapture the iteration graphs
+    sync(ctx);
+    return WMPC_OK;
+  });
+}
+
+int wmpc_set_min_branch_stage(wmpc_ctx* ctx, int stage) {
+  return run(ctx, [&]() -> int {
+    ARG(stage >= 0 && stage < ctx->H, "stage out of range");
+    ctx->kstar_min = stage;
+    return WMPC_OK;
+  });
+}
+
+int wmpc_sync(wmpc_ctx* ctx) {
+  return run(ctx, [&]() -> int {
+    sync(ctx);
+    return WMPC_OK;
+  });
+}
+
+int wmpc_shard_set_exchange(wmpc_ctx* ctx, void* device_buffer) {
+  return run(ctx, [&]() -> int {
+    ctx->xbuf = static_cast<double*>(device_buffer);
+    return WMPC_OK;
+  });
+}
+
+int wmpc_shard_step(wmpc_ctx* ctx, int phase) {
+  return run(ctx, [&]() -> int {
+    if (ctx->shard_k < 0 || ctx->max_iter <= 0) {
+      ctx->err = "wmpc_shard_setup and wmpc_apg_begin must precede wmpc_shard_step";
+      return WMPC_E_STATE;
+    }
+    ARG(phase == 0 || phase == 1, "phase must be 0 or 1");
+    ARG(ctx->it_host < ctx->max_iter, "iteration count exceeds the theta table");
+    ARG(ctx->rep_group.second == 0 || ctx->xbuf, "exchange buffer not set");
+    if (ctx->ell_w == 4) shard_step<4>(ctx, phase);
+    else shard_step<8>(ctx, phase);
+    if (phase == 1) ctx->it_host += 1;
+    return WMPC_OK;
+  });
+}
+
+int wmpc_shard_fix_R(wmpc_ctx* ctx, int phase) {
+  return run(ctx, [&]() -> int {
+    if (ctx->shard_k < 0 || !ctx->nodes || !ctx->xbuf) {
+      ctx->err = "wmpc_shard_setup, node data and the exchange buffer must precede wmpc_shard_fix_R";
+      return WMPC_E_STATE;
+    }
+    ARG(phase == 0 || phase == 1, "phase must be 0 or 1");
+    if (ctx->n_rep_global == 0) return WMPC_OK;
+    if (phase == 0) CK(cudaMemsetAsync(ctx->xbuf, 0, sizeof(double) * 256 * (size_t)ctx->n_rep_global, ctx->stream));
+    DevView d = view(ctx);
+    ctx->launches++;
+    k_shard_R<<<(int)(((size_t)ctx->n * 32 + 255) / 256), 256, 0, ctx->stream>>>(d, ctx->nodes->e_off, ctx->rep_gidx,
+                                                                              ctx->xbuf, phase, ctx->nodes->R);
+    check_launch(ctx);
+    sync(ctx);
+    return WMPC_OK;
+  });
+}
+
+int wmpc_cert_absmax(wmpc_ctx* ctx, double* absmax) {
+  return run(ctx, [&]() -> int {
+    ARG(absmax, "null argument");
+    const size_t nU = (size_t)ctx->n * ctx->nu;
+    const int nb0 = grid_for(nU);
+    ctx->launches += 2;
+    k_absmax_partial<<<nb0, 256, 0, ctx->stream>>>(ctx->Ua, nU, ctx->part);
+    k_finish<1><<<1, 256, 0, ctx->stream>>>(ctx->part, nb0, 1, 0, 1, ctx->scal);
+    check_launch(ctx);
+    d2h(ctx, absmax, ctx->scal, sizeof(double));
+    sync(ctx);
+    return WMPC_OK;
+  });
+}
+
+int wmpc_cert_dykstra(wmpc_ctx* ctx, int max_sweeps, double* mv) {
+  return run(ctx, [&]() -> int {
+    int st = need_ready(ctx);
+    if (st) return st;
+    ARG(mv && max_sweeps >= 1 && max_sweeps <= 512, "bad Dykstra arguments");
+    std::vector<unsigned long long> bits(max_sweeps, 0ull);
+    if (ctx->ns > 0) {
+      DevView d = view(ctx);
+      DykOps po{ctx->pj_kp, ctx->pj_kc, ctx->pj_ecp, ctx->pj_ecr, ctx->pj_kv, ctx->pj_ecv};
+      CK(cudaMemsetAsync(ctx->dk_mv, 0, sizeof(unsigned long long) * 512, ctx->stream));
+      ctx->launches++;
+      k_dyk_warp<<<(ctx->n + 7) / 8, 256, 0, ctx->stream>>>(d, po, ctx->Ua, nullptr, ctx->dk_mv, ctx->dk_sweeps,
+                                                            max_sweeps, 1);
+      check_launch(ctx);
+      d2h(ctx, bits.data(), ctx->dk_mv, sizeof(unsigned long long) * max_sweeps);
+      sync(ctx);
+    }
+    for (int i = 0; i < max_sweeps; ++i) std::memcpy(mv + i, &bits[i], sizeof(double));
+    return WMPC_OK;
+  });
+}
+
+int wmpc_shard_dual_eval(wmpc_ctx* ctx, int phase) {
+  return run(ctx, [&]() -> int {
+    int st = need_ready(ctx);
+    if (st) return st;
+    ARG(phase == 0 || phase == 1, "phase must be 0 or 1");
+    if (!ctx->fast || !ctx->use_graphk) {
+      ctx->err = "sharded certificate needs the structured graph path";
+      return WMPC_E_STATE;
+    }
+    const double* y = ctx->Y[ctx->it_host % 3];
+    if (ctx->ell_w == 4) dual_eval_graph<4>(ctx, y, phase);
+    else dual_eval_graph<8>(ctx, y, phase);
+    return WMPC_OK;
+  });
+}
+
+int wmpc_cert_terms(wmpc_ctx* ctx, int sweeps, double* terms) {
+  return run(ctx, [&]() -> int {
+    int st = need_ready(ctx);
+    if (st) return st;
+    ARG(terms && sweeps >= 1 && sweeps <= 512, "bad certificate arguments");
+    DevView d = view(ctx);
+    const size_t nU = (size_t)ctx->n * ctx->nu;
+    if (ctx->ns == 0) {
+      ctx->launches++;
+      k_clip_inputs<<<grid_for(nU), 256, 0, ctx->stream>>>(d, ctx->Ua, ctx->Uf);
+    } else {
+      h2d(ctx, ctx->dk_sweeps, &sweeps, sizeof(int));
+      DykOps po{ctx->pj_kp, ctx->pj_kc, ctx->pj_ecp, ctx->pj_ecr, ctx->pj_kv, ctx->pj_ecv};
+      ctx->launches++;
+      k_dyk_warp<<<(ctx->n + 7) / 8, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, sweeps,
+                                                            2);
+    }
+    for (int s = 0; s < ctx->H; ++s) {
+      int cnt = ctx->off[s + 1] - ctx->off[s];
+      ctx->launches++;
+      k_rollout_stage<<<grid_for((size_t)cnt * ctx->nt), 256, 0, ctx->stream>>>(d, ctx->off[s], cnt, ctx->Uf, ctx->Xf);
+    }
+    check_launch(ctx);
+    double tp[4], td[4], g[2];
+    cost_terms(ctx, d, ctx->Uf, ctx->Xf, nullptr, 1, tp);
+    const double* y = ctx->Y[ctx->it_host % 3];
+    DevView dc = d;
+    dc.U = ctx->Uc;
+    dc.X = ctx->Xc;
+    cost_terms(ctx, dc, ctx->Uc, ctx->Xc, y, 0, td);
+    gconj_raw(ctx, d, y, g);
+    for (int i = 0; i < 4; ++i) {
+      terms[i] = tp[i];
+      terms[4 + i] = td[i];
+    }
+    terms[8] = g[0];
+    terms[9] = g[1];
+    return WMPC_OK;
+  });
+}
+
+void wmpc_u0_rows(int nu, int mu1, const double* prob, const double* rows, const double* u_min, const double* u_max,
+                  double* u0) {
+  for (int j = 0; j < nu; ++j) {
+    double s = 0.0;
+    for (int r = 0; r < mu1; ++r) s = std::fma(prob[r], rows[(size_t)r * nu + j], s);
+    const double lo = u_min[j], hi = u_max[j];
+    const double m = std::isnan(s) ? s : (s > lo ? s : lo);  // np.clip (k_u0)
+    u0[j] = std::isnan(m) ? m : (m < hi ? m : hi);
+  }
 }
 
 }  // extern "C"

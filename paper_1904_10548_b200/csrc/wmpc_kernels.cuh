@@ -585,6 +585,37 @@ __global__ void k_node_R(DevView d, const double* __restrict__ e_off, double* Ro
   }
 }
 
+// Subtree sharding: R of a replicated row sums over children on several ranks.
+// phase 0: this rank's accounted children into the exchange buffer;
+// phase 1 (after the cross-rank sum): the full R back into the row.
+__global__ void k_shard_R(DevView d, const double* __restrict__ e_off, const int* __restrict__ rep_gidx,
+                          double* xbuf, int phase, double* Rout) {
+  const int nu = d.nu;
+  int lane = threadIdx.x & 31;
+  int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= d.n || rep_gidx[r] < 0) return;
+  double* xb = xbuf + (size_t)rep_gidx[r] * 256;
+  for (int j = lane; j < nu; j += 32) {
+    if (phase == 1) {
+      Rout[(size_t)r * nu + j] = xb[j];
+      continue;
+    }
+    double acc = 0.0;
+    for (int e = d.cptr[r]; e < d.cptr[r + 1]; ++e) {
+      int c = d.cidx[e];
+      if (!d.acct[c]) continue;
+      double ew = 0.0;
+      if (d.w_scalar) {
+        ew = e_off[(size_t)c * nu + j] * d.w_c;
+      } else {
+        for (int k = 0; k < nu; ++k) ew = fma(e_off[(size_t)c * nu + k], d.Wu[(size_t)k * nu + j], ew);
+      }
+      acc += (-2.0 * d.prob[c]) * ew;
+    }
+    xb[j] = acc;
+  }
+}
+
 // Chain-local prefix of e_off for the scan-form kernel: for the node at chain
 // position t, sum_{t' < t} e_off[chain node t'] (sequential, top to leaf).
 __global__ void k_chain_ebar(const int* __restrict__ chain_node, int nchain, int nst, int nu,

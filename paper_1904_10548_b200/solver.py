@@ -217,6 +217,14 @@ def _upload_structure(dev: _DeviceTree, instance, basis, e_pinv, lam, t_mat, d_g
 def factor_step(instance, structure_from: FactorCache | None = None) -> FactorCache:
     """Build or rebind the factor cache (solver.py:150-239); the per-node part
     runs on the GPU (kernel ``k_node_offsets``)."""
+    return _factor(instance, structure_from, private=False)
+
+
+def _factor(instance, structure_from: FactorCache | None, private: bool,
+            min_branch_stage: int = 0) -> FactorCache:
+    """factor_step; ``private`` gives the cache its own native context instead
+    of the per-structure pool (shard.py: several shards of one structure live
+    in one process); ``min_branch_stage``: see wmpc_set_min_branch_stage."""
     m = instance.model
     sig = _structure_signature(instance)
     if structure_from is not None:
@@ -239,8 +247,10 @@ def factor_step(instance, structure_from: FactorCache | None = None) -> FactorCa
         H = len(instance.stage_slices)
         kappa = 2.0 * w_min * p_min / (H * max(instance.n_nonroot, 1))
         lipschitz = None
-        dev = _device_for(sig, instance)
+        dev = _DeviceTree(instance) if private else _device_for(sig, instance)
         fresh_structure = True
+        if min_branch_stage:
+            dev.ctx.call("wmpc_set_min_branch_stage", int(min_branch_stage))
     if fresh_structure:
         _upload_structure(dev, instance, basis, e_pinv, lam, t_mat, d_gain)
     nodes = dev.take_nodes()
