@@ -179,6 +179,14 @@ int wmpc_shard_step(wmpc_ctx* ctx, int phase);
  * ranks: phase 0 writes this rank's accounted children, the caller sums the
  * exchange buffer across ranks, phase 1 stores the totals. Once per factor. */
 int wmpc_shard_fix_R(wmpc_ctx* ctx, int phase);
+/* Device-side exchange over NCCL (one communicator per context, ranks =
+ * shards): with it, wmpc_apg_run replays CUDA graphs that contain the
+ * all-reduce between the two phases of every iteration, and
+ * wmpc_shard_exchange performs one (fix_R, certificate) on the stream.
+ * wmpc_nccl_unique_id fills 128 bytes (ncclUniqueId) on rank 0. */
+int wmpc_nccl_unique_id(void* out128);
+int wmpc_shard_nccl_init(wmpc_ctx* ctx, const void* id128, int nranks, int rank);
+int wmpc_shard_exchange(wmpc_ctx* ctx);
 /* Wait for the context's stream (before the caller touches the exchange buffer). */
 int wmpc_sync(wmpc_ctx* ctx);
 /* Certificate pieces for a sharded solve (solver.py:449-457, problem.py:221-250):

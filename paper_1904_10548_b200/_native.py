@@ -77,6 +77,9 @@ SIGNATURES = {
     "wmpc_shard_set_exchange": (C.c_int, [_vp, _vp]),
     "wmpc_shard_step": (C.c_int, [_vp, C.c_int]),
     "wmpc_sync": (C.c_int, [_vp]),
+    "wmpc_nccl_unique_id": (C.c_int, [_vp]),
+    "wmpc_shard_nccl_init": (C.c_int, [_vp, _vp, C.c_int, C.c_int]),
+    "wmpc_shard_exchange": (C.c_int, [_vp]),
     "wmpc_set_min_branch_stage": (C.c_int, [_vp, C.c_int]),
     "wmpc_shard_fix_R": (C.c_int, [_vp, C.c_int]),
     "wmpc_cert_absmax": (C.c_int, [_vp, _dp]),

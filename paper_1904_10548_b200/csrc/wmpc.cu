@@ -5,6 +5,8 @@
 // wmpc_apg_begin into a CUDA graph and replayed; nothing leaves HBM between
 // iterations except the scalars read at check iterations.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is resolved at run time (the process may already hold torch's)
 
 #include <algorithm>
 #include <climits>
@@ -92,6 +94,7 @@ struct wmpc_ctx {
   int* rep_gidx = nullptr;                     // per local row: global replicated index or -1
   double* xbuf = nullptr;                      // exchange buffer (caller-owned device memory)
   int n_rep_global = 0, shard_k = -1, kstar_min = 0;
+  ncclComm_t nccl = nullptr;                   // subtree sharding: exchange inside the iteration graph
   size_t sm_up = 0, sm_grp = 0, sm_down = 0, sm_prox = 0;
   int up_threads = 512, down_threads = 512, prox_warp = 1;
   int *ell_cnt = nullptr, *ell_idx = nullptr;
@@ -120,6 +123,35 @@ struct wmpc_ctx {
 namespace {
 
 struct Fail {};
+
+// NCCL entry points, resolved on first use from the libnccl already in the
+// process (torch's) or the system one: libwmpc does not link NCCL, so loading
+// it never pins an NCCL version ahead of torch.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+  api.init_rank = reinterpret_cast<decltype(api.init_rank)>(dlsym(h, "ncclCommInitRank"));
+  api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+  api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(h, "ncclCommDestroy"));
+  api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+  api.ok = api.get_unique_id && api.init_rank && api.all_reduce && api.destroy && api.error_string;
+  return api;
+}
 
 #define CK(call)                                                                        \
   do {                                                                                  \
@@ -770,6 +802,7 @@ FastView make_fastview(wmpc_ctx* ctx, int count);
 
 int graphk_kernels(const wmpc_ctx* ctx) {
   const int g = (int)ctx->gk_groups.size();
+  if (ctx->shard_k > 0) return 3 + g + 2 * (ctx->rep_group.second > 0) + (g == 0 && ctx->rep_group.second == 0);
   if (ctx->use_fused) return g + 1 + (g == 0 ? 1 : 0);
   return 3 + g + (g == 0 ? 1 : 0);
 }
@@ -799,7 +832,10 @@ void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
     k_prox_nodes<<<(ctx->n + SC_NPB - 1) / SC_NPB, SC_THREADS, ctx->sm_prox, st>>>(f);
 }
 
+void enqueue_shard_iteration(wmpc_ctx* ctx, const FastView& f);
+
 void capture_graphk(wmpc_ctx* ctx) {
+  if (ctx->shard_k > 0 && !ctx->nccl) return;  // host-mediated exchange: wmpc_shard_step, no graph
   if (ctx->gk_exec1 && ctx->gk_gamma == ctx->gamma && ctx->gk_maxit == ctx->max_iter) return;
   if (ctx->gk_exec1) cudaGraphExecDestroy(ctx->gk_exec1);
   if (ctx->gk_exec8) cudaGraphExecDestroy(ctx->gk_exec8);
@@ -808,7 +844,16 @@ void capture_graphk(wmpc_ctx* ctx) {
   for (int reps : {1, 8}) {
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
-    for (int i = 0; i < reps; ++i) enqueue_graphk_iteration(ctx, f);
+    try {
+      for (int i = 0; i < reps; ++i) {
+        if (ctx->shard_k > 0) enqueue_shard_iteration(ctx, f);
+        else enqueue_graphk_iteration(ctx, f);
+      }
+    } catch (Fail&) {  // leave the stream usable
+      cudaStreamEndCapture(ctx->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
     CK(cudaStreamEndCapture(ctx->stream, &g));
     CK(cudaGraphInstantiate(reps == 1 ? &ctx->gk_exec1 : &ctx->gk_exec8, g, 0));
     cudaGraphDestroy(g);
@@ -972,6 +1017,7 @@ void free_all(wmpc_ctx* c) {
     if (p) cudaFree(p);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->nccl) nccl_api().destroy(c->nccl);
   if (c->gk_exec1) cudaGraphExecDestroy(c->gk_exec1);
   if (c->gk_exec8) cudaGraphExecDestroy(c->gk_exec8);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -982,8 +1028,7 @@ void free_all(wmpc_ctx* c) {
 }
 
 template <int WE>
-void shard_step(wmpc_ctx* ctx, int phase) {
-  FastView f = make_fastview(ctx, 1);
+void shard_phase(wmpc_ctx* ctx, const FastView& f, int phase) {
   const bool rep = ctx->rep_group.second > 0;
   if (phase == 0) {
     int bump = 1;
@@ -1008,6 +1053,26 @@ void shard_step(wmpc_ctx* ctx, int phase) {
     ctx->launches += 2 + rep;
   }
   check_launch(ctx);
+}
+
+// The exchange on the device: sum of the ranks' buffers (in place) over NCCL.
+void exchange_dev(wmpc_ctx* ctx) {
+  NcclApi& api = nccl_api();
+  const ncclResult_t r = api.all_reduce(ctx->xbuf, ctx->xbuf, (size_t)256 * ctx->n_rep_global, ncclDouble, ncclSum,
+                                        ctx->nccl, ctx->stream);
+  if (r != ncclSuccess) {
+    ctx->err = std::string("NCCL all-reduce failed: ") + api.error_string(r);
+    throw Fail{};
+  }
+}
+
+// One sharded APG iteration with the exchange on the stream (graph-capturable).
+void enqueue_shard_iteration(wmpc_ctx* ctx, const FastView& f) {
+  if (ctx->ell_w == 4) shard_phase<4>(ctx, f, 0);
+  else shard_phase<8>(ctx, f, 0);
+  if (ctx->rep_group.second > 0) exchange_dev(ctx);
+  if (ctx->ell_w == 4) shard_phase<4>(ctx, f, 1);
+  else shard_phase<8>(ctx, f, 1);
 }
 
 }  // namespace
@@ -1558,8 +1623,8 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
 
 int wmpc_apg_run(wmpc_ctx* ctx, int count) {
   return run(ctx, [&]() -> int {
-    if (ctx->shard_k > 0) {
-      ctx->err = "a shard with replicated rows advances through wmpc_shard_step";
+    if (ctx->shard_k > 0 && !ctx->nccl) {
+      ctx->err = "a shard with replicated rows advances through wmpc_shard_step (or set up NCCL)";
       return WMPC_E_STATE;
     }
     if (ctx->fast && ctx->max_iter > 0) {
@@ -1583,8 +1648,8 @@ int wmpc_apg_run(wmpc_ctx* ctx, int count) {
 
 int wmpc_apg_run_timed(wmpc_ctx* ctx, int count, float* ms) {
   return run(ctx, [&]() -> int {
-    if (ctx->shard_k > 0) {
-      ctx->err = "a shard with replicated rows advances through wmpc_shard_step";
+    if (ctx->shard_k > 0 && !ctx->nccl) {
+      ctx->err = "a shard with replicated rows advances through wmpc_shard_step (or set up NCCL)";
       return WMPC_E_STATE;
     }
     if (ctx->fast && ctx->max_iter > 0) {
@@ -1863,6 +1928,54 @@ int wmpc_set_min_branch_stage(wmpc_ctx* ctx, int stage) {
   });
 }
 
+int wmpc_nccl_unique_id(void* out) {
+  ncclUniqueId id;
+  NcclApi& api = nccl_api();
+  if (!out || !api.ok) {
+    g_global_err = "libnccl.so.2 not available";
+    return WMPC_E_CUDA;
+  }
+  if (api.get_unique_id(&id) != ncclSuccess) return WMPC_E_CUDA;
+  std::memcpy(out, &id, sizeof(id));
+  return WMPC_OK;
+}
+
+int wmpc_shard_nccl_init(wmpc_ctx* ctx, const void* id, int nranks, int rank) {
+  return run(ctx, [&]() -> int {
+    ARG(id && nranks >= 1 && rank >= 0 && rank < nranks, "bad NCCL arguments");
+    CK(cudaSetDevice(ctx->dev));
+    NcclApi& api = nccl_api();
+    if (!api.ok) {
+      ctx->err = "libnccl.so.2 not available";
+      return WMPC_E_CUDA;
+    }
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    if (ctx->nccl) api.destroy(ctx->nccl);
+    ctx->nccl = nullptr;
+    const ncclResult_t r = api.init_rank(&ctx->nccl, nranks, uid, rank);
+    if (r != ncclSuccess) {
+      ctx->nccl = nullptr;
+      ctx->err = std::string("ncclCommInitRank failed: ") + api.error_string(r);
+      return WMPC_E_CUDA;
+    }
+    ctx->gk_gamma = -1.0;  // iteration graphs now carry the exchange
+    return WMPC_OK;
+  });
+}
+
+int wmpc_shard_exchange(wmpc_ctx* ctx) {
+  return run(ctx, [&]() -> int {
+    if (!ctx->nccl || !ctx->xbuf) {
+      ctx->err = "NCCL communicator and exchange buffer must be set";
+      return WMPC_E_STATE;
+    }
+    if (ctx->n_rep_global > 0) exchange_dev(ctx);
+    sync(ctx);
+    return WMPC_OK;
+  });
+}
+
 int wmpc_sync(wmpc_ctx* ctx) {
   return run(ctx, [&]() -> int {
     sync(ctx);
@@ -1886,8 +1999,9 @@ int wmpc_shard_step(wmpc_ctx* ctx, int phase) {
     ARG(phase == 0 || phase == 1, "phase must be 0 or 1");
     ARG(ctx->it_host < ctx->max_iter, "iteration count exceeds the theta table");
     ARG(ctx->rep_group.second == 0 || ctx->xbuf, "exchange buffer not set");
-    if (ctx->ell_w == 4) shard_step<4>(ctx, phase);
-    else shard_step<8>(ctx, phase);
+    FastView f = make_fastview(ctx, 1);
+    if (ctx->ell_w == 4) shard_phase<4>(ctx, f, phase);
+    else shard_phase<8>(ctx, f, phase);
     if (phase == 1) ctx->it_host += 1;
     return WMPC_OK;
   });

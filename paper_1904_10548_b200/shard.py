@@ -57,8 +57,9 @@ def _stage_offsets(instance) -> np.ndarray:
     return np.array([sl.start for sl in instance.stage_slices] + [instance.stage_slices[-1].stop])
 
 
-def plan(instance, size: int) -> list[ShardSpec]:
-    """Partition the non-root rows of ``instance`` over ``size`` ranks."""
+def plan(instance, size: int, k: int | None = None) -> list[ShardSpec]:
+    """Partition the non-root rows of ``instance`` over ``size`` ranks (shard
+    stage ``k``: default the shallowest with >= size nodes)."""
     if size < 1:
         raise ValueError("need at least one rank")
     off = _stage_offsets(instance)
@@ -66,7 +67,10 @@ def plan(instance, size: int) -> list[ShardSpec]:
     cand = np.flatnonzero(counts >= size)
     if cand.size == 0:
         raise ValueError(f"no stage has {size} nodes to shard over")
-    k = int(cand[0])
+    if k is None:
+        k = int(cand[0])
+    elif counts[k] < size:
+        raise ValueError(f"stage {k} has fewer than {size} nodes")
     n = instance.n_nonroot
     anc = instance.anc_row
     # subtree root (stage-k ancestor) of every row at stage >= k
@@ -158,6 +162,9 @@ class LocalCollective:
     def bcast_float(self, v: float) -> float:
         return v
 
+    def bcast_bytes(self, b: bytes) -> bytes:
+        return b
+
 
 class TorchCollective:
     """One shard per process over ``torch.distributed`` (NCCL or gloo)."""
@@ -196,6 +203,11 @@ class TorchCollective:
 
     def bcast_float(self, v: float) -> float:
         return float(self.max(np.array([v]))[0])
+
+    def bcast_bytes(self, b: bytes) -> bytes:
+        obj = [b]
+        self.dist.broadcast_object_list(obj, src=0, group=self.group)
+        return obj[0]
 
 
 # ------------------------------------------------------------------ the solve
@@ -241,7 +253,7 @@ def _check(shards, comm):
     return float(v[0]), float(v[1]), float(v[2])
 
 
-def _certificate(shards, comm, instance):
+def _certificate(shards, comm, instance, exchange):
     am = np.array([0.0])
     for sh in shards:
         a = np.zeros(1)
@@ -260,7 +272,7 @@ def _certificate(shards, comm, instance):
     for sh in shards:
         sh.ctx.call("wmpc_shard_dual_eval", 0)
     if shards[0].spec.k > 0:
-        _exchange(shards, comm)
+        exchange()
     for sh in shards:
         sh.ctx.call("wmpc_shard_dual_eval", 1)
     terms = np.zeros(10)
@@ -307,6 +319,124 @@ def _read(shards, comm, instance, averaged: bool):
     return u0, Z.reshape(-1), ZA.reshape(-1), Y.reshape(-1)
 
 
+def _u0_only(shards, comm, instance, averaged: bool) -> np.ndarray:
+    """u0 from the stage-1 rows alone (gathered in global order)."""
+    m = instance.model
+    nu = m.n_inputs
+    s1 = instance.stage_slices[0]
+    rows_vals = []
+    for sh in shards:
+        _, z, za, _ = S._read(sh.ctx, sh.inst, averaged, u0=False, primal=not averaged, avg=averaged, dual=False)
+        src = (za if averaged else z).reshape(sh.inst.n_nonroot, -1)
+        keep = sh.spec.acct.astype(bool) & (sh.spec.rows < s1.stop)
+        rows_vals.append((sh.spec.rows[keep], src[keep, :nu]))
+    U1 = np.empty((s1.stop - s1.start, nu))
+    for rows, vals in [p for group in comm.gather(rows_vals) for p in group]:
+        U1[rows - s1.start] = vals
+    u0 = np.empty(nu)
+    nat.load().wmpc_u0_rows(nu, U1.shape[0], nat.ptr(np.ascontiguousarray(instance.prob[s1])), nat.ptr(U1),
+                            nat.ptr(nat.f64(m.u_min)), nat.ptr(nat.f64(m.u_max)), nat.ptr(u0))
+    return u0
+
+
+class ShardedSolver:
+    """The shards one process runs (all of them when emulating), built once:
+    factor step, shard setup and the replicated rows' R; ``solve`` may then be
+    called repeatedly (bench.py)."""
+
+    def __init__(self, instance, specs: list[ShardSpec] | None = None, comm=None, size: int | None = None,
+                 device_exchange: bool | None = None):
+        self.instance = instance
+        self.comm = comm or LocalCollective()
+        self.specs = specs if specs is not None else plan(instance, size or 1)
+        self.shards = [_Shard(instance, sp) for sp in self.specs]
+        if device_exchange is None:
+            device_exchange = isinstance(self.comm, TorchCollective) and self.comm.nccl
+        # NCCL on the solver stream: the exchange sits inside the iteration graph
+        self.device_exchange = bool(device_exchange) and self.specs[0].k > 0
+        if self.device_exchange:
+            if len(self.shards) != 1:
+                raise ValueError("the device exchange runs one shard per process")
+            sp = self.specs[0]
+            uid = (nat.C.c_char * 128)()
+            if sp.rank == 0 and nat.load().wmpc_nccl_unique_id(uid) != nat.WMPC_OK:
+                raise RuntimeError("ncclGetUniqueId failed")
+            raw = self.comm.bcast_bytes(bytes(uid))
+            uid = (nat.C.c_char * 128).from_buffer_copy(raw)
+            self.shards[0].ctx.call("wmpc_shard_nccl_init", uid, int(sp.size), int(sp.rank))
+        if self.specs[0].k > 0:  # replicated rows' R spans ranks (solver.py:269-274)
+            for sh in self.shards:
+                sh.ctx.call("wmpc_shard_fix_R", 0)
+            self._exchange()
+            for sh in self.shards:
+                sh.ctx.call("wmpc_shard_fix_R", 1)
+        self.lipschitz = None
+
+    def _exchange(self) -> None:
+        if self.device_exchange:
+            self.shards[0].ctx.call("wmpc_shard_exchange")
+        else:
+            _exchange(self.shards, self.comm)
+
+    def solve(self, config: S.SolverConfig | None = None, results: str = "all") -> S.SolverResult:
+        """``solve`` (solver.py:398-543) over the shards; every rank returns the
+        full result (``results="u0"``: only u0 and the scalars)."""
+        import time
+        config = config or S.SolverConfig()
+        comm, shards, instance = self.comm, self.shards, self.instance
+        gamma = config.gamma
+        lipschitz = self.lipschitz
+        if gamma is None:  # the global operator norm, estimated once on the whole tree
+            if lipschitz is None:
+                lam = S.estimate_lipschitz(S.factor_step(instance), instance) if self.specs[0].rank == 0 else 0.0
+                lipschitz = self.lipschitz = comm.bcast_float(lam)
+            gamma = 1.0 / lipschitz
+        theta = S.theta_sequence(config.max_iter)
+        beta = S._beta_table(theta)
+        for sh in shards:
+            S._upload_bounds(sh.ctx, sh.inst)
+            sh.ctx.call("wmpc_apg_begin", float(gamma), int(config.max_iter), nat.ptr(theta), nat.ptr(beta))
+        exchange = self.specs[0].k > 0
+        started = time.perf_counter()
+        residual = dchange = gap = objective = float("inf")
+        iterations, termination = config.max_iter, "max_iter"
+        gce = config.gap_check_every
+        done = 0
+        while done < config.max_iter:
+            step = min(gce - (done % gce), config.max_iter - done)
+            if exchange and not self.device_exchange:
+                for _ in range(step):
+                    for sh in shards:
+                        sh.ctx.call("wmpc_shard_step", 0)
+                    _exchange(shards, comm)
+                    for sh in shards:
+                        sh.ctx.call("wmpc_shard_step", 1)
+            else:
+                for sh in shards:
+                    sh.ctx.call("wmpc_apg_run", int(step))
+            done += step
+            if done % gce == 0:
+                residual, scale, dchange = _check(shards, comm)
+                if residual <= config.tol * (1.0 + scale):
+                    gap, objective = _certificate(shards, comm, instance, self._exchange)
+                    if gap <= config.tol * (1.0 + abs(objective)):
+                        iterations, termination = done, "converged"
+                        break
+        if termination == "max_iter":
+            residual, scale, dchange = _check(shards, comm)
+            gap, objective = _certificate(shards, comm, instance, self._exchange)
+        elapsed = time.perf_counter() - started
+        if results == "u0":
+            u0 = _u0_only(shards, comm, instance, config.averaged_primal)
+            primal = primal_avg = dual = None
+        else:
+            u0, primal, primal_avg, dual = _read(shards, comm, instance, config.averaged_primal)
+        return S.SolverResult(u0=u0, primal=primal, primal_avg=primal_avg, dual=dual, iterations=iterations,
+                              termination=termination, primal_residual=residual, dual_change=dchange,
+                              duality_gap=gap, objective=objective, solve_time_s=elapsed, gamma=gamma,
+                              lipschitz=lipschitz)
+
+
 def solve_sharded(instance, config: S.SolverConfig | None = None, specs: list[ShardSpec] | None = None,
                   comm=None, size: int | None = None) -> S.SolverResult:
     """``solve`` (solver.py:398-543) over subtree shards.
@@ -315,61 +445,4 @@ def solve_sharded(instance, config: S.SolverConfig | None = None, specs: list[Sh
     size)``, emulated in this process). ``comm``: the cross-process collective
     (default ``LocalCollective``). Every rank returns the full result.
     """
-    import time
-    config = config or S.SolverConfig()
-    comm = comm or LocalCollective()
-    if specs is None:
-        specs = plan(instance, size or 1)
-    shards = [_Shard(instance, sp) for sp in specs]
-    if specs[0].k > 0:  # replicated rows' R spans ranks (solver.py:269-274)
-        for sh in shards:
-            sh.ctx.call("wmpc_shard_fix_R", 0)
-        _exchange(shards, comm)
-        for sh in shards:
-            sh.ctx.call("wmpc_shard_fix_R", 1)
-    gamma = config.gamma
-    lipschitz = None
-    if gamma is None:  # the global operator norm, estimated once on the whole tree
-        lam = S.estimate_lipschitz(S.factor_step(instance), instance) if specs[0].rank == 0 else 0.0
-        lipschitz = comm.bcast_float(lam)
-        gamma = 1.0 / lipschitz
-    theta = S.theta_sequence(config.max_iter)
-    beta = S._beta_table(theta)
-    for sh in shards:
-        S._upload_bounds(sh.ctx, sh.inst)
-        sh.ctx.call("wmpc_apg_begin", float(gamma), int(config.max_iter), nat.ptr(theta), nat.ptr(beta))
-    exchange = specs[0].k > 0
-    started = time.perf_counter()
-    residual = dchange = gap = objective = float("inf")
-    iterations, termination = config.max_iter, "max_iter"
-    gce = config.gap_check_every
-    done = 0
-    while done < config.max_iter:
-        step = min(gce - (done % gce), config.max_iter - done)
-        if exchange:
-            for _ in range(step):
-                for sh in shards:
-                    sh.ctx.call("wmpc_shard_step", 0)
-                _exchange(shards, comm)
-                for sh in shards:
-                    sh.ctx.call("wmpc_shard_step", 1)
-        else:
-            for sh in shards:
-                sh.ctx.call("wmpc_apg_run", int(step))
-        done += step
-        if done % gce == 0:
-            residual, scale, dchange = _check(shards, comm)
-            if residual <= config.tol * (1.0 + scale):
-                gap, objective = _certificate(shards, comm, instance)
-                if gap <= config.tol * (1.0 + abs(objective)):
-                    iterations, termination = done, "converged"
-                    break
-    if termination == "max_iter":
-        residual, scale, dchange = _check(shards, comm)
-        gap, objective = _certificate(shards, comm, instance)
-    elapsed = time.perf_counter() - started
-    u0, primal, primal_avg, dual = _read(shards, comm, instance, config.averaged_primal)
-    return S.SolverResult(u0=u0, primal=primal, primal_avg=primal_avg, dual=dual, iterations=iterations,
-                          termination=termination, primal_residual=residual, dual_change=dchange,
-                          duality_gap=gap, objective=objective, solve_time_s=elapsed, gamma=gamma,
-                          lipschitz=lipschitz)
+    return ShardedSolver(instance, specs=specs, comm=comm, size=size).solve(config)
