@@ -106,6 +106,9 @@ int wmpc_operator_trace(wmpc_ctx* ctx, double* trace);
 int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* theta,
                    const double* beta);
 int wmpc_apg_run(wmpc_ctx* ctx, int count);
+/* Warm start (closed loop; the reference always starts at y = 0,
+ * solver.py:430-431): right after wmpc_apg_begin, y0 = y_prev = the given dual. */
+int wmpc_apg_warm(wmpc_ctx* ctx, const double* y0);
 int wmpc_apg_check(wmpc_ctx* ctx, double* primal_residual, double* image_scale,
                    double* dual_change, int* first_nonfinite_nu);
 /* Duality-gap certificate at the current dual iterate (solver.py:449-457):

@@ -1928,6 +1928,30 @@ int wmpc_set_min_branch_stage(wmpc_ctx* ctx, int stage) {
   });
 }
 
+int wmpc_apg_warm(wmpc_ctx* ctx, const double* y0) {
+  return run(ctx, [&]() -> int {
+    ARG(y0, "null argument");
+    if (ctx->max_iter <= 0 || ctx->it_host != 0) {
+      ctx->err = "wmpc_apg_warm must directly follow wmpc_apg_begin";
+      return WMPC_E_STATE;
+    }
+    const size_t len = (size_t)ctx->n * ctx->W;
+    h2d(ctx, ctx->Y[0], y0, sizeof(double) * len);
+    CK(cudaMemcpyAsync(ctx->Y[2], ctx->Y[0], sizeof(double) * len, cudaMemcpyDeviceToDevice, ctx->stream));
+    DevView d = view(ctx);
+    ctx->launches++;
+    k_collapse<<<grid_for((size_t)ctx->n * ctx->ly), 256, 0, ctx->stream>>>(d, ctx->Y[0], ctx->Yc);
+    if (ctx->fast && ctx->use_graphk && ctx->use_fused) {  // the fused path's up pass of iteration 0
+      FastView f = make_fastview(ctx, 1);
+      if (ctx->ell_w == 4) gk_up<4>(ctx, f); else gk_up<8>(ctx, f);
+      ctx->launches++;
+    }
+    check_launch(ctx);
+    sync(ctx);
+    return WMPC_OK;
+  });
+}
+
 int wmpc_nccl_unique_id(void* out) {
   ncclUniqueId id;
   NcclApi& api = nccl_api();

@@ -89,6 +89,15 @@ class NetworkModel:
         return self.A @ np.asarray(x, float) + self.B @ np.asarray(u, float) \
             + self.Gd @ np.asarray(d, float)
 
+    def coupling_residual(self, u, d) -> np.ndarray:
+        """Mixing-node residual ``E u + Ed d`` (``network.py:157-164``)."""
+        u, d = np.asarray(u, float), np.asarray(d, float)
+        if u.shape != (self.n_inputs,):
+            raise ValueError(f"input must have shape ({self.n_inputs},), got {u.shape}")
+        if d.shape != (self.n_demands,):
+            raise ValueError(f"demand must have shape ({self.n_demands},), got {d.shape}")
+        return self.E @ u + self.Ed @ d
+
 
 def _require_spd(mat: np.ndarray, what: str) -> None:
     if mat.ndim != 2 or mat.shape[0] != mat.shape[1]:

@@ -375,14 +375,15 @@ def _certificate(ctx):
 
 
 def solve(instance, config: SolverConfig | None = None, cache: FactorCache | None = None,
-          iterate_hook: IterateHook | None = None) -> SolverResult:
+          iterate_hook: IterateHook | None = None, y_init=None) -> SolverResult:
     """Accelerated dual proximal gradient on the GPU (solver.py:398-543).
 
     Iterations run as CUDA-graph replays in chunks ending at the reference's
     check iterations ((nu+1) % gap_check_every == 0); only the residual,
     scale, dual change and non-finite flag cross to the host there. With an
     ``iterate_hook`` the loop advances one iteration per replay and copies
-    the iterates to the host for the hook (debug path).
+    the iterates to the host for the hook (debug path). ``y_init``: optional
+    dual warm start (closed loop; the reference always starts from 0).
     """
     config = config or SolverConfig()
     if cache is None:
@@ -400,6 +401,11 @@ def solve(instance, config: SolverConfig | None = None, cache: FactorCache | Non
     theta = theta_sequence(config.max_iter)
     beta = _beta_table(theta)
     ctx.call("wmpc_apg_begin", float(gamma), int(config.max_iter), nat.ptr(theta), nat.ptr(beta))
+    if y_init is not None:
+        y0 = nat.f64(y_init)
+        if y0.shape != (instance.n_dual,):
+            raise ValueError(f"y_init must have shape ({instance.n_dual},)")
+        ctx.call("wmpc_apg_warm", nat.ptr(y0))
     started = time.perf_counter()
     residual = dchange = gap = objective = float("inf")
     iterations, termination = config.max_iter, "max_iter"

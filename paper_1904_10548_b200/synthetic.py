@@ -121,3 +121,44 @@ def barcelona_instance(branching, seed: int = 0, horizon: int = HORIZON,
 
 def config_instance(name: str, seed: int = 0):
     return barcelona_instance(CONFIGS[name], seed=seed)
+
+
+def closed_loop_scenario(branching=None, h_sim: int = 168, seed: int = 0, horizon: int = HORIZON,
+                         noise: float = 0.05) -> dict:
+    """Config C5: a closed-loop run on the Barcelona-dimension
+    network. Demands and prices follow a daily cycle (hourly steps); the
+    forecaster issues the noise-free cycle for the next ``horizon`` hours, the
+    realizations add N(0, noise^2) relative errors; the tree template carries
+    the same relative errors per node. Default tree: C3's 512 scenarios."""
+    from .forecast import ForecastSeries
+    branching = CONFIGS["C3"] if branching is None else branching
+    model = barcelona_network(seed)
+    rng = np.random.default_rng(2000 + seed)
+    nd, nu = model.n_demands, model.n_inputs
+    base_d = 5.0 + 5.0 * rng.random(nd)
+    phase = rng.uniform(0, 2 * np.pi, nd)
+    base_a = 0.02 + 0.01 * rng.random(nu)
+
+    def cycle(t):
+        t = np.asarray(t, float)[:, None]
+        d = base_d * (1.0 + 0.3 * np.sin(2 * np.pi * t / 24.0 + phase))
+        peak = ((t % 24) >= 8) & ((t % 24) < 22)
+        a = base_a * np.where(peak, 1.5, 0.7)
+        return d, a
+
+    def forecaster(k: int) -> ForecastSeries:
+        d, a = cycle(np.arange(k, k + horizon))
+        return ForecastSeries(d_hat=d, alpha_hat=a)
+
+    d_real, a_real = cycle(np.arange(h_sim))
+    d_real = np.maximum(d_real * (1.0 + noise * rng.standard_normal(d_real.shape)), 0.0)
+    a_real = a_real * (1.0 + noise * rng.standard_normal(a_real.shape))
+    tree = uniform_tree(branching, horizon, nd, nu)
+    eps = noise * rng.standard_normal((tree.n_nodes, nd + nu))
+    st = np.maximum(tree.stage - 1, 0)
+    d0, a0 = cycle(np.arange(horizon))
+    eps *= np.concatenate([d0[st], a0[st]], axis=1)
+    eps[0] = 0.0
+    tree.eps = eps
+    return dict(model=model, tree_template=tree, forecaster=forecaster, realized_demand=d_real,
+                realized_price=a_real, x0=np.full(model.n_tanks, 2500.0), weights=CostWeights(**WEIGHTS))

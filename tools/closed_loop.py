@@ -1,0 +1,31 @@
+"""Config C5: closed-loop receding horizon, 168 hourly steps on the 512-scenario
+tree (C3), tol = 5e-2, cold (reference behaviour) vs warm-started dual.
+python tools/closed_loop.py [h_sim] > profiles/...json"""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+from paper_1904_10548_b200 import SolverConfig
+from paper_1904_10548_b200.simulate import (SimulationConfig, kpi_complexity, kpi_economic, kpi_safety,
+                                            run_closed_loop)
+from paper_1904_10548_b200.synthetic import CONFIGS, closed_loop_scenario
+
+h = int(sys.argv[1]) if len(sys.argv) > 1 else 168
+sc = closed_loop_scenario(CONFIGS["C3"], h_sim=h)
+out = {"config": "C5: barcelona-63t-114u-88d-17m, tree C3 [4,4,4,2,2,2] (512 scenarios, 10,196 nodes), "
+                 f"H=24, {h} hourly steps, tol 5e-2, gap check every 25, max_iter 5000"}
+for warm in (False, True):
+    cfg = SimulationConfig(h_sim=h, weights=sc["weights"], x0=sc["x0"], warm_start=warm,
+                           solver=SolverConfig(max_iter=5000, tol=5e-2, gap_check_every=25))
+    t0 = time.perf_counter()
+    log = run_closed_loop(sc["model"], sc["tree_template"], sc["forecaster"], sc["realized_demand"],
+                          sc["realized_price"], cfg)
+    wall = time.perf_counter() - t0
+    out["warm" if warm else "cold"] = {
+        "wall_s": wall, "solve_s_total": float(log.solve_time_s.sum()),
+        "kpi_economic": kpi_economic(log), "kpi_safety_m3": kpi_safety(log),
+        "kpi_complexity_s": kpi_complexity(log), "iterations_total": int(log.iterations.sum()),
+        "iterations_mean": float(log.iterations.mean()), "iterations_max": int(log.iterations.max()),
+        "steps_at_max_iter": int((log.iterations >= 5000).sum()),
+        "median_step_ms": float(np.median(log.solve_time_s) * 1e3)}
+    print(json.dumps(out["warm" if warm else "cold"]), file=sys.stderr, flush=True)
+print(json.dumps(out))
