@@ -348,12 +348,22 @@ def estimate_lipschitz(cache: FactorCache, instance, rel_tol: float = 1e-3, max_
     return est
 
 
-def _read(ctx, instance, averaged: bool, u0=True, primal=True, avg=True, dual=True):
+def _result_buffers(instance) -> tuple:
+    """Result arrays with their pages already touched: allocated while the
+    device runs the APG loop, so the final copies do not page-fault."""
     nu = instance.model.n_inputs
-    out_u0 = np.empty(nu) if u0 else None
-    out_p = np.empty(instance.n_primal) if primal else None
-    out_a = np.empty(instance.n_primal) if avg else None
-    out_d = np.empty(instance.n_dual) if dual else None
+    out = (np.empty(nu), np.empty(instance.n_primal), np.empty(instance.n_primal), np.empty(instance.n_dual))
+    for a in out[1:]:
+        a.fill(0.0)  # touch every page now (calloc'd zeros would fault during the copy)
+    return out
+
+
+def _read(ctx, instance, averaged: bool, u0=True, primal=True, avg=True, dual=True, out=None):
+    nu = instance.model.n_inputs
+    if out is None:
+        out = (np.empty(nu) if u0 else None, np.empty(instance.n_primal) if primal else None,
+               np.empty(instance.n_primal) if avg else None, np.empty(instance.n_dual) if dual else None)
+    out_u0, out_p, out_a, out_d = out
     ctx.call("wmpc_apg_read", int(averaged), nat.ptr(out_u0), nat.ptr(out_p), nat.ptr(out_a),
              nat.ptr(out_d))
     return out_u0, out_p, out_a, out_d
@@ -411,12 +421,15 @@ def solve(instance, config: SolverConfig | None = None, cache: FactorCache | Non
     iterations, termination = config.max_iter, "max_iter"
     gce = config.gap_check_every
     done = 0
+    bufs = None
     while done < config.max_iter:
         if iterate_hook is not None:
             step = 1
         else:
             step = min(gce - (done % gce), config.max_iter - done)
         ctx.call("wmpc_apg_run", int(step))
+        if bufs is None and iterate_hook is None:
+            bufs = _result_buffers(instance)  # host work overlapping the device loop
         done += step
         if iterate_hook is not None:
             residual, scale, dchange = _check(ctx)
@@ -434,7 +447,7 @@ def solve(instance, config: SolverConfig | None = None, cache: FactorCache | Non
         residual, scale, dchange = _check(ctx)
         gap, objective = _certificate(ctx)
     elapsed = time.perf_counter() - started
-    u0, primal, primal_avg, dual = _read(ctx, instance, config.averaged_primal)
+    u0, primal, primal_avg, dual = _read(ctx, instance, config.averaged_primal, out=bufs)
     return SolverResult(u0=u0, primal=primal, primal_avg=primal_avg, dual=dual,
                         iterations=iterations, termination=termination,
                         primal_residual=residual, dual_change=dchange, duality_gap=gap,
