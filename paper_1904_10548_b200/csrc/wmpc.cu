@@ -96,7 +96,8 @@ struct wmpc_ctx {
   int n_rep_global = 0, shard_k = -1, kstar_min = 0;
   ncclComm_t nccl = nullptr;                   // subtree sharding: exchange inside the iteration graph
   size_t sm_up = 0, sm_grp = 0, sm_down = 0, sm_prox = 0;
-  int up_threads = 512, down_threads = 512, prox_warp = 1;
+  int up_threads = 512, down_threads = 512, prox_warp = 1, use_pu = 0;
+  size_t sm_pu = 0;
   int *ell_cnt = nullptr, *ell_idx = nullptr;
   double* ell_val = nullptr;
   int ell_w = 4;
@@ -301,7 +302,12 @@ size_t fast_smem_bytes(const wmpc_ctx* c, int MC, int nrow, int rec, int cpc, in
 // A = I, W = cI, n_u even, n_s <= 32, and every stage factor equal to the
 // null(E) projector (T_s = P/(2c), D_s = P up to 1e-12 relative).
 template <int WE>
+void gk_pu(wmpc_ctx* ctx, const FastView& f) {
+  k_chain_pu<WE><<<ctx->nchain, 256, ctx->sm_pu, ctx->stream>>>(f);
+}
+template <int WE>
 void gk_attrs(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
+  if (ctx->sm_pu) CK(cudaFuncSetAttribute(k_chain_pu<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->sm_pu));
   CK(cudaFuncSetAttribute(k_chain_up<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
   CK(cudaFuncSetAttribute(k_chain_down<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
   CK(cudaFuncSetAttribute(k_branch_grp<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grp));
@@ -489,10 +495,18 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
       for (int e = ecp[k]; e < ecp[k + 1]; ++e) owners[nu + nt + k].push_back({ecr[e], ecv[e]});
     for (int i = 0; i < ns; ++i)
       for (int e = kp[i]; e < kp[i + 1]; ++e) owners[2 * nu + nt + i].push_back({kc[e], kv[e]});
-    size_t w = 1;
-    for (auto& o : owners) w = std::max(w, o.size());
+    size_t w = 1, wbc = 0, wbr = 0, wec = 0, wkr = 0;
+    for (size_t o = 0; o < owners.size(); ++o) {
+      const size_t c = owners[o].size();
+      w = std::max(w, c);
+      if (o < (size_t)nu) wbc = std::max(wbc, c);
+      else if (o < (size_t)(nu + nt)) wbr = std::max(wbr, c);
+      else if (o < (size_t)(2 * nu + nt)) wec = std::max(wec, c);
+      else wkr = std::max(wkr, c);
+    }
     if (w > 8) return;  // wide operators: the persistent kernels handle them
-    const int we = w <= 4 ? 4 : 8;
+    // variant 4: per-operator widths (2, 3, 1, 4), stored with stride 4
+    const int we = (wbc <= 2 && wbr <= 3 && wec <= 1 && wkr <= 4) ? 4 : 8;
     std::vector<int> cnt(owners.size()), idx(owners.size() * we, 0);
     std::vector<double> val(owners.size() * we, 0.0);
     for (size_t o = 0; o < owners.size(); ++o) {
@@ -547,6 +561,13 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   if (ctx->Yc_save) cudaFree(ctx->Yc_save);
   ctx->Yc_save = nullptr;
   dalloc(ctx, &ctx->Yc_save, (size_t)ctx->n * ly);
+  {  // prox fused with the next up pass (k_chain_pu)
+    const int ra = ly + nu + 2;
+    ctx->sm_pu = sizeof(double) * ((size_t)nst * (ra + FAST_MAXNS) + (size_t)(256 / 64) * 128);
+    const char* e = getenv("WMPC_PU");
+    ctx->use_pu = e && e[0] == '1' && ctx->sm_pu <= cap && nt <= 64 && nu <= 128 ? 1 : 0;
+    if (ctx->sm_pu > cap) ctx->sm_pu = 0;
+  }
   if (ctx->ell_w == 4) gk_attrs<4>(ctx, up, down, grp);
   else gk_attrs<8>(ctx, up, down, grp);
   CK(cudaFuncSetAttribute(k_prox_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox));
@@ -804,6 +825,7 @@ int graphk_kernels(const wmpc_ctx* ctx) {
   const int g = (int)ctx->gk_groups.size();
   if (ctx->shard_k > 0) return 3 + g + 2 * (ctx->rep_group.second > 0) + (g == 0 && ctx->rep_group.second == 0);
   if (ctx->use_fused) return g + 1 + (g == 0 ? 1 : 0);
+  if (ctx->use_pu) return g + 2 + (g == 0 ? 1 : 0);
   return 3 + g + (g == 0 ? 1 : 0);
 }
 
@@ -815,6 +837,18 @@ void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
   if (ctx->use_fused) {  // up pass of iteration 0 runs in wmpc_apg_begin
     if (ctx->ell_w == 4) gk_grp<4>(ctx, f, 1); else gk_grp<8>(ctx, f, 1);
     k_chain_fused<<<nc, ctx->fused_threads, ctx->sm_fused, st>>>(f);
+    return;
+  }
+  if (ctx->use_pu) {  // up pass of iteration 0 runs in wmpc_apg_begin
+    if (ctx->ell_w == 4) {
+      gk_grp<4>(ctx, f, 1);
+      gk_down<4>(ctx, f);
+      gk_pu<4>(ctx, f);
+    } else {
+      gk_grp<8>(ctx, f, 1);
+      gk_down<8>(ctx, f);
+      gk_pu<8>(ctx, f);
+    }
     return;
   }
   if (ctx->ell_w == 4) {
@@ -1394,7 +1428,7 @@ int wmpc_kernel_launches_per_iteration(const wmpc_ctx* ctx) {
 
 int wmpc_fast_path(const wmpc_ctx* ctx) {
   if (!ctx || !ctx->fast) return 0;
-  if (ctx->use_graphk) return ctx->use_fused ? 310 : 300;
+  if (ctx->use_graphk) return ctx->use_fused ? 310 : (ctx->use_pu ? 320 : 300);
   if (ctx->use_scan) return 200 + ctx->fast_mc;
   return ctx->use_warp ? 100 + ctx->warp_nrow : ctx->fast_mc;
 }
@@ -1591,7 +1625,7 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
     if (ctx->fast) {
       if (ctx->use_graphk) {
         capture_graphk(ctx);
-        if (ctx->use_fused) {  // up pass of iteration 0 (Yc = 0)
+        if (ctx->use_fused || ctx->use_pu) {  // up pass of iteration 0 (Yc = 0)
           FastView f = make_fastview(ctx, 1);
           if (ctx->ell_w == 4) gk_up<4>(ctx, f); else gk_up<8>(ctx, f);
           ctx->launches++;
@@ -1941,7 +1975,7 @@ int wmpc_apg_warm(wmpc_ctx* ctx, const double* y0) {
     DevView d = view(ctx);
     ctx->launches++;
     k_collapse<<<grid_for((size_t)ctx->n * ctx->ly), 256, 0, ctx->stream>>>(d, ctx->Y[0], ctx->Yc);
-    if (ctx->fast && ctx->use_graphk && ctx->use_fused) {  // the fused path's up pass of iteration 0
+    if (ctx->fast && ctx->use_graphk && (ctx->use_fused || ctx->use_pu)) {  // the up pass of iteration 0
       FastView f = make_fastview(ctx, 1);
       if (ctx->ell_w == 4) gk_up<4>(ctx, f); else gk_up<8>(ctx, f);
       ctx->launches++;

@@ -119,20 +119,21 @@ __device__ __forceinline__ int chain_row(const FastView& f, int t, int ci) { ret
 enum { ELL_BC = 0 };  // owner offsets: B by column [0,nu), B by row [nu,nu+nt), E by column, K by row
 template <int WE>
 struct Ell {
-  int n;
   int idx[WE];
   double val[WE];
 };
+// Entries past an owner's count are stored as (0, 0.0): no predication, and a
+// zero weight times a finite operand adds nothing (a dense product would
+// propagate a non-finite operand the same way).
 template <int WE>
 __device__ __forceinline__ Ell<WE> ell_load(const FastView& f, int owner) {
   Ell<WE> o;
-  o.n = f.ell_cnt[owner];
   const int* ip = f.ell_idx + (size_t)owner * f.ell_w;
   const double* vp = f.ell_val + (size_t)owner * f.ell_w;
 #pragma unroll
   for (int e = 0; e < WE; ++e) {
-    o.idx[e] = e < o.n ? ip[e] : 0;
-    o.val[e] = e < o.n ? vp[e] : 0.0;
+    o.idx[e] = ip[e];
+    o.val[e] = vp[e];
   }
   return o;
 }
@@ -140,10 +141,16 @@ template <int WE>
 __device__ __forceinline__ double ell_dot(const Ell<WE>& o, const double* x) {
   double s = 0.0;
 #pragma unroll
-  for (int e = 0; e < WE; ++e)
-    if (e < o.n) s = fma(o.val[e], x[o.idx[e]], s);
+  for (int e = 0; e < WE; ++e) s = fma(o.val[e], x[o.idx[e]], s);
   return s;
 }
+// Per-operator widths of a variant: V = 4 is the water-network shape (a flow
+// touches <= 2 tanks and <= 1 mixing node, a tank has <= 3 flows, a mixing
+// row of K <= 4 flows); V = 8 is the generic fallback.
+template <int V>
+struct EllW {
+  static constexpr int BC = V == 4 ? 2 : 8, BR = V == 4 ? 3 : 8, EC = V == 4 ? 1 : 8, KR = V == 4 ? 4 : 8;
+};
 __device__ __forceinline__ int own_bc(const DevView& d, int k) { return k; }
 __device__ __forceinline__ int own_br(const DevView& d, int j) { return d.nu + j; }
 __device__ __forceinline__ int own_ec(const DevView& d, int k) { return d.nu + d.nt + k; }
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(512) k_chain_up(FastView f) {
   cp_commit();
   const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
   const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
-  const Ell<WE> bc = ell_load<WE>(f, own_bc(d, k < nu ? k : 0));
+  const Ell<EllW<WE>::BC> bc = ell_load<EllW<WE>::BC>(f, own_bc(d, k < nu ? k : 0));
   cp_wait<0>();
   __syncthreads();
   if (threadIdx.x < nt) {  // wbar suffix scan in place: wbar_t = Yx_t + wbar_{t+1}
@@ -203,12 +210,12 @@ __global__ void __launch_bounds__(512) k_chain_up(FastView f) {
   }
   __syncthreads();
   if (i < ns) {  // T = K S
-    const Ell<WE> kr = ell_load<WE>(f, own_kr(d, i));
+    const Ell<EllW<WE>::KR> kr = ell_load<EllW<WE>::KR>(f, own_kr(d, i));
     for (int t = ti; t < nst - 1; t += si) T[t * FAST_MAXNS + i] = ell_dot(kr, rec + (size_t)t * ra + ly);
   }
   __syncthreads();
   if (k < nu) {  // L = (a + (S - E^T T)) / (2c p)
-    const Ell<WE> ec = ell_load<WE>(f, own_ec(d, k));
+    const Ell<EllW<WE>::EC> ec = ell_load<EllW<WE>::EC>(f, own_ec(d, k));
     for (int t = tk; t < nst; t += sk) {
       const double* R = rec + (size_t)t * ra;
       const double a = R[lx + k];
@@ -323,7 +330,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
       for (int w = 1; w < NW; ++w) s += part[w * 256 + 128 + k];
     }
     double b1 = 0.0, b2 = 0.0;
-    const Ell<WE> bc = ell_load<WE>(f, own_bc(d, k));
+    const Ell<EllW<WE>::BC> bc = ell_load<EllW<WE>::BC>(f, own_bc(d, k));
     b1 = ell_dot(bc, W1);
     b2 = ell_dot(bc, W2);
     av[k] = (d.Yc[(size_t)r * ly + lx + k] + b1) + np.R[(size_t)r * nu + k];
@@ -333,13 +340,13 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
   __syncthreads();
   if (threadIdx.x < nu) f.Asub[(size_t)r * nu + threadIdx.x] = av[threadIdx.x] + Sv[threadIdx.x];
   if (threadIdx.x < d.ns) {
-    const Ell<WE> kr = ell_load<WE>(f, own_kr(d, threadIdx.x));
+    const Ell<EllW<WE>::KR> kr = ell_load<EllW<WE>::KR>(f, own_kr(d, threadIdx.x));
     T[threadIdx.x] = ell_dot(kr, Sv);
   }
   __syncthreads();
   if (threadIdx.x < nu) {
     const int k = threadIdx.x;
-    const Ell<WE> ec = ell_load<WE>(f, own_ec(d, k));
+    const Ell<EllW<WE>::EC> ec = ell_load<EllW<WE>::EC>(f, own_ec(d, k));
     f.Lb[(size_t)r * nu + k] = (av[k] + (Sv[k] - ell_dot(ec, T))) * f.aux[(size_t)r * 2];
   }
 }
@@ -389,12 +396,12 @@ __global__ void __launch_bounds__(512) k_chain_down(FastView f) {
   }
   __syncthreads();
   if (i < ns) {  // T = K z
-    const Ell<WE> kr = ell_load<WE>(f, own_kr(d, i));
+    const Ell<EllW<WE>::KR> kr = ell_load<EllW<WE>::KR>(f, own_kr(d, i));
     for (int m = ti; m < nr; m += si) T[m * FAST_MAXNS + i] = ell_dot(kr, rec + (size_t)m * rd);
   }
   __syncthreads();
   if (k < nu) {  // u = e_off + (z - E^T T), in the z slot
-    const Ell<WE> ec = ell_load<WE>(f, own_ec(d, k));
+    const Ell<EllW<WE>::EC> ec = ell_load<EllW<WE>::EC>(f, own_ec(d, k));
     for (int m = tk; m < nr; m += sk) {
       double* R = rec + (size_t)m * rd;
       const double u = R[nu + k] + (R[k] - ell_dot(ec, T + m * FAST_MAXNS));
@@ -404,7 +411,7 @@ __global__ void __launch_bounds__(512) k_chain_down(FastView f) {
   }
   __syncthreads();
   if (j < nt) {  // u B^T into the dead e_off slot
-    const Ell<WE> br = ell_load<WE>(f, own_br(d, j));
+    const Ell<EllW<WE>::BR> br = ell_load<EllW<WE>::BR>(f, own_br(d, j));
     for (int m = tj; m < nr; m += sj) {
       double* R = rec + (size_t)m * rd;
       R[nu + j] = ell_dot(br, R);
@@ -499,7 +506,7 @@ __device__ __forceinline__ ProxIt prox_it(const FastView& f) {
 }
 // x: the node's state row (lx stride not needed: x[j]), returns bad.
 __device__ __forceinline__ bool prox_x_warp(const FastView& f, const ProxIt& P, int r, const double* x_row,
-                                            double* sd2) {
+                                            double* sd2, double* yc_row) {
   const DevView& d = f.d;
   const int nt = d.nt, W = d.W, lx = d.lx, ly = d.ly, lane = threadIdx.x & 31;
   const size_t rw = (size_t)r * W;
@@ -565,14 +572,15 @@ __device__ __forceinline__ bool prox_x_warp(const FastView& f, const ProxIt& P, 
       if (P.next) {
         const double w1 = dadd(p1, dmul(P.beta1, dsub(p1, y1[q])));
         const double w2 = dadd(p2, dmul(P.beta1, dsub(p2, y2[q])));
-        d.Yc[(size_t)r * ly + j] = dadd(w1, w2);
+        yc_row[j] = dadd(w1, w2);
       }
     }
   }
   __syncwarp();
   return bad;
 }
-__device__ __forceinline__ bool prox_u_warp(const FastView& f, const ProxIt& P, int r, const double* u_row) {
+__device__ __forceinline__ bool prox_u_warp(const FastView& f, const ProxIt& P, int r, const double* u_row,
+                                            double* yc_row) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, W = d.W, lx = d.lx, ly = d.ly, lane = threadIdx.x & 31;
   const size_t rw = (size_t)r * W;
@@ -602,7 +610,7 @@ __device__ __forceinline__ bool prox_u_warp(const FastView& f, const ProxIt& P, 
       const double p3 = dsub(v3, dmul(P.gamma, np_clip(V3, d.umin[k], d.umax[k])));
       yn[k] = p3;
       bad |= !isfinite(p3);
-      if (P.next) d.Yc[(size_t)r * ly + lx + k] = dadd(p3, dmul(P.beta1, dsub(p3, y3[q])));
+      if (P.next) yc_row[lx + k] = dadd(p3, dmul(P.beta1, dsub(p3, y3[q])));
     }
   }
   return bad;
@@ -617,8 +625,9 @@ __global__ void __launch_bounds__(256) k_prox_warp(FastView f) {
   const int r = blockIdx.x * PW_ROWS + m;
   if (r >= d.n) return;
   const ProxIt P = prox_it(f);
-  const bool bad = (warp & 1) == 0 ? prox_x_warp(f, P, r, d.X + (size_t)r * d.lx, sd2[m])
-                                   : prox_u_warp(f, P, r, d.U + (size_t)r * d.nu);
+  double* yc = d.Yc + (size_t)r * d.ly;
+  const bool bad = (warp & 1) == 0 ? prox_x_warp(f, P, r, d.X + (size_t)r * d.lx, sd2[m], yc)
+                                   : prox_u_warp(f, P, r, d.U + (size_t)r * d.nu, yc);
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(d.bad_nu, P.it);
 }
 
@@ -632,6 +641,106 @@ __global__ void k_collapse(DevView d, const double* __restrict__ y, double* Yc) 
     const int c = (int)(i - r * ly);
     const double* yr = y + r * W;
     Yc[i] = c < nt ? yr[c] + yr[nt + c] : (c < lx ? 0.0 : (c - lx < nu ? yr[2 * nt + c - lx] : 0.0));
+  }
+}
+
+// ---------------------------------------------------------------- k_chain_pu
+// Prox of iteration it fused with the up pass of iteration it+1, one CTA per
+// chain: warp pairs run the barrier-free warp prox over the chain rows (and
+// the ancestors this chain owns, whose Yc goes to HBM for k_branch_grp); the
+// chain rows' next collapsed dual Yc stays in shared memory and feeds the
+// suffix scans of k_chain_up directly (no Yc round trip through HBM).
+// Shared: rec nst x (ly + nu + 2) [Yc->wbar,a | R->S | aux], T nst x 32,
+// sd2 (warps/2) x 128.
+template <int WE>
+__global__ void __launch_bounds__(256) k_chain_pu(FastView f) {
+  const DevView& d = f.d;
+  const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly, ns = d.ns;
+  const int kb = f.kstar, nst = d.H - kb, ci = blockIdx.x;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int ra = ly + nu + 2;
+  double* rec = reinterpret_cast<double*>(smem_raw);
+  double* T = rec + (size_t)nst * ra;
+  double* sd2 = T + (size_t)nst * FAST_MAXNS;
+  const NodePtrs np = *d.np;
+  const ProxIt P = prox_it(f);
+  // R and aux of the chain rows arrive while the prox runs
+  FOR_RC(nst - 1, 6, (nu >> 1), t, k)
+    cp16(rec + (size_t)t * ra + ly + 2 * k, np.R + (size_t)chain_row(f, t, ci) * nu + 2 * k);
+  if (threadIdx.x < nst) cp16(rec + (size_t)threadIdx.x * ra + ly + nu, f.aux + (size_t)chain_row(f, threadIdx.x, ci) * 2);
+  cp_commit();
+  // ---- prox: owned ancestors, then chain rows; warp pair w takes rows w, w + pairs, ...
+  const unsigned own = kb > 0 ? f.cown[ci] : 0u;
+  const int pairs = blockDim.x >> 6, pw = threadIdx.x >> 6, role = (threadIdx.x >> 5) & 1;
+  const int n_own = __popc(own);
+  bool bad = false;
+  for (int p = pw; p < n_own + nst; p += pairs) {
+    int r;
+    double* yc;
+    if (p < n_own) {
+      unsigned w = own;
+      for (int c = 0; c < p; ++c) w &= w - 1;
+      r = f.cpath[(size_t)ci * kb + (__ffs(w) - 1)];
+      yc = d.Yc + (size_t)r * ly;
+    } else {
+      r = chain_row(f, p - n_own, ci);
+      yc = rec + (size_t)(p - n_own) * ra;
+    }
+    bad |= role == 0 ? prox_x_warp(f, P, r, d.X + (size_t)r * lx, sd2 + (size_t)pw * 128, yc)
+                     : prox_u_warp(f, P, r, d.U + (size_t)r * nu, yc);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicMin(d.bad_nu, P.it);
+  if (!P.next) return;
+  cp_wait<0>();
+  __syncthreads();
+  // ---- up pass of iteration it+1 (as k_chain_up, rec rows already hold Yc)
+  const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
+  const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
+  if (threadIdx.x < nt) {
+    const int j = threadIdx.x;
+    double acc = 0.0;
+    for (int t = nst - 1; t >= 0; --t) {
+      const double yx = rec[(size_t)t * ra + j];
+      acc = t == nst - 1 ? yx : yx + acc;
+      rec[(size_t)t * ra + j] = acc;
+    }
+    d.wbar[(size_t)chain_row(f, 0, ci) * lx + j] = acc;
+  }
+  __syncthreads();
+  if (k < nu) {
+    const Ell<EllW<WE>::BC> bc = ell_load<EllW<WE>::BC>(f, own_bc(d, k));
+    for (int t = tk; t < nst; t += sk) {
+      double* R = rec + (size_t)t * ra;
+      double a = R[lx + k] + ell_dot(bc, R);
+      if (t < nst - 1) a = a + R[ly + k];
+      R[lx + k] = a;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < nu) {
+    double acc = 0.0;
+    for (int t = nst - 1; t >= 0; --t) {
+      double* R = rec + (size_t)t * ra;
+      R[ly + threadIdx.x] = acc;
+      const double a = R[lx + threadIdx.x];
+      acc = t == nst - 1 ? a : a + acc;
+    }
+    f.Asub[(size_t)chain_row(f, 0, ci) * nu + threadIdx.x] = acc;
+  }
+  __syncthreads();
+  if (i < ns) {
+    const Ell<EllW<WE>::KR> kr = ell_load<EllW<WE>::KR>(f, own_kr(d, i));
+    for (int t = ti; t < nst - 1; t += si) T[t * FAST_MAXNS + i] = ell_dot(kr, rec + (size_t)t * ra + ly);
+  }
+  __syncthreads();
+  if (k < nu) {
+    const Ell<EllW<WE>::EC> ec = ell_load<EllW<WE>::EC>(f, own_ec(d, k));
+    for (int t = tk; t < nst; t += sk) {
+      const double* R = rec + (size_t)t * ra;
+      const double a = R[lx + k];
+      const double l = t < nst - 1 ? a + (R[ly + k] - ell_dot(ec, T + t * FAST_MAXNS)) : a;
+      f.Lb[(size_t)chain_row(f, t, ci) * nu + k] = l * R[ly + nu];
+    }
   }
 }
 

@@ -114,26 +114,28 @@ def test_reciprocal_division_is_exact():
     assert bad.value == 0
 
 
-@pytest.mark.parametrize("kernel", ["graph", "graph-fused", "scan", "cta", "warp"])
+@pytest.mark.parametrize("kernel", ["graph", "graph-fused", "graph-pu", "scan", "cta", "warp"])
 @pytest.mark.parametrize("cfg", ["C1", "C2"])
 def test_every_structured_kernel_matches_general(cfg, kernel):
     inst = config_instance(cfg)
     gamma = 1.0 / 2e9
     old = os.environ.get("WMPC_KERNEL")
     os.environ["WMPC_KERNEL"] = kernel.split("-")[0]
-    if kernel.endswith("fused"):
-        os.environ["WMPC_FUSED"] = "1"
+    extra = {"graph-fused": "WMPC_FUSED", "graph-pu": "WMPC_PU"}.get(kernel)
+    if extra:
+        os.environ[extra] = "1"
     try:
         rf, mf = _solve(inst, 40, gamma, True, gce=17)
     finally:
-        os.environ.pop("WMPC_FUSED", None)
+        if extra:
+            os.environ.pop(extra, None)
         if old is None:
             del os.environ["WMPC_KERNEL"]
         else:
             os.environ["WMPC_KERNEL"] = old
     rg, _ = _solve(inst, 40, gamma, False, gce=17)
     # a variant whose shared-memory footprint does not fit falls back to the CTA kernel (1..99)
-    allowed = {"graph": [300], "graph-fused": [310], "scan": list(range(200, 300)) + list(range(1, 100)),
+    allowed = {"graph": [300], "graph-fused": [310], "graph-pu": [320], "scan": list(range(200, 300)) + list(range(1, 100)),
                "warp": list(range(100, 200)) + list(range(1, 100)), "cta": list(range(1, 100))}[kernel]
     assert mf in allowed, mf
     for k in ("u0", "primal", "primal_avg", "dual"):
