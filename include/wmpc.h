@@ -106,6 +106,11 @@ int wmpc_operator_trace(wmpc_ctx* ctx, double* trace);
 int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* theta,
                    const double* beta);
 int wmpc_apg_run(wmpc_ctx* ctx, int count);
+/* fp32 mode: the dual-gradient kernels (chain/branch passes,
+ * Yc, L, U, X, node data) run in fp32; y, the prox, the ergodic averages, the
+ * checks and the certificate stay fp64. Needs the structured graph path;
+ * before wmpc_apg_begin. Own tolerance (tests: 1e-4 relative). */
+int wmpc_set_precision(wmpc_ctx* ctx, int fp32);
 /* Warm start (closed loop; the reference always starts at y = 0,
  * solver.py:430-431): right after wmpc_apg_begin, y0 = y_prev = the given dual. */
 int wmpc_apg_warm(wmpc_ctx* ctx, const double* y0);

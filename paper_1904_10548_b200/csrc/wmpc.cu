@@ -97,6 +97,11 @@ struct wmpc_ctx {
   ncclComm_t nccl = nullptr;                   // subtree sharding: exchange inside the iteration graph
   size_t sm_up = 0, sm_grp = 0, sm_down = 0, sm_prox = 0;
   int up_threads = 512, down_threads = 512, prox_warp = 1, use_pu = 0;
+  int fp32 = 0;                                 // SolverConfig.precision == "fp32"
+  float *f32_Yc = nullptr, *f32_Lb = nullptr, *f32_Asub = nullptr, *f32_wbar = nullptr, *f32_U = nullptr,
+        *f32_X = nullptr, *f32_eoff = nullptr, *f32_R = nullptr, *f32_g = nullptr, *f32_aux = nullptr,
+        *f32_ell = nullptr;
+  size_t ell_len = 0;
   size_t sm_pu = 0;
   int *ell_cnt = nullptr, *ell_idx = nullptr;
   double* ell_val = nullptr;
@@ -305,33 +310,52 @@ template <int WE>
 void gk_pu(wmpc_ctx* ctx, const FastView& f) {
   k_chain_pu<WE><<<ctx->nchain, 256, ctx->sm_pu, ctx->stream>>>(f);
 }
+template <int WE, typename TG>
+void gk_attrs_t(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
+  CK(cudaFuncSetAttribute(k_chain_up<WE, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
+  CK(cudaFuncSetAttribute(k_chain_down<WE, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
+  CK(cudaFuncSetAttribute(k_branch_grp<WE, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grp));
+}
 template <int WE>
 void gk_attrs(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
   if (ctx->sm_pu) CK(cudaFuncSetAttribute(k_chain_pu<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->sm_pu));
-  CK(cudaFuncSetAttribute(k_chain_up<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
-  CK(cudaFuncSetAttribute(k_chain_down<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
-  CK(cudaFuncSetAttribute(k_branch_grp<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grp));
+  gk_attrs_t<WE, double>(ctx, up, down, grp);
+  gk_attrs_t<WE, float>(ctx, up, down, grp);
 }
-template <int WE>
+template <int WE, typename TG = double>
 void gk_up(wmpc_ctx* ctx, const FastView& f) {
-  k_chain_up<WE><<<ctx->nchain, ctx->up_threads, ctx->sm_up, ctx->stream>>>(f);
+  k_chain_up<WE, TG><<<ctx->nchain, ctx->up_threads, ctx->sm_up, ctx->stream>>>(f);
 }
-template <int WE>
+template <int WE, typename TG = double>
 void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump) {
   for (const auto& g : ctx->gk_groups) {
-    k_branch_grp<WE><<<g.second, SC_THREADS, ctx->sm_grp, ctx->stream>>>(f, g.first, bump, GRP_FULL);
+    k_branch_grp<WE, TG><<<g.second, SC_THREADS, ctx->sm_grp, ctx->stream>>>(f, g.first, bump, GRP_FULL);
     bump = 0;
   }
 }
 template <int WE>
 void gk_rep(wmpc_ctx* ctx, const FastView& f, int mode, int bump) {
   if (ctx->rep_group.second > 0)
-    k_branch_grp<WE><<<ctx->rep_group.second, SC_THREADS, ctx->sm_grp, ctx->stream>>>(f, ctx->rep_group.first, bump,
-                                                                                        mode);
+    k_branch_grp<WE, double><<<ctx->rep_group.second, SC_THREADS, ctx->sm_grp, ctx->stream>>>(
+        f, ctx->rep_group.first, bump, mode);
 }
-template <int WE>
+template <int WE, typename TG = double>
 void gk_down(wmpc_ctx* ctx, const FastView& f) {
-  k_chain_down<WE><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);
+  k_chain_down<WE, TG><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);
+}
+template <typename TG>
+void gk_prox(wmpc_ctx* ctx, const FastView& f) {
+  if (ctx->prox_warp)
+    k_prox_warp<TG><<<(ctx->n + PW_ROWS - 1) / PW_ROWS, 256, 0, ctx->stream>>>(f);
+  else
+    k_prox_nodes<<<(ctx->n + SC_NPB - 1) / SC_NPB, SC_THREADS, ctx->sm_prox, ctx->stream>>>(f);
+}
+template <int WE, typename TG>
+void gk_iteration(wmpc_ctx* ctx, const FastView& f) {
+  gk_up<WE, TG>(ctx, f);
+  gk_grp<WE, TG>(ctx, f, 1);
+  gk_down<WE, TG>(ctx, f);
+  gk_prox<TG>(ctx, f);
 }
 
 // Branching-region stage groups, bottom-up, with <= 32 items per row, and
@@ -520,6 +544,7 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
     upload_vec(ctx, &ctx->ell_idx, idx);
     upload_vec(ctx, &ctx->ell_val, val);
     ctx->ell_w = we;
+    ctx->ell_len = val.size();
   }
   ctx->h_cptr = cptr;
   ctx->h_cidx = cidx;
@@ -851,19 +876,11 @@ void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
     }
     return;
   }
-  if (ctx->ell_w == 4) {
-    gk_up<4>(ctx, f);
-    gk_grp<4>(ctx, f, 1);
-    gk_down<4>(ctx, f);
+  if (ctx->fp32) {
+    if (ctx->ell_w == 4) gk_iteration<4, float>(ctx, f); else gk_iteration<8, float>(ctx, f);
   } else {
-    gk_up<8>(ctx, f);
-    gk_grp<8>(ctx, f, 1);
-    gk_down<8>(ctx, f);
+    if (ctx->ell_w == 4) gk_iteration<4, double>(ctx, f); else gk_iteration<8, double>(ctx, f);
   }
-  if (ctx->prox_warp)
-    k_prox_warp<<<(ctx->n + PW_ROWS - 1) / PW_ROWS, 256, 0, st>>>(f);
-  else
-    k_prox_nodes<<<(ctx->n + SC_NPB - 1) / SC_NPB, SC_THREADS, ctx->sm_prox, st>>>(f);
 }
 
 void enqueue_shard_iteration(wmpc_ctx* ctx, const FastView& f);
@@ -929,7 +946,7 @@ void dual_eval_graph(wmpc_ctx* ctx, const double* y, int phase) {
   }
   if (phase != 0) {
     if (ctx->rep_group.second > 0) gk_rep<WE>(ctx, f, GRP_FINISH, 0);
-    k_chain_down<WE><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);
+    k_chain_down<WE, double><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);
     CK(cudaMemcpyAsync(ctx->Yc, ctx->Yc_save, sizeof(double) * (size_t)ctx->n * ctx->ly, cudaMemcpyDeviceToDevice,
                        ctx->stream));
     ctx->launches += 1 + (ctx->rep_group.second > 0);
@@ -973,6 +990,8 @@ FastView make_fastview(wmpc_ctx* ctx, int count) {
   f.ell_idx = ctx->ell_idx;
   f.ell_val = ctx->ell_val;
   f.ell_w = ctx->ell_w;
+  f.g32 = G32{ctx->f32_Yc, ctx->f32_Lb, ctx->f32_Asub, ctx->f32_wbar, ctx->f32_U, ctx->f32_X,
+              ctx->f32_eoff, ctx->f32_R, ctx->f32_g, ctx->f32_aux, ctx->f32_ell};
   f.xbuf = ctx->xbuf;
   f.rep_gidx = ctx->rep_gidx;
   f.pb = ctx->fused_pb;
@@ -1044,7 +1063,8 @@ void free_all(wmpc_ctx* c) {
                   c->bad_row, c->part, c->scal, c->d_np, c->chain_node,
                   c->bc_ptr, c->bc_row, c->br_ptr, c->br_col, c->off_dev, c->bc_val, c->br_val,
                   c->e_ptr, c->e_col, c->e_val, c->aux,
-                  c->Lb, c->Asub, c->blob, c->store_it, c->Yc_save, c->acct, c->rep_gidx, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
+                  c->Lb, c->Asub, c->blob, c->store_it, c->f32_Yc, c->f32_Lb, c->f32_Asub, c->f32_wbar, c->f32_U,
+                  c->f32_X, c->f32_eoff, c->f32_R, c->f32_g, c->f32_aux, c->f32_ell, c->Yc_save, c->acct, c->rep_gidx, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
                   c->pj_ecv, c->dk_mv, c->dk_sweeps, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
                   c->prof};
   for (void* p : ptrs)
@@ -1080,10 +1100,7 @@ void shard_phase(wmpc_ctx* ctx, const FastView& f, int phase) {
   } else {
     if (rep) gk_rep<WE>(ctx, f, GRP_FINISH, 0);
     gk_down<WE>(ctx, f);
-    if (ctx->prox_warp)
-      k_prox_warp<<<(ctx->n + PW_ROWS - 1) / PW_ROWS, 256, 0, ctx->stream>>>(f);
-    else
-      k_prox_nodes<<<(ctx->n + SC_NPB - 1) / SC_NPB, SC_THREADS, ctx->sm_prox, ctx->stream>>>(f);
+    gk_prox<double>(ctx, f);
     ctx->launches += 2 + rep;
   }
   check_launch(ctx);
@@ -1623,6 +1640,15 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
     ctx->it_host = 0;
     sync(ctx);
     if (ctx->fast) {
+      if (ctx->use_graphk && ctx->fp32) {  // node data in fp32, Yc32 = 0
+        const size_t n = ctx->n;
+        CK(cudaMemsetAsync(ctx->f32_Yc, 0, sizeof(float) * n * ctx->ly, ctx->stream));
+        ctx->launches += 3;
+        k_convert<<<grid_for(n * ctx->nu), 256, 0, ctx->stream>>>(ctx->nodes->e_off, ctx->f32_eoff, n * ctx->nu);
+        k_convert<<<grid_for(n * ctx->nu), 256, 0, ctx->stream>>>(ctx->nodes->R, ctx->f32_R, n * ctx->nu);
+        k_convert<<<grid_for(n * ctx->lx), 256, 0, ctx->stream>>>(ctx->nodes->g, ctx->f32_g, n * ctx->lx);
+        check_launch(ctx);
+      }
       if (ctx->use_graphk) {
         capture_graphk(ctx);
         if (ctx->use_fused || ctx->use_pu) {  // up pass of iteration 0 (Yc = 0)
@@ -1809,6 +1835,11 @@ int wmpc_apg_read(wmpc_ctx* ctx, int averaged, double* u0, double* primal, doubl
   return run(ctx, [&]() -> int {
     DevView d = view(ctx);
     const size_t n = ctx->n;
+    if (ctx->fp32 && ctx->it_host > 0) {  // the last iterate lives in the fp32 arrays
+      ctx->launches += 2;
+      k_convert<<<grid_for(n * ctx->nu), 256, 0, ctx->stream>>>(ctx->f32_U, ctx->U, n * ctx->nu);
+      k_convert<<<grid_for(n * ctx->lx), 256, 0, ctx->stream>>>(ctx->f32_X, ctx->X, n * ctx->lx);
+    }
     if (u0) {
       ctx->launches++;
       k_u0<<<1, 128, 0, ctx->stream>>>(d, averaged ? ctx->Ua : ctx->U, ctx->off[1], ctx->zbuf);
@@ -1962,6 +1993,36 @@ int wmpc_set_min_branch_stage(wmpc_ctx* ctx, int stage) {
   });
 }
 
+int wmpc_set_precision(wmpc_ctx* ctx, int fp32) {
+  return run(ctx, [&]() -> int {
+    if (!fp32) {
+      if (ctx->fp32) ctx->gk_gamma = -1.0;
+      ctx->fp32 = 0;
+      return WMPC_OK;
+    }
+    if (!ctx->fast || !ctx->use_graphk || ctx->use_fused || ctx->use_pu || ctx->shard_k >= 0) {
+      ctx->err = "fp32 mode needs the structured graph path (A = I, W = cI), unsharded";
+      return WMPC_E_STATE;
+    }
+    const size_t n = ctx->n, nu = ctx->nu, lx = ctx->lx, ly = ctx->ly;
+    const size_t na = (size_t)(ctx->n_branch + ctx->nchain) * nu;
+    if (!ctx->f32_Yc) {
+      dalloc(ctx, &ctx->f32_Yc, n * ly); dalloc(ctx, &ctx->f32_Lb, n * nu); dalloc(ctx, &ctx->f32_Asub, na);
+      dalloc(ctx, &ctx->f32_wbar, n * lx); dalloc(ctx, &ctx->f32_U, n * nu); dalloc(ctx, &ctx->f32_X, n * lx);
+      dalloc(ctx, &ctx->f32_eoff, n * nu); dalloc(ctx, &ctx->f32_R, n * nu); dalloc(ctx, &ctx->f32_g, n * lx);
+      dalloc(ctx, &ctx->f32_aux, n * 2); dalloc(ctx, &ctx->f32_ell, ctx->ell_len);
+    }
+    ctx->launches += 2;
+    k_convert<<<grid_for(n * 2), 256, 0, ctx->stream>>>(ctx->aux, ctx->f32_aux, n * 2);
+    k_convert<<<grid_for(ctx->ell_len), 256, 0, ctx->stream>>>(ctx->ell_val, ctx->f32_ell, ctx->ell_len);
+    check_launch(ctx);
+    sync(ctx);
+    if (!ctx->fp32) ctx->gk_gamma = -1.0;  // recapture the iteration graphs
+    ctx->fp32 = 1;
+    return WMPC_OK;
+  });
+}
+
 int wmpc_apg_warm(wmpc_ctx* ctx, const double* y0) {
   return run(ctx, [&]() -> int {
     ARG(y0, "null argument");
@@ -1975,6 +2036,11 @@ int wmpc_apg_warm(wmpc_ctx* ctx, const double* y0) {
     DevView d = view(ctx);
     ctx->launches++;
     k_collapse<<<grid_for((size_t)ctx->n * ctx->ly), 256, 0, ctx->stream>>>(d, ctx->Y[0], ctx->Yc);
+    if (ctx->fp32) {
+      ctx->launches++;
+      k_convert<<<grid_for((size_t)ctx->n * ctx->ly), 256, 0, ctx->stream>>>(ctx->Yc, ctx->f32_Yc,
+                                                                             (size_t)ctx->n * ctx->ly);
+    }
     if (ctx->fast && ctx->use_graphk && (ctx->use_fused || ctx->use_pu)) {  // the up pass of iteration 0
       FastView f = make_fastview(ctx, 1);
       if (ctx->ell_w == 4) gk_up<4>(ctx, f); else gk_up<8>(ctx, f);

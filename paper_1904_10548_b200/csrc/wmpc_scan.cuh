@@ -117,19 +117,46 @@ __device__ __forceinline__ int chain_row(const FastView& f, int t, int ci) { ret
 // (or row) for a whole phase and loops over tree rows, so the operator entries
 // are loaded once (from L1) instead of walked through shared memory per row.
 enum { ELL_BC = 0 };  // owner offsets: B by column [0,nu), B by row [nu,nu+nt), E by column, K by row
-template <int WE>
+// Gradient-side arrays (Yc, L, subtree totals, U, X, node data, operators) in
+// the precision TG of the dual-gradient kernels: double (default) or float
+// (fp32 mode, SolverConfig.precision == "fp32"); y, the averages and every
+// prox/certificate computation stay fp64.
+template <typename TG>
+struct GA {
+  TG *Yc, *Lb, *Asub, *wbar, *U, *X;
+  const TG *e_off, *R, *g, *aux, *ell_val;
+};
+template <typename TG>
+__device__ __forceinline__ GA<TG> ga(const FastView& f);
+template <>
+__device__ __forceinline__ GA<double> ga<double>(const FastView& f) {
+  const NodePtrs np = *f.d.np;
+  return GA<double>{f.d.Yc, f.Lb, f.Asub, f.d.wbar, f.d.U, f.d.X, np.e_off, np.R, np.g, f.aux, f.ell_val};
+}
+template <>
+__device__ __forceinline__ GA<float> ga<float>(const FastView& f) {
+  return GA<float>{f.g32.Yc, f.g32.Lb, f.g32.Asub, f.g32.wbar, f.g32.U, f.g32.X, f.g32.e_off, f.g32.R, f.g32.g,
+                   f.g32.aux, f.g32.ell_val};
+}
+// async copy of two elements (16 B for double, 8 B for float)
+__device__ __forceinline__ void cpair(double* dst, const double* src) { cp16(dst, src); }
+__device__ __forceinline__ void cpair(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+template <int WE, typename TG = double>
 struct Ell {
   int idx[WE];
-  double val[WE];
+  TG val[WE];
 };
 // Entries past an owner's count are stored as (0, 0.0): no predication, and a
 // zero weight times a finite operand adds nothing (a dense product would
 // propagate a non-finite operand the same way).
-template <int WE>
-__device__ __forceinline__ Ell<WE> ell_load(const FastView& f, int owner) {
-  Ell<WE> o;
+template <int WE, typename TG = double>
+__device__ __forceinline__ Ell<WE, TG> ell_load(const FastView& f, int owner) {
+  Ell<WE, TG> o;
   const int* ip = f.ell_idx + (size_t)owner * f.ell_w;
-  const double* vp = f.ell_val + (size_t)owner * f.ell_w;
+  const TG* vp = ga<TG>(f).ell_val + (size_t)owner * f.ell_w;
 #pragma unroll
   for (int e = 0; e < WE; ++e) {
     o.idx[e] = ip[e];
@@ -137,9 +164,9 @@ __device__ __forceinline__ Ell<WE> ell_load(const FastView& f, int owner) {
   }
   return o;
 }
-template <int WE>
-__device__ __forceinline__ double ell_dot(const Ell<WE>& o, const double* x) {
-  double s = 0.0;
+template <int WE, typename TG>
+__device__ __forceinline__ TG ell_dot(const Ell<WE, TG>& o, const TG* x) {
+  TG s = 0;
 #pragma unroll
   for (int e = 0; e < WE; ++e) s = fma(o.val[e], x[o.idx[e]], s);
   return s;
@@ -159,68 +186,68 @@ __device__ __forceinline__ int own_kr(const DevView& d, int i) { return 2 * d.nu
 // ---------------------------------------------------------------- k_chain_up
 // Shared: rec nst x (ly + nu + 2) [Yx->wbar | Yu->a | R->S->PS | aux],
 // T nst x FAST_MAXNS (in-place phases keep 4 CTAs per SM at H = 24).
-template <int WE>
+template <int WE, typename TG>
 __global__ void __launch_bounds__(512) k_chain_up(FastView f) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly, ns = d.ns;
   const int nst = d.H - f.kstar, ci = blockIdx.x;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int ra = ly + nu + 2;
-  double* rec = reinterpret_cast<double*>(smem_raw);
-  double* T = rec + (size_t)nst * ra;
-  const NodePtrs np = *d.np;
-  FOR_RC(nst, 7, (ly >> 1), t, k) cp16(rec + (size_t)t * ra + 2 * k, d.Yc + (size_t)chain_row(f, t, ci) * ly + 2 * k);
+  TG* rec = reinterpret_cast<TG*>(smem_raw);
+  TG* T = rec + (size_t)nst * ra;
+  const GA<TG> G = ga<TG>(f);
+  FOR_RC(nst, 7, (ly >> 1), t, k) cpair(rec + (size_t)t * ra + 2 * k, G.Yc + (size_t)chain_row(f, t, ci) * ly + 2 * k);
   FOR_RC(nst - 1, 6, (nu >> 1), t, k)
-    cp16(rec + (size_t)t * ra + ly + 2 * k, np.R + (size_t)chain_row(f, t, ci) * nu + 2 * k);
-  if (threadIdx.x < nst) cp16(rec + (size_t)threadIdx.x * ra + ly + nu, f.aux + (size_t)chain_row(f, threadIdx.x, ci) * 2);
+    cpair(rec + (size_t)t * ra + ly + 2 * k, G.R + (size_t)chain_row(f, t, ci) * nu + 2 * k);
+  if (threadIdx.x < nst) cpair(rec + (size_t)threadIdx.x * ra + ly + nu, G.aux + (size_t)chain_row(f, threadIdx.x, ci) * 2);
   cp_commit();
   const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
   const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
-  const Ell<EllW<WE>::BC> bc = ell_load<EllW<WE>::BC>(f, own_bc(d, k < nu ? k : 0));
+  const Ell<EllW<WE>::BC, TG> bc = ell_load<EllW<WE>::BC, TG>(f, own_bc(d, k < nu ? k : 0));
   cp_wait<0>();
   __syncthreads();
   if (threadIdx.x < nt) {  // wbar suffix scan in place: wbar_t = Yx_t + wbar_{t+1}
     const int j = threadIdx.x;
-    double acc = 0.0;
+    TG acc = 0;
     for (int t = nst - 1; t >= 0; --t) {
-      const double yx = rec[(size_t)t * ra + j];
+      const TG yx = rec[(size_t)t * ra + j];
       acc = t == nst - 1 ? yx : yx + acc;
       rec[(size_t)t * ra + j] = acc;
     }
-    d.wbar[(size_t)chain_row(f, 0, ci) * lx + j] = acc;
+    G.wbar[(size_t)chain_row(f, 0, ci) * lx + j] = acc;
   }
   __syncthreads();
   if (k < nu)
     for (int t = tk; t < nst; t += sk) {  // a = (Yu + wbar B) + R, over Yu
-      double* R = rec + (size_t)t * ra;
-      double a = R[lx + k] + ell_dot(bc, R);
+      TG* R = rec + (size_t)t * ra;
+      TG a = R[lx + k] + ell_dot(bc, R);
       if (t < nst - 1) a = a + R[ly + k];
       R[lx + k] = a;
     }
   __syncthreads();
   if (threadIdx.x < nu) {  // S_t = A_{t+1} over R, A_t = a_t + S_t
-    double acc = 0.0;
+    TG acc = 0;
     for (int t = nst - 1; t >= 0; --t) {
-      double* R = rec + (size_t)t * ra;
+      TG* R = rec + (size_t)t * ra;
       R[ly + threadIdx.x] = acc;
-      const double a = R[lx + threadIdx.x];
+      const TG a = R[lx + threadIdx.x];
       acc = t == nst - 1 ? a : a + acc;
     }
-    f.Asub[(size_t)chain_row(f, 0, ci) * nu + threadIdx.x] = acc;
+    G.Asub[(size_t)chain_row(f, 0, ci) * nu + threadIdx.x] = acc;
   }
   __syncthreads();
   if (i < ns) {  // T = K S
-    const Ell<EllW<WE>::KR> kr = ell_load<EllW<WE>::KR>(f, own_kr(d, i));
+    const Ell<EllW<WE>::KR, TG> kr = ell_load<EllW<WE>::KR, TG>(f, own_kr(d, i));
     for (int t = ti; t < nst - 1; t += si) T[t * FAST_MAXNS + i] = ell_dot(kr, rec + (size_t)t * ra + ly);
   }
   __syncthreads();
   if (k < nu) {  // L = (a + (S - E^T T)) / (2c p)
-    const Ell<EllW<WE>::EC> ec = ell_load<EllW<WE>::EC>(f, own_ec(d, k));
+    const Ell<EllW<WE>::EC, TG> ec = ell_load<EllW<WE>::EC, TG>(f, own_ec(d, k));
     for (int t = tk; t < nst; t += sk) {
-      const double* R = rec + (size_t)t * ra;
-      const double a = R[lx + k];
-      const double l = t < nst - 1 ? a + (R[ly + k] - ell_dot(ec, T + t * FAST_MAXNS)) : a;
-      f.Lb[(size_t)chain_row(f, t, ci) * nu + k] = l * R[ly + nu];
+      const TG* R = rec + (size_t)t * ra;
+      const TG a = R[lx + k];
+      const TG l = t < nst - 1 ? a + (R[ly + k] - ell_dot(ec, T + t * FAST_MAXNS)) : a;
+      G.Lb[(size_t)chain_row(f, t, ci) * nu + k] = l * R[ly + nu];
     }
   }
 }
@@ -241,7 +268,7 @@ __global__ void __launch_bounds__(512) k_chain_up(FastView f) {
 // all-reduce over ranks, mode GRP_FINISH reads them back and finishes the row
 // identically on every rank. bump: first kernel of an APG iteration.
 enum { GRP_FULL = 0, GRP_PARTIAL = 1, GRP_FINISH = 2 };
-template <int WE>
+template <int WE, typename TG>
 __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, int bump, int mode) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly;
@@ -249,32 +276,32 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
   constexpr int NW = SC_THREADS / 32;
   if (bump && blockIdx.x == 0 && threadIdx.x == 0) *d.iter += 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* part = reinterpret_cast<double*>(smem_raw);  // NW x 256: [s1 64 | s2 64 | su 128]
-  double* W1 = part + NW * 256;  // lx
-  double* W2 = W1 + lx;          // lx
-  double* av = W2 + lx;          // nu
-  double* Sv = av + nu;          // nu
-  double* T = Sv + nu;           // FAST_MAXNS
-  const NodePtrs np = *d.np;
+  TG* part = reinterpret_cast<TG*>(smem_raw);  // NW x 256: [s1 64 | s2 64 | su 128]
+  TG* W1 = part + NW * 256;  // lx
+  TG* W2 = W1 + lx;          // lx
+  TG* av = W2 + lx;          // nu
+  TG* Sv = av + nu;          // nu
+  TG* T = Sv + nu;           // FAST_MAXNS
+  const GA<TG> G = ga<TG>(f);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double s1[2] = {0.0, 0.0}, s2[2] = {0.0, 0.0}, su[4] = {0.0, 0.0, 0.0, 0.0};
+  TG s1[2] = {0, 0}, s2[2] = {0, 0}, su[4] = {0, 0, 0, 0};
   const int e0 = mode == GRP_FINISH ? 0 : f.gi_ptr[r], e1 = mode == GRP_FINISH ? 0 : f.gi_ptr[r + 1];
   for (int e = e0 + warp; e < e1; e += NW) {
     const int item = f.gi_item[e];
     const size_t row = (size_t)(item >> 1);
     const bool fr = item & 1;
-    const double w = (double)f.gi_w[e];
-    const double* px = fr ? d.wbar + row * lx : d.Yc + row * ly;
-    double vx[2], vu[4];
+    const TG w = (TG)f.gi_w[e];
+    const TG* px = fr ? G.wbar + row * lx : G.Yc + row * ly;
+    TG vx[2], vu[4];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int c = lane + 32 * i;
-      vx[i] = c < nt ? px[c] : 0.0;
+      vx[i] = c < nt ? px[c] : TG(0);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int c = lane + 32 * i;
-      vu[i] = c < nu ? (fr ? f.Asub[row * nu + c] : d.Yc[row * ly + lx + c] + np.R[row * nu + c]) : 0.0;
+      vu[i] = c < nu ? (fr ? G.Asub[row * nu + c] : G.Yc[row * ly + lx + c] + G.R[row * nu + c]) : TG(0);
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -284,7 +311,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
 #pragma unroll
     for (int i = 0; i < 4; ++i) su[i] += vu[i];
   }
-  double* pw = part + warp * 256;
+  TG* pw = part + warp * 256;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     pw[lane + 32 * i] = s1[i];
@@ -293,10 +320,10 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
 #pragma unroll
   for (int i = 0; i < 4; ++i) pw[128 + lane + 32 * i] = su[i];
   __syncthreads();
-  double* xb = mode == GRP_FULL ? nullptr : f.xbuf + (size_t)f.rep_gidx[r] * 256;
+  double* xb = mode == GRP_FULL ? nullptr : f.xbuf + (size_t)f.rep_gidx[r] * 256;  // fp64 (sharding: TG = double)
   if (mode == GRP_PARTIAL) {  // item sums to the exchange buffer
     for (int c = threadIdx.x; c < 256; c += blockDim.x) {
-      double a = part[c];
+      TG a = part[c];
       for (int w = 1; w < NW; ++w) a += part[w * 256 + c];
       xb[c] = a;
     }
@@ -304,7 +331,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
   }
   if (threadIdx.x < nt) {
     const int j = threadIdx.x;
-    double a1, a2;
+    TG a1, a2;
     if (xb) {
       a1 = xb[j];
       a2 = xb[64 + j];
@@ -316,38 +343,38 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
         a2 += part[w * 256 + 64 + j];
       }
     }
-    W1[j] = d.Yc[(size_t)r * ly + j] + a1;
+    W1[j] = G.Yc[(size_t)r * ly + j] + a1;
     W2[j] = a2;
   }
   __syncthreads();
   if (threadIdx.x < nu) {
     const int k = threadIdx.x;
-    double s;
+    TG s;
     if (xb) {
       s = xb[128 + k];
     } else {
       s = part[128 + k];
       for (int w = 1; w < NW; ++w) s += part[w * 256 + 128 + k];
     }
-    double b1 = 0.0, b2 = 0.0;
-    const Ell<EllW<WE>::BC> bc = ell_load<EllW<WE>::BC>(f, own_bc(d, k));
+    TG b1 = 0, b2 = 0;
+    const Ell<EllW<WE>::BC, TG> bc = ell_load<EllW<WE>::BC, TG>(f, own_bc(d, k));
     b1 = ell_dot(bc, W1);
     b2 = ell_dot(bc, W2);
-    av[k] = (d.Yc[(size_t)r * ly + lx + k] + b1) + np.R[(size_t)r * nu + k];
+    av[k] = (G.Yc[(size_t)r * ly + lx + k] + b1) + G.R[(size_t)r * nu + k];
     Sv[k] = s + b2;
   }
-  if (threadIdx.x < nt) d.wbar[(size_t)r * lx + threadIdx.x] = W1[threadIdx.x];
+  if (threadIdx.x < nt) G.wbar[(size_t)r * lx + threadIdx.x] = W1[threadIdx.x];
   __syncthreads();
-  if (threadIdx.x < nu) f.Asub[(size_t)r * nu + threadIdx.x] = av[threadIdx.x] + Sv[threadIdx.x];
+  if (threadIdx.x < nu) G.Asub[(size_t)r * nu + threadIdx.x] = av[threadIdx.x] + Sv[threadIdx.x];
   if (threadIdx.x < d.ns) {
-    const Ell<EllW<WE>::KR> kr = ell_load<EllW<WE>::KR>(f, own_kr(d, threadIdx.x));
+    const Ell<EllW<WE>::KR, TG> kr = ell_load<EllW<WE>::KR, TG>(f, own_kr(d, threadIdx.x));
     T[threadIdx.x] = ell_dot(kr, Sv);
   }
   __syncthreads();
   if (threadIdx.x < nu) {
     const int k = threadIdx.x;
-    const Ell<EllW<WE>::EC> ec = ell_load<EllW<WE>::EC>(f, own_ec(d, k));
-    f.Lb[(size_t)r * nu + k] = (av[k] + (Sv[k] - ell_dot(ec, T))) * f.aux[(size_t)r * 2];
+    const Ell<EllW<WE>::EC, TG> ec = ell_load<EllW<WE>::EC, TG>(f, own_ec(d, k));
+    G.Lb[(size_t)r * nu + k] = (av[k] + (Sv[k] - ell_dot(ec, T))) * G.aux[(size_t)r * 2];
   }
 }
 
@@ -358,37 +385,37 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
 //   x_m = (x_{m-1} + u_m B^T) + g_m,  x_{-1} = p.
 // Ancestor rows are written by the chain that owns them (cown).
 // Shared: rec H x (2nu + lx) [L->z->u | e_off->Bu | g], T H x FAST_MAXNS, rows H.
-template <int WE>
+template <int WE, typename TG>
 __global__ void __launch_bounds__(512) k_chain_down(FastView f) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ns = d.ns;
   const int kb = f.kstar, nr = d.H, ci = blockIdx.x;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int rd = 2 * nu + lx;
-  double* rec = reinterpret_cast<double*>(smem_raw);
-  double* T = rec + (size_t)nr * rd;
+  TG* rec = reinterpret_cast<TG*>(smem_raw);
+  TG* T = rec + (size_t)nr * rd;
   int* rows = reinterpret_cast<int*>(T + (size_t)nr * FAST_MAXNS);
-  const NodePtrs np = *d.np;
+  const GA<TG> G = ga<TG>(f);
   if (threadIdx.x < nr) {
     const int m = threadIdx.x;
     rows[m] = m < kb ? f.cpath[(size_t)ci * kb + m] : chain_row(f, m - kb, ci);
   }
   __syncthreads();
-  FOR_RC(nr, 6, (nu >> 1), m, k) cp16(rec + (size_t)m * rd + 2 * k, f.Lb + (size_t)rows[m] * nu + 2 * k);
-  FOR_RC(nr, 6, (nu >> 1), m, k) cp16(rec + (size_t)m * rd + nu + 2 * k, np.e_off + (size_t)rows[m] * nu + 2 * k);
-  FOR_RC(nr, 5, (lx >> 1), m, k) cp16(rec + (size_t)m * rd + 2 * nu + 2 * k, np.g + (size_t)rows[m] * lx + 2 * k);
+  FOR_RC(nr, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * k, G.Lb + (size_t)rows[m] * nu + 2 * k);
+  FOR_RC(nr, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + nu + 2 * k, G.e_off + (size_t)rows[m] * nu + 2 * k);
+  FOR_RC(nr, 5, (lx >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * nu + 2 * k, G.g + (size_t)rows[m] * lx + 2 * k);
   cp_commit();
   const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
   const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
   const int j = threadIdx.x & 63, tj = threadIdx.x >> 6, sj = blockDim.x >> 6;
   const unsigned own = kb > 0 ? f.cown[ci] : 0u;
-  const double qk = k < nu ? d.q[k] : 0.0;
+  const TG qk = k < nu ? (TG)d.q[k] : TG(0);
   cp_wait<0>();
   __syncthreads();
   if (threadIdx.x < nu) {
-    double ls = 0.0, es = qk;
+    TG ls = 0, es = qk;
     for (int m = 0; m < nr; ++m) {
-      double* R = rec + (size_t)m * rd;
+      TG* R = rec + (size_t)m * rd;
       ls = m == 0 ? R[k] : ls + R[k];
       R[k] = es - ls;  // z over L
       es = es + R[nu + k];
@@ -396,34 +423,34 @@ __global__ void __launch_bounds__(512) k_chain_down(FastView f) {
   }
   __syncthreads();
   if (i < ns) {  // T = K z
-    const Ell<EllW<WE>::KR> kr = ell_load<EllW<WE>::KR>(f, own_kr(d, i));
+    const Ell<EllW<WE>::KR, TG> kr = ell_load<EllW<WE>::KR, TG>(f, own_kr(d, i));
     for (int m = ti; m < nr; m += si) T[m * FAST_MAXNS + i] = ell_dot(kr, rec + (size_t)m * rd);
   }
   __syncthreads();
   if (k < nu) {  // u = e_off + (z - E^T T), in the z slot
-    const Ell<EllW<WE>::EC> ec = ell_load<EllW<WE>::EC>(f, own_ec(d, k));
+    const Ell<EllW<WE>::EC, TG> ec = ell_load<EllW<WE>::EC, TG>(f, own_ec(d, k));
     for (int m = tk; m < nr; m += sk) {
-      double* R = rec + (size_t)m * rd;
-      const double u = R[nu + k] + (R[k] - ell_dot(ec, T + m * FAST_MAXNS));
+      TG* R = rec + (size_t)m * rd;
+      const TG u = R[nu + k] + (R[k] - ell_dot(ec, T + m * FAST_MAXNS));
       R[k] = u;
-      if (m >= kb || ((own >> m) & 1u)) d.U[(size_t)rows[m] * nu + k] = u;
+      if (m >= kb || ((own >> m) & 1u)) G.U[(size_t)rows[m] * nu + k] = u;
     }
   }
   __syncthreads();
   if (j < nt) {  // u B^T into the dead e_off slot
-    const Ell<EllW<WE>::BR> br = ell_load<EllW<WE>::BR>(f, own_br(d, j));
+    const Ell<EllW<WE>::BR, TG> br = ell_load<EllW<WE>::BR, TG>(f, own_br(d, j));
     for (int m = tj; m < nr; m += sj) {
-      double* R = rec + (size_t)m * rd;
+      TG* R = rec + (size_t)m * rd;
       R[nu + j] = ell_dot(br, R);
     }
   }
   __syncthreads();
   if (threadIdx.x < nt) {
-    double x = d.p[threadIdx.x];
+    TG x = (TG)d.p[threadIdx.x];
     for (int m = 0; m < nr; ++m) {
-      const double* R = rec + (size_t)m * rd;
+      const TG* R = rec + (size_t)m * rd;
       x = (x + R[nu + threadIdx.x]) + R[2 * nu + threadIdx.x];
-      if (m >= kb || ((own >> m) & 1u)) d.X[(size_t)rows[m] * lx + threadIdx.x] = x;
+      if (m >= kb || ((own >> m) & 1u)) G.X[(size_t)rows[m] * lx + threadIdx.x] = x;
     }
   }
 }
@@ -505,8 +532,9 @@ __device__ __forceinline__ ProxIt prox_it(const FastView& f) {
   return p;
 }
 // x: the node's state row (lx stride not needed: x[j]), returns bad.
-__device__ __forceinline__ bool prox_x_warp(const FastView& f, const ProxIt& P, int r, const double* x_row,
-                                            double* sd2, double* yc_row) {
+template <typename TG>
+__device__ __forceinline__ bool prox_x_warp(const FastView& f, const ProxIt& P, int r, const TG* x_row,
+                                            double* sd2, TG* yc_row) {
   const DevView& d = f.d;
   const int nt = d.nt, W = d.W, lx = d.lx, ly = d.ly, lane = threadIdx.x & 31;
   const size_t rw = (size_t)r * W;
@@ -519,7 +547,7 @@ __device__ __forceinline__ bool prox_x_warp(const FastView& f, const ProxIt& P, 
   for (int q = 0; q < 2; ++q) {
     const int j = lane + 32 * q;
     const bool ok = j < nt;
-    xv[q] = ok ? x_row[j] : 0.0;
+    xv[q] = ok ? (double)x_row[j] : 0.0;
     xa[q] = ok && P.it > 0 ? d.Xa[(size_t)r * lx + j] : 0.0;
     y1[q] = ok ? y[j] : 0.0;
     y2[q] = ok ? y[nt + j] : 0.0;
@@ -572,15 +600,16 @@ __device__ __forceinline__ bool prox_x_warp(const FastView& f, const ProxIt& P, 
       if (P.next) {
         const double w1 = dadd(p1, dmul(P.beta1, dsub(p1, y1[q])));
         const double w2 = dadd(p2, dmul(P.beta1, dsub(p2, y2[q])));
-        yc_row[j] = dadd(w1, w2);
+        yc_row[j] = (TG)dadd(w1, w2);
       }
     }
   }
   __syncwarp();
   return bad;
 }
-__device__ __forceinline__ bool prox_u_warp(const FastView& f, const ProxIt& P, int r, const double* u_row,
-                                            double* yc_row) {
+template <typename TG>
+__device__ __forceinline__ bool prox_u_warp(const FastView& f, const ProxIt& P, int r, const TG* u_row,
+                                            TG* yc_row) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, W = d.W, lx = d.lx, ly = d.ly, lane = threadIdx.x & 31;
   const size_t rw = (size_t)r * W;
@@ -593,7 +622,7 @@ __device__ __forceinline__ bool prox_u_warp(const FastView& f, const ProxIt& P, 
   for (int q = 0; q < Q; ++q) {
     const int k = lane + 32 * q;
     const bool ok = k < nu;
-    uv[q] = ok ? u_row[k] : 0.0;
+    uv[q] = ok ? (double)u_row[k] : 0.0;
     ua[q] = ok && P.it > 0 ? d.Ua[(size_t)r * nu + k] : 0.0;
     y3[q] = ok ? y[k] : 0.0;
     m3[q] = ok ? ym[k] : 0.0;
@@ -610,13 +639,14 @@ __device__ __forceinline__ bool prox_u_warp(const FastView& f, const ProxIt& P, 
       const double p3 = dsub(v3, dmul(P.gamma, np_clip(V3, d.umin[k], d.umax[k])));
       yn[k] = p3;
       bad |= !isfinite(p3);
-      if (P.next) yc_row[lx + k] = dadd(p3, dmul(P.beta1, dsub(p3, y3[q])));
+      if (P.next) yc_row[lx + k] = (TG)dadd(p3, dmul(P.beta1, dsub(p3, y3[q])));
     }
   }
   return bad;
 }
 
 constexpr int PW_ROWS = 4;  // nodes per 256-thread CTA
+template <typename TG>
 __global__ void __launch_bounds__(256) k_prox_warp(FastView f) {
   const DevView& d = f.d;
   __shared__ double sd2[PW_ROWS][128];
@@ -625,10 +655,18 @@ __global__ void __launch_bounds__(256) k_prox_warp(FastView f) {
   const int r = blockIdx.x * PW_ROWS + m;
   if (r >= d.n) return;
   const ProxIt P = prox_it(f);
-  double* yc = d.Yc + (size_t)r * d.ly;
-  const bool bad = (warp & 1) == 0 ? prox_x_warp(f, P, r, d.X + (size_t)r * d.lx, sd2[m], yc)
-                                   : prox_u_warp(f, P, r, d.U + (size_t)r * d.nu, yc);
+  const GA<TG> G = ga<TG>(f);
+  TG* yc = G.Yc + (size_t)r * d.ly;
+  const bool bad = (warp & 1) == 0 ? prox_x_warp<TG>(f, P, r, G.X + (size_t)r * d.lx, sd2[m], yc)
+                                   : prox_u_warp<TG>(f, P, r, G.U + (size_t)r * d.nu, yc);
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(d.bad_nu, P.it);
+}
+
+// fp64 -> fp32 copy (fp32 mode node data) and back (fp32 iterates for results).
+template <typename A, typename B>
+__global__ void k_convert(const A* __restrict__ src, B* dst, size_t len) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = (B)src[i];
 }
 
 // Collapsed dual of a given y (no extrapolation): Yc = [y1 + y2 | y3], for
@@ -686,8 +724,8 @@ __global__ void __launch_bounds__(256) k_chain_pu(FastView f) {
       r = chain_row(f, p - n_own, ci);
       yc = rec + (size_t)(p - n_own) * ra;
     }
-    bad |= role == 0 ? prox_x_warp(f, P, r, d.X + (size_t)r * lx, sd2 + (size_t)pw * 128, yc)
-                     : prox_u_warp(f, P, r, d.U + (size_t)r * nu, yc);
+    bad |= role == 0 ? prox_x_warp<double>(f, P, r, d.X + (size_t)r * lx, sd2 + (size_t)pw * 128, yc)
+                     : prox_u_warp<double>(f, P, r, d.U + (size_t)r * nu, yc);
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicMin(d.bad_nu, P.it);
   if (!P.next) return;

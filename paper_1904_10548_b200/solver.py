@@ -41,6 +41,9 @@ class SolverConfig:
     averaged_primal: bool = True
     threads: int = 1  # accepted for API parity; the GPU path ignores it
     gap_check_every: int = 25
+    # "fp64" (the reference's arithmetic) or "fp32": dual-gradient kernels in
+    # fp32, dual iterate / prox / certificate in fp64 (own tolerance; GPU only)
+    precision: str = "fp64"
 
     def __post_init__(self) -> None:
         if self.max_iter < 1:
@@ -53,6 +56,8 @@ class SolverConfig:
             raise ValueError("threads must be at least 1")
         if self.gap_check_every < 1:
             raise ValueError("gap_check_every must be at least 1")
+        if self.precision not in ("fp64", "fp32"):
+            raise ValueError("precision must be 'fp64' or 'fp32'")
 
 
 @dataclass
@@ -410,6 +415,7 @@ def solve(instance, config: SolverConfig | None = None, cache: FactorCache | Non
     _upload_bounds(ctx, instance)
     theta = theta_sequence(config.max_iter)
     beta = _beta_table(theta)
+    ctx.call("wmpc_set_precision", 1 if config.precision == "fp32" else 0)
     ctx.call("wmpc_apg_begin", float(gamma), int(config.max_iter), nat.ptr(theta), nat.ptr(beta))
     if y_init is not None:
         y0 = nat.f64(y_init)

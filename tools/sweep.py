@@ -14,6 +14,7 @@ def loop_time(cfg, iters, env):
     ctx = cache._bind()
     S._upload_bounds(ctx, inst)
     th = S.theta_sequence(iters + 5); be = S._beta_table(th)
+    ctx.call("wmpc_set_precision", 1 if env.get("FP32") == "1" else 0)
     ctx.call("wmpc_apg_begin", 1 / 5e9, iters + 5, nat.ptr(th), nat.ptr(be))
     ctx.call("wmpc_apg_run", 5)
     ms = nat.C.c_float()
