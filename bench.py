@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--cpu-sample-iters", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true")
+    ap.add_argument("--no-large", action="store_true")
     return ap.parse_args()
 
 
@@ -214,10 +216,40 @@ def ncu_traffic(cfg: str):
         return None
 
 
+def roofline_large(peak: float, peak_src: str, iters: int = 50) -> dict:
+    """Device time per APG iteration on C4 (79,188 nodes, 630 MB per
+    iteration: HBM-bound) against the same algorithmic bytes."""
+    from paper_1904_10548_b200 import factor_step
+    from paper_1904_10548_b200 import _native as nat
+    from paper_1904_10548_b200 import solver as S
+    from paper_1904_10548_b200.synthetic import config_instance
+    inst = config_instance("C4")
+    cache = factor_step(inst)
+    ctx = cache._bind()
+    S._upload_bounds(ctx, inst)
+    th = S.theta_sequence(iters + 5)
+    be = S._beta_table(th)
+    out = {}
+    for prec in (0, 1):
+        ctx.call("wmpc_set_precision", prec)
+        ctx.call("wmpc_apg_begin", 1.0 / 2e9, iters + 5, nat.ptr(th), nat.ptr(be))
+        ctx.call("wmpc_apg_run", 5)
+        ms = nat.C.c_float(0.0)
+        ctx.call("wmpc_apg_run_timed", iters, nat.C.byref(ms))
+        t = ms.value / iters / 1e3
+        ach = BYTES_PER_NODE_ITER * inst.n_nonroot / t / 1e9
+        out["fp32" if prec else "fp64"] = {"us_per_iteration": t * 1e6, "achieved": ach, "frac": ach / peak}
+    ctx.call("wmpc_set_precision", 0)
+    return {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src, "nodes": inst.n_nonroot,
+            "algorithmic_bytes_per_iteration": BYTES_PER_NODE_ITER * inst.n_nonroot, **out,
+            "how": f"{iters} graph-replayed iterations after 5 warm-up, CUDA events on the solver stream; "
+                   "~1.4 GB of per-iteration traffic streams from HBM (126 MB L2: no flush needed)"}
+
+
 def kernel_desc(mode: int, per_iter: int) -> str:
     if mode == 300:
         return (f"one APG iteration = CUDA graph of {per_iter} kernels (k_chain_up, k_branch_grp per stage "
-                "group, k_chain_down, k_prox_nodes); timed per iteration")
+                "group, k_chain_down, k_prox_warp); timed per iteration")
     if mode == 310:
         return f"one APG iteration = CUDA graph of {per_iter} kernels (k_branch_grp per stage group, k_chain_fused)"
     if mode >= 200:
@@ -342,8 +374,9 @@ def run_ours(args):
     beta = S._beta_table(theta)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
 
-    def device_step():
+    def device_step(fp32: bool = False):
         """One solve with the instance resident in HBM; returns (step ms, loop ms)."""
+        ctx.call("wmpc_set_precision", 1 if fp32 else 0)
         ctx.call("wmpc_timer_start")
         ctx.call("wmpc_apg_begin", float(gamma), iters, nat.ptr(theta), nat.ptr(beta))
         loop = nat.C.c_float(0.0)
@@ -418,6 +451,29 @@ def run_ours(args):
                "api": "factor_step(structure_from) + solve() per step"}
         assert res.iterations == iters
 
+    # fp32 mode (SolverConfig.precision="fp32", own 1e-4 tolerance): reported beside, not the value
+    fp32 = None
+    if mode == 300 and not args.no_fp32:
+        for _ in range(2):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            device_step(fp32=True)
+        f_ms, f_loop = [], []
+        for _ in range(K):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            a, b = device_step(fp32=True)
+            f_ms.append(a)
+            f_loop.append(b)
+        ctx.call("wmpc_set_precision", 0)
+        fp32 = {"value": K * iters / (sum(f_ms) / 1e3), "unit": UNIT,
+                "us_per_iteration": sum(f_loop) / (K * iters) * 1e3, "tolerance": "1e-4 relative (tests/test_gpu_fp32.py)",
+                "what": "dual-gradient kernels in fp32; y, prox, averages, certificate in fp64"}
+    # the large tree (C4) for the HBM roofline (the headline tree is L2-resident)
+    large = None
+    if args.config != "C4" and not args.no_large:
+        large = roofline_large(peak, peak_src)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, iters, args.cpu_sample_iters)
@@ -433,7 +489,7 @@ def run_ours(args):
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": cfgd, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks.summary(),
-                "loop_ms_per_solve": loop_total / K}
+                "loop_ms_per_solve": loop_total / K, "fp32_mode": fp32, "roofline_C4": large}
         print(json.dumps(line), flush=True)
 
 
