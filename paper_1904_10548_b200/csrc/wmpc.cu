@@ -98,6 +98,7 @@ struct wmpc_ctx {
   size_t sm_up = 0, sm_grp = 0, sm_down = 0, sm_prox = 0;
   int up_threads = 512, down_threads = 512, prox_warp = 1, use_pu = 0;
   int fp32 = 0;                                 // SolverConfig.precision == "fp32"
+  int pdl = 1;                                  // programmatic dependent launch between graph kernels
   float *f32_Yc = nullptr, *f32_Lb = nullptr, *f32_Asub = nullptr, *f32_wbar = nullptr, *f32_U = nullptr,
         *f32_X = nullptr, *f32_eoff = nullptr, *f32_R = nullptr, *f32_g = nullptr, *f32_aux = nullptr,
         *f32_ell = nullptr;
@@ -306,6 +307,24 @@ size_t fast_smem_bytes(const wmpc_ctx* c, int MC, int nrow, int rec, int cpc, in
 // Decide whether the structured persistent kernel applies and lay out its data:
 // A = I, W = cI, n_u even, n_s <= 32, and every stage factor equal to the
 // null(E) projector (T_s = P/(2c), D_s = P up to 1e-12 relative).
+// Launch with programmatic stream serialization (PDL) when enabled: the kernel
+// may start while its predecessor drains; griddepcontrol.wait in the kernel
+// orders the dependent loads (captured into the graph as programmatic edges).
+template <typename... KArgs, typename... Args>
+void launch_pdl(wmpc_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx->pdl ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+
 template <int WE>
 void gk_pu(wmpc_ctx* ctx, const FastView& f) {
   k_chain_pu<WE><<<ctx->nchain, 256, ctx->sm_pu, ctx->stream>>>(f);
@@ -324,12 +343,13 @@ void gk_attrs(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
 }
 template <int WE, typename TG = double>
 void gk_up(wmpc_ctx* ctx, const FastView& f) {
-  k_chain_up<WE, TG><<<ctx->nchain, ctx->up_threads, ctx->sm_up, ctx->stream>>>(f);
+  launch_pdl(ctx, k_chain_up<WE, TG>, dim3(ctx->nchain), dim3(ctx->up_threads), ctx->sm_up, f);
 }
 template <int WE, typename TG = double>
 void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump) {
   for (const auto& g : ctx->gk_groups) {
-    k_branch_grp<WE, TG><<<g.second, SC_THREADS, ctx->sm_grp, ctx->stream>>>(f, g.first, bump, GRP_FULL);
+    launch_pdl(ctx, k_branch_grp<WE, TG>, dim3(g.second), dim3(SC_THREADS), ctx->sm_grp, f, g.first, bump,
+               (int)GRP_FULL);
     bump = 0;
   }
 }
@@ -341,21 +361,24 @@ void gk_rep(wmpc_ctx* ctx, const FastView& f, int mode, int bump) {
 }
 template <int WE, typename TG = double>
 void gk_down(wmpc_ctx* ctx, const FastView& f) {
-  k_chain_down<WE, TG><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);
+  launch_pdl(ctx, k_chain_down<WE, TG>, dim3(ctx->nchain), dim3(ctx->down_threads), ctx->sm_down, f);
 }
 template <typename TG>
 void gk_prox(wmpc_ctx* ctx, const FastView& f) {
   if (ctx->prox_warp)
-    k_prox_warp<TG><<<(ctx->n + PW_ROWS - 1) / PW_ROWS, 256, 0, ctx->stream>>>(f);
+    launch_pdl(ctx, k_prox_warp<TG>, dim3((ctx->n + PW_ROWS - 1) / PW_ROWS), dim3(256), 0, f);
   else
     k_prox_nodes<<<(ctx->n + SC_NPB - 1) / SC_NPB, SC_THREADS, ctx->sm_prox, ctx->stream>>>(f);
 }
 template <int WE, typename TG>
 void gk_iteration(wmpc_ctx* ctx, const FastView& f) {
-  gk_up<WE, TG>(ctx, f);
-  gk_grp<WE, TG>(ctx, f, 1);
-  gk_down<WE, TG>(ctx, f);
-  gk_prox<TG>(ctx, f);
+  // WMPC_SKIP (timing experiments only: results are wrong): letters u g d p drop kernels
+  const char* skip = getenv("WMPC_SKIP");
+  auto on = [&](char c) { return !skip || !std::strchr(skip, c); };
+  if (on('u')) gk_up<WE, TG>(ctx, f);
+  if (on('g')) gk_grp<WE, TG>(ctx, f, 1);
+  if (on('d')) gk_down<WE, TG>(ctx, f);
+  if (on('p')) gk_prox<TG>(ctx, f);
 }
 
 // Branching-region stage groups, bottom-up, with <= 32 items per row, and
@@ -598,6 +621,7 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   CK(cudaFuncSetAttribute(k_prox_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox));
   ctx->sm_up = up; ctx->sm_down = down; ctx->sm_grp = grp; ctx->sm_prox = prox;
   ctx->up_threads = ctx->down_threads = 512;  // measured: 512 beats 256 on C2 and C4
+  if (const char* e = getenv("WMPC_PDL")) ctx->pdl = e[0] != '0';
   if (const char* e = getenv("WMPC_UPT")) ctx->up_threads = atoi(e) >= 512 ? 512 : 256;
   if (const char* e = getenv("WMPC_DNT")) ctx->down_threads = atoi(e) >= 512 ? 512 : 256;
   ctx->prox_warp = nt <= 64 && nu <= 128 ? 1 : 0;

@@ -113,6 +113,14 @@ __device__ __forceinline__ void proj_rows(const DevView& d, const Ops& op, const
 
 __device__ __forceinline__ int chain_row(const FastView& f, int t, int ci) { return f.n_branch + t * f.nchain + ci; }
 
+// Programmatic dependent launch (the graph kernels are launched with
+// programmatic stream serialization): a kernel issues the loads that do not
+// depend on its predecessor (node data, operators, older iterates), then
+// waits for the predecessor grid, then lets its own successor launch.
+// Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Register-resident sparse operators (ELL, width WE): a thread owns one column
 // (or row) for a whole phase and loops over tree rows, so the operator entries
 // are loaded once (from L1) instead of walked through shared memory per row.
@@ -196,10 +204,12 @@ __global__ void __launch_bounds__(512) k_chain_up(FastView f) {
   TG* rec = reinterpret_cast<TG*>(smem_raw);
   TG* T = rec + (size_t)nst * ra;
   const GA<TG> G = ga<TG>(f);
-  FOR_RC(nst, 7, (ly >> 1), t, k) cpair(rec + (size_t)t * ra + 2 * k, G.Yc + (size_t)chain_row(f, t, ci) * ly + 2 * k);
   FOR_RC(nst - 1, 6, (nu >> 1), t, k)
     cpair(rec + (size_t)t * ra + ly + 2 * k, G.R + (size_t)chain_row(f, t, ci) * nu + 2 * k);
   if (threadIdx.x < nst) cpair(rec + (size_t)threadIdx.x * ra + ly + nu, G.aux + (size_t)chain_row(f, threadIdx.x, ci) * 2);
+  pdl_wait();  // Yc comes from the prox of the previous iteration
+  pdl_trigger();
+  FOR_RC(nst, 7, (ly >> 1), t, k) cpair(rec + (size_t)t * ra + 2 * k, G.Yc + (size_t)chain_row(f, t, ci) * ly + 2 * k);
   cp_commit();
   const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
   const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
@@ -274,6 +284,8 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly;
   const int r = r0 + blockIdx.x;
   constexpr int NW = SC_THREADS / 32;
+  pdl_wait();  // chain totals / lower groups of this iteration
+  pdl_trigger();
   if (bump && blockIdx.x == 0 && threadIdx.x == 0) *d.iter += 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   TG* part = reinterpret_cast<TG*>(smem_raw);  // NW x 256: [s1 64 | s2 64 | su 128]
@@ -401,9 +413,11 @@ __global__ void __launch_bounds__(512) k_chain_down(FastView f) {
     rows[m] = m < kb ? f.cpath[(size_t)ci * kb + m] : chain_row(f, m - kb, ci);
   }
   __syncthreads();
-  FOR_RC(nr, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * k, G.Lb + (size_t)rows[m] * nu + 2 * k);
   FOR_RC(nr, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + nu + 2 * k, G.e_off + (size_t)rows[m] * nu + 2 * k);
   FOR_RC(nr, 5, (lx >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * nu + 2 * k, G.g + (size_t)rows[m] * lx + 2 * k);
+  pdl_wait();  // L of the branching rows comes from the last group kernel
+  pdl_trigger();
+  FOR_RC(nr, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * k, G.Lb + (size_t)rows[m] * nu + 2 * k);
   cp_commit();
   const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
   const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
@@ -534,7 +548,7 @@ __device__ __forceinline__ ProxIt prox_it(const FastView& f) {
 // x: the node's state row (lx stride not needed: x[j]), returns bad.
 template <typename TG>
 __device__ __forceinline__ bool prox_x_warp(const FastView& f, const ProxIt& P, int r, const TG* x_row,
-                                            double* sd2, TG* yc_row) {
+                                            double* sd2, TG* yc_row, bool pdl = false) {
   const DevView& d = f.d;
   const int nt = d.nt, W = d.W, lx = d.lx, ly = d.ly, lane = threadIdx.x & 31;
   const size_t rw = (size_t)r * W;
@@ -547,12 +561,17 @@ __device__ __forceinline__ bool prox_x_warp(const FastView& f, const ProxIt& P, 
   for (int q = 0; q < 2; ++q) {
     const int j = lane + 32 * q;
     const bool ok = j < nt;
-    xv[q] = ok ? (double)x_row[j] : 0.0;
     xa[q] = ok && P.it > 0 ? d.Xa[(size_t)r * lx + j] : 0.0;
     y1[q] = ok ? y[j] : 0.0;
     y2[q] = ok ? y[nt + j] : 0.0;
     m1[q] = ok ? ym[j] : 0.0;
     m2[q] = ok ? ym[nt + j] : 0.0;
+  }
+  if (pdl) pdl_wait();  // x comes from the down pass (the predecessor)
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int j = lane + 32 * q;
+    xv[q] = j < nt ? (double)x_row[j] : 0.0;
   }
   double v1[2], v2[2], V1[2], V2[2], c1[2], c2[2];
 #pragma unroll
@@ -609,7 +628,7 @@ __device__ __forceinline__ bool prox_x_warp(const FastView& f, const ProxIt& P, 
 }
 template <typename TG>
 __device__ __forceinline__ bool prox_u_warp(const FastView& f, const ProxIt& P, int r, const TG* u_row,
-                                            TG* yc_row) {
+                                            TG* yc_row, bool pdl = false) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, W = d.W, lx = d.lx, ly = d.ly, lane = threadIdx.x & 31;
   const size_t rw = (size_t)r * W;
@@ -622,10 +641,15 @@ __device__ __forceinline__ bool prox_u_warp(const FastView& f, const ProxIt& P, 
   for (int q = 0; q < Q; ++q) {
     const int k = lane + 32 * q;
     const bool ok = k < nu;
-    uv[q] = ok ? (double)u_row[k] : 0.0;
     ua[q] = ok && P.it > 0 ? d.Ua[(size_t)r * nu + k] : 0.0;
     y3[q] = ok ? y[k] : 0.0;
     m3[q] = ok ? ym[k] : 0.0;
+  }
+  if (pdl) pdl_wait();  // u comes from the down pass (the predecessor)
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int k = lane + 32 * q;
+    uv[q] = k < nu ? (double)u_row[k] : 0.0;
   }
   bool bad = false;
 #pragma unroll
@@ -657,8 +681,9 @@ __global__ void __launch_bounds__(256) k_prox_warp(FastView f) {
   const ProxIt P = prox_it(f);
   const GA<TG> G = ga<TG>(f);
   TG* yc = G.Yc + (size_t)r * d.ly;
-  const bool bad = (warp & 1) == 0 ? prox_x_warp<TG>(f, P, r, G.X + (size_t)r * d.lx, sd2[m], yc)
-                                   : prox_u_warp<TG>(f, P, r, G.U + (size_t)r * d.nu, yc);
+  const bool bad = (warp & 1) == 0 ? prox_x_warp<TG>(f, P, r, G.X + (size_t)r * d.lx, sd2[m], yc, true)
+                                   : prox_u_warp<TG>(f, P, r, G.U + (size_t)r * d.nu, yc, true);
+  pdl_trigger();
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(d.bad_nu, P.it);
 }
 
