@@ -99,6 +99,7 @@ struct wmpc_ctx {
   int up_threads = 512, down_threads = 512, prox_warp = 1, use_pu = 0;
   int fp32 = 0;                                 // SolverConfig.precision == "fp32"
   int pdl = 1;                                  // programmatic dependent launch between graph kernels
+  int grp_items = 16;                           // max items per row in one branching stage group (measured)
   float *f32_Yc = nullptr, *f32_Lb = nullptr, *f32_Asub = nullptr, *f32_wbar = nullptr, *f32_U = nullptr,
         *f32_X = nullptr, *f32_eoff = nullptr, *f32_R = nullptr, *f32_g = nullptr, *f32_aux = nullptr,
         *f32_ell = nullptr;
@@ -427,7 +428,7 @@ void build_groups(wmpc_ctx* ctx, int k_rep, const int* acct) {
     while (s_lo > k_rep) {
       int mx = 0;
       for (int r = off[s_lo - 1]; r < off[s_lo]; ++r) mx = std::max(mx, items_of(r, s_hi, nullptr, nullptr));
-      if (mx > 32) break;
+      if (mx > ctx->grp_items) break;
       --s_lo;
     }
     groups.push_back({s_lo, s_hi});
@@ -571,6 +572,7 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   }
   ctx->h_cptr = cptr;
   ctx->h_cidx = cidx;
+  if (const char* e = getenv("WMPC_GRP_ITEMS")) ctx->grp_items = std::max(1, atoi(e));
   build_groups(ctx, 0, nullptr);
   // chain root paths and ancestor ownership (first chain below a row writes it)
   std::vector<int> cpath((size_t)std::max(nchain * kstar, 1), 0);

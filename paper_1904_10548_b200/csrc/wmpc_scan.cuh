@@ -284,9 +284,6 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly;
   const int r = r0 + blockIdx.x;
   constexpr int NW = SC_THREADS / 32;
-  pdl_wait();  // chain totals / lower groups of this iteration
-  pdl_trigger();
-  if (bump && blockIdx.x == 0 && threadIdx.x == 0) *d.iter += 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   TG* part = reinterpret_cast<TG*>(smem_raw);  // NW x 256: [s1 64 | s2 64 | su 128]
   TG* W1 = part + NW * 256;  // lx
@@ -296,32 +293,94 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
   TG* T = Sv + nu;           // FAST_MAXNS
   const GA<TG> G = ga<TG>(f);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  TG s1[2] = {0, 0}, s2[2] = {0, 0}, su[4] = {0, 0, 0, 0};
+  // ---- before the predecessor finishes: everything that does not come from it
+  // (item lists, operators, this row's own data, in-group rows' Yc and R: the
+  // previous iteration's prox finished before the predecessor started)
+  const int k = threadIdx.x;
+  const Ell<EllW<WE>::BC, TG> bc = ell_load<EllW<WE>::BC, TG>(f, own_bc(d, k < nu ? k : 0));
+  const Ell<EllW<WE>::KR, TG> kr = ell_load<EllW<WE>::KR, TG>(f, own_kr(d, k < d.ns ? k : 0));
+  const Ell<EllW<WE>::EC, TG> ec = ell_load<EllW<WE>::EC, TG>(f, own_ec(d, k < nu ? k : 0));
+  const TG own_yx = k < nt ? G.Yc[(size_t)r * ly + k] : TG(0);
+  const TG own_yu = k < nu ? G.Yc[(size_t)r * ly + lx + k] : TG(0);
+  const TG own_R = k < nu ? G.R[(size_t)r * nu + k] : TG(0);
+  const TG own_aux = G.aux[(size_t)r * 2];
   const int e0 = mode == GRP_FINISH ? 0 : f.gi_ptr[r], e1 = mode == GRP_FINISH ? 0 : f.gi_ptr[r + 1];
-  for (int e = e0 + warp; e < e1; e += NW) {
+  constexpr int MQ = 2;  // items per warp prefetched ahead of the wait
+  int itm[MQ];
+  TG wq[MQ], vx[MQ][2], vu[MQ][4];
+#pragma unroll
+  for (int q = 0; q < MQ; ++q) {
+    const int e = e0 + warp + NW * q;
+    itm[q] = e < e1 ? f.gi_item[e] : -1;
+    wq[q] = e < e1 ? (TG)f.gi_w[e] : TG(0);
+    const bool in_group = itm[q] >= 0 && !(itm[q] & 1);
+    const size_t row = in_group ? (size_t)(itm[q] >> 1) : 0;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int c = lane + 32 * i;
+      vx[q][i] = in_group && c < nt ? G.Yc[row * ly + c] : TG(0);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = lane + 32 * i;
+      vu[q][i] = in_group && c < nu ? G.Yc[row * ly + lx + c] + G.R[row * nu + c] : TG(0);
+    }
+  }
+  pdl_wait();  // chain totals / lower groups of this iteration
+  pdl_trigger();
+  if (bump && blockIdx.x == 0 && threadIdx.x == 0) *d.iter += 1;
+  TG s1[2] = {0, 0}, s2[2] = {0, 0}, su[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int q = 0; q < MQ; ++q) {
+    if (itm[q] >= 0 && (itm[q] & 1)) {  // frontier rows: totals of the predecessor
+      const size_t row = (size_t)(itm[q] >> 1);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int c = lane + 32 * i;
+        vx[q][i] = c < nt ? G.wbar[row * lx + c] : TG(0);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = lane + 32 * i;
+        vu[q][i] = c < nu ? G.Asub[row * nu + c] : TG(0);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MQ; ++q) {
+    if (itm[q] < 0) break;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      s1[i] += vx[q][i];
+      s2[i] = fma(wq[q], vx[q][i], s2[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) su[i] += vu[q][i];
+  }
+  for (int e = e0 + warp + NW * MQ; e < e1; e += NW) {  // rows with more than MQ items per warp
     const int item = f.gi_item[e];
     const size_t row = (size_t)(item >> 1);
     const bool fr = item & 1;
     const TG w = (TG)f.gi_w[e];
     const TG* px = fr ? G.wbar + row * lx : G.Yc + row * ly;
-    TG vx[2], vu[4];
+    TG x2[2], u4[4];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int c = lane + 32 * i;
-      vx[i] = c < nt ? px[c] : TG(0);
+      x2[i] = c < nt ? px[c] : TG(0);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int c = lane + 32 * i;
-      vu[i] = c < nu ? (fr ? G.Asub[row * nu + c] : G.Yc[row * ly + lx + c] + G.R[row * nu + c]) : TG(0);
+      u4[i] = c < nu ? (fr ? G.Asub[row * nu + c] : G.Yc[row * ly + lx + c] + G.R[row * nu + c]) : TG(0);
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      s1[i] += vx[i];
-      s2[i] = fma(w, vx[i], s2[i]);
+      s1[i] += x2[i];
+      s2[i] = fma(w, x2[i], s2[i]);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) su[i] += vu[i];
+    for (int i = 0; i < 4; ++i) su[i] += u4[i];
   }
   TG* pw = part + warp * 256;
 #pragma unroll
@@ -341,26 +400,24 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
     }
     return;
   }
-  if (threadIdx.x < nt) {
-    const int j = threadIdx.x;
+  if (k < nt) {
     TG a1, a2;
     if (xb) {
-      a1 = xb[j];
-      a2 = xb[64 + j];
+      a1 = xb[k];
+      a2 = xb[64 + k];
     } else {
-      a1 = part[j];
-      a2 = part[64 + j];
+      a1 = part[k];
+      a2 = part[64 + k];
       for (int w = 1; w < NW; ++w) {
-        a1 += part[w * 256 + j];
-        a2 += part[w * 256 + 64 + j];
+        a1 += part[w * 256 + k];
+        a2 += part[w * 256 + 64 + k];
       }
     }
-    W1[j] = G.Yc[(size_t)r * ly + j] + a1;
-    W2[j] = a2;
+    W1[k] = own_yx + a1;
+    W2[k] = a2;
   }
   __syncthreads();
-  if (threadIdx.x < nu) {
-    const int k = threadIdx.x;
+  if (k < nu) {
     TG s;
     if (xb) {
       s = xb[128 + k];
@@ -368,26 +425,15 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
       s = part[128 + k];
       for (int w = 1; w < NW; ++w) s += part[w * 256 + 128 + k];
     }
-    TG b1 = 0, b2 = 0;
-    const Ell<EllW<WE>::BC, TG> bc = ell_load<EllW<WE>::BC, TG>(f, own_bc(d, k));
-    b1 = ell_dot(bc, W1);
-    b2 = ell_dot(bc, W2);
-    av[k] = (G.Yc[(size_t)r * ly + lx + k] + b1) + G.R[(size_t)r * nu + k];
-    Sv[k] = s + b2;
+    av[k] = (own_yu + ell_dot(bc, W1)) + own_R;
+    Sv[k] = s + ell_dot(bc, W2);
   }
-  if (threadIdx.x < nt) G.wbar[(size_t)r * lx + threadIdx.x] = W1[threadIdx.x];
+  if (k < nt) G.wbar[(size_t)r * lx + k] = W1[k];
   __syncthreads();
-  if (threadIdx.x < nu) G.Asub[(size_t)r * nu + threadIdx.x] = av[threadIdx.x] + Sv[threadIdx.x];
-  if (threadIdx.x < d.ns) {
-    const Ell<EllW<WE>::KR, TG> kr = ell_load<EllW<WE>::KR, TG>(f, own_kr(d, threadIdx.x));
-    T[threadIdx.x] = ell_dot(kr, Sv);
-  }
+  if (k < nu) G.Asub[(size_t)r * nu + k] = av[k] + Sv[k];
+  if (k < d.ns) T[k] = ell_dot(kr, Sv);
   __syncthreads();
-  if (threadIdx.x < nu) {
-    const int k = threadIdx.x;
-    const Ell<EllW<WE>::EC, TG> ec = ell_load<EllW<WE>::EC, TG>(f, own_ec(d, k));
-    G.Lb[(size_t)r * nu + k] = (av[k] + (Sv[k] - ell_dot(ec, T))) * G.aux[(size_t)r * 2];
-  }
+  if (k < nu) G.Lb[(size_t)r * nu + k] = (av[k] + (Sv[k] - ell_dot(ec, T))) * own_aux;
 }
 
 // ---------------------------------------------------------------- k_chain_down
