@@ -99,6 +99,7 @@ struct wmpc_ctx {
   int up_threads = 512, down_threads = 512, prox_warp = 1, use_pu = 0;
   int fp32 = 0;                                 // SolverConfig.precision == "fp32"
   int pdl = 1;                                  // programmatic dependent launch between graph kernels
+  int chain_occ = 0;                            // chain kernels: register cap for occupancy (many chains)
   int grp_items = 16;                           // max items per row in one branching stage group (measured)
   float *f32_Yc = nullptr, *f32_Lb = nullptr, *f32_Asub = nullptr, *f32_wbar = nullptr, *f32_U = nullptr,
         *f32_X = nullptr, *f32_eoff = nullptr, *f32_R = nullptr, *f32_g = nullptr, *f32_aux = nullptr,
@@ -332,8 +333,10 @@ void gk_pu(wmpc_ctx* ctx, const FastView& f) {
 }
 template <int WE, typename TG>
 void gk_attrs_t(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
-  CK(cudaFuncSetAttribute(k_chain_up<WE, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
-  CK(cudaFuncSetAttribute(k_chain_down<WE, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
+  CK(cudaFuncSetAttribute(k_chain_up<WE, TG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
+  CK(cudaFuncSetAttribute(k_chain_down<WE, TG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
+  CK(cudaFuncSetAttribute(k_chain_up<WE, TG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
+  CK(cudaFuncSetAttribute(k_chain_down<WE, TG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
   CK(cudaFuncSetAttribute(k_branch_grp<WE, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grp));
 }
 template <int WE>
@@ -344,7 +347,10 @@ void gk_attrs(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
 }
 template <int WE, typename TG = double>
 void gk_up(wmpc_ctx* ctx, const FastView& f) {
-  launch_pdl(ctx, k_chain_up<WE, TG>, dim3(ctx->nchain), dim3(ctx->up_threads), ctx->sm_up, f);
+  if (ctx->chain_occ)
+    launch_pdl(ctx, k_chain_up<WE, TG, true>, dim3(ctx->nchain), dim3(ctx->up_threads), ctx->sm_up, f);
+  else
+    launch_pdl(ctx, k_chain_up<WE, TG, false>, dim3(ctx->nchain), dim3(ctx->up_threads), ctx->sm_up, f);
 }
 template <int WE, typename TG = double>
 void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump) {
@@ -362,7 +368,10 @@ void gk_rep(wmpc_ctx* ctx, const FastView& f, int mode, int bump) {
 }
 template <int WE, typename TG = double>
 void gk_down(wmpc_ctx* ctx, const FastView& f) {
-  launch_pdl(ctx, k_chain_down<WE, TG>, dim3(ctx->nchain), dim3(ctx->down_threads), ctx->sm_down, f);
+  if (ctx->chain_occ)
+    launch_pdl(ctx, k_chain_down<WE, TG, true>, dim3(ctx->nchain), dim3(ctx->down_threads), ctx->sm_down, f);
+  else
+    launch_pdl(ctx, k_chain_down<WE, TG, false>, dim3(ctx->nchain), dim3(ctx->down_threads), ctx->sm_down, f);
 }
 template <typename TG>
 void gk_prox(wmpc_ctx* ctx, const FastView& f) {
@@ -623,6 +632,7 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   CK(cudaFuncSetAttribute(k_prox_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox));
   ctx->sm_up = up; ctx->sm_down = down; ctx->sm_grp = grp; ctx->sm_prox = prox;
   ctx->up_threads = ctx->down_threads = 512;  // measured: 512 beats 256 on C2 and C4
+  ctx->chain_occ = ctx->nchain > 4 * ctx->sms ? 1 : 0;  // measured: C4 (4096 chains) +4 %; C2, C3 (<= 512) better without
   if (const char* e = getenv("WMPC_PDL")) ctx->pdl = e[0] != '0';
   if (const char* e = getenv("WMPC_UPT")) ctx->up_threads = atoi(e) >= 512 ? 512 : 256;
   if (const char* e = getenv("WMPC_DNT")) ctx->down_threads = atoi(e) >= 512 ? 512 : 256;
@@ -972,7 +982,10 @@ void dual_eval_graph(wmpc_ctx* ctx, const double* y, int phase) {
   }
   if (phase != 0) {
     if (ctx->rep_group.second > 0) gk_rep<WE>(ctx, f, GRP_FINISH, 0);
-    k_chain_down<WE, double><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);
+    if (ctx->chain_occ)
+      k_chain_down<WE, double, true><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);
+    else
+      k_chain_down<WE, double, false><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);
     CK(cudaMemcpyAsync(ctx->Yc, ctx->Yc_save, sizeof(double) * (size_t)ctx->n * ctx->ly, cudaMemcpyDeviceToDevice,
                        ctx->stream));
     ctx->launches += 1 + (ctx->rep_group.second > 0);
@@ -1016,6 +1029,7 @@ FastView make_fastview(wmpc_ctx* ctx, int count) {
   f.ell_idx = ctx->ell_idx;
   f.ell_val = ctx->ell_val;
   f.ell_w = ctx->ell_w;
+  f.lb_prewait = ctx->gk_groups.empty() ? 0 : 1;
   f.g32 = G32{ctx->f32_Yc, ctx->f32_Lb, ctx->f32_Asub, ctx->f32_wbar, ctx->f32_U, ctx->f32_X,
               ctx->f32_eoff, ctx->f32_R, ctx->f32_g, ctx->f32_aux, ctx->f32_ell};
   f.xbuf = ctx->xbuf;

@@ -194,8 +194,10 @@ __device__ __forceinline__ int own_kr(const DevView& d, int i) { return 2 * d.nu
 // ---------------------------------------------------------------- k_chain_up
 // Shared: rec nst x (ly + nu + 2) [Yx->wbar | Yu->a | R->S->PS | aux],
 // T nst x FAST_MAXNS (in-place phases keep 4 CTAs per SM at H = 24).
-template <int WE, typename TG>
-__global__ void __launch_bounds__(512) k_chain_up(FastView f) {
+// OCC: many chains (several waves) -> cap registers for 3 CTAs per SM; few
+// chains (one wave, latency-bound) -> let the compiler keep more in registers.
+template <int WE, typename TG, bool OCC>
+__global__ void __launch_bounds__(512, OCC ? 3 : 1) k_chain_up(FastView f) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly, ns = d.ns;
   const int nst = d.H - f.kstar, ci = blockIdx.x;
@@ -207,13 +209,15 @@ __global__ void __launch_bounds__(512) k_chain_up(FastView f) {
   FOR_RC(nst - 1, 6, (nu >> 1), t, k)
     cpair(rec + (size_t)t * ra + ly + 2 * k, G.R + (size_t)chain_row(f, t, ci) * nu + 2 * k);
   if (threadIdx.x < nst) cpair(rec + (size_t)threadIdx.x * ra + ly + nu, G.aux + (size_t)chain_row(f, threadIdx.x, ci) * 2);
+  const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
+  const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
+  const Ell<EllW<WE>::BC, TG> bc = ell_load<EllW<WE>::BC, TG>(f, own_bc(d, k < nu ? k : 0));
+  const Ell<EllW<WE>::KR, TG> kr = ell_load<EllW<WE>::KR, TG>(f, own_kr(d, i < ns ? i : 0));
+  const Ell<EllW<WE>::EC, TG> ec = ell_load<EllW<WE>::EC, TG>(f, own_ec(d, k < nu ? k : 0));
   pdl_wait();  // Yc comes from the prox of the previous iteration
   pdl_trigger();
   FOR_RC(nst, 7, (ly >> 1), t, k) cpair(rec + (size_t)t * ra + 2 * k, G.Yc + (size_t)chain_row(f, t, ci) * ly + 2 * k);
   cp_commit();
-  const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
-  const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
-  const Ell<EllW<WE>::BC, TG> bc = ell_load<EllW<WE>::BC, TG>(f, own_bc(d, k < nu ? k : 0));
   cp_wait<0>();
   __syncthreads();
   if (threadIdx.x < nt) {  // wbar suffix scan in place: wbar_t = Yx_t + wbar_{t+1}
@@ -247,12 +251,10 @@ __global__ void __launch_bounds__(512) k_chain_up(FastView f) {
   }
   __syncthreads();
   if (i < ns) {  // T = K S
-    const Ell<EllW<WE>::KR, TG> kr = ell_load<EllW<WE>::KR, TG>(f, own_kr(d, i));
     for (int t = ti; t < nst - 1; t += si) T[t * FAST_MAXNS + i] = ell_dot(kr, rec + (size_t)t * ra + ly);
   }
   __syncthreads();
   if (k < nu) {  // L = (a + (S - E^T T)) / (2c p)
-    const Ell<EllW<WE>::EC, TG> ec = ell_load<EllW<WE>::EC, TG>(f, own_ec(d, k));
     for (int t = tk; t < nst; t += sk) {
       const TG* R = rec + (size_t)t * ra;
       const TG a = R[lx + k];
@@ -443,8 +445,8 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
 //   x_m = (x_{m-1} + u_m B^T) + g_m,  x_{-1} = p.
 // Ancestor rows are written by the chain that owns them (cown).
 // Shared: rec H x (2nu + lx) [L->z->u | e_off->Bu | g], T H x FAST_MAXNS, rows H.
-template <int WE, typename TG>
-__global__ void __launch_bounds__(512) k_chain_down(FastView f) {
+template <int WE, typename TG, bool OCC>
+__global__ void __launch_bounds__(512, OCC ? 3 : 1) k_chain_down(FastView f) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ns = d.ns;
   const int kb = f.kstar, nr = d.H, ci = blockIdx.x;
@@ -461,13 +463,21 @@ __global__ void __launch_bounds__(512) k_chain_down(FastView f) {
   __syncthreads();
   FOR_RC(nr, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + nu + 2 * k, G.e_off + (size_t)rows[m] * nu + 2 * k);
   FOR_RC(nr, 5, (lx >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * nu + 2 * k, G.g + (size_t)rows[m] * lx + 2 * k);
-  pdl_wait();  // L of the branching rows comes from the last group kernel
-  pdl_trigger();
-  FOR_RC(nr, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * k, G.Lb + (size_t)rows[m] * nu + 2 * k);
-  cp_commit();
+  // the chain rows' L were written by k_chain_up, which finished before the
+  // group kernels (our predecessor) started: fetch them before the wait
+  const int m_pre = f.lb_prewait ? kb : nr;
+  FOR_RC(nr - m_pre, 6, (nu >> 1), m, k)
+    cpair(rec + (size_t)(m_pre + m) * rd + 2 * k, G.Lb + (size_t)rows[m_pre + m] * nu + 2 * k);
   const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
   const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
   const int j = threadIdx.x & 63, tj = threadIdx.x >> 6, sj = blockDim.x >> 6;
+  const Ell<EllW<WE>::KR, TG> kr = ell_load<EllW<WE>::KR, TG>(f, own_kr(d, i < ns ? i : 0));
+  const Ell<EllW<WE>::EC, TG> ec = ell_load<EllW<WE>::EC, TG>(f, own_ec(d, k < nu ? k : 0));
+  const Ell<EllW<WE>::BR, TG> br = ell_load<EllW<WE>::BR, TG>(f, own_br(d, j < nt ? j : 0));
+  pdl_wait();  // L of the branching rows comes from the last group kernel
+  pdl_trigger();
+  FOR_RC(m_pre, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * k, G.Lb + (size_t)rows[m] * nu + 2 * k);
+  cp_commit();
   const unsigned own = kb > 0 ? f.cown[ci] : 0u;
   const TG qk = k < nu ? (TG)d.q[k] : TG(0);
   cp_wait<0>();
@@ -483,12 +493,10 @@ __global__ void __launch_bounds__(512) k_chain_down(FastView f) {
   }
   __syncthreads();
   if (i < ns) {  // T = K z
-    const Ell<EllW<WE>::KR, TG> kr = ell_load<EllW<WE>::KR, TG>(f, own_kr(d, i));
     for (int m = ti; m < nr; m += si) T[m * FAST_MAXNS + i] = ell_dot(kr, rec + (size_t)m * rd);
   }
   __syncthreads();
   if (k < nu) {  // u = e_off + (z - E^T T), in the z slot
-    const Ell<EllW<WE>::EC, TG> ec = ell_load<EllW<WE>::EC, TG>(f, own_ec(d, k));
     for (int m = tk; m < nr; m += sk) {
       TG* R = rec + (size_t)m * rd;
       const TG u = R[nu + k] + (R[k] - ell_dot(ec, T + m * FAST_MAXNS));
@@ -498,7 +506,6 @@ __global__ void __launch_bounds__(512) k_chain_down(FastView f) {
   }
   __syncthreads();
   if (j < nt) {  // u B^T into the dead e_off slot
-    const Ell<EllW<WE>::BR, TG> br = ell_load<EllW<WE>::BR, TG>(f, own_br(d, j));
     for (int m = tj; m < nr; m += sj) {
       TG* R = rec + (size_t)m * rd;
       R[nu + j] = ell_dot(br, R);
