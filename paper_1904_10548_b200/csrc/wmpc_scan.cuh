@@ -160,15 +160,42 @@ struct Ell {
 // Entries past an owner's count are stored as (0, 0.0): no predication, and a
 // zero weight times a finite operand adds nothing (a dense product would
 // propagate a non-finite operand the same way).
+// Owners are stored with stride ell_w (4 or 8, >= WE): one owner's entries
+// are read with 16-byte vector loads (idx as int4, values as double2/float4).
 template <int WE, typename TG = double>
 __device__ __forceinline__ Ell<WE, TG> ell_load(const FastView& f, int owner) {
   Ell<WE, TG> o;
   const int* ip = f.ell_idx + (size_t)owner * f.ell_w;
   const TG* vp = ga<TG>(f).ell_val + (size_t)owner * f.ell_w;
+  constexpr int NI = (WE + 3) / 4;
+  int ib[4 * NI];
 #pragma unroll
-  for (int e = 0; e < WE; ++e) {
-    o.idx[e] = ip[e];
-    o.val[e] = vp[e];
+  for (int q = 0; q < NI; ++q) {
+    const int4 v = reinterpret_cast<const int4*>(ip)[q];
+    ib[4 * q] = v.x; ib[4 * q + 1] = v.y; ib[4 * q + 2] = v.z; ib[4 * q + 3] = v.w;
+  }
+#pragma unroll
+  for (int e = 0; e < WE; ++e) o.idx[e] = ib[e];
+  if constexpr (sizeof(TG) == 8) {
+    constexpr int NV = (WE + 1) / 2;
+    double vb[2 * NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const double2 v = reinterpret_cast<const double2*>(vp)[q];
+      vb[2 * q] = v.x; vb[2 * q + 1] = v.y;
+    }
+#pragma unroll
+    for (int e = 0; e < WE; ++e) o.val[e] = (TG)vb[e];
+  } else {
+    constexpr int NV = (WE + 3) / 4;
+    float vb[4 * NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const float4 v = reinterpret_cast<const float4*>(vp)[q];
+      vb[4 * q] = v.x; vb[4 * q + 1] = v.y; vb[4 * q + 2] = v.z; vb[4 * q + 3] = v.w;
+    }
+#pragma unroll
+    for (int e = 0; e < WE; ++e) o.val[e] = (TG)vb[e];
   }
   return o;
 }
