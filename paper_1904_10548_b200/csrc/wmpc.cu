@@ -77,6 +77,7 @@ struct wmpc_ctx {
   double *pj_kv = nullptr, *pj_ecv = nullptr;
   unsigned long long* dk_mv = nullptr;
   int* dk_sweeps = nullptr;
+  int* dk_fix = nullptr;                       // certificate Dykstra: per-node settled sweep (pass 1)
   int use_graphk = 0, n_branch = 0, use_fused = 0, fused_pb = 1, fused_ring_off = 0, fused_threads = 1024;
   size_t sm_fused = 0;
   int* store_it = nullptr;
@@ -341,6 +342,8 @@ void gk_attrs_t(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
 }
 template <int WE>
 void gk_attrs(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
+  CK(cudaFuncSetAttribute(k_chain_rollout<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(sizeof(double) * (size_t)ctx->H * (ctx->nu + ctx->lx) + sizeof(int) * 32)));
   if (ctx->sm_pu) CK(cudaFuncSetAttribute(k_chain_pu<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->sm_pu));
   gk_attrs_t<WE, double>(ctx, up, down, grp);
   gk_attrs_t<WE, float>(ctx, up, down, grp);
@@ -993,6 +996,26 @@ void dual_eval_graph(wmpc_ctx* ctx, const double* y, int phase) {
   check_launch(ctx);
 }
 
+// x from u along every root path: one chain-parallel launch in graph mode
+// (H <= 32), else one launch per stage.
+void rollout(wmpc_ctx* ctx, const DevView& d, const double* U, double* X) {
+  if (ctx->fast && ctx->use_graphk && ctx->H <= 32) {
+    FastView f = make_fastview(ctx, 1);
+    const size_t smem = sizeof(double) * (size_t)ctx->H * (ctx->nu + ctx->lx) + sizeof(int) * 32;
+    ctx->launches++;
+    if (ctx->ell_w == 4)
+      k_chain_rollout<4><<<ctx->nchain, 256, smem, ctx->stream>>>(f, U, X);
+    else
+      k_chain_rollout<8><<<ctx->nchain, 256, smem, ctx->stream>>>(f, U, X);
+    return;
+  }
+  for (int s = 0; s < ctx->H; ++s) {
+    int cnt = ctx->off[s + 1] - ctx->off[s];
+    ctx->launches++;
+    k_rollout_stage<<<grid_for((size_t)cnt * ctx->nt), 256, 0, ctx->stream>>>(d, ctx->off[s], cnt, U, X);
+  }
+}
+
 FastView make_fastview(wmpc_ctx* ctx, int count) {
   FastView f;
   f.d = view(ctx);
@@ -1105,7 +1128,7 @@ void free_all(wmpc_ctx* c) {
                   c->e_ptr, c->e_col, c->e_val, c->aux,
                   c->Lb, c->Asub, c->blob, c->store_it, c->f32_Yc, c->f32_Lb, c->f32_Asub, c->f32_wbar, c->f32_U,
                   c->f32_X, c->f32_eoff, c->f32_R, c->f32_g, c->f32_aux, c->f32_ell, c->Yc_save, c->acct, c->rep_gidx, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
-                  c->pj_ecv, c->dk_mv, c->dk_sweeps, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
+                  c->pj_ecv, c->dk_mv, c->dk_sweeps, c->dk_fix, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
                   c->prof};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1360,6 +1383,7 @@ int wmpc_set_structure(wmpc_ctx* ctx, const double* A, const double* B, const do
       upload_vec(ctx, &ctx->pj_ecv, ecv);
       if (!ctx->dk_mv) dalloc(ctx, &ctx->dk_mv, 512);
       if (!ctx->dk_sweeps) dalloc(ctx, &ctx->dk_sweeps, 1);
+      if (!ctx->dk_fix) dalloc(ctx, &ctx->dk_fix, (size_t)n);
     }
     sync(ctx);
     configure_fast(ctx, B, E, e_pinv, T, D, cptr, cidx);
@@ -1833,17 +1857,14 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
       CK(cudaMemsetAsync(ctx->dk_mv, 0, sizeof(unsigned long long) * 512, ctx->stream));
       const int nbw = (ctx->n + 7) / 8;
       ctx->launches += 3;
-      k_dyk_warp<<<nbw, 256, 0, ctx->stream>>>(d, po, ctx->Ua, nullptr, ctx->dk_mv, ctx->dk_sweeps, 500, 1);
+      k_dyk_warp<<<nbw, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 1,
+                                                ctx->dk_fix);
       k_dyk_count<<<1, 32, 0, ctx->stream>>>(ctx->dk_mv, 500, ctx->scal + 8, ctx->dk_sweeps);
-      k_dyk_warp<<<nbw, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 2);
+      k_dyk_warp<<<nbw, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 2,
+                                                ctx->dk_fix);
     }
     // 2. rollout (problem.py:207-218)
-    for (int s = 0; s < ctx->H; ++s) {
-      int cnt = ctx->off[s + 1] - ctx->off[s];
-      ctx->launches++;
-      k_rollout_stage<<<grid_for((size_t)cnt * ctx->nt), 256, 0, ctx->stream>>>(d, ctx->off[s], cnt, ctx->Uf,
-                                                                                 ctx->Xf);
-    }
+    rollout(ctx, d, ctx->Uf, ctx->Xf);
     check_launch(ctx);
     // 3. primal value (solver.py:453)
     double tp[4];
@@ -2217,7 +2238,7 @@ int wmpc_cert_dykstra(wmpc_ctx* ctx, int max_sweeps, double* mv) {
       CK(cudaMemsetAsync(ctx->dk_mv, 0, sizeof(unsigned long long) * 512, ctx->stream));
       ctx->launches++;
       k_dyk_warp<<<(ctx->n + 7) / 8, 256, 0, ctx->stream>>>(d, po, ctx->Ua, nullptr, ctx->dk_mv, ctx->dk_sweeps,
-                                                            max_sweeps, 1);
+                                                            max_sweeps, 1, nullptr);
       check_launch(ctx);
       d2h(ctx, bits.data(), ctx->dk_mv, sizeof(unsigned long long) * max_sweeps);
       sync(ctx);
@@ -2258,13 +2279,9 @@ int wmpc_cert_terms(wmpc_ctx* ctx, int sweeps, double* terms) {
       DykOps po{ctx->pj_kp, ctx->pj_kc, ctx->pj_ecp, ctx->pj_ecr, ctx->pj_kv, ctx->pj_ecv};
       ctx->launches++;
       k_dyk_warp<<<(ctx->n + 7) / 8, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, sweeps,
-                                                            2);
+                                                            2, nullptr);
     }
-    for (int s = 0; s < ctx->H; ++s) {
-      int cnt = ctx->off[s + 1] - ctx->off[s];
-      ctx->launches++;
-      k_rollout_stage<<<grid_for((size_t)cnt * ctx->nt), 256, 0, ctx->stream>>>(d, ctx->off[s], cnt, ctx->Uf, ctx->Xf);
-    }
+    rollout(ctx, d, ctx->Uf, ctx->Xf);
     check_launch(ctx);
     double tp[4], td[4], g[2];
     cost_terms(ctx, d, ctx->Uf, ctx->Xf, nullptr, 1, tp);

@@ -696,9 +696,13 @@ struct DykOps {
   const double *kv, *ecv;
 };
 constexpr int DYK_MAXQ = 4;  // nu <= 128
+// fix (optional): pass 1 stores its final state in u_out and, per node, the
+// sweep count after which that state no longer changes (max_sweeps when it
+// never settled); pass 2 then only recomputes the nodes whose pass-1 state is
+// not already the state after the global sweep count.
 __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const double* __restrict__ u_in,
                                                   double* __restrict__ u_out, unsigned long long* mv,
-                                                  const int* sweeps_in, int max_sweeps, int pass) {
+                                                  const int* sweeps_in, int max_sweeps, int pass, int* fix) {
   __shared__ double sA[8][128];
   __shared__ double sT[8][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -706,6 +710,8 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
   if (r >= d.n) return;
   const int nu = d.nu, ns = d.ns;
   const int nsw = pass == 1 ? max_sweeps : *sweeps_in;
+  if (pass == 2 && fix && nsw >= fix[r]) return;  // pass 1 already left the answer in u_out
+  int settled = nsw;
   double cur[DYK_MAXQ], pc[DYK_MAXQ], qc[DYK_MAXQ], c[DYK_MAXQ], lo[DYK_MAXQ], hi[DYK_MAXQ];
   const double* sh = d.np->shift + (size_t)r * ns;
 #pragma unroll
@@ -757,10 +763,14 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
     }
     for (int o = 16; o > 0; o >>= 1) moved = np_max(moved, __shfl_xor_sync(0xffffffffu, moved, o));
     if (pass == 1 && lane == 0 && moved > 0.0) atomicMax(mv + s, (unsigned long long)__double_as_longlong(moved));
-    if (__all_sync(0xffffffffu, same)) break;  // exact fixed point: every later sweep repeats it
+    if (__all_sync(0xffffffffu, same)) {  // exact fixed point: every later sweep repeats it
+      settled = s;
+      break;
+    }
     __syncwarp();
   }
-  if (pass == 2) {
+  if (pass == 1 && fix && lane == 0) fix[r] = settled;
+  if (pass == 2 || (fix && u_out)) {
 #pragma unroll
     for (int q = 0; q < DYK_MAXQ; ++q) {
       const int k = lane + 32 * q;

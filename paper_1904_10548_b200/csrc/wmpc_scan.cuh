@@ -549,6 +549,53 @@ __global__ void __launch_bounds__(512, OCC ? 3 : 1) k_chain_down(FastView f) {
   }
 }
 
+// ---------------------------------------------------------------- k_chain_rollout
+// Certificate rollout (problem.py:207-218) x = (x_anc + u B^T) + g over every
+// root path in one launch (one CTA per chain, ancestors included), instead of
+// one launch per stage. Shared: rec H x (nu + lx) [u -> Bu | g].
+template <int WE>
+__global__ void __launch_bounds__(256) k_chain_rollout(FastView f, const double* __restrict__ Uin, double* Xout) {
+  const DevView& d = f.d;
+  const int nt = d.nt, nu = d.nu, lx = d.lx;
+  const int kb = f.kstar, nr = d.H, ci = blockIdx.x;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int rd = nu + lx;
+  double* rec = reinterpret_cast<double*>(smem_raw);
+  int* rows = reinterpret_cast<int*>(rec + (size_t)nr * rd);
+  const NodePtrs np = *d.np;
+  if (threadIdx.x < nr) {
+    const int m = threadIdx.x;
+    rows[m] = m < kb ? f.cpath[(size_t)ci * kb + m] : chain_row(f, m - kb, ci);
+  }
+  __syncthreads();
+  FOR_RC(nr, 6, (nu >> 1), m, k) cp16(rec + (size_t)m * rd + 2 * k, Uin + (size_t)rows[m] * nu + 2 * k);
+  FOR_RC(nr, 5, (lx >> 1), m, k) cp16(rec + (size_t)m * rd + nu + 2 * k, np.g + (size_t)rows[m] * lx + 2 * k);
+  cp_commit();
+  const int j = threadIdx.x & 63, tj = threadIdx.x >> 6, sj = blockDim.x >> 6;
+  const Ell<EllW<WE>::BR, double> br = ell_load<EllW<WE>::BR, double>(f, own_br(d, j < nt ? j : 0));
+  const unsigned own = kb > 0 ? f.cown[ci] : 0u;
+  cp_wait<0>();
+  __syncthreads();
+  double bu[8];  // u B^T of this thread's rows (column j), before the u slots are reused
+  int nb = 0;
+  if (j < nt)
+    for (int m = tj; m < nr && nb < 8; m += sj) bu[nb++] = ell_dot(br, rec + (size_t)m * rd);
+  __syncthreads();
+  if (j < nt) {
+    nb = 0;
+    for (int m = tj; m < nr && nb < 8; m += sj) rec[(size_t)m * rd + j] = bu[nb++];
+  }
+  __syncthreads();
+  if (threadIdx.x < nt) {
+    double x = d.p[threadIdx.x];
+    for (int m = 0; m < nr; ++m) {
+      const double* R = rec + (size_t)m * rd;
+      x = (x + R[threadIdx.x]) + R[nu + threadIdx.x];
+      if (m >= kb || ((own >> m) & 1u)) Xout[(size_t)rows[m] * lx + threadIdx.x] = x;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- k_prox_nodes
 // Node-parallel Moreau prox (bit-exact), ergodic averages, next collapsed dual.
 __global__ void __launch_bounds__(SC_THREADS) k_prox_nodes(FastView f) {
