@@ -101,6 +101,9 @@ struct wmpc_ctx {
   int fp32 = 0;                                 // SolverConfig.precision == "fp32"
   int pdl = 1;                                  // programmatic dependent launch between graph kernels
   int chain_occ = 0;                            // chain kernels: register cap for occupancy (many chains)
+  int rfree = 1;                                // R-free iteration form (graph path, unsharded, unfused)
+  double* ut = nullptr;                         // u at Yc = 0 (rfree), per solve
+  float* ut32 = nullptr;
   int grp_items = 16;                           // max items per row in one branching stage group (measured)
   float *f32_Yc = nullptr, *f32_Lb = nullptr, *f32_Asub = nullptr, *f32_wbar = nullptr, *f32_U = nullptr,
         *f32_X = nullptr, *f32_eoff = nullptr, *f32_R = nullptr, *f32_g = nullptr, *f32_aux = nullptr,
@@ -623,6 +626,10 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   if (ctx->Yc_save) cudaFree(ctx->Yc_save);
   ctx->Yc_save = nullptr;
   dalloc(ctx, &ctx->Yc_save, (size_t)ctx->n * ly);
+  if (ctx->ut) cudaFree(ctx->ut);
+  ctx->ut = nullptr;
+  dalloc(ctx, &ctx->ut, (size_t)ctx->n * nu);
+  if (const char* e = getenv("WMPC_RFREE")) ctx->rfree = e[0] != '0';
   {  // prox fused with the next up pass (k_chain_pu)
     const int ra = ly + nu + 2;
     ctx->sm_pu = sizeof(double) * ((size_t)nst * (ra + FAST_MAXNS) + (size_t)(256 / 64) * 128);
@@ -970,6 +977,7 @@ void dual_eval_graph(wmpc_ctx* ctx, const double* y, int phase) {
   FastView f = make_fastview(ctx, 1);
   f.d.U = ctx->Uc;
   f.d.X = ctx->Xc;
+  f.rfree = 0;  // the minimiser of an arbitrary y: the full form with R
   const int nthr = 256;
   if (phase <= 0) {
     CK(cudaMemcpyAsync(ctx->Yc_save, ctx->Yc, sizeof(double) * (size_t)ctx->n * ctx->ly, cudaMemcpyDeviceToDevice,
@@ -1053,6 +1061,9 @@ FastView make_fastview(wmpc_ctx* ctx, int count) {
   f.ell_val = ctx->ell_val;
   f.ell_w = ctx->ell_w;
   f.lb_prewait = ctx->gk_groups.empty() ? 0 : 1;
+  f.rfree = ctx->rfree && ctx->shard_k < 0 && !ctx->use_fused && !ctx->use_pu ? 1 : 0;
+  f.ut = ctx->ut;
+  f.ut32 = ctx->ut32;
   f.g32 = G32{ctx->f32_Yc, ctx->f32_Lb, ctx->f32_Asub, ctx->f32_wbar, ctx->f32_U, ctx->f32_X,
               ctx->f32_eoff, ctx->f32_R, ctx->f32_g, ctx->f32_aux, ctx->f32_ell};
   f.xbuf = ctx->xbuf;
@@ -1126,7 +1137,7 @@ void free_all(wmpc_ctx* c) {
                   c->bad_row, c->part, c->scal, c->d_np, c->chain_node,
                   c->bc_ptr, c->bc_row, c->br_ptr, c->br_col, c->off_dev, c->bc_val, c->br_val,
                   c->e_ptr, c->e_col, c->e_val, c->aux,
-                  c->Lb, c->Asub, c->blob, c->store_it, c->f32_Yc, c->f32_Lb, c->f32_Asub, c->f32_wbar, c->f32_U,
+                  c->Lb, c->Asub, c->blob, c->store_it, c->ut, c->ut32, c->f32_Yc, c->f32_Lb, c->f32_Asub, c->f32_wbar, c->f32_U,
                   c->f32_X, c->f32_eoff, c->f32_R, c->f32_g, c->f32_aux, c->f32_ell, c->Yc_save, c->acct, c->rep_gidx, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
                   c->pj_ecv, c->dk_mv, c->dk_sweeps, c->dk_fix, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
                   c->prof};
@@ -1714,6 +1725,28 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
         check_launch(ctx);
       }
       if (ctx->use_graphk) {
+        FastView f0 = make_fastview(ctx, 1);
+        if (f0.rfree) {  // ut = u at Yc = 0 (Yc was just zeroed): one full up/branch/down pass
+          f0.rfree = 0;
+          f0.d.U = ctx->ut;
+          f0.d.X = ctx->Xc;
+          if (ctx->ell_w == 4) {
+            gk_up<4>(ctx, f0);
+            gk_grp<4>(ctx, f0, 0);
+            gk_down<4>(ctx, f0);
+          } else {
+            gk_up<8>(ctx, f0);
+            gk_grp<8>(ctx, f0, 0);
+            gk_down<8>(ctx, f0);
+          }
+          ctx->launches += 2 + ctx->gk_groups.size();
+          if (ctx->fp32) {
+            ctx->launches++;
+            k_convert<<<grid_for((size_t)ctx->n * ctx->nu), 256, 0, ctx->stream>>>(ctx->ut, ctx->ut32,
+                                                                                    (size_t)ctx->n * ctx->nu);
+          }
+          check_launch(ctx);
+        }
         capture_graphk(ctx);
         if (ctx->use_fused || ctx->use_pu) {  // up pass of iteration 0 (Yc = 0)
           FastView f = make_fastview(ctx, 1);
@@ -2072,6 +2105,7 @@ int wmpc_set_precision(wmpc_ctx* ctx, int fp32) {
       dalloc(ctx, &ctx->f32_wbar, n * lx); dalloc(ctx, &ctx->f32_U, n * nu); dalloc(ctx, &ctx->f32_X, n * lx);
       dalloc(ctx, &ctx->f32_eoff, n * nu); dalloc(ctx, &ctx->f32_R, n * nu); dalloc(ctx, &ctx->f32_g, n * lx);
       dalloc(ctx, &ctx->f32_aux, n * 2); dalloc(ctx, &ctx->f32_ell, ctx->ell_len);
+      dalloc(ctx, &ctx->ut32, n * nu);
     }
     ctx->launches += 2;
     k_convert<<<grid_for(n * 2), 256, 0, ctx->stream>>>(ctx->aux, ctx->f32_aux, n * 2);

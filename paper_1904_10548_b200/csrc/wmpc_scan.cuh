@@ -8,6 +8,10 @@
 //   lin_r  = a_r + P sum_{desc(r)} a,           L_r = lin_r / (2c p_r),
 //   u_r    = e_off_r + P(q + sum_{anc(r)} e_off - sum_{path(r)} L),
 //   x_r    = (x_anc + u_r B^T) + g_r.
+// R-free iteration (f.rfree): L is linear in Yc plus a constant part from R,
+// so u = ut - P(sum_{path} L_Y) with ut = u at Yc = 0 computed once per solve
+// (wmpc_apg_begin) and L_Y the Yc part: the per-iteration passes never read R,
+// and the down pass needs neither q nor the e_off prefix sums.
 // Rows at stages >= kstar form nchain chains laid out stage-major
 // (row = n_branch + t*nchain + chain). One APG iteration (solver.py:460-506)
 // is the graph
@@ -233,8 +237,10 @@ __global__ void __launch_bounds__(512, OCC ? 3 : 1) k_chain_up(FastView f) {
   TG* rec = reinterpret_cast<TG*>(smem_raw);
   TG* T = rec + (size_t)nst * ra;
   const GA<TG> G = ga<TG>(f);
-  FOR_RC(nst - 1, 6, (nu >> 1), t, k)
-    cpair(rec + (size_t)t * ra + ly + 2 * k, G.R + (size_t)chain_row(f, t, ci) * nu + 2 * k);
+  const bool withR = !f.rfree;
+  if (withR)
+    FOR_RC(nst - 1, 6, (nu >> 1), t, k)
+      cpair(rec + (size_t)t * ra + ly + 2 * k, G.R + (size_t)chain_row(f, t, ci) * nu + 2 * k);
   if (threadIdx.x < nst) cpair(rec + (size_t)threadIdx.x * ra + ly + nu, G.aux + (size_t)chain_row(f, threadIdx.x, ci) * 2);
   const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
   const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
@@ -262,7 +268,7 @@ __global__ void __launch_bounds__(512, OCC ? 3 : 1) k_chain_up(FastView f) {
     for (int t = tk; t < nst; t += sk) {  // a = (Yu + wbar B) + R, over Yu
       TG* R = rec + (size_t)t * ra;
       TG a = R[lx + k] + ell_dot(bc, R);
-      if (t < nst - 1) a = a + R[ly + k];
+      if (withR && t < nst - 1) a = a + R[ly + k];
       R[lx + k] = a;
     }
   __syncthreads();
@@ -331,7 +337,8 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
   const Ell<EllW<WE>::EC, TG> ec = ell_load<EllW<WE>::EC, TG>(f, own_ec(d, k < nu ? k : 0));
   const TG own_yx = k < nt ? G.Yc[(size_t)r * ly + k] : TG(0);
   const TG own_yu = k < nu ? G.Yc[(size_t)r * ly + lx + k] : TG(0);
-  const TG own_R = k < nu ? G.R[(size_t)r * nu + k] : TG(0);
+  const bool withR = !f.rfree;
+  const TG own_R = withR && k < nu ? G.R[(size_t)r * nu + k] : TG(0);
   const TG own_aux = G.aux[(size_t)r * 2];
   const int e0 = mode == GRP_FINISH ? 0 : f.gi_ptr[r], e1 = mode == GRP_FINISH ? 0 : f.gi_ptr[r + 1];
   constexpr int MQ = 2;  // items per warp prefetched ahead of the wait
@@ -352,7 +359,8 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int c = lane + 32 * i;
-      vu[q][i] = in_group && c < nu ? G.Yc[row * ly + lx + c] + G.R[row * nu + c] : TG(0);
+      vu[q][i] = in_group && c < nu ? (withR ? G.Yc[row * ly + lx + c] + G.R[row * nu + c]
+                                             : G.Yc[row * ly + lx + c]) : TG(0);
     }
   }
   pdl_wait();  // chain totals / lower groups of this iteration
@@ -401,7 +409,9 @@ __global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, i
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int c = lane + 32 * i;
-      u4[i] = c < nu ? (fr ? G.Asub[row * nu + c] : G.Yc[row * ly + lx + c] + G.R[row * nu + c]) : TG(0);
+      u4[i] = c < nu ? (fr ? G.Asub[row * nu + c]
+                           : (withR ? G.Yc[row * ly + lx + c] + G.R[row * nu + c] : G.Yc[row * ly + lx + c]))
+                     : TG(0);
     }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -488,7 +498,8 @@ __global__ void __launch_bounds__(512, OCC ? 3 : 1) k_chain_down(FastView f) {
     rows[m] = m < kb ? f.cpath[(size_t)ci * kb + m] : chain_row(f, m - kb, ci);
   }
   __syncthreads();
-  FOR_RC(nr, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + nu + 2 * k, G.e_off + (size_t)rows[m] * nu + 2 * k);
+  const TG* base = f.rfree ? (sizeof(TG) == 8 ? (const TG*)f.ut : (const TG*)f.ut32) : G.e_off;
+  FOR_RC(nr, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + nu + 2 * k, base + (size_t)rows[m] * nu + 2 * k);
   FOR_RC(nr, 5, (lx >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * nu + 2 * k, G.g + (size_t)rows[m] * lx + 2 * k);
   // the chain rows' L were written by k_chain_up, which finished before the
   // group kernels (our predecessor) started: fetch them before the wait
@@ -506,16 +517,17 @@ __global__ void __launch_bounds__(512, OCC ? 3 : 1) k_chain_down(FastView f) {
   FOR_RC(m_pre, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * k, G.Lb + (size_t)rows[m] * nu + 2 * k);
   cp_commit();
   const unsigned own = kb > 0 ? f.cown[ci] : 0u;
-  const TG qk = k < nu ? (TG)d.q[k] : TG(0);
+  const TG qk = k < nu && !f.rfree ? (TG)d.q[k] : TG(0);
   cp_wait<0>();
   __syncthreads();
   if (threadIdx.x < nu) {
     TG ls = 0, es = qk;
+    const bool rfree = f.rfree;
     for (int m = 0; m < nr; ++m) {
       TG* R = rec + (size_t)m * rd;
       ls = m == 0 ? R[k] : ls + R[k];
       R[k] = es - ls;  // z over L
-      es = es + R[nu + k];
+      if (!rfree) es = es + R[nu + k];
     }
   }
   __syncthreads();
