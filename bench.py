@@ -206,7 +206,8 @@ def load_peaks() -> tuple[float, str]:
 
 
 def ncu_traffic(cfg: str):
-    """Per-iteration DRAM bytes from the committed ncu capture, if any."""
+    """Per-iteration DRAM bytes (all kernels of one APG iteration) from the
+    committed ncu capture, profiles/traffic.json, if any."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
@@ -241,7 +242,8 @@ def roofline_large(peak: float, peak_src: str, iters: int = 50) -> dict:
         out["fp32" if prec else "fp64"] = {"us_per_iteration": t * 1e6, "achieved": ach, "frac": ach / peak}
     ctx.call("wmpc_set_precision", 0)
     return {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src, "nodes": inst.n_nonroot,
-            "algorithmic_bytes_per_iteration": BYTES_PER_NODE_ITER * inst.n_nonroot, **out,
+            "algorithmic_bytes_per_iteration": BYTES_PER_NODE_ITER * inst.n_nonroot,
+            "traffic": ncu_traffic("C4"), **out,
             "how": f"{iters} graph-replayed iterations after 5 warm-up, CUDA events on the solver stream; "
                    "~1.4 GB of per-iteration traffic streams from HBM (126 MB L2: no flush needed)"}
 
