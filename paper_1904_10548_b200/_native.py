@@ -98,11 +98,12 @@ def load() -> C.CDLL:
     """Load the in-tree library (raises if it has not been built)."""
     global _LIB
     if _LIB is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("WMPC_LIB_EXPERIMENT") or LIB_PATH  # A/B builds in tools/ only
+        if not os.path.exists(path):
             raise RuntimeError(
-                f"native library missing: {LIB_PATH}; build it with "
+                f"native library missing: {path}; build it with "
                 "`python -c 'import __graft_entry__ as g; g.build()'`")
-        lib = C.CDLL(LIB_PATH)
+        lib = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res
