@@ -493,19 +493,18 @@ __global__ void __launch_bounds__(512, OCC ? 3 : 1) k_chain_down(FastView f) {
   TG* T = rec + (size_t)nr * rd;
   int* rows = reinterpret_cast<int*>(T + (size_t)nr * FAST_MAXNS);
   const GA<TG> G = ga<TG>(f);
-  if (threadIdx.x < nr) {
-    const int m = threadIdx.x;
-    rows[m] = m < kb ? f.cpath[(size_t)ci * kb + m] : chain_row(f, m - kb, ci);
-  }
-  __syncthreads();
+  // global row of path position m: chain rows by arithmetic, ancestors from
+  // cpath (read per use: no CTA-wide wait for a row table before the copies)
+  auto grow = [&](int m) { return m < kb ? f.cpath[(size_t)ci * kb + m] : chain_row(f, m - kb, ci); };
+  if (threadIdx.x < nr) rows[threadIdx.x] = grow(threadIdx.x);  // for the stores (read after a barrier)
   const TG* base = f.rfree ? (sizeof(TG) == 8 ? (const TG*)f.ut : (const TG*)f.ut32) : G.e_off;
-  FOR_RC(nr, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + nu + 2 * k, base + (size_t)rows[m] * nu + 2 * k);
-  FOR_RC(nr, 5, (lx >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * nu + 2 * k, G.g + (size_t)rows[m] * lx + 2 * k);
+  FOR_RC(nr, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + nu + 2 * k, base + (size_t)grow(m) * nu + 2 * k);
+  FOR_RC(nr, 5, (lx >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * nu + 2 * k, G.g + (size_t)grow(m) * lx + 2 * k);
   // the chain rows' L were written by k_chain_up, which finished before the
   // group kernels (our predecessor) started: fetch them before the wait
   const int m_pre = f.lb_prewait ? kb : nr;
   FOR_RC(nr - m_pre, 6, (nu >> 1), m, k)
-    cpair(rec + (size_t)(m_pre + m) * rd + 2 * k, G.Lb + (size_t)rows[m_pre + m] * nu + 2 * k);
+    cpair(rec + (size_t)(m_pre + m) * rd + 2 * k, G.Lb + (size_t)grow(m_pre + m) * nu + 2 * k);
   const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
   const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
   const int j = threadIdx.x & 63, tj = threadIdx.x >> 6, sj = blockDim.x >> 6;
@@ -514,7 +513,7 @@ __global__ void __launch_bounds__(512, OCC ? 3 : 1) k_chain_down(FastView f) {
   const Ell<EllW<WE>::BR, TG> br = ell_load<EllW<WE>::BR, TG>(f, own_br(d, j < nt ? j : 0));
   pdl_wait();  // L of the branching rows comes from the last group kernel
   pdl_trigger();
-  FOR_RC(m_pre, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * k, G.Lb + (size_t)rows[m] * nu + 2 * k);
+  FOR_RC(m_pre, 6, (nu >> 1), m, k) cpair(rec + (size_t)m * rd + 2 * k, G.Lb + (size_t)grow(m) * nu + 2 * k);
   cp_commit();
   const unsigned own = kb > 0 ? f.cown[ci] : 0u;
   const TG qk = k < nu && !f.rfree ? (TG)d.q[k] : TG(0);
