@@ -1474,8 +1474,13 @@ int wmpc_set_node_data(wmpc_ctx* ctx, wmpc_nodes* nodes, const double* demand, c
     DevView d = view(ctx);
     int blocks = (int)((n * 32 + 255) / 256);
     ctx->launches++;
-    k_node_offsets<<<blocks, 256, 0, ctx->stream>>>(d, ctx->demand, ctx->Ed, nodes->shift, nodes->u_part,
-                                                     nodes->e_off, ctx->tmp, ctx->bad_row);
+    if (ctx->fast && ctx->ns > 0 && ctx->ns <= 32)  // projector structure verified (configure_fast)
+      k_node_offsets_proj<<<(int)((n + 7) / 8), 256, 0, ctx->stream>>>(
+          d, ctx->demand, ctx->Ed, ctx->pj_kp, ctx->pj_kc, ctx->pj_kv, ctx->pj_ecp, ctx->pj_ecr, ctx->pj_ecv,
+          1.0 / (2.0 * ctx->w_c), nodes->shift, nodes->u_part, nodes->e_off, ctx->bad_row);
+    else
+      k_node_offsets<<<blocks, 256, 0, ctx->stream>>>(d, ctx->demand, ctx->Ed, nodes->shift, nodes->u_part,
+                                                       nodes->e_off, ctx->tmp, ctx->bad_row);
     ctx->launches++;
     k_node_R<<<blocks, 256, 0, ctx->stream>>>(d, nodes->e_off, nodes->R);
     if (ctx->fast) {

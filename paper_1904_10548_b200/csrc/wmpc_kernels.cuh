@@ -563,6 +563,57 @@ __global__ void k_node_offsets(DevView d, const double* __restrict__ demand, con
   }
 }
 
+// Structured factor step (W = cI, every T_s = P/(2c), D_s = P, checked on the
+// host): Lam_s = Pi_{s+1} + 2W = 2c(2I - P) (2cI at the last stage) and
+// u_part = -E^+ shift lies in range(E^T), so e_off = u_part - (u_part Lam_s
+// + econ) T_s reduces to u_part - P econ / (2c): no per-node dense 114x114
+// products. P econ = econ - E^T (K econ) with K = (E E^T)^{-1} E sparse.
+__global__ void k_node_offsets_proj(DevView d, const double* __restrict__ demand, const double* __restrict__ Ed,
+                                    const int* __restrict__ kp, const int* __restrict__ kc,
+                                    const double* __restrict__ kv, const int* __restrict__ ecp,
+                                    const int* __restrict__ ecr, const double* __restrict__ ecv, double inv_2c,
+                                    double* shift, double* u_part, double* e_off, int* bad_row) {
+  __shared__ double st[8][32];
+  const int nu = d.nu, ns = d.ns, nd = d.nd;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = blockIdx.x * 8 + warp;
+  if (r >= d.n) return;
+  double* up = u_part + (size_t)r * nu;
+  const double* ec = d.econ + (size_t)r * nu;
+  if (lane < ns) {
+    double s = 0.0;
+    for (int k = 0; k < nd; ++k) s = fma(demand[(size_t)r * nd + k], Ed[(size_t)lane * nd + k], s);
+    shift[(size_t)r * ns + lane] = s;
+    st[warp][lane] = s;
+  }
+  __syncwarp();
+  for (int j = lane; j < nu; j += 32) {
+    double s = 0.0;
+    for (int i = 0; i < ns; ++i) s = fma(st[warp][i], d.e_pinv[(size_t)j * ns + i], s);
+    up[j] = -s;
+  }
+  __syncwarp();
+  bool bad = false;
+  if (lane < ns) {  // feasibility of E u = -Ed d (solver.py:213)
+    double s = 0.0;
+    for (int j = 0; j < nu; ++j) s = fma(up[j], d.E[(size_t)lane * nu + j], s);
+    const double rhs = st[warp][lane];
+    bad = fabs(s + rhs) > 1e-9 * (1.0 + fabs(rhs));
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(bad_row, r);
+  double t = 0.0;  // K econ
+  if (lane < ns)
+    for (int e = kp[lane]; e < kp[lane + 1]; ++e) t = fma(kv[e], ec[kc[e]], t);
+  __syncwarp();
+  if (lane < ns) st[warp][lane] = t;
+  __syncwarp();
+  for (int j = lane; j < nu; j += 32) {
+    double c = 0.0;
+    for (int e = ecp[j]; e < ecp[j + 1]; ++e) c = fma(ecv[e], st[warp][ecr[e]], c);
+    e_off[(size_t)r * nu + j] = up[j] - (ec[j] - c) * inv_2c;
+  }
+}
+
 // R_a = sum_c -2 p_c (e_off_c W), children ascending.
 __global__ void k_node_R(DevView d, const double* __restrict__ e_off, double* Rout) {
   const int nu = d.nu;
