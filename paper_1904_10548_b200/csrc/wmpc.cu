@@ -277,6 +277,20 @@ double gconj_value(wmpc_ctx* ctx, const DevView& d, const double* y) {
   return h[1] > 0.0 ? INFINITY : h[0];
 }
 
+// Dykstra operators: CSR always; the structured path's ELL copy (width 4,
+// zero-padded, the same entries) keeps them in registers across the sweeps.
+DykOps dyk_ops(const wmpc_ctx* ctx) {
+  DykOps po{ctx->pj_kp, ctx->pj_kc, ctx->pj_ecp, ctx->pj_ecr, ctx->pj_kv, ctx->pj_ecv, nullptr, nullptr, 0, 0, 0};
+  if (ctx->fast && ctx->use_graphk && ctx->ell_idx && ctx->ell_w == 4) {
+    po.eidx = ctx->ell_idx;
+    po.eval = ctx->ell_val;
+    po.ew = ctx->ell_w;
+    po.ec0 = ctx->nu + ctx->nt;
+    po.kr0 = 2 * ctx->nu + ctx->nt;
+  }
+  return po;
+}
+
 void gconj_raw(wmpc_ctx* ctx, const DevView& d, const double* y, double out[2]) {
   int nb = std::min(ctx->part_blocks, std::max(1, (ctx->n + 7) / 8));
   ctx->launches += 3;
@@ -1891,13 +1905,13 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
       k_absmax_partial<<<nb0, 256, 0, ctx->stream>>>(ctx->Ua, nU, ctx->part);
       ctx->launches++;
       k_dyk_tol<<<1, 256, 0, ctx->stream>>>(ctx->part, nb0, ctx->scal + 8);
-      DykOps po{ctx->pj_kp, ctx->pj_kc, ctx->pj_ecp, ctx->pj_ecr, ctx->pj_kv, ctx->pj_ecv};
+      DykOps po = dyk_ops(ctx);
       CK(cudaMemsetAsync(ctx->dk_mv, 0, sizeof(unsigned long long) * 512, ctx->stream));
       const int nbw = (ctx->n + 7) / 8;
       ctx->launches += 3;
       k_dyk_warp<<<nbw, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 1,
                                                 ctx->dk_fix);
-      k_dyk_count<<<1, 32, 0, ctx->stream>>>(ctx->dk_mv, 500, ctx->scal + 8, ctx->dk_sweeps);
+      k_dyk_count<<<1, 512, 0, ctx->stream>>>(ctx->dk_mv, 500, ctx->scal + 8, ctx->dk_sweeps);
       k_dyk_warp<<<nbw, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 2,
                                                 ctx->dk_fix);
     }
@@ -2273,7 +2287,7 @@ int wmpc_cert_dykstra(wmpc_ctx* ctx, int max_sweeps, double* mv) {
     std::vector<unsigned long long> bits(max_sweeps, 0ull);
     if (ctx->ns > 0) {
       DevView d = view(ctx);
-      DykOps po{ctx->pj_kp, ctx->pj_kc, ctx->pj_ecp, ctx->pj_ecr, ctx->pj_kv, ctx->pj_ecv};
+      DykOps po = dyk_ops(ctx);
       CK(cudaMemsetAsync(ctx->dk_mv, 0, sizeof(unsigned long long) * 512, ctx->stream));
       ctx->launches++;
       k_dyk_warp<<<(ctx->n + 7) / 8, 256, 0, ctx->stream>>>(d, po, ctx->Ua, nullptr, ctx->dk_mv, ctx->dk_sweeps,
@@ -2315,7 +2329,7 @@ int wmpc_cert_terms(wmpc_ctx* ctx, int sweeps, double* terms) {
       k_clip_inputs<<<grid_for(nU), 256, 0, ctx->stream>>>(d, ctx->Ua, ctx->Uf);
     } else {
       h2d(ctx, ctx->dk_sweeps, &sweeps, sizeof(int));
-      DykOps po{ctx->pj_kp, ctx->pj_kc, ctx->pj_ecp, ctx->pj_ecr, ctx->pj_kv, ctx->pj_ecv};
+      DykOps po = dyk_ops(ctx);
       ctx->launches++;
       k_dyk_warp<<<(ctx->n + 7) / 8, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, sweeps,
                                                             2, nullptr);

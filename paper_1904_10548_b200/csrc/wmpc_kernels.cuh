@@ -745,6 +745,10 @@ namespace wmpc {
 struct DykOps {
   const int *kp, *kc, *ecp, *ecr;
   const double *kv, *ecv;
+  // optional ELL copies (structured path): owners [.. | E cols at ec0 | K rows at kr0], stride ew
+  const int* eidx;
+  const double* eval;
+  int ew, ec0, kr0;
 };
 constexpr int DYK_MAXQ = 4;  // nu <= 128
 // fix (optional): pass 1 stores its final state in u_out and, per node, the
@@ -779,6 +783,30 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
     lo[q] = ok ? d.umin[k] : 0.0;
     hi[q] = ok ? d.umax[k] : 0.0;
   }
+  // operator entries in registers when the ELL copy is given (the water-network
+  // variant: K rows <= 4 entries, E columns <= 1, zero-padded)
+  constexpr int DWK = 4, DWE = 1;
+  const bool ell = po.eidx != nullptr;
+  int kix[DWK], eix[DYK_MAXQ][DWE];
+  double kvv[DWK], evv[DYK_MAXQ][DWE];
+  if (ell) {
+#pragma unroll
+    for (int e = 0; e < DWK; ++e) {
+      const size_t o = (size_t)(po.kr0 + (lane < ns ? lane : 0)) * po.ew + e;
+      kix[e] = po.eidx[o];
+      kvv[e] = po.eval[o];
+    }
+#pragma unroll
+    for (int q = 0; q < DYK_MAXQ; ++q) {
+      const int k = lane + 32 * q;
+#pragma unroll
+      for (int e = 0; e < DWE; ++e) {
+        const size_t o = (size_t)(po.ec0 + (k < nu ? k : 0)) * po.ew + e;
+        eix[q][e] = po.eidx[o];
+        evv[q][e] = po.eval[o];
+      }
+    }
+  }
   for (int s = 0; s < nsw; ++s) {
 #pragma unroll
     for (int q = 0; q < DYK_MAXQ; ++q) {
@@ -788,7 +816,12 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
     __syncwarp();
     if (lane < ns) {
       double t = 0.0;
-      for (int e = po.kp[lane]; e < po.kp[lane + 1]; ++e) t = fma(po.kv[e], sA[warp][po.kc[e]], t);
+      if (ell) {
+#pragma unroll
+        for (int e = 0; e < DWK; ++e) t = fma(kvv[e], sA[warp][kix[e]], t);
+      } else {
+        for (int e = po.kp[lane]; e < po.kp[lane + 1]; ++e) t = fma(po.kv[e], sA[warp][po.kc[e]], t);
+      }
       sT[warp][lane] = t;
     }
     __syncwarp();
@@ -799,7 +832,12 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
       const int k = lane + 32 * q;
       if (k < nu) {
         double corr = 0.0;
-        for (int e = po.ecp[k]; e < po.ecp[k + 1]; ++e) corr = fma(po.ecv[e], sT[warp][po.ecr[e]], corr);
+        if (ell) {
+#pragma unroll
+          for (int e = 0; e < DWE; ++e) corr = fma(evv[q][e], sT[warp][eix[q][e]], corr);
+        } else {
+          for (int e = po.ecp[k]; e < po.ecp[k + 1]; ++e) corr = fma(po.ecv[e], sT[warp][po.ecr[e]], corr);
+        }
         const double A = sA[warp][k];
         const double a = A - (corr + c[q]);
         const double pn = A - a;  // cur + pc - aff
@@ -812,8 +850,15 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
         cur[q] = nx;
       }
     }
-    for (int o = 16; o > 0; o >>= 1) moved = np_max(moved, __shfl_xor_sync(0xffffffffu, moved, o));
-    if (pass == 1 && lane == 0 && moved > 0.0) atomicMax(mv + s, (unsigned long long)__double_as_longlong(moved));
+    // warp max of a nonnegative double (NaN largest, as np.max propagates it)
+    // on its bit pattern: high words, then low words among the top holders
+    {
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(moved);
+      const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(bits >> 32));
+      const unsigned lo = __reduce_max_sync(0xffffffffu, (unsigned)(bits >> 32) == hi ? (unsigned)bits : 0u);
+      const unsigned long long mb = ((unsigned long long)hi << 32) | lo;
+      if (pass == 1 && lane == 0 && mb != 0ull) atomicMax(mv + s, mb);
+    }
     if (__all_sync(0xffffffffu, same)) {  // exact fixed point: every later sweep repeats it
       settled = s;
       break;
@@ -830,15 +875,20 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
   }
 }
 
-// Global sweep count: first sweep whose max movement is <= tol (or all).
+// Global sweep count: first sweep whose max movement is <= tol (or all);
+// one thread per sweep, min-reduced.
 __global__ void k_dyk_count(const unsigned long long* mv, int max_sweeps, const double* tol, int* sweeps) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int k = max_sweeps;
-  for (int s = 0; s < max_sweeps; ++s)
-    if (__longlong_as_double((long long)mv[s]) <= *tol) {
-      k = s + 1;
-      break;
-    }
-  *sweeps = k;
+  __shared__ int smin[32];
+  int best = max_sweeps;
+  const double tl = *tol;
+  for (int s = threadIdx.x; s < max_sweeps; s += blockDim.x)
+    if (__longlong_as_double((long long)mv[s]) <= tl) best = min(best, s + 1);
+  for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) smin[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = min(best, smin[w]);
+    *sweeps = best;
+  }
 }
 }  // namespace wmpc
