@@ -19,6 +19,7 @@
 #include "wmpc.h"
 #include "wmpc_warp.cuh"
 #include "wmpc_scan.cuh"
+#include "wmpc_chainw.cuh"
 
 using namespace wmpc;
 
@@ -101,6 +102,8 @@ struct wmpc_ctx {
   int fp32 = 0;                                 // SolverConfig.precision == "fp32"
   int pdl = 1;                                  // programmatic dependent launch between graph kernels
   int chain_occ = 0;                            // chain kernels: register cap for occupancy (many chains)
+  int chainw = 0, cw_pd = 2, cw_rd = 1;        // warp-per-chain kernels (wmpc_chainw.cuh), ring depth, rows ahead
+  int chainw32 = 0;                             // ... also in fp32 mode (register variant only)
   int rfree = 1;                                // R-free iteration form (graph path, unsharded, unfused)
   double* ut = nullptr;                         // u at Yc = 0 (rfree), per solve
   float* ut32 = nullptr;
@@ -349,8 +352,44 @@ template <int WE>
 void gk_pu(wmpc_ctx* ctx, const FastView& f) {
   k_chain_pu<WE><<<ctx->nchain, 256, ctx->sm_pu, ctx->stream>>>(f);
 }
+template <int WE, typename TG, int PD, bool RF>
+void cw_attrs1(wmpc_ctx* ctx) {
+  CK(cudaFuncSetAttribute(k_chain_up_w<WE, TG, PD, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(sizeof(TG) * CW_WARPS * cw_up_warp(PD, !RF))));
+  CK(cudaFuncSetAttribute(k_chain_down_w<WE, TG, PD, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(sizeof(TG) * CW_WARPS * cw_dn_warp(PD))));
+}
+template <int WE, typename TG, int PD>
+void cw_attrs(wmpc_ctx* ctx) {
+  cw_attrs1<WE, TG, PD, true>(ctx);
+  cw_attrs1<WE, TG, PD, false>(ctx);
+}
+template <int WE, typename TG, bool RF>
+void cw_up_r(wmpc_ctx* ctx, const FastView& f) {
+  if (ctx->cw_rd == 2) {
+    launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 2>, dim3((ctx->nchain + CW_WARPS - 1) / CW_WARPS),
+               dim3(CW_WARPS * 32), sizeof(TG) * CW_WARPS * cw_up_warp_r(), f);
+    return;
+  }
+  launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 1>, dim3((ctx->nchain + CW_WARPS - 1) / CW_WARPS), dim3(CW_WARPS * 32),
+             sizeof(TG) * CW_WARPS * cw_up_warp_r(), f);
+}
+template <int WE, typename TG, bool RF>
+void cw_down_r(wmpc_ctx* ctx, const FastView& f) {
+  if (ctx->cw_rd == 2) {
+    launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 2>, dim3((ctx->nchain + CW_WARPS - 1) / CW_WARPS),
+               dim3(CW_WARPS * 32), sizeof(TG) * CW_WARPS * cw_dn_warp_r(), f);
+    return;
+  }
+  launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 1>, dim3((ctx->nchain + CW_WARPS - 1) / CW_WARPS), dim3(CW_WARPS * 32),
+             sizeof(TG) * CW_WARPS * cw_dn_warp_r(), f);
+}
 template <int WE, typename TG>
 void gk_attrs_t(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
+  if constexpr (WE == 4) {
+    cw_attrs<WE, TG, 2>(ctx);
+    cw_attrs<WE, TG, 8>(ctx);
+  }
   CK(cudaFuncSetAttribute(k_chain_up<WE, TG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
   CK(cudaFuncSetAttribute(k_chain_down<WE, TG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
   CK(cudaFuncSetAttribute(k_chain_up<WE, TG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
@@ -365,8 +404,34 @@ void gk_attrs(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
   gk_attrs_t<WE, double>(ctx, up, down, grp);
   gk_attrs_t<WE, float>(ctx, up, down, grp);
 }
+template <int WE, typename TG, int PD>
+void cw_up(wmpc_ctx* ctx, const FastView& f) {
+  const dim3 grid((ctx->nchain + CW_WARPS - 1) / CW_WARPS), block(CW_WARPS * 32);
+  const size_t sm = sizeof(TG) * CW_WARPS * cw_up_warp(PD, !f.rfree);
+  if (f.rfree) launch_pdl(ctx, k_chain_up_w<WE, TG, PD, true>, grid, block, sm, f);
+  else launch_pdl(ctx, k_chain_up_w<WE, TG, PD, false>, grid, block, sm, f);
+}
+template <int WE, typename TG, int PD>
+void cw_down(wmpc_ctx* ctx, const FastView& f) {
+  const dim3 grid((ctx->nchain + CW_WARPS - 1) / CW_WARPS), block(CW_WARPS * 32);
+  const size_t sm = sizeof(TG) * CW_WARPS * cw_dn_warp(PD);
+  if (f.rfree) launch_pdl(ctx, k_chain_down_w<WE, TG, PD, true>, grid, block, sm, f);
+  else launch_pdl(ctx, k_chain_down_w<WE, TG, PD, false>, grid, block, sm, f);
+}
 template <int WE, typename TG = double>
 void gk_up(wmpc_ctx* ctx, const FastView& f) {
+  if constexpr (WE == 4)
+    if (ctx->chainw && (sizeof(TG) == 8 || ctx->chainw32)) {
+      // fp32: registers only (the 8-byte cp.async ring gave wrong results in fp32
+      // mode; the fp64 ring and both register variants are bit-identical to the
+      // CTA kernels: tests/test_gpu_fast_path.py)
+      const int pd = sizeof(TG) == 4 ? 1 : ctx->cw_pd;
+      if (pd == 8) cw_up<WE, TG, 8>(ctx, f);
+      else if (pd == 1 && f.rfree) cw_up_r<WE, TG, true>(ctx, f);
+      else if (pd == 1) cw_up_r<WE, TG, false>(ctx, f);
+      else cw_up<WE, TG, 2>(ctx, f);
+      return;
+    }
   if (ctx->chain_occ)
     launch_pdl(ctx, k_chain_up<WE, TG, true>, dim3(ctx->nchain), dim3(ctx->up_threads), ctx->sm_up, f);
   else
@@ -388,6 +453,15 @@ void gk_rep(wmpc_ctx* ctx, const FastView& f, int mode, int bump) {
 }
 template <int WE, typename TG = double>
 void gk_down(wmpc_ctx* ctx, const FastView& f) {
+  if constexpr (WE == 4)
+    if (ctx->chainw && (sizeof(TG) == 8 || ctx->chainw32)) {
+      const int pd = sizeof(TG) == 4 ? 1 : ctx->cw_pd;
+      if (pd == 8) cw_down<WE, TG, 8>(ctx, f);
+      else if (pd == 1 && f.rfree) cw_down_r<WE, TG, true>(ctx, f);
+      else if (pd == 1) cw_down_r<WE, TG, false>(ctx, f);
+      else cw_down<WE, TG, 2>(ctx, f);
+      return;
+    }
   if (ctx->chain_occ)
     launch_pdl(ctx, k_chain_down<WE, TG, true>, dim3(ctx->nchain), dim3(ctx->down_threads), ctx->sm_down, f);
   else
@@ -658,6 +732,23 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   ctx->up_threads = ctx->down_threads = 512;  // measured: 512 beats 256 on C2 and C4
   ctx->chain_occ = ctx->nchain > 4 * ctx->sms ? 1 : 0;  // measured: C4 (4096 chains) +4 %; C2, C3 (<= 512) better without
   if (const char* e = getenv("WMPC_PDL")) ctx->pdl = e[0] != '0';
+  {  // warp-per-chain kernels (wmpc_chainw.cuh). Measured (us per iteration, CTA kernels ->
+     // warp kernels): C2 128 chains 19.7 -> 27 (latency-bound: the CTA kernels run the
+     // phases of all rows in parallel), C3 512 chains 55.4 -> 53.4 (8-row ring),
+     // C4 4096 chains 331 -> 270 (ring of 2 or registers, equal; registers chosen).
+    const bool fits = ctx->ell_w == 4 && nu <= 128 && nu % 2 == 0 && nt <= 64 && lx % 2 == 0 && ly % 2 == 0 &&
+                      ctx->ns <= 32;
+    const int wps = (ctx->nchain + ctx->sms - 1) / std::max(ctx->sms, 1);
+    ctx->chainw = ctx->nchain > 2 * ctx->sms ? 1 : 0;
+    ctx->cw_pd = wps <= 4 ? 8 : 1;
+    ctx->cw_rd = 1;
+    if (const char* e = getenv("WMPC_CWPD")) ctx->cw_pd = atoi(e) >= 8 ? 8 : (atoi(e) >= 2 ? 2 : 1);
+    if (const char* e = getenv("WMPC_CWRD")) ctx->cw_rd = atoi(e) >= 2 ? 2 : 1;
+    // fp32 mode (register variant only): C3 47 (CTA) vs 52 us, C4 279 vs 226 us
+    ctx->chainw32 = wps > 4 ? 1 : 0;
+    if (const char* e = getenv("WMPC_CHAINW")) ctx->chainw = ctx->chainw32 = e[0] == '1';
+    if (!fits) ctx->chainw = ctx->chainw32 = 0;
+  }
   if (const char* e = getenv("WMPC_UPT")) ctx->up_threads = atoi(e) >= 512 ? 512 : 256;
   if (const char* e = getenv("WMPC_DNT")) ctx->down_threads = atoi(e) >= 512 ? 512 : 256;
   ctx->prox_warp = nt <= 64 && nu <= 128 ? 1 : 0;
@@ -1007,7 +1098,9 @@ void dual_eval_graph(wmpc_ctx* ctx, const double* y, int phase) {
   }
   if (phase != 0) {
     if (ctx->rep_group.second > 0) gk_rep<WE>(ctx, f, GRP_FINISH, 0);
-    if (ctx->chain_occ)
+    if (WE == 4 && ctx->chainw)
+      gk_down<WE>(ctx, f);
+    else if (ctx->chain_occ)
       k_chain_down<WE, double, true><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);
     else
       k_chain_down<WE, double, false><<<ctx->nchain, ctx->down_threads, ctx->sm_down, ctx->stream>>>(f);

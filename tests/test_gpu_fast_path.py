@@ -114,29 +114,68 @@ def test_reciprocal_division_is_exact():
     assert bad.value == 0
 
 
-@pytest.mark.parametrize("kernel", ["graph", "graph-fused", "graph-pu", "scan", "cta", "warp"])
+# env switches of the kernel variants (graph: CTA-per-chain kernels; chainw:
+# warp-per-chain kernels with an 8- or 2-row shared-memory ring, or rows
+# streamed through registers)
+VARIANT_ENV = {
+    "graph": {"WMPC_CHAINW": "0"},
+    "graph-fused": {"WMPC_FUSED": "1", "WMPC_CHAINW": "0"},
+    "graph-pu": {"WMPC_PU": "1", "WMPC_CHAINW": "0"},
+    "graph-chainw8": {"WMPC_CHAINW": "1", "WMPC_CWPD": "8"},
+    "graph-chainw2": {"WMPC_CHAINW": "1", "WMPC_CWPD": "2"},
+    "graph-chainwr": {"WMPC_CHAINW": "1", "WMPC_CWPD": "1"},
+    "graph-chainwr2": {"WMPC_CHAINW": "1", "WMPC_CWPD": "1", "WMPC_CWRD": "2"},
+}
+
+
+def _with_env(env, fn):
+    saved = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("kernel", ["graph", "graph-fused", "graph-pu", "graph-chainw8", "graph-chainw2",
+                                    "graph-chainwr", "graph-chainwr2", "scan", "cta", "warp"])
 @pytest.mark.parametrize("cfg", ["C1", "C2"])
 def test_every_structured_kernel_matches_general(cfg, kernel):
     inst = config_instance(cfg)
     gamma = 1.0 / 2e9
-    old = os.environ.get("WMPC_KERNEL")
-    os.environ["WMPC_KERNEL"] = kernel.split("-")[0]
-    extra = {"graph-fused": "WMPC_FUSED", "graph-pu": "WMPC_PU"}.get(kernel)
-    if extra:
-        os.environ[extra] = "1"
-    try:
-        rf, mf = _solve(inst, 40, gamma, True, gce=17)
-    finally:
-        if extra:
-            os.environ.pop(extra, None)
-        if old is None:
-            del os.environ["WMPC_KERNEL"]
-        else:
-            os.environ["WMPC_KERNEL"] = old
+    env = {"WMPC_KERNEL": kernel.split("-")[0], **VARIANT_ENV.get(kernel, {})}
+    rf, mf = _with_env(env, lambda: _solve(inst, 40, gamma, True, gce=17))
     rg, _ = _solve(inst, 40, gamma, False, gce=17)
     # a variant whose shared-memory footprint does not fit falls back to the CTA kernel (1..99)
     allowed = {"graph": [300], "graph-fused": [310], "graph-pu": [320], "scan": list(range(200, 300)) + list(range(1, 100)),
-               "warp": list(range(100, 200)) + list(range(1, 100)), "cta": list(range(1, 100))}[kernel]
+               "warp": list(range(100, 200)) + list(range(1, 100)), "cta": list(range(1, 100))}.get(kernel, [300])
     assert mf in allowed, mf
     for k in ("u0", "primal", "primal_avg", "dual"):
         assert rel_err(getattr(rf, k), getattr(rg, k)) <= 1e-11, k
+
+
+@pytest.mark.parametrize("variant", ["graph-chainw8", "graph-chainw2", "graph-chainwr", "graph-chainwr2"])
+@pytest.mark.parametrize("cfg,prec", [("C1", "fp64"), ("C3", "fp64"), ("C2", "fp32")])
+def test_chain_kernel_variants_bit_identical(cfg, prec, variant):
+    """The warp-per-chain kernels (wmpc_chainw.cuh) do the per-element
+    arithmetic of the CTA-per-chain kernels in the same order: every iterate,
+    average, certificate and u0 is bit-identical."""
+    inst = config_instance(cfg)
+    cfgs = SolverConfig(max_iter=40, tol=1e-30, gamma=1.0 / 2e9, gap_check_every=17, precision=prec)
+
+    def run(env):
+        def go():
+            cache = factor_step(inst)
+            assert nat.load().wmpc_fast_path(cache._bind().h) == 300
+            return solve(inst, cfgs, cache=cache)
+        return _with_env(env, go)
+
+    ra = run(VARIANT_ENV["graph"])
+    rb = run(VARIANT_ENV[variant])
+    for k in ("u0", "primal", "primal_avg", "dual"):
+        np.testing.assert_array_equal(getattr(ra, k), getattr(rb, k), err_msg=k)
+    assert ra.duality_gap == rb.duality_gap and ra.objective == rb.objective
