@@ -123,6 +123,15 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective);
  * be NULL. averaged selects the ergodic average for u0. */
 int wmpc_apg_read(wmpc_ctx* ctx, int averaged, double* u0, double* primal,
                   double* primal_avg, double* dual);
+/* wmpc_apg_read on a second stream: returns once the join kernels and copies
+ * are queued (they start when the work queued so far on the solver stream,
+ * i.e. the APG loop, is done) so the caller can run the certificate
+ * meanwhile; destinations must stay valid until wmpc_apg_read_wait. With
+ * page-locked destinations (wmpc_host_alloc) the copies are asynchronous.
+ * Replaces the tail of solver.py:520-543 (result assembly) with an overlapped readout. */
+int wmpc_apg_read_async(wmpc_ctx* ctx, int averaged, double* u0, double* primal, double* primal_avg,
+                        double* dual);
+int wmpc_apg_read_wait(wmpc_ctx* ctx);
 /* Iterations completed since wmpc_apg_begin. */
 int wmpc_apg_iterations(const wmpc_ctx* ctx);
 

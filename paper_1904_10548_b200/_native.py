@@ -8,6 +8,7 @@ library or a CUDA device is missing, every entry point raises.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import os
 
 import numpy as np
@@ -64,6 +65,8 @@ SIGNATURES = {
     "wmpc_apg_check": (C.c_int, [_vp, _dp, _dp, _dp, C.POINTER(C.c_int)]),
     "wmpc_certificate": (C.c_int, [_vp, _dp, _dp]),
     "wmpc_apg_read": (C.c_int, [_vp, C.c_int, _dp, _dp, _dp, _dp]),
+    "wmpc_apg_read_async": (C.c_int, [_vp, C.c_int, _dp, _dp, _dp, _dp]),
+    "wmpc_apg_read_wait": (C.c_int, [_vp]),
     "wmpc_apg_iterations": (C.c_int, [_vp]),
     "wmpc_kernel_launches_per_iteration": (C.c_int, [_vp]),
     "wmpc_fast_path": (C.c_int, [_vp]),
@@ -211,3 +214,36 @@ def pinned_copy(a) -> np.ndarray:
 
 
 _PINNED_KEEP: dict = {}
+
+
+class _PinnedPool:
+    """Page-locked result arrays, recycled: a block returns to the pool when
+    the last array (or view) over it is gone, so a caller that drops each
+    solve's results reuses the same blocks instead of paying for page
+    locking every solve."""
+
+    def __init__(self, keep: int = 8):
+        self.keep = keep
+        self.free: dict = {}
+
+    def empty(self, n: int) -> np.ndarray:
+        nbytes = 8 * max(int(n), 1)
+        lst = self.free.get(nbytes)
+        buf = lst.pop() if lst else _Pinned(nbytes)
+        raw = (C.c_double * max(int(n), 1)).from_address(buf.p.value)
+        # every array or view over the block keeps `raw` alive
+        weakref.finalize(raw, self._give, nbytes, buf)
+        return np.frombuffer(raw, dtype=np.float64, count=int(n))
+
+    def _give(self, nbytes, buf):
+        lst = self.free.setdefault(nbytes, [])
+        if len(lst) < self.keep:
+            lst.append(buf)
+
+
+_POOL = _PinnedPool()
+
+
+def pinned_empty(n: int) -> np.ndarray:
+    """Uninitialised float64 array of ``n`` elements in page-locked memory (pooled)."""
+    return _POOL.empty(n)

@@ -35,6 +35,9 @@ struct wmpc_nodes {
 struct wmpc_ctx {
   int dev = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream_rd = nullptr;  // result readout (wmpc_apg_read_async), overlapping the certificate
+  cudaEvent_t ev_rd = nullptr;
+  double *rb_u0 = nullptr, *rb_p = nullptr, *rb_a = nullptr;  // readout staging (device)
   int n = 0, H = 0, nt = 0, nu = 0, nd = 0, ns = 0, W = 0, P = 0, lx = 0, ly = 0;
   int a_identity = 0, w_scalar = 0;
   double w_c = 0.0;
@@ -1247,7 +1250,7 @@ void free_all(wmpc_ctx* c) {
                   c->Lb, c->Asub, c->blob, c->store_it, c->ut, c->ut32, c->f32_Yc, c->f32_Lb, c->f32_Asub, c->f32_wbar, c->f32_U,
                   c->f32_X, c->f32_eoff, c->f32_R, c->f32_g, c->f32_aux, c->f32_ell, c->Yc_save, c->acct, c->rep_gidx, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
                   c->pj_ecv, c->dk_mv, c->dk_sweeps, c->dk_fix, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
-                  c->prof};
+                  c->prof, c->rb_u0, c->rb_p, c->rb_a};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -1259,6 +1262,11 @@ void free_all(wmpc_ctx* c) {
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->ev2) cudaEventDestroy(c->ev2);
   if (c->ev3) cudaEventDestroy(c->ev3);
+  if (c->stream_rd) {
+    cudaStreamSynchronize(c->stream_rd);
+    cudaStreamDestroy(c->stream_rd);
+  }
+  if (c->ev_rd) cudaEventDestroy(c->ev_rd);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -2070,6 +2078,59 @@ int wmpc_apg_read(wmpc_ctx* ctx, int averaged, double* u0, double* primal, doubl
     if (dual) d2h(ctx, dual, ctx->Y[ctx->it_host % 3], sizeof(double) * n * ctx->W);
     check_launch(ctx);
     sync(ctx);
+    return WMPC_OK;
+  });
+}
+
+// Result readout on a second stream: the join kernels and device-to-host
+// copies run while the caller goes on (the certificate reads Ua and y and
+// writes only its own scratch, so it can run concurrently). Copies into
+// page-locked destinations are truly asynchronous; wmpc_apg_read_wait joins.
+int wmpc_apg_read_async(wmpc_ctx* ctx, int averaged, double* u0, double* primal, double* primal_avg,
+                        double* dual) {
+  return run(ctx, [&]() -> int {
+    DevView d = view(ctx);
+    const size_t n = ctx->n, np_ = n * ctx->P;
+    if (!ctx->stream_rd) {
+      CK(cudaStreamCreateWithFlags(&ctx->stream_rd, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ctx->ev_rd, cudaEventDisableTiming));
+      dalloc(ctx, &ctx->rb_u0, (size_t)ctx->nu);
+      dalloc(ctx, &ctx->rb_p, np_);
+      dalloc(ctx, &ctx->rb_a, np_);
+    }
+    if (ctx->fp32 && ctx->it_host > 0) {  // the last iterate lives in the fp32 arrays
+      ctx->launches += 2;
+      k_convert<<<grid_for(n * ctx->nu), 256, 0, ctx->stream>>>(ctx->f32_U, ctx->U, n * ctx->nu);
+      k_convert<<<grid_for(n * ctx->lx), 256, 0, ctx->stream>>>(ctx->f32_X, ctx->X, n * ctx->lx);
+    }
+    CK(cudaEventRecord(ctx->ev_rd, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->stream_rd, ctx->ev_rd, 0));
+    cudaStream_t s = ctx->stream_rd;
+    if (u0) {
+      ctx->launches++;
+      k_u0<<<1, 128, 0, s>>>(d, averaged ? ctx->Ua : ctx->U, ctx->off[1], ctx->rb_u0);
+      CK(cudaMemcpyAsync(u0, ctx->rb_u0, sizeof(double) * ctx->nu, cudaMemcpyDeviceToHost, s));
+    }
+    if (primal) {
+      ctx->launches++;
+      k_join_primal<<<grid_for(np_), 256, 0, s>>>(ctx->n, ctx->nu, ctx->nt, ctx->lx, ctx->U, ctx->X, ctx->rb_p);
+      CK(cudaMemcpyAsync(primal, ctx->rb_p, sizeof(double) * np_, cudaMemcpyDeviceToHost, s));
+    }
+    if (primal_avg) {
+      ctx->launches++;
+      k_join_primal<<<grid_for(np_), 256, 0, s>>>(ctx->n, ctx->nu, ctx->nt, ctx->lx, ctx->Ua, ctx->Xa, ctx->rb_a);
+      CK(cudaMemcpyAsync(primal_avg, ctx->rb_a, sizeof(double) * np_, cudaMemcpyDeviceToHost, s));
+    }
+    if (dual)
+      CK(cudaMemcpyAsync(dual, ctx->Y[ctx->it_host % 3], sizeof(double) * n * ctx->W, cudaMemcpyDeviceToHost, s));
+    check_launch(ctx);
+    return WMPC_OK;
+  });
+}
+
+int wmpc_apg_read_wait(wmpc_ctx* ctx) {
+  return run(ctx, [&]() -> int {
+    if (ctx->stream_rd) CK(cudaStreamSynchronize(ctx->stream_rd));
     return WMPC_OK;
   });
 }

@@ -354,13 +354,19 @@ def estimate_lipschitz(cache: FactorCache, instance, rel_tol: float = 1e-3, max_
 
 
 def _result_buffers(instance) -> tuple:
-    """Result arrays with their pages already touched: allocated while the
-    device runs the APG loop, so the final copies do not page-fault."""
+    """Result arrays in pooled page-locked memory (``nat.pinned_empty``): the
+    final device-to-host copies run asynchronously, overlapping the
+    certificate (``_read_async``)."""
     nu = instance.model.n_inputs
-    out = (np.empty(nu), np.empty(instance.n_primal), np.empty(instance.n_primal), np.empty(instance.n_dual))
-    for a in out[1:]:
-        a.fill(0.0)  # touch every page now (calloc'd zeros would fault during the copy)
-    return out
+    return (nat.pinned_empty(nu), nat.pinned_empty(instance.n_primal), nat.pinned_empty(instance.n_primal),
+            nat.pinned_empty(instance.n_dual))
+
+
+def _read_async(ctx, averaged: bool, out) -> None:
+    """Queue the result readout on the context's second stream (wmpc_apg_read_async)."""
+    out_u0, out_p, out_a, out_d = out
+    ctx.call("wmpc_apg_read_async", int(averaged), nat.ptr(out_u0), nat.ptr(out_p), nat.ptr(out_a),
+             nat.ptr(out_d))
 
 
 def _read(ctx, instance, averaged: bool, u0=True, primal=True, avg=True, dual=True, out=None):
@@ -449,11 +455,19 @@ def solve(instance, config: SolverConfig | None = None, cache: FactorCache | Non
                 if gap <= config.tol * (1.0 + abs(objective)):
                     iterations, termination = done, "converged"
                     break
-    if termination == "max_iter":
-        residual, scale, dchange = _check(ctx)
-        gap, objective = _certificate(ctx)
+    if bufs is None:
+        bufs = _result_buffers(instance)
+    try:
+        if termination == "max_iter":
+            residual, scale, dchange = _check(ctx)
+            _read_async(ctx, config.averaged_primal, bufs)  # copies overlap the certificate
+            gap, objective = _certificate(ctx)
+        else:
+            _read_async(ctx, config.averaged_primal, bufs)
+    finally:
+        ctx.call("wmpc_apg_read_wait")  # the copies land before bufs can be dropped
     elapsed = time.perf_counter() - started
-    u0, primal, primal_avg, dual = _read(ctx, instance, config.averaged_primal, out=bufs)
+    u0, primal, primal_avg, dual = bufs
     return SolverResult(u0=u0, primal=primal, primal_avg=primal_avg, dual=dual,
                         iterations=iterations, termination=termination,
                         primal_residual=residual, dual_change=dchange, duality_gap=gap,

@@ -21,8 +21,9 @@ for rep in range(6):
     ctx.call("wmpc_apg_run", iters); t.append(time.perf_counter())
     bufs = S._result_buffers(inst); t.append(time.perf_counter())
     S._check(ctx); t.append(time.perf_counter())
+    S._read_async(ctx, True, bufs)
     S._certificate(ctx); t.append(time.perf_counter())
-    S._read(ctx, inst, True, out=bufs); t.append(time.perf_counter())
+    ctx.call("wmpc_apg_read_wait"); t.append(time.perf_counter())
     d = np.diff(t) * 1e3
     print(f"bounds {d[0]:.2f} begin {d[1]:.2f} launch {d[2]:.2f} bufs {d[3]:.2f} check(wait) {d[4]:.2f} "
-          f"cert {d[5]:.2f} read {d[6]:.2f} total {sum(d):.2f} ms")
+          f"cert+read {d[5]:.2f} read_wait {d[6]:.2f} total {sum(d):.2f} ms")
