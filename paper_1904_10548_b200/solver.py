@@ -266,6 +266,7 @@ def _factor(instance, structure_from: FactorCache | None, private: bool,
     bad = np.zeros(1, dtype=np.int64)
     dev.ctx.call("wmpc_set_node_data", nodes.h, nat.ptr(demand) if m.n_mixing else None,
                  nat.ptr(Ed) if m.n_mixing else None, nat.ptr(gd), nat.ptr(econ), nat.ptr(bad))
+    dev.ctx._econ_src = instance.econ  # the context's econ now holds this array (see _upload_bounds)
     cache = FactorCache(null_basis=basis, e_pinv=e_pinv, d_gain=d_gain, t_mat=t_mat, lam=lam,
                         pi=pi, kappa=kappa, lipschitz=lipschitz, signature=sig, _dev=dev,
                         _nodes=nodes)
@@ -279,10 +280,18 @@ def _check_cache(cache: FactorCache, instance) -> None:
 
 
 def _upload_bounds(ctx: nat.Context, instance, with_econ: bool = True) -> None:
+    """Bounds, weights, p, q every solve (the reference's tests mutate them);
+    econ (n x n_u, 72 MB at C4) only when the context does not already hold
+    this instance's array: factor_step uploaded it with the node data, and
+    instances are immutable (problem.py:18-19), so a solve right after its
+    factor_step skips the copy."""
     m, w = instance.model, instance.weights
     arrs = [nat.f64(a) for a in (m.x_min, m.x_max, m.x_safe, m.u_min, m.u_max)]
     p, q = nat.f64(instance.p), nat.f64(instance.q)
-    econ = nat.f64(instance.econ) if with_econ else None
+    econ = None
+    if with_econ and getattr(ctx, "_econ_src", None) is not instance.econ:
+        econ = nat.f64(instance.econ)
+        ctx._econ_src = instance.econ
     ctx.call("wmpc_set_bounds", *[nat.ptr(a) for a in arrs], float(w.w_x), float(w.w_s),
              nat.ptr(p), nat.ptr(q), nat.ptr(econ))
 
