@@ -391,6 +391,7 @@ template <int WE, typename TG>
 void gk_attrs_t(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
   if constexpr (WE == 4) {
     cw_attrs<WE, TG, 2>(ctx);
+    cw_attrs<WE, TG, 4>(ctx);
     cw_attrs<WE, TG, 8>(ctx);
   }
   CK(cudaFuncSetAttribute(k_chain_up<WE, TG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
@@ -430,6 +431,7 @@ void gk_up(wmpc_ctx* ctx, const FastView& f) {
       // CTA kernels: tests/test_gpu_fast_path.py)
       const int pd = sizeof(TG) == 4 ? 1 : ctx->cw_pd;
       if (pd == 8) cw_up<WE, TG, 8>(ctx, f);
+      else if (pd == 4) cw_up<WE, TG, 4>(ctx, f);
       else if (pd == 1 && f.rfree) cw_up_r<WE, TG, true>(ctx, f);
       else if (pd == 1) cw_up_r<WE, TG, false>(ctx, f);
       else cw_up<WE, TG, 2>(ctx, f);
@@ -460,6 +462,7 @@ void gk_down(wmpc_ctx* ctx, const FastView& f) {
     if (ctx->chainw && (sizeof(TG) == 8 || ctx->chainw32)) {
       const int pd = sizeof(TG) == 4 ? 1 : ctx->cw_pd;
       if (pd == 8) cw_down<WE, TG, 8>(ctx, f);
+      else if (pd == 4) cw_down<WE, TG, 4>(ctx, f);
       else if (pd == 1 && f.rfree) cw_down_r<WE, TG, true>(ctx, f);
       else if (pd == 1) cw_down_r<WE, TG, false>(ctx, f);
       else cw_down<WE, TG, 2>(ctx, f);
@@ -745,7 +748,7 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
     ctx->chainw = ctx->nchain > 2 * ctx->sms ? 1 : 0;
     ctx->cw_pd = wps <= 4 ? 8 : 1;
     ctx->cw_rd = 1;
-    if (const char* e = getenv("WMPC_CWPD")) ctx->cw_pd = atoi(e) >= 8 ? 8 : (atoi(e) >= 2 ? 2 : 1);
+    if (const char* e = getenv("WMPC_CWPD")) ctx->cw_pd = atoi(e) >= 8 ? 8 : (atoi(e) >= 4 ? 4 : (atoi(e) >= 2 ? 2 : 1));
     if (const char* e = getenv("WMPC_CWRD")) ctx->cw_rd = atoi(e) >= 2 ? 2 : 1;
     // fp32 mode (register variant only): C3 47 (CTA) vs 52 us, C4 279 vs 226 us
     ctx->chainw32 = wps > 4 ? 1 : 0;

@@ -10,6 +10,7 @@
 //   k_dyk_*       problem.py:221-250 Dykstra restoration
 //   k_cost_*      problem.py:269-275, solver.py:390-395, problem.py:342-374
 #pragma once
+#include <type_traits>
 #include "wmpc_common.cuh"
 
 namespace wmpc {
@@ -807,7 +808,25 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
       }
     }
   }
-  for (int s = 0; s < nsw; ++s) {
+  // Fast path (warp-uniform): every input finite and below 1e150 in magnitude,
+  // so no sweep can produce a NaN (bounds may be infinite) and the NaN-aware
+  // clip / max reduce to plain compares with identical results.
+  bool fin = true;
+#pragma unroll
+  for (int q = 0; q < DYK_MAXQ; ++q) fin &= fabs(cur[q]) <= 1e150 && fabs(c[q]) <= 1e150;
+  if (ell) {
+#pragma unroll
+    for (int e = 0; e < DWK; ++e) fin &= fabs(kvv[e]) <= 1e150;
+#pragma unroll
+    for (int q = 0; q < DYK_MAXQ; ++q)
+#pragma unroll
+      for (int e = 0; e < DWE; ++e) fin &= fabs(evv[q][e]) <= 1e150;
+  }
+  const bool fast = __all_sync(0xffffffffu, fin);
+  // One sweep. CHECK: also test for an exact fixed point (done every 4th sweep:
+  // a node detected a few sweeps late only recomputes identical sweeps).
+  auto sweep = [&](int s, auto check_tag, auto fast_tag) -> bool {
+    constexpr bool CHECK = decltype(check_tag)::value, FAST = decltype(fast_tag)::value;
 #pragma unroll
     for (int q = 0; q < DYK_MAXQ; ++q) {
       const int k = lane + 32 * q;
@@ -841,10 +860,18 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
         const double A = sA[warp][k];
         const double a = A - (corr + c[q]);
         const double pn = A - a;  // cur + pc - aff
-        const double nx = np_clip(a + qc[q], lo[q], hi[q]);
-        const double qn = (a + qc[q]) - nx;
-        moved = np_max(moved, fabs(nx - cur[q]));
-        same &= nx == cur[q] && pn == pc[q] && qn == qc[q];
+        const double v = a + qc[q];
+        double nx;
+        if constexpr (FAST) {
+          const double m = v > lo[q] ? v : lo[q];
+          nx = m < hi[q] ? m : hi[q];
+        } else {
+          nx = np_clip(v, lo[q], hi[q]);
+        }
+        const double qn = v - nx;
+        if constexpr (FAST) moved = fmax(moved, fabs(nx - cur[q]));
+        else moved = np_max(moved, fabs(nx - cur[q]));
+        if constexpr (CHECK) same &= nx == cur[q] && pn == pc[q] && qn == qc[q];
         pc[q] = pn;
         qc[q] = qn;
         cur[q] = nx;
@@ -859,11 +886,21 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
       const unsigned long long mb = ((unsigned long long)hi << 32) | lo;
       if (pass == 1 && lane == 0 && mb != 0ull) atomicMax(mv + s, mb);
     }
-    if (__all_sync(0xffffffffu, same)) {  // exact fixed point: every later sweep repeats it
+    bool stop = false;
+    if constexpr (CHECK) stop = __all_sync(0xffffffffu, same);  // every later sweep repeats it
+    __syncwarp();
+    return stop;
+  };
+  for (int s = 0; s < nsw; ++s) {
+    const bool chk = (s & 3) == 3;
+    const bool stop = fast ? (chk ? sweep(s, std::true_type{}, std::true_type{})
+                                  : sweep(s, std::false_type{}, std::true_type{}))
+                           : (chk ? sweep(s, std::true_type{}, std::false_type{})
+                                  : sweep(s, std::false_type{}, std::false_type{}));
+    if (stop) {
       settled = s;
       break;
     }
-    __syncwarp();
   }
   if (pass == 1 && fix && lane == 0) fix[r] = settled;
   if (pass == 2 || (fix && u_out)) {

@@ -808,8 +808,11 @@ __device__ __forceinline__ bool prox_u_warp(const FastView& f, const ProxIt& P, 
 }
 
 constexpr int PW_ROWS = 4;  // nodes per 256-thread CTA
+#ifndef PW_MINB
+#define PW_MINB 4
+#endif
 template <typename TG>
-__global__ void __launch_bounds__(256, 4) k_prox_warp(FastView f) {
+__global__ void __launch_bounds__(256, PW_MINB) k_prox_warp(FastView f) {
   const DevView& d = f.d;
   __shared__ double sd2[PW_ROWS][128];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
