@@ -70,24 +70,54 @@ def workload(cfg: str) -> dict:
 # ----------------------------------------------------------------- clocks
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled during the timed region: NVML
+    every 2 ms (nvidia-smi, ~0.1 s per call, as the fallback)."""
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, set of reasons)
         self._stop = threading.Event()
         self._t = None
+        self.source = None
+
+    def _run_nvml(self) -> bool:
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                    N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+        except Exception:
+            return False
+        self.source = "nvml (2 ms)"
+        while not self._stop.is_set():
+            try:
+                sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, mx, {n for n, b in zip(self.NAMES, bits) if rs & b}))
+            except Exception:
+                pass
+            self._stop.wait(0.002)
+        return True
 
     def _run(self):
+        if self._run_nvml():
+            return
+        self.source = "nvidia-smi"
         cmd = ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
                "--format=csv,noheader,nounits"]
         while not self._stop.is_set():
             try:
                 out = subprocess.run(cmd, capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                f = [x.strip() for x in out.split(",")]
+                if len(f) == 6 and f[0].replace(".", "").isdigit():
+                    self.samples.append((float(f[0]), float(f[1]) if f[1].replace(".", "").isdigit() else None,
+                                         {n for n, v in zip(self.NAMES, f[2:]) if v.lower().startswith("active")}))
             except Exception:
                 pass
             self._stop.wait(0.2)
@@ -102,16 +132,11 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self) -> dict:
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for s in self.samples:
-            for name, val in zip(names, s[2:]):
-                if val.lower().startswith("active"):
-                    reasons.add(name)
+        sm = [s[0] for s in self.samples]
+        mx = [s[1] for s in self.samples if s[1] is not None]
+        reasons = set().union(*[s[2] for s in self.samples]) if self.samples else set()
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+                "reasons": sorted(reasons), "samples": len(self.samples), "source": self.source}
 
 
 # ------------------------------------------------------------ dist helpers
