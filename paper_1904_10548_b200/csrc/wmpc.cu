@@ -58,6 +58,7 @@ struct wmpc_ctx {
   double *Uc = nullptr, *Xc = nullptr, *Uf = nullptr, *Xf = nullptr, *U0 = nullptr, *X0 = nullptr;
   double *wbar = nullptr, *lin = nullptr, *Yc = nullptr;
   double *ys = nullptr, *gv = nullptr, *vv = nullptr, *zbuf = nullptr;
+  double* gd_stage = nullptr;  // factor step: demand_gd as uploaded (n x nt)
   double *theta = nullptr, *beta = nullptr;
   int max_iter = 0;
   int *iter = nullptr, *bad_nu = nullptr, *bad_row = nullptr;
@@ -1253,7 +1254,7 @@ void free_all(wmpc_ctx* c) {
                   c->Lb, c->Asub, c->blob, c->store_it, c->ut, c->ut32, c->f32_Yc, c->f32_Lb, c->f32_Asub, c->f32_wbar, c->f32_U,
                   c->f32_X, c->f32_eoff, c->f32_R, c->f32_g, c->f32_aux, c->f32_ell, c->Yc_save, c->acct, c->rep_gidx, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
                   c->pj_ecv, c->dk_mv, c->dk_sweeps, c->dk_fix, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
-                  c->prof, c->rb_u0, c->rb_p, c->rb_a};
+                  c->prof, c->rb_u0, c->rb_p, c->rb_a, c->gd_stage};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -1583,11 +1584,14 @@ int wmpc_set_node_data(wmpc_ctx* ctx, wmpc_nodes* nodes, const double* demand, c
       h2d(ctx, ctx->demand, demand, sizeof(double) * n * ctx->nd);
       h2d(ctx, ctx->Ed, Ed, sizeof(double) * ctx->ns * ctx->nd);
     }
-    CK(cudaMemcpy2DAsync(nodes->g, sizeof(double) * ctx->lx, demand_gd, sizeof(double) * ctx->nt,
-                         sizeof(double) * ctx->nt, n, cudaMemcpyHostToDevice, ctx->stream));
+    // demand_gd in one contiguous copy, padded to lx on the device (a pitched
+    // host copy of 504-byte rows is several times slower)
+    if (!ctx->gd_stage) dalloc(ctx, &ctx->gd_stage, n * ctx->nt);
+    h2d(ctx, ctx->gd_stage, demand_gd, sizeof(double) * n * ctx->nt);
+    ctx->launches++;
+    k_pad_rows<<<grid_for(n * ctx->lx), 256, 0, ctx->stream>>>(ctx->gd_stage, ctx->nt, nodes->g, ctx->lx, (int)n,
+                                                              ctx->bad_row);
     h2d(ctx, ctx->econ, econ, sizeof(double) * n * ctx->nu);
-    int big = INT_MAX;
-    h2d(ctx, ctx->bad_row, &big, sizeof(int));
     point_nodes(ctx, nodes);
     DevView d = view(ctx);
     int blocks = (int)((n * 32 + 255) / 256);

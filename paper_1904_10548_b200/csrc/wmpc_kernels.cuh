@@ -10,6 +10,7 @@
 //   k_dyk_*       problem.py:221-250 Dykstra restoration
 //   k_cost_*      problem.py:269-275, solver.py:390-395, problem.py:342-374
 #pragma once
+#include <climits>
 #include <type_traits>
 #include "wmpc_common.cuh"
 
@@ -713,6 +714,18 @@ __global__ void k_scale_into(const double* __restrict__ src, size_t len, const d
 }
 
 // u0 = sum_{stage 1} p_r U_r, clipped (solver.py:525-528).
+// factor step: demand_gd rows (n x nt, contiguous as uploaded) into the padded
+// node layout (n x lx, zero pad), and the infeasibility sentinel
+__global__ void k_pad_rows(const double* __restrict__ src, int nt, double* dst, int lx, int n, int* sentinel) {
+  const size_t tot = (size_t)n * lx;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / lx;
+    const int j = (int)(i - r * lx);
+    dst[i] = j < nt ? src[r * nt + j] : 0.0;
+  }
+  if (sentinel && blockIdx.x == 0 && threadIdx.x == 0) *sentinel = INT_MAX;
+}
+
 __global__ void k_u0(DevView d, const double* __restrict__ Uin, int cnt1, double* out) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d.nu; j += gridDim.x * blockDim.x) {
     double s = 0.0;
