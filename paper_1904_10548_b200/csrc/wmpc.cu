@@ -298,6 +298,12 @@ DykOps dyk_ops(const wmpc_ctx* ctx) {
   return po;
 }
 
+template <typename... A>
+void launch_dyk(wmpc_ctx* ctx, int grid, const DykOps& po, A... args) {
+  if (po.eidx) k_dyk_warp<true><<<grid, 256, 0, ctx->stream>>>(args...);
+  else k_dyk_warp<false><<<grid, 256, 0, ctx->stream>>>(args...);
+}
+
 void gconj_raw(wmpc_ctx* ctx, const DevView& d, const double* y, double out[2]) {
   int nb = std::min(ctx->part_blocks, std::max(1, (ctx->n + 7) / 8));
   ctx->launches += 3;
@@ -2017,10 +2023,10 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
       CK(cudaMemsetAsync(ctx->dk_mv, 0, sizeof(unsigned long long) * 512, ctx->stream));
       const int nbw = (ctx->n + 7) / 8;
       ctx->launches += 3;
-      k_dyk_warp<<<nbw, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 1,
+      launch_dyk(ctx, nbw, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 1,
                                                 ctx->dk_fix);
       k_dyk_count<<<1, 512, 0, ctx->stream>>>(ctx->dk_mv, 500, ctx->scal + 8, ctx->dk_sweeps);
-      k_dyk_warp<<<nbw, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 2,
+      launch_dyk(ctx, nbw, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 2,
                                                 ctx->dk_fix);
     }
     // 2. rollout (problem.py:207-218)
@@ -2451,7 +2457,7 @@ int wmpc_cert_dykstra(wmpc_ctx* ctx, int max_sweeps, double* mv) {
       DykOps po = dyk_ops(ctx);
       CK(cudaMemsetAsync(ctx->dk_mv, 0, sizeof(unsigned long long) * 512, ctx->stream));
       ctx->launches++;
-      k_dyk_warp<<<(ctx->n + 7) / 8, 256, 0, ctx->stream>>>(d, po, ctx->Ua, nullptr, ctx->dk_mv, ctx->dk_sweeps,
+      launch_dyk(ctx, (ctx->n + 7) / 8, po, d, po, ctx->Ua, nullptr, ctx->dk_mv, ctx->dk_sweeps,
                                                             max_sweeps, 1, nullptr);
       check_launch(ctx);
       d2h(ctx, bits.data(), ctx->dk_mv, sizeof(unsigned long long) * max_sweeps);
@@ -2492,7 +2498,7 @@ int wmpc_cert_terms(wmpc_ctx* ctx, int sweeps, double* terms) {
       h2d(ctx, ctx->dk_sweeps, &sweeps, sizeof(int));
       DykOps po = dyk_ops(ctx);
       ctx->launches++;
-      k_dyk_warp<<<(ctx->n + 7) / 8, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, sweeps,
+      launch_dyk(ctx, (ctx->n + 7) / 8, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, sweeps,
                                                             2, nullptr);
     }
     rollout(ctx, d, ctx->Uf, ctx->Xf);

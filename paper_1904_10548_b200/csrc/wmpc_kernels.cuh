@@ -769,6 +769,10 @@ constexpr int DYK_MAXQ = 4;  // nu <= 128
 // sweep count after which that state no longer changes (max_sweeps when it
 // never settled); pass 2 then only recomputes the nodes whose pass-1 state is
 // not already the state after the global sweep count.
+// ELL: the operators come as the register ELL copy (po.eidx); slots past n_u
+// then carry zero state and zero operator entries, so the sweep needs no
+// per-slot branch (a zero slot never moves and is always "same").
+template <bool ELL>
 __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const double* __restrict__ u_in,
                                                   double* __restrict__ u_out, unsigned long long* mv,
                                                   const int* sweeps_in, int max_sweeps, int pass, int* fix) {
@@ -800,7 +804,7 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
   // operator entries in registers when the ELL copy is given (the water-network
   // variant: K rows <= 4 entries, E columns <= 1, zero-padded)
   constexpr int DWK = 4, DWE = 1;
-  const bool ell = po.eidx != nullptr;
+  constexpr bool ell = ELL;
   int kix[DWK], eix[DYK_MAXQ][DWE];
   double kvv[DWK], evv[DYK_MAXQ][DWE];
   if (ell) {
@@ -816,8 +820,8 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
 #pragma unroll
       for (int e = 0; e < DWE; ++e) {
         const size_t o = (size_t)(po.ec0 + (k < nu ? k : 0)) * po.ew + e;
-        eix[q][e] = po.eidx[o];
-        evv[q][e] = po.eval[o];
+        eix[q][e] = k < nu ? po.eidx[o] : 0;
+        evv[q][e] = k < nu ? po.eval[o] : 0.0;
       }
     }
   }
@@ -827,7 +831,7 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
   bool fin = true;
 #pragma unroll
   for (int q = 0; q < DYK_MAXQ; ++q) fin &= fabs(cur[q]) <= 1e150 && fabs(c[q]) <= 1e150;
-  if (ell) {
+  if constexpr (ELL) {
 #pragma unroll
     for (int e = 0; e < DWK; ++e) fin &= fabs(kvv[e]) <= 1e150;
 #pragma unroll
@@ -843,17 +847,17 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
 #pragma unroll
     for (int q = 0; q < DYK_MAXQ; ++q) {
       const int k = lane + 32 * q;
-      if (k < nu) sA[warp][k] = cur[q] + pc[q];
+      if (ELL || k < nu) sA[warp][k] = cur[q] + pc[q];
     }
     __syncwarp();
-    if (lane < ns) {
+    if constexpr (ELL) {  // zero rows past n_s
       double t = 0.0;
-      if (ell) {
 #pragma unroll
-        for (int e = 0; e < DWK; ++e) t = fma(kvv[e], sA[warp][kix[e]], t);
-      } else {
-        for (int e = po.kp[lane]; e < po.kp[lane + 1]; ++e) t = fma(po.kv[e], sA[warp][po.kc[e]], t);
-      }
+      for (int e = 0; e < DWK; ++e) t = fma(kvv[e], sA[warp][kix[e]], t);
+      sT[warp][lane] = t;
+    } else if (lane < ns) {
+      double t = 0.0;
+      for (int e = po.kp[lane]; e < po.kp[lane + 1]; ++e) t = fma(po.kv[e], sA[warp][po.kc[e]], t);
       sT[warp][lane] = t;
     }
     __syncwarp();
@@ -862,9 +866,9 @@ __global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const do
 #pragma unroll
     for (int q = 0; q < DYK_MAXQ; ++q) {
       const int k = lane + 32 * q;
-      if (k < nu) {
+      if (ELL || k < nu) {
         double corr = 0.0;
-        if (ell) {
+        if constexpr (ELL) {
 #pragma unroll
           for (int e = 0; e < DWE; ++e) corr = fma(evv[q][e], sT[warp][eix[q][e]], corr);
         } else {
