@@ -269,6 +269,24 @@ void cost_terms(wmpc_ctx* ctx, const DevView& d, const double* Uin, const double
   sync(ctx);
 }
 
+// Device-side variants for the certificate: results stay in device memory
+// (out[0..3] cost terms; out[0] g* value, out[1] > 0 when y is outside dom g*)
+// so the whole certificate needs one host round trip.
+void cost_terms_dev(wmpc_ctx* ctx, const DevView& d, const double* Uin, const double* Xin, const double* y, int pen,
+                    double* out) {
+  int nb = std::min(ctx->part_blocks, std::max(1, (ctx->n + 7) / 8));
+  ctx->launches += 2;
+  k_cost_partial<<<nb, 256, 0, ctx->stream>>>(d, Uin, Xin, y, pen, ctx->part);
+  k_finish<0><<<1, 256, 0, ctx->stream>>>(ctx->part, nb, 4, 0, 4, out);
+}
+void gconj_dev(wmpc_ctx* ctx, const DevView& d, const double* y, double* out) {
+  int nb = std::min(ctx->part_blocks, std::max(1, (ctx->n + 7) / 8));
+  ctx->launches += 3;
+  k_gconj_partial<<<nb, 256, 0, ctx->stream>>>(d, y, 1e-9, ctx->part);
+  k_finish<0><<<1, 256, 0, ctx->stream>>>(ctx->part, nb, 2, 0, 1, out);
+  k_finish<1><<<1, 256, 0, ctx->stream>>>(ctx->part, nb, 2, 1, 1, out);
+}
+
 double gconj_value(wmpc_ctx* ctx, const DevView& d, const double* y) {
   int nb = std::min(ctx->part_blocks, std::max(1, (ctx->n + 7) / 8));
   ctx->launches++;
@@ -1380,7 +1398,7 @@ int wmpc_create(const wmpc_dims* dims, wmpc_ctx** out) {
     dalloc(ctx, &ctx->d_np, 1);
     ctx->part_blocks = 1184;
     dalloc(ctx, &ctx->part, (size_t)ctx->part_blocks * 4);
-    dalloc(ctx, &ctx->scal, 16);
+    dalloc(ctx, &ctx->scal, 32);  // [0,8) general, [8] Dykstra tol, [16,26) certificate terms
     size_t smax = std::max(smem_fwd(ctx), smem_bwd(ctx, 0));
     if (smax > 48 * 1024) {
       CK(cudaFuncSetAttribute(k_fwd_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
@@ -2032,10 +2050,8 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
     // 2. rollout (problem.py:207-218)
     rollout(ctx, d, ctx->Uf, ctx->Xf);
     check_launch(ctx);
-    // 3. primal value (solver.py:453)
-    double tp[4];
-    cost_terms(ctx, d, ctx->Uf, ctx->Xf, nullptr, 1, tp);
-    double primal = tp[0] + (ctx->w_x * tp[2] + ctx->w_s * tp[3]);
+    // 3. primal value (solver.py:453): terms into scal[16..20)
+    cost_terms_dev(ctx, d, ctx->Uf, ctx->Xf, nullptr, 1, ctx->scal + 16);
     // 4. dual value at the current iterate (solver.py:454-456)
     const double* y = ctx->Y[ctx->it_host % 3];
     DevView dc = d;
@@ -2047,10 +2063,17 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
     } else {
       launch_dg(ctx, dc, y, 0);
     }
-    double td[4];
-    cost_terms(ctx, dc, ctx->Uc, ctx->Xc, y, 0, td);
+    cost_terms_dev(ctx, dc, ctx->Uc, ctx->Xc, y, 0, ctx->scal + 20);
+    gconj_dev(ctx, d, y, ctx->scal + 24);
+    check_launch(ctx);
+    double h[10];  // the certificate's only host round trip
+    d2h(ctx, h, ctx->scal + 16, sizeof(h));
+    sync(ctx);
+    const double* tp = h;
+    const double* td = h + 4;
+    double primal = tp[0] + (ctx->w_x * tp[2] + ctx->w_s * tp[3]);
     double inner = td[0] + td[1];
-    double gc = gconj_value(ctx, d, y);
+    double gc = h[9] > 0.0 ? INFINITY : h[8];
     double dual = inner - gc;
     if (gap) *gap = primal - dual;
     if (objective) *objective = primal;
