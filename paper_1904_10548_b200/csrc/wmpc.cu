@@ -112,6 +112,7 @@ struct wmpc_ctx {
   double* ut = nullptr;                         // u at Yc = 0 (rfree), per solve
   float* ut32 = nullptr;
   int grp_items = 16;                           // max items per row in one branching stage group (measured)
+  int grp_items_few = 16;                       // ... when the stage has at most one row per SM
   float *f32_Yc = nullptr, *f32_Lb = nullptr, *f32_Asub = nullptr, *f32_wbar = nullptr, *f32_U = nullptr,
         *f32_X = nullptr, *f32_eoff = nullptr, *f32_R = nullptr, *f32_g = nullptr, *f32_aux = nullptr,
         *f32_ell = nullptr;
@@ -562,7 +563,9 @@ void build_groups(wmpc_ctx* ctx, int k_rep, const int* acct) {
     while (s_lo > k_rep) {
       int mx = 0;
       for (int r = off[s_lo - 1]; r < off[s_lo]; ++r) mx = std::max(mx, items_of(r, s_hi, nullptr, nullptr));
-      if (mx > ctx->grp_items) break;
+      // a stage of few rows is latency-bound: more items per row cost less than one more kernel
+      const int lim = off[s_lo] - off[s_lo - 1] <= ctx->sms ? ctx->grp_items_few : ctx->grp_items;
+      if (mx > lim) break;
       --s_lo;
     }
     groups.push_back({s_lo, s_hi});
@@ -707,6 +710,10 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   ctx->h_cptr = cptr;
   ctx->h_cidx = cidx;
   if (const char* e = getenv("WMPC_GRP_ITEMS")) ctx->grp_items = std::max(1, atoi(e));
+  // measured (us per iteration, 16 -> 64): C2 19.8 -> 22.6 (few chains: keep 16),
+  // C3 52.4 -> 51.0, C4 269.7 -> 268.0
+  ctx->grp_items_few = nchain > ctx->sms ? std::max(ctx->grp_items, 64) : ctx->grp_items;
+  if (const char* e = getenv("WMPC_GRP_FEW")) ctx->grp_items_few = std::max(1, atoi(e));
   build_groups(ctx, 0, nullptr);
   // chain root paths and ancestor ownership (first chain below a row writes it)
   std::vector<int> cpath((size_t)std::max(nchain * kstar, 1), 0);
