@@ -37,6 +37,8 @@ for kind in ("tank1", "net3"):
     os.chdir(out)
     try:
         assert ref_main(["solve", *args, "--out", "."]) == 0
+        # certainty-equivalent prices (zero_price_errors before attaching the forecast)
+        assert ref_main(["solve", *args, "--nominal-prices", "--out", "nominal"]) == 0
     finally:
         os.chdir(cwd)
     # the reference readers' view of every document (our readers must agree)
