@@ -502,7 +502,7 @@ void gk_down(wmpc_ctx* ctx, const FastView& f) {
 template <typename TG>
 void gk_prox(wmpc_ctx* ctx, const FastView& f) {
   if (ctx->prox_warp)
-    launch_pdl(ctx, k_prox_warp<TG>, dim3((ctx->n + PW_ROWS - 1) / PW_ROWS), dim3(256), 0, f);
+    launch_pdl(ctx, k_prox_warp<TG>, dim3((ctx->n + PW_ROWS - 1) / PW_ROWS), dim3(64 * PW_ROWS), 0, f);
   else
     k_prox_nodes<<<(ctx->n + SC_NPB - 1) / SC_NPB, SC_THREADS, ctx->sm_prox, ctx->stream>>>(f);
 }
