@@ -22,7 +22,10 @@
 
 namespace wmpc {
 
-constexpr int CW_WARPS = 4;  // chains (warps) per CTA
+#ifndef CW_WARPS_N
+#define CW_WARPS_N 4
+#endif
+constexpr int CW_WARPS = CW_WARPS_N;  // chains (warps) per CTA
 #ifndef CW_MINB
 #define CW_MINB 1
 #endif
