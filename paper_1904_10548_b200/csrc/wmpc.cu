@@ -319,8 +319,10 @@ DykOps dyk_ops(const wmpc_ctx* ctx) {
 
 template <typename... A>
 void launch_dyk(wmpc_ctx* ctx, int grid, const DykOps& po, A... args) {
-  if (po.eidx) k_dyk_warp<true><<<grid, 256, 0, ctx->stream>>>(args...);
-  else k_dyk_warp<false><<<grid, 256, 0, ctx->stream>>>(args...);
+  (void)grid;  // one warp per node, DYK_WPB nodes per CTA
+  const int g = (ctx->n + DYK_WPB - 1) / DYK_WPB;
+  if (po.eidx) k_dyk_warp<true><<<g, DYK_WPB * 32, 0, ctx->stream>>>(args...);
+  else k_dyk_warp<false><<<g, DYK_WPB * 32, 0, ctx->stream>>>(args...);
 }
 
 void gconj_raw(wmpc_ctx* ctx, const DevView& d, const double* y, double out[2]) {

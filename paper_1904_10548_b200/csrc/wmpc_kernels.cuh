@@ -772,14 +772,17 @@ constexpr int DYK_MAXQ = 4;  // nu <= 128
 // ELL: the operators come as the register ELL copy (po.eidx); slots past n_u
 // then carry zero state and zero operator entries, so the sweep needs no
 // per-slot branch (a zero slot never moves and is always "same").
+#ifndef DYK_WPB
+#define DYK_WPB 4  // nodes (warps) per CTA (measured: 4 beats 8 and 2 by 3-5 % at C3)
+#endif
 template <bool ELL>
-__global__ void __launch_bounds__(256) k_dyk_warp(DevView d, DykOps po, const double* __restrict__ u_in,
+__global__ void __launch_bounds__(DYK_WPB * 32) k_dyk_warp(DevView d, DykOps po, const double* __restrict__ u_in,
                                                   double* __restrict__ u_out, unsigned long long* mv,
                                                   const int* sweeps_in, int max_sweeps, int pass, int* fix) {
-  __shared__ double sA[8][128];
-  __shared__ double sT[8][32];
+  __shared__ double sA[DYK_WPB][128];
+  __shared__ double sT[DYK_WPB][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * 8 + warp;
+  const int r = blockIdx.x * DYK_WPB + warp;
   if (r >= d.n) return;
   const int nu = d.nu, ns = d.ns;
   const int nsw = pass == 1 ? max_sweeps : *sweeps_in;
