@@ -473,7 +473,7 @@ void gk_up(wmpc_ctx* ctx, const FastView& f) {
 template <int WE, typename TG = double>
 void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump) {
   for (const auto& g : ctx->gk_groups) {
-    launch_pdl(ctx, k_branch_grp<WE, TG>, dim3(g.second), dim3(SC_THREADS), ctx->sm_grp, f, g.first, bump,
+    launch_pdl(ctx, k_branch_grp<WE, TG>, dim3(g.second), dim3(GRP_THREADS), ctx->sm_grp, f, g.first, bump,
                (int)GRP_FULL);
     bump = 0;
   }
@@ -481,7 +481,7 @@ void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump) {
 template <int WE>
 void gk_rep(wmpc_ctx* ctx, const FastView& f, int mode, int bump) {
   if (ctx->rep_group.second > 0)
-    k_branch_grp<WE, double><<<ctx->rep_group.second, SC_THREADS, ctx->sm_grp, ctx->stream>>>(
+    k_branch_grp<WE, double><<<ctx->rep_group.second, GRP_THREADS, ctx->sm_grp, ctx->stream>>>(
         f, ctx->rep_group.first, bump, mode);
 }
 template <int WE, typename TG = double>
@@ -649,7 +649,7 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   const BlobLayout bl = blob_layout(nt, nu, ns, knz, enz, bnz);
   const size_t cap = 227 * 1024;
   const size_t up = sizeof(double) * (size_t)nst * (ly + nu + 2 + FAST_MAXNS);
-  const size_t grp = sizeof(double) * ((size_t)(SC_THREADS / 32) * 256 + 2 * lx + 2 * nu + FAST_MAXNS);
+  const size_t grp = sizeof(double) * ((size_t)(GRP_THREADS / 32) * 256 + 2 * lx + 2 * nu + FAST_MAXNS);
   const size_t down = sizeof(double) * (size_t)H * (2 * nu + lx + FAST_MAXNS) + sizeof(int) * ((H + 3) & ~3);
   const size_t prox = sizeof(double) * ((size_t)SC_NPB * (ctx->fast_rec + nu + lx + 2) + 3 * nt + 2 * nu) +
                       sizeof(int) * SC_NPB + 16;

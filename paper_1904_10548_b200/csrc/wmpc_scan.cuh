@@ -30,6 +30,10 @@
 namespace wmpc {
 
 constexpr int SC_THREADS = 256;
+#ifndef GRP_THREADS_N
+#define GRP_THREADS_N 256
+#endif
+constexpr int GRP_THREADS = GRP_THREADS_N;  // k_branch_grp CTA (>= 128: one thread per u element)
 constexpr int SC_NPB = 4;    // nodes per CTA in k_prox_nodes
 constexpr int SC_MAXK = 30;  // max branching depth (bits of cown)
 
@@ -314,11 +318,11 @@ __global__ void __launch_bounds__(512, OCC ? 3 : 1) k_chain_up(FastView f) {
 // identically on every rank. bump: first kernel of an APG iteration.
 enum { GRP_FULL = 0, GRP_PARTIAL = 1, GRP_FINISH = 2 };
 template <int WE, typename TG>
-__global__ void __launch_bounds__(SC_THREADS) k_branch_grp(FastView f, int r0, int bump, int mode) {
+__global__ void __launch_bounds__(GRP_THREADS) k_branch_grp(FastView f, int r0, int bump, int mode) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly;
   const int r = r0 + blockIdx.x;
-  constexpr int NW = SC_THREADS / 32;
+  constexpr int NW = GRP_THREADS / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   TG* part = reinterpret_cast<TG*>(smem_raw);  // NW x 256: [s1 64 | s2 64 | su 128]
   TG* W1 = part + NW * 256;  // lx
