@@ -399,21 +399,21 @@ template <int WE, typename TG, bool RF>
 void cw_up_r(wmpc_ctx* ctx, const FastView& f) {
   if (ctx->cw_rd == 2) {
     launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 2>, dim3((ctx->nchain + CW_WARPS - 1) / CW_WARPS),
-               dim3(CW_WARPS * 32), sizeof(TG) * CW_WARPS * cw_up_warp_r(), f);
+               dim3(CW_WARPS * 32), sizeof(TG) * (CW_WARPS * cw_up_warp_r() + (CW_SMV ? CW_UP_SLOTS * 32 : 0)), f);
     return;
   }
   launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 1>, dim3((ctx->nchain + CW_WARPS - 1) / CW_WARPS), dim3(CW_WARPS * 32),
-             sizeof(TG) * CW_WARPS * cw_up_warp_r(), f);
+             sizeof(TG) * (CW_WARPS * cw_up_warp_r() + (CW_SMV ? CW_UP_SLOTS * 32 : 0)), f);
 }
 template <int WE, typename TG, bool RF>
 void cw_down_r(wmpc_ctx* ctx, const FastView& f) {
   if (ctx->cw_rd == 2) {
     launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 2>, dim3((ctx->nchain + CW_WARPS - 1) / CW_WARPS),
-               dim3(CW_WARPS * 32), sizeof(TG) * CW_WARPS * cw_dn_warp_r(), f);
+               dim3(CW_WARPS * 32), sizeof(TG) * (CW_WARPS * cw_dn_warp_r() + (CW_SMV ? CW_DN_SLOTS * 32 : 0)), f);
     return;
   }
   launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 1>, dim3((ctx->nchain + CW_WARPS - 1) / CW_WARPS), dim3(CW_WARPS * 32),
-             sizeof(TG) * CW_WARPS * cw_dn_warp_r(), f);
+             sizeof(TG) * (CW_WARPS * cw_dn_warp_r() + (CW_SMV ? CW_DN_SLOTS * 32 : 0)), f);
 }
 template <int WE, typename TG>
 void gk_attrs_t(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {

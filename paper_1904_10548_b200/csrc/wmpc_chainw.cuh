@@ -387,8 +387,66 @@ __device__ __forceinline__ typename V2T<TG>::T ldg2_if(const TG* p, bool ok) {
 __host__ __device__ inline int cw_up_warp_r() { return 64 + 128 + 32; }
 __host__ __device__ inline int cw_dn_warp_r() { return 128 + 128 + 32; }
 
+// Register-light operators for the _r kernels (CW_SMV): the ELL values are the
+// same for every chain, so one copy per CTA sits in a shared table laid out
+// [slot][lane] (conflict-free); a lane keeps only its operand addresses and
+// the address of its first value. Same products, same order: bit-identical to
+// the register-resident form. CW_R_MINB caps registers for more resident
+// chains per SM.
+#ifndef CW_SMV
+#define CW_SMV 1
+#endif
+#ifndef CW_R_MINB
+#define CW_R_MINB 7
+#endif
+constexpr int CW_R_MB = CW_SMV ? CW_R_MINB : CW_MINB;
+constexpr int CW_UP_SLOTS = 16, CW_DN_SLOTS = 14;  // bc 4x2 + ec 4x1 + kr 4 | ec 4x1 + kr 4 + br 2x3
+template <int W, typename TG>
+struct EllV {
+  unsigned a[W];
+  unsigned v;  // shared address of entry 0's value; entry e at v + e * 32 * sizeof(TG)
+};
+template <int W, typename TG>
+__device__ __forceinline__ EllV<W, TG> ellv_bind(const Ell<W, TG>& o, const TG* vec, TG* tab, int& slot, int lane,
+                                                 bool writer) {
+  EllV<W, TG> b;
+  const unsigned base = smem_u32(vec);
+#pragma unroll
+  for (int e = 0; e < W; ++e) {
+    b.a[e] = base + (unsigned)o.idx[e] * (unsigned)sizeof(TG);
+    if (writer) tab[(slot + e) * 32 + lane] = o.val[e];
+  }
+  b.v = smem_u32(tab + slot * 32 + lane);
+  slot += W;
+  return b;
+}
+template <int W, typename TG>
+__device__ __forceinline__ TG ellv_dot(const EllV<W, TG>& b) {
+  TG x[W], w[W];
+#pragma unroll
+  for (int e = 0; e < W; ++e) {
+    x[e] = lds_t(b.a[e], TG(0));
+    w[e] = lds_t(b.v + (unsigned)(e * 32 * sizeof(TG)), TG(0));
+  }
+  TG s = 0;
+#pragma unroll
+  for (int e = 0; e < W; ++e) s = fma(w[e], x[e], s);
+  return s;
+}
+#if CW_SMV
+template <int W, typename TG>
+using EllR = EllV<W, TG>;
+#define CW_BIND(o, vec) ellv_bind(o, vec, vtab, vslot, lane, warp == 0)
+#define CW_DOT(b) ellv_dot(b)
+#else
+template <int W, typename TG>
+using EllR = EllS<W, TG>;
+#define CW_BIND(o, vec) ell_bind(o, vec)
+#define CW_DOT(b) ells_dot(b)
+#endif
+
 template <int WE, typename TG, bool RF, int RD>
-__global__ void __launch_bounds__(CW_WARPS * 32, CW_MINB) k_chain_up_r(FastView f) {
+__global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_up_r(FastView f) {
   using V = typename V2T<TG>::T;
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly, ns = d.ns;
@@ -400,19 +458,26 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_MINB) k_chain_up_r(FastView 
   TG* wb = reinterpret_cast<TG*>(smem_raw) + (size_t)warp * cw_up_warp_r();  // 64
   TG* sb = wb + 64;                                                           // 128
   TG* tb = sb + 128;                                                          // 32
+  TG* vtab = reinterpret_cast<TG*>(smem_raw) + (size_t)CW_WARPS * cw_up_warp_r();  // CW_UP_SLOTS x 32 (CW_SMV)
+  int vslot = 0;
+  (void)vtab;
+  (void)vslot;
   const GA<TG> G = ga<TG>(f);
   const int l2 = 2 * lane;
   const bool ok0 = l2 < nu, ok1 = 64 + l2 < nu, okx = l2 < nt;
   const unsigned o1 = ok1 ? 64 + l2 : 0;
-  EllS<EllW<WE>::BC, TG> bc[4];
-  EllS<EllW<WE>::EC, TG> ec[4];
+  EllR<EllW<WE>::BC, TG> bc[4];
+  EllR<EllW<WE>::EC, TG> ec[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int k = cw_ku(lane, q);
-    bc[q] = ell_bind(ell_own<EllW<WE>::BC, TG>(f, own_bc(d, k), k < nu), wb);
-    ec[q] = ell_bind(ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu), tb);
+    bc[q] = CW_BIND((ell_own<EllW<WE>::BC, TG>(f, own_bc(d, k), k < nu)), wb);
+    ec[q] = CW_BIND((ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu)), tb);
   }
-  const EllS<EllW<WE>::KR, TG> kr = ell_bind(ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < ns), sb);
+  const EllR<EllW<WE>::KR, TG> kr = CW_BIND((ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < ns)), sb);
+#if CW_SMV
+  __syncthreads();  // the value table is written by warp 0
+#endif
   pdl_wait();  // Yc comes from the prox of the previous iteration
   pdl_trigger();
   if (ci >= f.nchain) return;
@@ -454,7 +519,7 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_MINB) k_chain_up_r(FastView 
     TG a[4], S[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      TG v = yu[q] + ells_dot(bc[q]);
+      TG v = yu[q] + CW_DOT(bc[q]);
       if constexpr (withR && !last) {
         const TG rr[4] = {cur.r0.x, cur.r0.y, cur.r1.x, cur.r1.y};
         v = v + rr[q];
@@ -468,10 +533,10 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_MINB) k_chain_up_r(FastView 
       st2(sb + l2, S[0], S[1]);
       st2(sb + 64 + l2, S[2], S[3]);
       __syncwarp();
-      tb[lane] = ells_dot(kr);  // zero past ns
+      tb[lane] = CW_DOT(kr);  // zero past ns
       __syncwarp();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) l[q] = a[q] + (S[q] - ells_dot(ec[q]));
+      for (int q = 0; q < 4; ++q) l[q] = a[q] + (S[q] - CW_DOT(ec[q]));
     } else {
 #pragma unroll
       for (int q = 0; q < 4; ++q) l[q] = a[q];
@@ -497,7 +562,7 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_MINB) k_chain_up_r(FastView 
 }
 
 template <int WE, typename TG, bool RF, int RD>
-__global__ void __launch_bounds__(CW_WARPS * 32, CW_MINB) k_chain_down_r(FastView f) {
+__global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_down_r(FastView f) {
   using V = typename V2T<TG>::T;
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ns = d.ns;
@@ -542,16 +607,23 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_MINB) k_chain_down_r(FastVie
     load_bg(cur, r0);
     if (l0pre) load_L(cur, r0);
   }
-  EllS<EllW<WE>::EC, TG> ec[4];
+  TG* vtab = reinterpret_cast<TG*>(smem_raw) + (size_t)CW_WARPS * cw_dn_warp_r();  // CW_DN_SLOTS x 32 (CW_SMV)
+  int vslot = 0;
+  (void)vtab;
+  (void)vslot;
+  EllR<EllW<WE>::EC, TG> ec[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int k = cw_ku(lane, q);
-    ec[q] = ell_bind(ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu), tb);
+    ec[q] = CW_BIND((ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu)), tb);
   }
-  const EllS<EllW<WE>::KR, TG> kr = ell_bind(ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < ns), zb);
-  EllS<EllW<WE>::BR, TG> br[2];
+  const EllR<EllW<WE>::KR, TG> kr = CW_BIND((ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < ns)), zb);
+  EllR<EllW<WE>::BR, TG> br[2];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) br[h] = ell_bind(ell_own<EllW<WE>::BR, TG>(f, own_br(d, l2 + h), l2 + h < nt), ub);
+  for (int h = 0; h < 2; ++h) br[h] = CW_BIND((ell_own<EllW<WE>::BR, TG>(f, own_br(d, l2 + h), l2 + h < nt)), ub);
+#if CW_SMV
+  __syncthreads();  // the value table is written by warp 0
+#endif
   pdl_wait();  // L of the branching rows comes from the last group kernel
   pdl_trigger();
   if (!live) return;
@@ -595,11 +667,11 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_MINB) k_chain_down_r(FastVie
     st2(zb + l2, z[0], z[1]);
     st2(zb + 64 + l2, z[2], z[3]);
     __syncwarp();
-    tb[lane] = ells_dot(kr);  // zero past ns
+    tb[lane] = CW_DOT(kr);  // zero past ns
     __syncwarp();
     TG u[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) u[q] = b[q] + (z[q] - ells_dot(ec[q]));
+    for (int q = 0; q < 4; ++q) u[q] = b[q] + (z[q] - CW_DOT(ec[q]));
     const bool wr = m >= kb || ((own >> m) & 1u);
     TG* Up = G.U + r * (unsigned)nu;
     if (wr && ok0) st2(Up + l2, u[0], u[1]);
@@ -608,7 +680,7 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_MINB) k_chain_down_r(FastVie
     st2(ub + 64 + l2, u[2], u[3]);
     __syncwarp();
 #pragma unroll
-    for (int h = 0; h < 2; ++h) xs[h] = (xs[h] + ells_dot(br[h])) + (h ? cur.g.y : cur.g.x);
+    for (int h = 0; h < 2; ++h) xs[h] = (xs[h] + CW_DOT(br[h])) + (h ? cur.g.y : cur.g.x);
     TG* Xp = G.X + r * (unsigned)lx + l2;
     if (wr && x2) st2(Xp, xs[0], xs[1]);
     if (wr && okx && !x2) Xp[0] = xs[0];
