@@ -366,6 +366,10 @@ def run_sharded(args, world, rank, local):
     value = K * iters / (total_ms / 1e3)  # one solve split over the ranks: whole-job iterations/s
     e2e = None
     if not args.no_e2e:
+        res = None
+        for _ in range(2):  # results kept alive as in the timed loop (pinned result pool)
+            res = sv.solve(cfg)
+        torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
         for _ in range(K):
@@ -489,9 +493,13 @@ def run_ours(args):
         inst.demand = pin(inst.demand)
         inst.demand_gd = pin(inst.demand_gd)
         inst.econ = pin(inst.econ)
-        for _ in range(max(1, args.warmup)):
+        # the warm-up keeps each result alive like the timed loop does, so the
+        # pinned result pool holds both sets before timing (a pinned allocation
+        # inside the timed region cost 10-200 ms)
+        res = None
+        for _ in range(max(2, args.warmup)):
             c2 = factor_step(inst, structure_from=cache)
-            solve(inst, cfg, cache=c2)
+            res = solve(inst, cfg, cache=c2)
         torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
