@@ -8,7 +8,8 @@
 // results):
 //   * lane l owns the element pairs (2l, 2l+1) and (64+2l, 65+2l) of the u
 //     vectors, (2l, 2l+1) of the x vectors and row l of K, with their ELL
-//     operator entries in registers;
+//     operator entries in registers (the _r kernels keep only the operand
+//     addresses there and read the values from a per-CTA table: CW_SMV);
 //   * rows stream through a per-warp shared-memory ring of PD rows filled by
 //     cp.async; every lane copies exactly the pairs it reads, so the ring needs
 //     no warp barrier (only the three small exchange vectors do: one
