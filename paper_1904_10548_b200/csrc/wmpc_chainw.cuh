@@ -434,6 +434,22 @@ __device__ __forceinline__ TG ellv_dot(const EllV<W, TG>& b) {
   for (int e = 0; e < W; ++e) s = fma(w[e], x[e], s);
   return s;
 }
+// The width-1 E operator keeps its values in registers in fp32 (measured: C4
+// fp32 203 -> 199 us); in fp64 the 8 extra registers spill at 72 (+3 us).
+template <int W, typename TG>
+using EllRE = std::conditional_t<CW_SMV && sizeof(TG) == 8, EllV<W, TG>, EllS<W, TG>>;
+template <int W, typename TG>
+__device__ __forceinline__ EllRE<W, TG> cw_bind_e(const Ell<W, TG>& o, const TG* vec, TG* tab, int& slot, int lane,
+                                                  bool writer) {
+  if constexpr (std::is_same_v<EllRE<W, TG>, EllV<W, TG>>) return ellv_bind(o, vec, tab, slot, lane, writer);
+  else return ell_bind(o, vec);
+}
+template <int W, typename TG>
+__device__ __forceinline__ TG cw_dot_e(const EllV<W, TG>& b) { return ellv_dot(b); }
+template <int W, typename TG>
+__device__ __forceinline__ TG cw_dot_e(const EllS<W, TG>& b) { return ells_dot(b); }
+#define CW_BIND_E(o, vec) cw_bind_e(o, vec, vtab, vslot, lane, warp == 0)
+#define CW_DOT_E(b) cw_dot_e(b)
 #if CW_SMV
 template <int W, typename TG>
 using EllR = EllV<W, TG>;
@@ -468,12 +484,12 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_up_r(FastView 
   const bool ok0 = l2 < nu, ok1 = 64 + l2 < nu, okx = l2 < nt;
   const unsigned o1 = ok1 ? 64 + l2 : 0;
   EllR<EllW<WE>::BC, TG> bc[4];
-  EllR<EllW<WE>::EC, TG> ec[4];
+  EllRE<EllW<WE>::EC, TG> ec[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int k = cw_ku(lane, q);
     bc[q] = CW_BIND((ell_own<EllW<WE>::BC, TG>(f, own_bc(d, k), k < nu)), wb);
-    ec[q] = CW_BIND((ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu)), tb);
+    ec[q] = CW_BIND_E((ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu)), tb);
   }
   const EllR<EllW<WE>::KR, TG> kr = CW_BIND((ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < ns)), sb);
 #if CW_SMV
@@ -537,7 +553,7 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_up_r(FastView 
       tb[lane] = CW_DOT(kr);  // zero past ns
       __syncwarp();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) l[q] = a[q] + (S[q] - CW_DOT(ec[q]));
+      for (int q = 0; q < 4; ++q) l[q] = a[q] + (S[q] - CW_DOT_E(ec[q]));
     } else {
 #pragma unroll
       for (int q = 0; q < 4; ++q) l[q] = a[q];
@@ -612,11 +628,11 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_down_r(FastVie
   int vslot = 0;
   (void)vtab;
   (void)vslot;
-  EllR<EllW<WE>::EC, TG> ec[4];
+  EllRE<EllW<WE>::EC, TG> ec[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int k = cw_ku(lane, q);
-    ec[q] = CW_BIND((ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu)), tb);
+    ec[q] = CW_BIND_E((ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu)), tb);
   }
   const EllR<EllW<WE>::KR, TG> kr = CW_BIND((ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < ns)), zb);
   EllR<EllW<WE>::BR, TG> br[2];
@@ -672,7 +688,7 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_down_r(FastVie
     __syncwarp();
     TG u[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) u[q] = b[q] + (z[q] - CW_DOT(ec[q]));
+    for (int q = 0; q < 4; ++q) u[q] = b[q] + (z[q] - CW_DOT_E(ec[q]));
     const bool wr = m >= kb || ((own >> m) & 1u);
     TG* Up = G.U + r * (unsigned)nu;
     if (wr && ok0) st2(Up + l2, u[0], u[1]);
