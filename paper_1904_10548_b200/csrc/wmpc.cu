@@ -121,6 +121,7 @@ struct wmpc_ctx {
   int *ell_cnt = nullptr, *ell_idx = nullptr;
   double* ell_val = nullptr;
   int ell_w = 4;
+  int ell_vf = 0;                               // B, E ELL values exact in fp32 (WMPC_ELL_VF=0 disables)
   cudaGraphExec_t gk_exec1 = nullptr, gk_exec8 = nullptr;
   double gk_gamma = -1.0;
   int gk_maxit = -1;
@@ -397,23 +398,27 @@ void cw_attrs(wmpc_ctx* ctx) {
 }
 template <int WE, typename TG, bool RF>
 void cw_up_r(wmpc_ctx* ctx, const FastView& f) {
+  const dim3 grid((ctx->nchain + CW_WARPS - 1) / CW_WARPS), block(CW_WARPS * 32);
+  const size_t sm = sizeof(TG) * (CW_WARPS * cw_up_warp_r() + (CW_SMV ? CW_UP_SLOTS * 32 : 0));
   if (ctx->cw_rd == 2) {
-    launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 2>, dim3((ctx->nchain + CW_WARPS - 1) / CW_WARPS),
-               dim3(CW_WARPS * 32), sizeof(TG) * (CW_WARPS * cw_up_warp_r() + (CW_SMV ? CW_UP_SLOTS * 32 : 0)), f);
+    if (ctx->ell_vf) launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 2, true>, grid, block, sm, f);
+    else launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 2, false>, grid, block, sm, f);
     return;
   }
-  launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 1>, dim3((ctx->nchain + CW_WARPS - 1) / CW_WARPS), dim3(CW_WARPS * 32),
-             sizeof(TG) * (CW_WARPS * cw_up_warp_r() + (CW_SMV ? CW_UP_SLOTS * 32 : 0)), f);
+  if (ctx->ell_vf) launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 1, true>, grid, block, sm, f);
+  else launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 1, false>, grid, block, sm, f);
 }
 template <int WE, typename TG, bool RF>
 void cw_down_r(wmpc_ctx* ctx, const FastView& f) {
+  const dim3 grid((ctx->nchain + CW_WARPS - 1) / CW_WARPS), block(CW_WARPS * 32);
+  const size_t sm = sizeof(TG) * (CW_WARPS * cw_dn_warp_r() + (CW_SMV ? CW_DN_SLOTS * 32 : 0));
   if (ctx->cw_rd == 2) {
-    launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 2>, dim3((ctx->nchain + CW_WARPS - 1) / CW_WARPS),
-               dim3(CW_WARPS * 32), sizeof(TG) * (CW_WARPS * cw_dn_warp_r() + (CW_SMV ? CW_DN_SLOTS * 32 : 0)), f);
+    if (ctx->ell_vf) launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 2, true>, grid, block, sm, f);
+    else launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 2, false>, grid, block, sm, f);
     return;
   }
-  launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 1>, dim3((ctx->nchain + CW_WARPS - 1) / CW_WARPS), dim3(CW_WARPS * 32),
-             sizeof(TG) * (CW_WARPS * cw_dn_warp_r() + (CW_SMV ? CW_DN_SLOTS * 32 : 0)), f);
+  if (ctx->ell_vf) launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 1, true>, grid, block, sm, f);
+  else launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 1, false>, grid, block, sm, f);
 }
 template <int WE, typename TG>
 void gk_attrs_t(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
@@ -706,6 +711,12 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
     upload_vec(ctx, &ctx->ell_cnt, cnt);
     upload_vec(ctx, &ctx->ell_idx, idx);
     upload_vec(ctx, &ctx->ell_val, val);
+    // B and E values (owners before the K rows) exact in fp32: the warp chain
+    // kernels store them as float in their shared operator table
+    ctx->ell_vf = 1;
+    for (size_t i = 0; i < (size_t)(2 * nu + nt) * we && i < val.size(); ++i)
+      ctx->ell_vf &= (double)(float)val[i] == val[i];
+    if (const char* e = getenv("WMPC_ELL_VF")) ctx->ell_vf &= e[0] != '0';
     ctx->ell_w = we;
     ctx->ell_len = val.size();
   }

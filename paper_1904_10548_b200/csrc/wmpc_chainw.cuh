@@ -402,68 +402,67 @@ __host__ __device__ inline int cw_dn_warp_r() { return 128 + 128 + 32; }
 #endif
 constexpr int CW_R_MB = CW_SMV ? CW_R_MINB : CW_MINB;
 constexpr int CW_UP_SLOTS = 16, CW_DN_SLOTS = 14;  // bc 4x2 + ec 4x1 + kr 4 | ec 4x1 + kr 4 + br 2x3
-template <int W, typename TG>
+// VF: the B and E values are stored as float when every one of them is exact
+// in fp32 (wmpc_ctx::ell_vf, checked on the host; +-1 for the Barcelona-type
+// networks): one shared wavefront per 32 lanes instead of two, and the
+// float -> double conversion is exact, so the products are unchanged.
+template <int W, typename TG, typename TV = TG>
 struct EllV {
   unsigned a[W];
-  unsigned v;  // shared address of entry 0's value; entry e at v + e * 32 * sizeof(TG)
+  unsigned v;  // shared address of entry 0's value; entry e at v + e * 32 * sizeof(TV)
 };
-template <int W, typename TG>
-__device__ __forceinline__ EllV<W, TG> ellv_bind(const Ell<W, TG>& o, const TG* vec, TG* tab, int& slot, int lane,
-                                                 bool writer) {
-  EllV<W, TG> b;
+template <typename TV, int W, typename TG>
+__device__ __forceinline__ EllV<W, TG, TV> ellv_bind(const Ell<W, TG>& o, const TG* vec, unsigned char* tab, int& off,
+                                                     int lane, bool writer) {
+  EllV<W, TG, TV> b;
   const unsigned base = smem_u32(vec);
+  TV* t = reinterpret_cast<TV*>(tab + off);
 #pragma unroll
   for (int e = 0; e < W; ++e) {
     b.a[e] = base + (unsigned)o.idx[e] * (unsigned)sizeof(TG);
-    if (writer) tab[(slot + e) * 32 + lane] = o.val[e];
+    if (writer) t[e * 32 + lane] = (TV)o.val[e];
   }
-  b.v = smem_u32(tab + slot * 32 + lane);
-  slot += W;
+  b.v = smem_u32(t + lane);
+  off += W * 32 * (int)sizeof(TV);
   return b;
 }
-template <int W, typename TG>
-__device__ __forceinline__ TG ellv_dot(const EllV<W, TG>& b) {
+template <int W, typename TG, typename TV>
+__device__ __forceinline__ TG ellv_dot(const EllV<W, TG, TV>& b) {
   TG x[W], w[W];
 #pragma unroll
   for (int e = 0; e < W; ++e) {
     x[e] = lds_t(b.a[e], TG(0));
-    w[e] = lds_t(b.v + (unsigned)(e * 32 * sizeof(TG)), TG(0));
+    w[e] = (TG)lds_t(b.v + (unsigned)(e * 32 * sizeof(TV)), TV(0));
   }
   TG s = 0;
 #pragma unroll
   for (int e = 0; e < W; ++e) s = fma(w[e], x[e], s);
   return s;
 }
-// The width-1 E operator keeps its values in registers in fp32 (measured: C4
-// fp32 203 -> 199 us); in fp64 the 8 extra registers spill at 72 (+3 us).
+template <int W, typename TG, typename TV>
+__device__ __forceinline__ TG cw_dot(const EllV<W, TG, TV>& b) { return ellv_dot(b); }
 template <int W, typename TG>
-using EllRE = std::conditional_t<CW_SMV && sizeof(TG) == 8, EllV<W, TG>, EllS<W, TG>>;
+__device__ __forceinline__ TG cw_dot(const EllS<W, TG>& b) { return ells_dot(b); }
+// K values (TG) / B values (TB) / E values (TB; in fp32 the width-1 E
+// operator keeps its values in registers: C4 fp32 203 -> 199 us, while in
+// fp64 the 8 extra registers spill at 72, +3 us)
 template <int W, typename TG>
-__device__ __forceinline__ EllRE<W, TG> cw_bind_e(const Ell<W, TG>& o, const TG* vec, TG* tab, int& slot, int lane,
-                                                  bool writer) {
-  if constexpr (std::is_same_v<EllRE<W, TG>, EllV<W, TG>>) return ellv_bind(o, vec, tab, slot, lane, writer);
-  else return ell_bind(o, vec);
+using EllRK = std::conditional_t<CW_SMV, EllV<W, TG>, EllS<W, TG>>;
+template <int W, typename TG, typename TB>
+using EllRB = std::conditional_t<CW_SMV, EllV<W, TG, TB>, EllS<W, TG>>;
+template <int W, typename TG, typename TB>
+using EllRE = std::conditional_t<CW_SMV && sizeof(TG) == 8, EllV<W, TG, TB>, EllS<W, TG>>;
+template <typename R, typename TV, int W, typename TG>
+__device__ __forceinline__ R cw_bind(const Ell<W, TG>& o, const TG* vec, unsigned char* tab, int& off, int lane,
+                                     bool writer) {
+  if constexpr (std::is_same_v<R, EllS<W, TG>>) return ell_bind(o, vec);
+  else return ellv_bind<TV>(o, vec, tab, off, lane, writer);
 }
-template <int W, typename TG>
-__device__ __forceinline__ TG cw_dot_e(const EllV<W, TG>& b) { return ellv_dot(b); }
-template <int W, typename TG>
-__device__ __forceinline__ TG cw_dot_e(const EllS<W, TG>& b) { return ells_dot(b); }
-#define CW_BIND_E(o, vec) cw_bind_e(o, vec, vtab, vslot, lane, warp == 0)
-#define CW_DOT_E(b) cw_dot_e(b)
-#if CW_SMV
-template <int W, typename TG>
-using EllR = EllV<W, TG>;
-#define CW_BIND(o, vec) ellv_bind(o, vec, vtab, vslot, lane, warp == 0)
-#define CW_DOT(b) ellv_dot(b)
-#else
-template <int W, typename TG>
-using EllR = EllS<W, TG>;
-#define CW_BIND(o, vec) ell_bind(o, vec)
-#define CW_DOT(b) ells_dot(b)
-#endif
+#define CW_DOT(b) cw_dot(b)
 
-template <int WE, typename TG, bool RF, int RD>
+template <int WE, typename TG, bool RF, int RD, bool VF>
 __global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_up_r(FastView f) {
+  using TB = std::conditional_t<VF && sizeof(TG) == 8, float, TG>;  // B, E value storage
   using V = typename V2T<TG>::T;
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly, ns = d.ns;
@@ -475,23 +474,23 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_up_r(FastView 
   TG* wb = reinterpret_cast<TG*>(smem_raw) + (size_t)warp * cw_up_warp_r();  // 64
   TG* sb = wb + 64;                                                           // 128
   TG* tb = sb + 128;                                                          // 32
-  TG* vtab = reinterpret_cast<TG*>(smem_raw) + (size_t)CW_WARPS * cw_up_warp_r();  // CW_UP_SLOTS x 32 (CW_SMV)
-  int vslot = 0;
+  unsigned char* vtab = smem_raw + sizeof(TG) * (size_t)CW_WARPS * cw_up_warp_r();  // <= CW_UP_SLOTS x 32 (CW_SMV)
+  int voff = 0;
   (void)vtab;
-  (void)vslot;
+  (void)voff;
   const GA<TG> G = ga<TG>(f);
   const int l2 = 2 * lane;
   const bool ok0 = l2 < nu, ok1 = 64 + l2 < nu, okx = l2 < nt;
   const unsigned o1 = ok1 ? 64 + l2 : 0;
-  EllR<EllW<WE>::BC, TG> bc[4];
-  EllRE<EllW<WE>::EC, TG> ec[4];
+  EllRB<EllW<WE>::BC, TG, TB> bc[4];
+  EllRE<EllW<WE>::EC, TG, TB> ec[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int k = cw_ku(lane, q);
-    bc[q] = CW_BIND((ell_own<EllW<WE>::BC, TG>(f, own_bc(d, k), k < nu)), wb);
-    ec[q] = CW_BIND_E((ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu)), tb);
+    bc[q] = cw_bind<EllRB<EllW<WE>::BC, TG, TB>, TB>(ell_own<EllW<WE>::BC, TG>(f, own_bc(d, k), k < nu), wb, vtab, voff, lane, warp == 0);
+    ec[q] = cw_bind<EllRE<EllW<WE>::EC, TG, TB>, TB>(ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu), tb, vtab, voff, lane, warp == 0);
   }
-  const EllR<EllW<WE>::KR, TG> kr = CW_BIND((ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < ns)), sb);
+  const EllRK<EllW<WE>::KR, TG> kr = cw_bind<EllRK<EllW<WE>::KR, TG>, TG>(ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < ns), sb, vtab, voff, lane, warp == 0);
 #if CW_SMV
   __syncthreads();  // the value table is written by warp 0
 #endif
@@ -553,7 +552,7 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_up_r(FastView 
       tb[lane] = CW_DOT(kr);  // zero past ns
       __syncwarp();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) l[q] = a[q] + (S[q] - CW_DOT_E(ec[q]));
+      for (int q = 0; q < 4; ++q) l[q] = a[q] + (S[q] - CW_DOT(ec[q]));
     } else {
 #pragma unroll
       for (int q = 0; q < 4; ++q) l[q] = a[q];
@@ -578,8 +577,9 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_up_r(FastView 
   if (ok1) st2(G.Asub + (size_t)r_top * nu + 64 + l2, acc[2], acc[3]);
 }
 
-template <int WE, typename TG, bool RF, int RD>
+template <int WE, typename TG, bool RF, int RD, bool VF>
 __global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_down_r(FastView f) {
+  using TB = std::conditional_t<VF && sizeof(TG) == 8, float, TG>;  // B, E value storage
   using V = typename V2T<TG>::T;
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ns = d.ns;
@@ -624,20 +624,21 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_down_r(FastVie
     load_bg(cur, r0);
     if (l0pre) load_L(cur, r0);
   }
-  TG* vtab = reinterpret_cast<TG*>(smem_raw) + (size_t)CW_WARPS * cw_dn_warp_r();  // CW_DN_SLOTS x 32 (CW_SMV)
-  int vslot = 0;
+  unsigned char* vtab = smem_raw + sizeof(TG) * (size_t)CW_WARPS * cw_dn_warp_r();  // <= CW_DN_SLOTS x 32 (CW_SMV)
+  int voff = 0;
   (void)vtab;
-  (void)vslot;
-  EllRE<EllW<WE>::EC, TG> ec[4];
+  (void)voff;
+  EllRE<EllW<WE>::EC, TG, TB> ec[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int k = cw_ku(lane, q);
-    ec[q] = CW_BIND_E((ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu)), tb);
+    ec[q] = cw_bind<EllRE<EllW<WE>::EC, TG, TB>, TB>(ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu), tb, vtab, voff, lane, warp == 0);
   }
-  const EllR<EllW<WE>::KR, TG> kr = CW_BIND((ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < ns)), zb);
-  EllR<EllW<WE>::BR, TG> br[2];
+  const EllRK<EllW<WE>::KR, TG> kr = cw_bind<EllRK<EllW<WE>::KR, TG>, TG>(ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < ns), zb, vtab, voff, lane, warp == 0);
+  EllRB<EllW<WE>::BR, TG, TB> br[2];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) br[h] = CW_BIND((ell_own<EllW<WE>::BR, TG>(f, own_br(d, l2 + h), l2 + h < nt)), ub);
+  for (int h = 0; h < 2; ++h)
+    br[h] = cw_bind<EllRB<EllW<WE>::BR, TG, TB>, TB>(ell_own<EllW<WE>::BR, TG>(f, own_br(d, l2 + h), l2 + h < nt), ub, vtab, voff, lane, warp == 0);
 #if CW_SMV
   __syncthreads();  // the value table is written by warp 0
 #endif
@@ -688,7 +689,7 @@ __global__ void __launch_bounds__(CW_WARPS * 32, CW_R_MB) k_chain_down_r(FastVie
     __syncwarp();
     TG u[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) u[q] = b[q] + (z[q] - CW_DOT_E(ec[q]));
+    for (int q = 0; q < 4; ++q) u[q] = b[q] + (z[q] - CW_DOT(ec[q]));
     const bool wr = m >= kb || ((own >> m) & 1u);
     TG* Up = G.U + r * (unsigned)nu;
     if (wr && ok0) st2(Up + l2, u[0], u[1]);
