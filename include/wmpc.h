@@ -143,6 +143,14 @@ int wmpc_kernel_launches_per_iteration(const wmpc_ctx* ctx);
  * the row-tile size for the step-recursive CTA kernel, 0 when the general
  * per-stage kernels run. */
 int wmpc_fast_path(const wmpc_ctx* ctx);
+/* Kernel selection of the bound structure, for tests and bench provenance:
+ * out[0] wmpc_fast_path, [1] fused one-kernel iteration (k_chain_dp) in use,
+ * [2] warp-per-chain up/down kernels, [3] their ring depth, [4] branch stage
+ * groups, [5] chains, [6] first chain stage, [7] B/E values as float, [8] fp32
+ * mode, [9] k_chain_dp warps per CTA, [10] its grid, [11] chains per warp,
+ * [12] kernels per iteration, [13] branching rows, [14] SMs. Returns the
+ * number of fields (writes at most cap). No reference counterpart. */
+int wmpc_path_info(const wmpc_ctx* ctx, int* out, int cap);
 
 /* Timing helpers for bench.py: run `count` iterations between CUDA events on
  * the context's stream; *ms = elapsed device time. */

@@ -70,6 +70,7 @@ SIGNATURES = {
     "wmpc_apg_iterations": (C.c_int, [_vp]),
     "wmpc_kernel_launches_per_iteration": (C.c_int, [_vp]),
     "wmpc_fast_path": (C.c_int, [_vp]),
+    "wmpc_path_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.c_int]),
     "wmpc_profile_fast": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_int]),
     "wmpc_last_debug_ms": (C.c_float, [_vp]),
     "wmpc_debug_div": (C.c_int, [_dp, _dp, C.c_int, C.POINTER(C.c_uint64)]),
@@ -129,6 +130,17 @@ def f64(a) -> np.ndarray:
 
 class NativeError(RuntimeError):
     pass
+
+
+PATH_FIELDS = ("fast_path", "fused_dp", "chainw", "ring_depth", "branch_groups", "nchain", "kstar",
+               "ell_vf", "fp32", "dp_wpc", "dp_grid", "dp_cpw", "kernels_per_iteration", "n_branch", "sms")
+
+
+def path_info(ctx: "Context") -> dict:
+    """Kernel selection of the context's structure (wmpc_path_info)."""
+    buf = (C.c_int * 32)()
+    n = load().wmpc_path_info(ctx.h, buf, 32)
+    return {k: int(buf[i]) for i, k in enumerate(PATH_FIELDS[:max(n, 0)])}
 
 
 class Context:
@@ -207,13 +219,16 @@ def pinned_copy(a) -> np.ndarray:
     a = np.ascontiguousarray(a, dtype=np.float64)
     buf = _Pinned(max(a.nbytes, 8))
     raw = (C.c_double * max(a.size, 1)).from_address(buf.p.value)
+    # every array or view over the block keeps `raw` alive; the block is
+    # freed with the last of them (no id-keyed registry: ADVICE r1)
+    weakref.finalize(raw, _free_pinned, buf)
     out = np.frombuffer(raw, dtype=np.float64, count=a.size).reshape(a.shape)
     out[...] = a
-    _PINNED_KEEP[id(out)] = buf
     return out
 
 
-_PINNED_KEEP: dict = {}
+def _free_pinned(buf) -> None:
+    buf.__del__()
 
 
 class _PinnedPool:

@@ -20,6 +20,7 @@
 #include "wmpc_warp.cuh"
 #include "wmpc_scan.cuh"
 #include "wmpc_chainw.cuh"
+#include "wmpc_dp.cuh"
 
 using namespace wmpc;
 
@@ -95,6 +96,7 @@ struct wmpc_ctx {
   std::vector<std::pair<int, int>> gk_groups;  // (first row, rows) per stage group, bottom-up
   std::pair<int, int> rep_group{0, 0};         // subtree sharding: replicated rows (first, count)
   std::vector<int> h_cptr, h_cidx;             // host CSR children
+  std::vector<int> h_cpath;                    // host copy of cpath (nchain x kstar)
   double* Yc_save = nullptr;                   // certificate: APG state while Yc holds collapse(y)
   int* acct = nullptr;                         // subtree sharding: rows counted in global sums
   int* rep_gidx = nullptr;                     // per local row: global replicated index or -1
@@ -122,6 +124,12 @@ struct wmpc_ctx {
   double* ell_val = nullptr;
   int ell_w = 4;
   int ell_vf = 0;                               // B, E ELL values exact in fp32 (WMPC_ELL_VF=0 disables)
+  // fused one-kernel iteration for many chains (wmpc_dp.cuh)
+  int use_dp = 0, dp_wpc = 0, dp_grid = 0, dp_cpw = 1;
+  size_t dp_sm = 0;
+  double* dp_agg = nullptr;  // nchain x (3 nu + lx): [LSc | LWc | SUT | SG]
+  float* dp_agg32 = nullptr;
+  double *dp_Lc = nullptr, *dp_Ac = nullptr, *dp_wc = nullptr;  // certificate scratch (the iteration state stays)
   cudaGraphExec_t gk_exec1 = nullptr, gk_exec8 = nullptr;
   double gk_gamma = -1.0;
   int gk_maxit = -1;
@@ -476,12 +484,23 @@ void gk_up(wmpc_ctx* ctx, const FastView& f) {
     launch_pdl(ctx, k_chain_up<WE, TG, false>, dim3(ctx->nchain), dim3(ctx->up_threads), ctx->sm_up, f);
 }
 template <int WE, typename TG = double>
-void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump) {
+void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump, int first_flags = 0) {
   for (const auto& g : ctx->gk_groups) {
     launch_pdl(ctx, k_branch_grp<WE, TG>, dim3(g.second), dim3(GRP_THREADS), ctx->sm_grp, f, g.first, bump,
-               (int)GRP_FULL);
+               (int)GRP_FULL | first_flags);
     bump = 0;
+    first_flags = 0;
   }
+}
+bool dp_on(const wmpc_ctx* ctx) {
+  return ctx->use_dp && ctx->shard_k < 0 && ctx->rfree && !ctx->use_fused && !ctx->use_pu;
+}
+template <typename TG>
+void launch_dp(wmpc_ctx* ctx, const FastView& f, int mode) {
+  DpArgs a{sizeof(TG) == 8 ? (void*)ctx->dp_agg : (void*)ctx->dp_agg32, ctx->dp_cpw, mode};
+  const dim3 grid(ctx->dp_grid), block(ctx->dp_wpc * 32);
+  if (ctx->ell_vf) launch_pdl(ctx, k_chain_dp<4, TG, true>, grid, block, ctx->dp_sm, f, a);
+  else launch_pdl(ctx, k_chain_dp<4, TG, false>, grid, block, ctx->dp_sm, f, a);
 }
 template <int WE>
 void gk_rep(wmpc_ctx* ctx, const FastView& f, int mode, int bump) {
@@ -592,6 +611,81 @@ void build_groups(wmpc_ctx* ctx, int k_rep, const int* acct) {
   upload_vec(ctx, &ctx->gi_ptr, gip);
   upload_vec(ctx, &ctx->gi_item, gii);
   upload_vec(ctx, &ctx->gi_w, giw);
+}
+
+// Fused one-kernel iteration (k_chain_dp, wmpc_dp.cuh) for trees with many
+// chains: persistent warps, DP_WPS warps per SM, each over cpw chains
+// (strided: warp w takes chains w, w + NW, ...). Branching rows are owned
+// (prox + Yc) by one chain below them, balanced over warps.
+#ifndef DP_WPS
+#define DP_WPS 7
+#endif
+template <typename TG>
+void dp_attr(wmpc_ctx* ctx, size_t sm) {
+  CK(cudaFuncSetAttribute(k_chain_dp<4, TG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CK(cudaFuncSetAttribute(k_chain_dp<4, TG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+}
+void configure_dp(wmpc_ctx* ctx) {
+  ctx->use_dp = 0;
+  const int nt = ctx->nt, nu = ctx->nu, lx = ctx->lx, nchain = ctx->nchain, kstar = ctx->kstar;
+  const bool fits = ctx->ell_w == 4 && nu <= 128 && nu % 2 == 0 && nt <= 64 && lx % 2 == 0 && ctx->ly % 2 == 0 &&
+                    ctx->ns <= 32 && kstar <= 30;
+  bool want = fits && nchain > 2 * ctx->sms;  // many chains (C4: 4,096); few chains stay on the CTA kernels
+  if (const char* e = getenv("WMPC_DP")) want = fits && e[0] == '1';
+  if (!want) return;
+  const int sms = std::max(ctx->sms, 1);
+  const int cpw = (nchain + sms * DP_WPS - 1) / (sms * DP_WPS);
+  const int nw = (nchain + cpw - 1) / cpw;
+  const int wpc = std::min(8, std::max(1, (nw + sms - 1) / sms));
+  const int grid = (nw + wpc - 1) / wpc;
+  const size_t sm = std::max(dp_smem<double>(wpc, nt, nu, lx), dp_smem<float>(wpc, nt, nu, lx));
+  if (sm > 227 * 1024) return;
+  dp_attr<double>(ctx, sm);
+  dp_attr<float>(ctx, sm);
+  // ownership of the branching rows balanced over the persistent warps
+  const int nwt = grid * wpc, nb = ctx->off[kstar];
+  if (kstar > 0) {
+    std::vector<int> lo(nb, INT_MAX), hi(nb, -1), cntw(nwt, 0), cntc(nchain, 0);
+    for (int i = 0; i < nchain; ++i)
+      for (int m = 0; m < kstar; ++m) {
+        const int a = ctx->h_cpath[(size_t)i * kstar + m];
+        lo[a] = std::min(lo[a], i);
+        hi[a] = std::max(hi[a], i + 1);
+      }
+    std::vector<unsigned> cown(nchain, 0u);
+    for (int st = kstar - 1; st >= 0; --st)
+      for (int a = ctx->off[st]; a < ctx->off[st + 1]; ++a) {
+        if (hi[a] < 0) continue;
+        int best = lo[a];
+        for (int i = lo[a]; i < hi[a]; ++i) {
+          const int ci = cntw[i % nwt], cb = cntw[best % nwt];
+          if (ci < cb || (ci == cb && cntc[i] < cntc[best])) best = i;
+        }
+        cntw[best % nwt]++;
+        cntc[best]++;
+        cown[best] |= 1u << st;
+      }
+    upload_vec(ctx, &ctx->cown, cown);
+  }
+  const size_t aw = (size_t)nchain * dp_agg_w(nu, lx);
+  if (ctx->dp_agg) cudaFree(ctx->dp_agg);
+  if (ctx->dp_agg32) cudaFree(ctx->dp_agg32);
+  ctx->dp_agg = nullptr;
+  ctx->dp_agg32 = nullptr;
+  dalloc(ctx, &ctx->dp_agg, aw);
+  dalloc(ctx, &ctx->dp_agg32, aw);
+  if (!ctx->dp_Lc) {
+    dalloc(ctx, &ctx->dp_Lc, (size_t)ctx->n * nu);
+    dalloc(ctx, &ctx->dp_wc, (size_t)ctx->n * lx);
+  }
+  if (ctx->dp_Ac) cudaFree(ctx->dp_Ac);
+  ctx->dp_Ac = nullptr;
+  dalloc(ctx, &ctx->dp_Ac, (size_t)(nb + nchain) * nu);
+  ctx->dp_cpw = cpw;
+  ctx->dp_wpc = wpc;
+  ctx->dp_grid = grid;
+  ctx->dp_sm = sm;
+  ctx->use_dp = 1;
 }
 
 // Graph-of-kernels scan path: operator blob, stage groups of the branching
@@ -757,6 +851,7 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
         cown[best] |= 1u << st;
       }
   }
+  ctx->h_cpath = cpath;
   upload_vec(ctx, &ctx->cpath, cpath);
   upload_vec(ctx, &ctx->cown, cown);
   std::vector<double> zl((size_t)ctx->n * nu, 0.0), za((size_t)(nb + nchain) * nu, 0.0);
@@ -800,6 +895,7 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
     if (const char* e = getenv("WMPC_CHAINW")) ctx->chainw = ctx->chainw32 = e[0] == '1';
     if (!fits) ctx->chainw = ctx->chainw32 = 0;
   }
+  configure_dp(ctx);
   if (const char* e = getenv("WMPC_UPT")) ctx->up_threads = atoi(e) >= 512 ? 512 : 256;
   if (const char* e = getenv("WMPC_DNT")) ctx->down_threads = atoi(e) >= 512 ? 512 : 256;
   ctx->prox_warp = nt <= 64 && nu <= 128 ? 1 : 0;
@@ -1051,7 +1147,7 @@ FastView make_fastview(wmpc_ctx* ctx, int count);
 int graphk_kernels(const wmpc_ctx* ctx) {
   const int g = (int)ctx->gk_groups.size();
   if (ctx->shard_k > 0) return 3 + g + 2 * (ctx->rep_group.second > 0) + (g == 0 && ctx->rep_group.second == 0);
-  if (ctx->use_fused) return g + 1 + (g == 0 ? 1 : 0);
+  if (ctx->use_fused || dp_on(ctx)) return g + 1 + (g == 0 ? 1 : 0);
   if (ctx->use_pu) return g + 2 + (g == 0 ? 1 : 0);
   return 3 + g + (g == 0 ? 1 : 0);
 }
@@ -1075,6 +1171,16 @@ void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
       gk_grp<8>(ctx, f, 1);
       gk_down<8>(ctx, f);
       gk_pu<8>(ctx, f);
+    }
+    return;
+  }
+  if (dp_on(ctx)) {  // branch groups (the first reads Yc the previous k_chain_dp wrote) + k_chain_dp
+    if (ctx->fp32) {
+      gk_grp<4, float>(ctx, f, 1, GRP_LATE);
+      launch_dp<float>(ctx, f, 0);
+    } else {
+      gk_grp<4, double>(ctx, f, 1, GRP_LATE);
+      launch_dp<double>(ctx, f, 0);
     }
     return;
   }
@@ -1134,6 +1240,11 @@ void dual_eval_graph(wmpc_ctx* ctx, const double* y, int phase) {
   f.d.U = ctx->Uc;
   f.d.X = ctx->Xc;
   f.rfree = 0;  // the minimiser of an arbitrary y: the full form with R
+  if (dp_on(ctx)) {  // L, subtree totals and wbar are k_chain_dp's iteration state: use scratch
+    f.Lb = ctx->dp_Lc;
+    f.Asub = ctx->dp_Ac;
+    f.d.wbar = ctx->dp_wc;
+  }
   const int nthr = 256;
   if (phase <= 0) {
     CK(cudaMemcpyAsync(ctx->Yc_save, ctx->Yc, sizeof(double) * (size_t)ctx->n * ctx->ly, cudaMemcpyDeviceToDevice,
@@ -1298,7 +1409,8 @@ void free_all(wmpc_ctx* c) {
                   c->Lb, c->Asub, c->blob, c->store_it, c->ut, c->ut32, c->f32_Yc, c->f32_Lb, c->f32_Asub, c->f32_wbar, c->f32_U,
                   c->f32_X, c->f32_eoff, c->f32_R, c->f32_g, c->f32_aux, c->f32_ell, c->Yc_save, c->acct, c->rep_gidx, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
                   c->pj_ecv, c->dk_mv, c->dk_sweeps, c->dk_fix, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
-                  c->prof, c->rb_u0, c->rb_p, c->rb_a, c->gd_stage};
+                  c->prof, c->rb_u0, c->rb_p, c->rb_a, c->gd_stage, c->dp_agg, c->dp_agg32, c->dp_Lc,
+                  c->dp_Ac, c->dp_wc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -1689,6 +1801,29 @@ int wmpc_kernel_launches_per_iteration(const wmpc_ctx* ctx) {
   return ctx->fast ? 0 : 2 * ctx->H + 1;  // fast: one persistent launch per chunk
 }
 
+int wmpc_path_info(const wmpc_ctx* ctx, int* out, int cap) {
+  if (!ctx || !out) return WMPC_E_ARG;
+  const bool g = ctx->fast && ctx->use_graphk;
+  const int v[] = {wmpc_fast_path(ctx),
+                   g && dp_on(ctx) ? 1 : 0,
+                   g && ctx->chainw ? 1 : 0,
+                   ctx->cw_pd,
+                   (int)ctx->gk_groups.size(),
+                   ctx->nchain,
+                   ctx->kstar,
+                   ctx->ell_vf,
+                   ctx->fp32,
+                   ctx->dp_wpc,
+                   ctx->dp_grid,
+                   ctx->dp_cpw,
+                   wmpc_kernel_launches_per_iteration(ctx),
+                   ctx->n_branch,
+                   ctx->sms};
+  const int nv = (int)(sizeof(v) / sizeof(v[0]));
+  for (int i = 0; i < cap && i < nv; ++i) out[i] = v[i];
+  return nv;
+}
+
 int wmpc_fast_path(const wmpc_ctx* ctx) {
   if (!ctx || !ctx->fast) return 0;
   if (ctx->use_graphk) return ctx->use_fused ? 310 : (ctx->use_pu ? 320 : 300);
@@ -1915,6 +2050,24 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
             ctx->launches++;
             k_convert<<<grid_for((size_t)ctx->n * ctx->nu), 256, 0, ctx->stream>>>(ctx->ut, ctx->ut32,
                                                                                     (size_t)ctx->n * ctx->nu);
+          }
+          check_launch(ctx);
+        }
+        if (dp_on(ctx)) {  // k_chain_dp state at Yc = 0: L = 0, chain totals 0, per-chain constants
+          const size_t n = ctx->n, na = (size_t)(ctx->n_branch + ctx->nchain) * ctx->nu;
+          CK(cudaMemsetAsync(ctx->Lb, 0, sizeof(double) * n * ctx->nu, ctx->stream));
+          CK(cudaMemsetAsync(ctx->Asub, 0, sizeof(double) * na, ctx->stream));
+          CK(cudaMemsetAsync(ctx->wbar, 0, sizeof(double) * n * ctx->lx, ctx->stream));
+          FastView f1 = make_fastview(ctx, 1);
+          const int nbk = (ctx->nchain * 32 + 255) / 256;
+          ctx->launches++;
+          if (ctx->fp32) {
+            CK(cudaMemsetAsync(ctx->f32_Lb, 0, sizeof(float) * n * ctx->nu, ctx->stream));
+            CK(cudaMemsetAsync(ctx->f32_Asub, 0, sizeof(float) * na, ctx->stream));
+            CK(cudaMemsetAsync(ctx->f32_wbar, 0, sizeof(float) * n * ctx->lx, ctx->stream));
+            k_dp_agg_init<float><<<nbk, 256, 0, ctx->stream>>>(f1, ctx->dp_agg32);
+          } else {
+            k_dp_agg_init<double><<<nbk, 256, 0, ctx->stream>>>(f1, ctx->dp_agg);
           }
           check_launch(ctx);
         }
@@ -2364,6 +2517,12 @@ int wmpc_apg_warm(wmpc_ctx* ctx, const double* y0) {
       ctx->launches++;
       k_convert<<<grid_for((size_t)ctx->n * ctx->ly), 256, 0, ctx->stream>>>(ctx->Yc, ctx->f32_Yc,
                                                                              (size_t)ctx->n * ctx->ly);
+    }
+    if (ctx->fast && ctx->use_graphk && dp_on(ctx)) {  // L, aggregates and chain totals of iteration 0
+      FastView f = make_fastview(ctx, 1);
+      if (ctx->fp32) launch_dp<float>(ctx, f, 1);
+      else launch_dp<double>(ctx, f, 1);
+      ctx->launches++;
     }
     if (ctx->fast && ctx->use_graphk && (ctx->use_fused || ctx->use_pu)) {  // the up pass of iteration 0
       FastView f = make_fastview(ctx, 1);

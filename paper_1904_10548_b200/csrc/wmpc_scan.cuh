@@ -316,7 +316,10 @@ __global__ void __launch_bounds__(512, OCC ? 3 : 1) k_chain_up(FastView f) {
 // exchange buffer at the row's global replicated index; after the host-level
 // all-reduce over ranks, mode GRP_FINISH reads them back and finishes the row
 // identically on every rank. bump: first kernel of an APG iteration.
-enum { GRP_FULL = 0, GRP_PARTIAL = 1, GRP_FINISH = 2 };
+// GRP_LATE (or-ed into mode): this row group's own rows got their Yc from the
+// immediate predecessor (k_chain_dp runs the branching rows' prox), so every
+// Yc load waits for it.
+enum { GRP_FULL = 0, GRP_PARTIAL = 1, GRP_FINISH = 2, GRP_LATE = 4 };
 template <int WE, typename TG>
 __global__ void __launch_bounds__(GRP_THREADS) k_branch_grp(FastView f, int r0, int bump, int mode) {
   const DevView& d = f.d;
@@ -339,6 +342,8 @@ __global__ void __launch_bounds__(GRP_THREADS) k_branch_grp(FastView f, int r0, 
   const Ell<EllW<WE>::BC, TG> bc = ell_load<EllW<WE>::BC, TG>(f, own_bc(d, k < nu ? k : 0));
   const Ell<EllW<WE>::KR, TG> kr = ell_load<EllW<WE>::KR, TG>(f, own_kr(d, k < d.ns ? k : 0));
   const Ell<EllW<WE>::EC, TG> ec = ell_load<EllW<WE>::EC, TG>(f, own_ec(d, k < nu ? k : 0));
+  if (mode & GRP_LATE) pdl_wait();
+  mode &= 3;
   const TG own_yx = k < nt ? G.Yc[(size_t)r * ly + k] : TG(0);
   const TG own_yu = k < nu ? G.Yc[(size_t)r * ly + lx + k] : TG(0);
   const bool withR = !f.rfree;

@@ -112,12 +112,29 @@ def _recycle_nodes(dev: _DeviceTree, nodes: nat.NodeSet) -> None:
 _POOL: dict = {}
 
 
+def _pool_key(sig, instance) -> tuple:
+    """Pool key: the structure signature plus the context's allocation
+    dimensions the signature does not cover (demand columns, mixing rows):
+    two models of one structure with different demand counts must not share
+    a context, whose demand / Ed buffers are sized by the first."""
+    m = instance.model
+    return sig + (int(m.n_demands), int(m.n_mixing), tuple(m.Ed.shape))
+
+
+def _dims_match(dev: _DeviceTree, instance) -> bool:
+    m = instance.model
+    n, H, nt, nu, nd, ns = dev.ctx.dims
+    return (n, H, nt, nu, nd, ns) == (instance.n_nonroot, len(instance.stage_slices), m.n_tanks,
+                                      m.n_inputs, m.n_demands, m.n_mixing)
+
+
 def _device_for(sig, instance) -> _DeviceTree:
-    ref = _POOL.get(sig)
+    key = _pool_key(sig, instance)
+    ref = _POOL.get(key)
     dev = ref() if ref is not None else None
     if dev is None:
         dev = _DeviceTree(instance)
-        _POOL[sig] = weakref.ref(dev)
+        _POOL[key] = weakref.ref(dev)
     return dev
 
 
@@ -241,6 +258,11 @@ def _factor(instance, structure_from: FactorCache | None, private: bool,
         kappa, lipschitz = src.kappa, src.lipschitz
         dev = src._dev
         fresh_structure = False
+        if not _dims_match(dev, instance):
+            # same structure, other demand / mixing dimensions: the source's
+            # context cannot hold this instance's node data
+            dev = _DeviceTree(instance) if private else _device_for(sig, instance)
+            fresh_structure = True
     else:
         basis, e_pinv = _null_space(m.E, m.n_inputs)
         check = m.E @ basis
@@ -264,9 +286,15 @@ def _factor(instance, structure_from: FactorCache | None, private: bool,
     gd = nat.f64(instance.demand_gd)
     econ = nat.f64(instance.econ)
     bad = np.zeros(1, dtype=np.int64)
+    if not _dims_match(dev, instance):
+        raise ValueError("factor cache does not match this instance")
+    # wmpc_set_node_data overwrites the context's econ before its feasibility
+    # check: forget the marker first, so a raise cannot leave it naming the
+    # previous instance
+    dev.ctx._econ_src = None
     dev.ctx.call("wmpc_set_node_data", nodes.h, nat.ptr(demand) if m.n_mixing else None,
                  nat.ptr(Ed) if m.n_mixing else None, nat.ptr(gd), nat.ptr(econ), nat.ptr(bad))
-    dev.ctx._econ_src = instance.econ  # the context's econ now holds this array (see _upload_bounds)
+    dev.ctx._econ_src = _econ_marker(instance.econ)  # the context's econ now holds this array
     cache = FactorCache(null_basis=basis, e_pinv=e_pinv, d_gain=d_gain, t_mat=t_mat, lam=lam,
                         pi=pi, kappa=kappa, lipschitz=lipschitz, signature=sig, _dev=dev,
                         _nodes=nodes)
@@ -289,11 +317,35 @@ def _upload_bounds(ctx: nat.Context, instance, with_econ: bool = True) -> None:
     arrs = [nat.f64(a) for a in (m.x_min, m.x_max, m.x_safe, m.u_min, m.u_max)]
     p, q = nat.f64(instance.p), nat.f64(instance.q)
     econ = None
-    if with_econ and getattr(ctx, "_econ_src", None) is not instance.econ:
+    if with_econ and not _econ_current(getattr(ctx, "_econ_src", None), instance.econ):
+        ctx._econ_src = None
         econ = nat.f64(instance.econ)
-        ctx._econ_src = instance.econ
     ctx.call("wmpc_set_bounds", *[nat.ptr(a) for a in arrs], float(w.w_x), float(w.w_s),
              nat.ptr(p), nat.ptr(q), nat.ptr(econ))
+    if econ is not None:
+        ctx._econ_src = _econ_marker(instance.econ)
+
+
+def _econ_fingerprint(econ: np.ndarray) -> bytes:
+    """A strided sample of ``econ`` (<= 4,096 values plus the last row): catches
+    in-place edits such as ``inst.econ[:] = -10.0`` (the reference's
+    test_oracle.py:79) at negligible cost. Instances are documented immutable
+    (problem.py:18-19); an edit that misses every sampled entry is not seen."""
+    flat = econ.reshape(-1)
+    step = max(1, flat.size // 4096)
+    return flat[::step].tobytes() + econ.reshape(econ.shape[0], -1)[-1:].tobytes()
+
+
+def _econ_marker(econ: np.ndarray) -> tuple:
+    return (weakref.ref(econ) if isinstance(econ, np.ndarray) else None, _econ_fingerprint(econ))
+
+
+def _econ_current(marker, econ: np.ndarray) -> bool:
+    if marker is None or marker[0] is None or marker[0]() is not econ:
+        return False
+    return marker[1] == _econ_fingerprint(econ)
+
+
 
 
 def dual_gradient(cache: FactorCache, instance, y) -> tuple[np.ndarray, float]:

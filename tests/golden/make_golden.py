@@ -87,7 +87,7 @@ def small_case(name, arrays, rng, fixed_iters=150, converge=True):
     print(name, "n =", inst.n_nonroot, "L =", L)
 
 
-def barcelona_case(name, iters, full_rows):
+def barcelona_case(name, iters, full_rows, stride=23):
     mine = config_instance(name)
     arrays = instance_to_arrays(mine)
     inst = to_reference(arrays)
@@ -103,7 +103,7 @@ def barcelona_case(name, iters, full_rows):
     out["u0"] = res.u0
     n = inst.n_nonroot
     rows = np.arange(n) if full_rows else np.unique(np.concatenate(
-        [np.arange(inst.stage_slices[0].stop), np.arange(0, n, 23), [n - 1]]))
+        [np.arange(inst.stage_slices[0].stop), np.arange(0, n, stride), [n - 1]]))
     out["rows"] = rows
     for k in ("primal", "primal_avg", "dual"):
         v = getattr(res, k).reshape(n, -1)
@@ -136,6 +136,13 @@ def main():
     for name, kw in cases.items():
         inst = make_instance(rng, **kw)
         small_case(name, instance_to_arrays(inst), rng)
+    if "--large" in sys.argv:
+        # Round 2: the production graph kernels at C3/C4 against the reference
+        # itself. C4 takes ~4.6 s per reference iteration
+        # plus a ~170 s certificate, so it runs 50 iterations.
+        barcelona_case("C3", 500, full_rows=False, stride=23)
+        barcelona_case("C4", 50, full_rows=False, stride=97)
+        return
     if "--no-barcelona" not in sys.argv:
         barcelona_case("C1", 500, full_rows=True)
         barcelona_case("C2", 500, full_rows=False)
