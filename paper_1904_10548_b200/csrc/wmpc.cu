@@ -22,6 +22,10 @@
 #include "wmpc_chainw.cuh"
 #include "wmpc_dp.cuh"
 
+// k_chain_dp's instantiated network shape (the Barcelona-dimension network of
+// BASELINE.json; other shapes run the graph path)
+constexpr int DP_NT = 63, DP_NU = 114;
+
 using namespace wmpc;
 
 static thread_local std::string g_global_err;
@@ -127,8 +131,10 @@ struct wmpc_ctx {
   // fused one-kernel iteration for many chains (wmpc_dp.cuh)
   int use_dp = 0, dp_wpc = 0, dp_grid = 0, dp_cpw = 1;
   size_t dp_sm = 0;
-  double* dp_agg = nullptr;  // nchain x (3 nu + lx): [LSc | LWc | SUT | SG]
+  double* dp_agg = nullptr;  // nchain x (3 nu + lx): [LSc | LWc | SUTp | SGp]
   float* dp_agg32 = nullptr;
+  double* dp_putg = nullptr;  // n_branch x (nu + lx): root-path prefixes [PUT | PG]
+  float* dp_putg32 = nullptr;
   double *dp_Lc = nullptr, *dp_Ac = nullptr, *dp_wc = nullptr;  // certificate scratch (the iteration state stays)
   cudaGraphExec_t gk_exec1 = nullptr, gk_exec8 = nullptr;
   double gk_gamma = -1.0;
@@ -492,15 +498,16 @@ void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump, int first_flags = 0) {
     first_flags = 0;
   }
 }
+// fp64 only: in fp32 mode the four-kernel graph measured faster (C4 200 vs 258 us)
 bool dp_on(const wmpc_ctx* ctx) {
-  return ctx->use_dp && ctx->shard_k < 0 && ctx->rfree && !ctx->use_fused && !ctx->use_pu;
+  return ctx->use_dp && !ctx->fp32 && ctx->shard_k < 0 && ctx->rfree && !ctx->use_fused && !ctx->use_pu;
 }
 template <typename TG>
-void launch_dp(wmpc_ctx* ctx, const FastView& f, int mode) {
-  DpArgs a{sizeof(TG) == 8 ? (void*)ctx->dp_agg : (void*)ctx->dp_agg32, ctx->dp_cpw, mode};
+void launch_dp(wmpc_ctx* ctx, const FastView& f) {
+  DpArgs a{sizeof(TG) == 8 ? (void*)ctx->dp_agg : (void*)ctx->dp_agg32,
+           sizeof(TG) == 8 ? (const void*)ctx->dp_putg : (const void*)ctx->dp_putg32, ctx->dp_cpw};
   const dim3 grid(ctx->dp_grid), block(ctx->dp_wpc * 32);
-  if (ctx->ell_vf) launch_pdl(ctx, k_chain_dp<4, TG, true>, grid, block, ctx->dp_sm, f, a);
-  else launch_pdl(ctx, k_chain_dp<4, TG, false>, grid, block, ctx->dp_sm, f, a);
+  launch_pdl(ctx, k_chain_dp<DP_NT, DP_NU, TG>, grid, block, ctx->dp_sm, f, a);
 }
 template <int WE>
 void gk_rep(wmpc_ctx* ctx, const FastView& f, int mode, int bump) {
@@ -622,21 +629,21 @@ void build_groups(wmpc_ctx* ctx, int k_rep, const int* acct) {
 #endif
 template <typename TG>
 void dp_attr(wmpc_ctx* ctx, size_t sm) {
-  CK(cudaFuncSetAttribute(k_chain_dp<4, TG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  CK(cudaFuncSetAttribute(k_chain_dp<4, TG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CK(cudaFuncSetAttribute(k_chain_dp<DP_NT, DP_NU, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
 }
 void configure_dp(wmpc_ctx* ctx) {
   ctx->use_dp = 0;
   const int nt = ctx->nt, nu = ctx->nu, lx = ctx->lx, nchain = ctx->nchain, kstar = ctx->kstar;
-  const bool fits = ctx->ell_w == 4 && nu <= 128 && nu % 2 == 0 && nt <= 64 && lx % 2 == 0 && ctx->ly % 2 == 0 &&
-                    ctx->ns <= 32 && kstar <= 30;
-  bool want = fits && nchain > 2 * ctx->sms;  // many chains (C4: 4,096); few chains stay on the CTA kernels
+  const bool fits = ctx->ell_w == 4 && nt == DP_NT && nu == DP_NU && ctx->ns <= 32 && kstar <= 30;
+  // many chains per SM (C4: 4,096 chains, 27.7 per SM: 236 vs 256 us per iteration); at C3 (512 chains,
+  // 3.5 per SM) one warp per chain is latency-bound (116 vs 52 us): the graph path stays
+  bool want = fits && nchain >= 8 * ctx->sms;
   if (const char* e = getenv("WMPC_DP")) want = fits && e[0] == '1';
   if (!want) return;
   const int sms = std::max(ctx->sms, 1);
   const int cpw = (nchain + sms * DP_WPS - 1) / (sms * DP_WPS);
   const int nw = (nchain + cpw - 1) / cpw;
-  const int wpc = std::min(8, std::max(1, (nw + sms - 1) / sms));
+  const int wpc = std::min(DP_MAXT / 32, std::max(1, (nw + sms - 1) / sms));
   const int grid = (nw + wpc - 1) / wpc;
   const size_t sm = std::max(dp_smem<double>(wpc, nt, nu, lx), dp_smem<float>(wpc, nt, nu, lx));
   if (sm > 227 * 1024) return;
@@ -674,6 +681,12 @@ void configure_dp(wmpc_ctx* ctx) {
   ctx->dp_agg32 = nullptr;
   dalloc(ctx, &ctx->dp_agg, aw);
   dalloc(ctx, &ctx->dp_agg32, aw);
+  if (ctx->dp_putg) cudaFree(ctx->dp_putg);
+  if (ctx->dp_putg32) cudaFree(ctx->dp_putg32);
+  ctx->dp_putg = nullptr;
+  ctx->dp_putg32 = nullptr;
+  dalloc(ctx, &ctx->dp_putg, (size_t)std::max(nb, 1) * (nu + lx));
+  dalloc(ctx, &ctx->dp_putg32, (size_t)std::max(nb, 1) * (nu + lx));
   if (!ctx->dp_Lc) {
     dalloc(ctx, &ctx->dp_Lc, (size_t)ctx->n * nu);
     dalloc(ctx, &ctx->dp_wc, (size_t)ctx->n * lx);
@@ -1177,10 +1190,10 @@ void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
   if (dp_on(ctx)) {  // branch groups (the first reads Yc the previous k_chain_dp wrote) + k_chain_dp
     if (ctx->fp32) {
       gk_grp<4, float>(ctx, f, 1, GRP_LATE);
-      launch_dp<float>(ctx, f, 0);
+      launch_dp<float>(ctx, f);
     } else {
       gk_grp<4, double>(ctx, f, 1, GRP_LATE);
-      launch_dp<double>(ctx, f, 0);
+      launch_dp<double>(ctx, f);
     }
     return;
   }
@@ -1409,7 +1422,7 @@ void free_all(wmpc_ctx* c) {
                   c->Lb, c->Asub, c->blob, c->store_it, c->ut, c->ut32, c->f32_Yc, c->f32_Lb, c->f32_Asub, c->f32_wbar, c->f32_U,
                   c->f32_X, c->f32_eoff, c->f32_R, c->f32_g, c->f32_aux, c->f32_ell, c->Yc_save, c->acct, c->rep_gidx, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
                   c->pj_ecv, c->dk_mv, c->dk_sweeps, c->dk_fix, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
-                  c->prof, c->rb_u0, c->rb_p, c->rb_a, c->gd_stage, c->dp_agg, c->dp_agg32, c->dp_Lc,
+                  c->prof, c->rb_u0, c->rb_p, c->rb_a, c->gd_stage, c->dp_agg, c->dp_agg32, c->dp_putg, c->dp_putg32, c->dp_Lc,
                   c->dp_Ac, c->dp_wc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -2059,15 +2072,15 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
           CK(cudaMemsetAsync(ctx->Asub, 0, sizeof(double) * na, ctx->stream));
           CK(cudaMemsetAsync(ctx->wbar, 0, sizeof(double) * n * ctx->lx, ctx->stream));
           FastView f1 = make_fastview(ctx, 1);
-          const int nbk = (ctx->nchain * 32 + 255) / 256;
+          const int nbk = ((ctx->nchain + ctx->n_branch) * 32 + 255) / 256;
           ctx->launches++;
           if (ctx->fp32) {
             CK(cudaMemsetAsync(ctx->f32_Lb, 0, sizeof(float) * n * ctx->nu, ctx->stream));
             CK(cudaMemsetAsync(ctx->f32_Asub, 0, sizeof(float) * na, ctx->stream));
             CK(cudaMemsetAsync(ctx->f32_wbar, 0, sizeof(float) * n * ctx->lx, ctx->stream));
-            k_dp_agg_init<float><<<nbk, 256, 0, ctx->stream>>>(f1, ctx->dp_agg32);
+            k_dp_agg_init<float><<<nbk, 256, 0, ctx->stream>>>(f1, ctx->dp_agg32, ctx->dp_putg32);
           } else {
-            k_dp_agg_init<double><<<nbk, 256, 0, ctx->stream>>>(f1, ctx->dp_agg);
+            k_dp_agg_init<double><<<nbk, 256, 0, ctx->stream>>>(f1, ctx->dp_agg, ctx->dp_putg);
           }
           check_launch(ctx);
         }
@@ -2519,10 +2532,16 @@ int wmpc_apg_warm(wmpc_ctx* ctx, const double* y0) {
                                                                              (size_t)ctx->n * ctx->ly);
     }
     if (ctx->fast && ctx->use_graphk && dp_on(ctx)) {  // L, aggregates and chain totals of iteration 0
-      FastView f = make_fastview(ctx, 1);
-      if (ctx->fp32) launch_dp<float>(ctx, f, 1);
-      else launch_dp<double>(ctx, f, 1);
-      ctx->launches++;
+      FastView f = make_fastview(ctx, 1);  // the up pass of Yc(0) (R-free), then the L aggregates
+      const int nbk = (ctx->nchain * 32 + 255) / 256;
+      if (ctx->fp32) {
+        gk_up<4, float>(ctx, f);
+        k_dp_agg_L<float><<<nbk, 256, 0, ctx->stream>>>(f, ctx->dp_agg32);
+      } else {
+        gk_up<4, double>(ctx, f);
+        k_dp_agg_L<double><<<nbk, 256, 0, ctx->stream>>>(f, ctx->dp_agg);
+      }
+      ctx->launches += 2;
     }
     if (ctx->fast && ctx->use_graphk && (ctx->use_fused || ctx->use_pu)) {  // the up pass of iteration 0
       FastView f = make_fastview(ctx, 1);

@@ -26,198 +26,288 @@
 // rounding differs (parity is checked against the reference at 1e-8, the
 // north_star's tolerance, not bit-for-bit against the unfused kernels).
 //
-// Ancestor rows (branching stages) are walked top-down first, as in
-// k_chain_down_r; the one chain that owns a branching row (cown, balanced per
-// warp on the host) runs its prox and writes its Yc for the branch-group
-// kernels of the next iteration. The kernel is persistent over chains: warp w
-// handles chains w, w + NW, w + 2 NW, ...
+// The same aggregation covers the kb ancestor rows (branching stages): with
+// W_anc = sum_{m < kb} ls_m and the per-solve path constants SUTp / SGp (sums
+// of ut / g over the chain's whole root path),
+//   x_{N-1} = p + B (SUTp - P (W_anc + N LS_anc + LWc)) + SGp,
+// so an ancestor row costs one L-row read (L2) and two vector adds, not a
+// projector; the one chain that owns a branching row (cown, balanced per warp
+// on the host) also computes that row's u, x (from the per-branch-row path
+// prefixes PUT / PG) and runs its prox, writing its Yc for the branch-group
+// kernels of the next iteration. The kernel is persistent: warp w takes chains
+// w, w + NW, w + 2 NW, ...
 //
-// Per warp, a ring of DP_D stages [L | ut | g | y | y_prev | Ua | Xa] is filled
-// by cp.async.bulk (one elected lane, one mbarrier per stage, expect_tx); a
-// stage is re-armed as soon as the warp has read it into registers, so loads
-// run DP_D - 1 rows ahead. fp32 mode: L, ut, g, Yc are fp32 (rows not 16-byte
-// multiples, so those three are read with plain loads); the prox operands
-// stay fp64 and go through the ring.
+// Memory: per warp, a DP_D-stage ring of the prox operands [y | y_prev | Ua |
+// Xa] (5.3 KB per row) filled by 16-byte cp.async.cg (L2 -> shared, no
+// registers; released as soon as the row's prox has read it), and L, ut, g
+// one row ahead in registers. 14 warps per SM (the bulk_stream microbenchmark:
+// 12-16 warps per SM with one row in flight each reach the HBM ceiling).
+// fp32 mode: L, ut, g and the aggregates are fp32; the prox operands fp64.
 #pragma once
 #include "wmpc_chainw.cuh"
 
 namespace wmpc {
 
 #ifndef DP_D_N
-#define DP_D_N 3
+#define DP_D_N 2
 #endif
 constexpr int DP_D = DP_D_N;   // ring stages per warp
 constexpr int DP_BND = 448;    // bounds table: xmin 64 | xmax 64 | xsafe 64 | umin 128 | umax 128
 constexpr int DP_XCH = 352;    // per-warp exchange vectors (TG): wb 64 | zb 128 | ub 128 | tb 32
 constexpr int DP_VSLOTS = 22;  // operator value table: bc 8 | ec 4 | kr 4 | br 6 (x 32 lanes)
+#ifndef DP_MAXT
+#define DP_MAXT 256  // up to 8 warps per CTA, one CTA per SM
+#endif
+#ifndef DP_MAXREG
+#define DP_MAXREG 255  // <= 8 warps per SM: 2 per sub-partition, no spills (measured: 7 warps x 224 regs 236 us vs 10 warps x 168 regs (spills) 349 us at C4)
+#endif
 
 struct DpArgs {
-  void* agg;     // nchain x (3 nu + lx), TG: [LSc | LWc | SUT | SG]
-  int cpw;       // chains per warp
-  int mode;      // 0: iteration, 1: up pass only (Yc from memory: warm start)
+  void* agg;         // nchain x (3 nu + lx), TG: [LSc | LWc | SUTp | SGp]
+  const void* putg;  // n_branch x (nu + lx), TG: root-path prefix sums [PUT | PG] of each branching row
+  int cpw;           // chains per warp
 };
 
-__host__ __device__ inline int dp_stage(int nt, int nu, int lx) { return 3 * nu + 2 * lx + 2 * (2 * nt + nu); }
+__host__ __device__ inline int dp_stage(int nt, int nu, int lx) { return 2 * (2 * nt + nu) + nu + lx; }
 __host__ __device__ inline int dp_agg_w(int nu, int lx) { return 3 * nu + lx; }
+// Per-CTA pointer block of k_chain_dp in shared memory: under register
+// pressure the compiler re-reads these from shared memory (short latency)
+// instead of re-loading the bound node-state pointers from global memory.
+template <typename TG>
+struct alignas(16) DpPtrs {
+  const double *yb, *ymb;
+  double *ynb, *Ua, *Xa;
+  TG *Lb, *U, *X, *Yc, *wbar, *Asub, *agg;
+  const TG *UT, *g, *aux, *putg;
+  const int* cpath;
+  const unsigned* cown;
+  int store, pad;
+};
+
+template <typename TG>
+__host__ __device__ inline int dp_stage_t(int nt, int nu, int lx) {  // k_chain_dp's ring stage (doubles)
+  return dp_stage(nt, nu, lx) + (sizeof(TG) == 8 ? 2 * nu + lx + 2 : 0);
+}
 template <typename TG>
 __host__ __device__ inline size_t dp_smem(int wpc, int nt, int nu, int lx) {
-  return sizeof(double) * (DP_BND + (size_t)wpc * DP_D * dp_stage(nt, nu, lx)) + 8 * (size_t)wpc * DP_D +
-         sizeof(TG) * (size_t)wpc * DP_XCH + sizeof(double) * (size_t)wpc * 128 + 8 * DP_VSLOTS * 32 + 16;
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* b) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  asm volatile(
-      "{.reg .pred p; DPW%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra DPW%=;}" ::"r"(
-          smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-// global -> shared bulk copy completing on mbarrier b (bytes % 16 == 0, both 16-byte aligned)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(b))
-      : "memory");
+  return sizeof(double) * (DP_BND + 8 + DP_VSLOTS * 32) + sizeof(DpPtrs<TG>) +
+         (size_t)wpc * (sizeof(double) * (DP_D * (size_t)dp_stage_t<TG>(nt, nu, lx) + 128) + sizeof(TG) * DP_XCH);
 }
 
 template <typename TG>
-__device__ __forceinline__ typename V2T<TG>::T ld2s(const TG* p) {  // shared or global, aligned pair
+__device__ __forceinline__ typename V2T<TG>::T ld2s(const TG* p) {  // aligned pair (shared or global)
   return *reinterpret_cast<const typename V2T<TG>::T*>(p);
 }
+template <typename TG>
+__device__ __forceinline__ typename V2T<TG>::T ld2cg(const TG* p) {  // aligned pair, L2 (predecessor-written data)
+  return __ldcg(reinterpret_cast<const typename V2T<TG>::T*>(p));
+}
+// numpy clip / maximum (numpy/_core _NPY_MIN/_NPY_MAX: NaN x propagates; bounds are never NaN)
+// written with unordered comparisons: one compare and one select per bound
+__device__ __forceinline__ double np_clip_u(double x, double lo, double hi) {
+  const double m = !(x <= lo) ? x : lo;
+  return !(m >= hi) ? m : hi;
+}
+__device__ __forceinline__ double np_max_u(double a, double b) { return !(a < b) ? a : b; }
 
-template <int WE, typename TG, bool VF>
-__global__ void __launch_bounds__(256, 1) k_chain_dp(FastView f, DpArgs A) {
-  using TB = std::conditional_t<VF && sizeof(TG) == 8, float, TG>;  // B, E value storage
-  constexpr bool TMA_DG = sizeof(TG) == 8;  // L, ut, g, aggregates through the ring (fp64 rows are 16-byte multiples)
+// numpy pairwise sum of d2[0..n) (n <= 64) by an 8-lane group: lane8 g sums
+// d2[g], d2[g+8], ... below n - n%8 in order, a 3-level tree, then the tail
+// in order (pw_group8 of wmpc_fast.cuh with the loop bounds of n <= 64).
+__device__ __forceinline__ double pw_group8_64(const double* d2, int n, int lane8, unsigned mask) {
+  if (n < 8) {
+    double res = 0.0;
+    if (lane8 == 0)
+      for (int i = 0; i < n; ++i) res = dadd(res, d2[i]);
+    return res;
+  }
+  const int nb = n - (n % 8);
+  double r = d2[lane8];
+#pragma unroll
+  for (int q = 1; q < 8; ++q)
+    if (8 * q < nb) r = dadd(r, d2[lane8 + 8 * q]);
+  double s = dadd(r, __shfl_down_sync(mask, r, 1, 8));
+  double t = dadd(s, __shfl_down_sync(mask, s, 2, 8));
+  double res = dadd(t, __shfl_down_sync(mask, t, 4, 8));
+  if (lane8 == 0) {
+    double tv[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) tv[q] = nb + q < n ? d2[nb + q] : 0.0;
+#pragma unroll
+    for (int q = 0; q < 7; ++q)
+      if (nb + q < n) res = dadd(res, tv[q]);
+  }
+  return res;
+}
+
+// Compile-time network dimensions (NT tanks, NU flows; the instantiated shape
+// is the Barcelona-dimension 63 / 114 network, other shapes run the graph
+// path): every offset and loop bound is a constant, so no dimension or index
+// is rematerialised under register pressure (the runtime-dimension version
+// spent 30 % of its instructions on that and on runtime copy loops).
+template <int NT, int NU, typename TG>
+__global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
+  static_assert(NT <= 64 && NU <= 128 && NU % 2 == 0 && NU > 64, "lane layout: pairs (2l, 2l+1) and (64+2l, 65+2l)");
+  constexpr int LX = NT + (NT & 1), LY = LX + NU, W = 2 * NT + NU;
+  // stage: [y W | y_prev W | Ua NU | Xa LX] and, in fp64, the chain row's down
+  // operands [L NU | ut NU | g LX | aux 2] (fp32 rows are not 16-byte multiples:
+  // those come through registers one row ahead)
+  constexpr bool SDG = sizeof(TG) == 8;
+  constexpr int oYm = W, oUa = 2 * W, oXa = 2 * W + NU, oL = 2 * W + NU + LX, oB = oL + NU, oG = oB + NU,
+                oAx = oG + LX, STG = SDG ? oAx + 2 : oL;
+  constexpr int AW = 3 * NU + LX, PW = NU + LX;
+  constexpr int WE = 4;
+  constexpr int NB = NT - NT % 8;  // pairwise-sum block part of a tank norm
   const DevView& d = f.d;
-  const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly, W = d.W;
-  const int kb = f.kstar, H = d.H, N = H - kb, S = H + 1;
+  const int kb = f.kstar, N = d.H - kb;
   const int wpc = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int STG = dp_stage(nt, nu, lx), AW = dp_agg_w(nu, lx);
-  const int oL = 0, oB = nu, oG = 2 * nu, oY = 2 * nu + lx, oYm = oY + W, oUa = oYm + W, oXa = oUa + nu;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* bnd = reinterpret_cast<double*>(smem_raw);
-  double* ring_all = bnd + DP_BND;
-  double* ring = ring_all + (size_t)warp * DP_D * STG;
-  uint64_t* mbar_all = reinterpret_cast<uint64_t*>(ring_all + (size_t)wpc * DP_D * STG);
-  uint64_t* mbar = mbar_all + warp * DP_D;
-  TG* xch_all = reinterpret_cast<TG*>(mbar_all + wpc * DP_D);
-  TG* wb = xch_all + (size_t)warp * DP_XCH;  // 64
-  TG* zb = wb + 64;                          // 128
-  TG* ub = zb + 128;                         // 128
-  TG* tb = ub + 128;                         // 32
-  double* sd2_all = reinterpret_cast<double*>(xch_all + (size_t)wpc * DP_XCH);
-  double* sd2 = sd2_all + warp * 128;
-  unsigned char* vtab = reinterpret_cast<unsigned char*>(sd2_all + wpc * 128);
-  const GA<TG> G = ga<TG>(f);
+  double* bnd = reinterpret_cast<double*>(smem_raw);         // DP_BND
+  double* pv = bnd + DP_BND;                                 // 8: gamma, 1/gamma, beta, theta, 1-theta, beta1, w_x, w_s
+  DpPtrs<TG>* PT = reinterpret_cast<DpPtrs<TG>*>(pv + 8);
+  unsigned char* vtab = reinterpret_cast<unsigned char*>(PT + 1);  // DP_VSLOTS x 32 doubles
+  unsigned char* wbase = vtab + 8 * DP_VSLOTS * 32;
+  const size_t wbytes = sizeof(double) * (DP_D * STG + 128) + sizeof(TG) * DP_XCH;
+  double* ring = reinterpret_cast<double*>(wbase + warp * wbytes);
+  double* sd2 = ring + DP_D * STG;  // 128
+  TG* wb = reinterpret_cast<TG*>(sd2 + 128);  // 64
+  TG* zb = wb + 64;                           // 128
+  TG* ub = zb + 128;                          // 128
+  TG* tb = ub + 128;                          // 32
   const int l2 = 2 * lane;
-  const bool ok0 = l2 < nu, ok1 = 64 + l2 < nu, okx = l2 < nt, okx2 = l2 + 1 < nt;
-  const unsigned o1 = ok1 ? 64 + l2 : 0;
+  const bool ok1 = 64 + l2 < NU, okx2 = l2 + 1 < NT;  // ok0 (l2 < NU) and okx (l2 < NT) hold for every lane
+  const int o1 = ok1 ? 64 + l2 : l2;                   // second u pair (a valid in-row offset when absent)
   const unsigned nchain = f.nchain, nbr = f.n_branch;
-  // ---- prologue (overlaps the predecessor under PDL): bounds, operators, barriers
   for (int i = threadIdx.x; i < DP_BND; i += blockDim.x) {
     double v = 0.0;
-    if (i < 64) v = i < nt ? d.xmin[i] : 0.0;
-    else if (i < 128) v = i - 64 < nt ? d.xmax[i - 64] : 0.0;
-    else if (i < 192) v = i - 128 < nt ? d.xsafe[i - 128] : 0.0;
-    else if (i < 320) v = i - 192 < nu ? d.umin[i - 192] : 0.0;
-    else v = i - 320 < nu ? d.umax[i - 320] : 0.0;
+    if (i < 64) v = i < NT ? d.xmin[i] : 0.0;
+    else if (i < 128) v = i - 64 < NT ? d.xmax[i - 64] : 0.0;
+    else if (i < 192) v = i - 128 < NT ? d.xsafe[i - 128] : 0.0;
+    else if (i < 320) v = i - 192 < NU ? d.umin[i - 192] : 0.0;
+    else v = i - 320 < NU ? d.umax[i - 320] : 0.0;
     bnd[i] = v;
   }
   int voff = 0;
-  (void)voff;
-  EllRB<EllW<WE>::BC, TG, TB> bc[4];
-  EllRE<EllW<WE>::EC, TG, TB> ec[4];
+  EllV<EllW<WE>::BC, TG, TG> bc[4];
+  EllV<EllW<WE>::EC, TG, TG> ec[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int k = cw_ku(lane, q);
-    bc[q] = cw_bind<EllRB<EllW<WE>::BC, TG, TB>, TB>(ell_own<EllW<WE>::BC, TG>(f, own_bc(d, k), k < nu), wb, vtab,
-                                                      voff, lane, warp == 0);
-    ec[q] = cw_bind<EllRE<EllW<WE>::EC, TG, TB>, TB>(ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < nu), tb, vtab,
-                                                      voff, lane, warp == 0);
+    bc[q] = ellv_bind<TG>(ell_own<EllW<WE>::BC, TG>(f, own_bc(d, k), k < NU), wb, vtab, voff, lane, warp == 0);
+    ec[q] = ellv_bind<TG>(ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < NU), tb, vtab, voff, lane, warp == 0);
   }
-  const EllRK<EllW<WE>::KR, TG> kr = cw_bind<EllRK<EllW<WE>::KR, TG>, TG>(
-      ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < d.ns), zb, vtab, voff, lane, warp == 0);
-  EllRB<EllW<WE>::BR, TG, TB> br[2];
+  const EllV<EllW<WE>::KR, TG, TG> kr =
+      ellv_bind<TG>(ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < d.ns), zb, vtab, voff, lane, warp == 0);
+  EllV<EllW<WE>::BR, TG, TG> br[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h)
-    br[h] = cw_bind<EllRB<EllW<WE>::BR, TG, TB>, TB>(ell_own<EllW<WE>::BR, TG>(f, own_br(d, l2 + h), l2 + h < nt),
-                                                      ub, vtab, voff, lane, warp == 0);
-  if (lane == 0) {
-    for (int s = 0; s < DP_D; ++s) mbar_init(mbar + s);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
+    br[h] = ellv_bind<TG>(ell_own<EllW<WE>::BR, TG>(f, own_br(d, l2 + h), l2 + h < NT), ub, vtab, voff, lane,
+                          warp == 0);
   pdl_wait();  // L of the branching rows comes from the last group kernel; iter from the first
   pdl_trigger();
-  const bool up_only = A.mode == 1;
-  const ProxIt P = up_only ? ProxIt{} : prox_it(f);
-  const bool next = up_only || P.next;  // the up pass of the next iteration runs
-  const bool store = !up_only && P.it == *f.store_it;
-  const double* yb = up_only ? nullptr : ybuf(d, P.it);
-  const double* ymb = up_only ? nullptr : ybuf(d, P.it + 2);
-  double* ynb = up_only ? nullptr : ybuf_w(d, P.it + 1);
-  TG* agg = reinterpret_cast<TG*>(A.agg);
+  const int it = *d.iter - 1;
+  const bool next = it + 1 < f.max_iter;
+  if (threadIdx.x == 0) {
+    const ProxIt P = prox_it(f);
+    pv[0] = P.gamma; pv[1] = P.ig; pv[2] = P.beta; pv[3] = P.theta; pv[4] = P.om; pv[5] = P.beta1;
+    pv[6] = d.w_x; pv[7] = d.w_s;
+    const GA<TG> G = ga<TG>(f);
+    DpPtrs<TG> t;
+    t.yb = ybuf(d, it); t.ymb = ybuf(d, it + 2); t.ynb = ybuf_w(d, it + 1); t.Ua = d.Ua; t.Xa = d.Xa;
+    t.Lb = G.Lb; t.U = G.U; t.X = G.X; t.Yc = G.Yc; t.wbar = G.wbar; t.Asub = G.Asub;
+    t.agg = reinterpret_cast<TG*>(A.agg);
+    t.UT = sizeof(TG) == 8 ? (const TG*)f.ut : (const TG*)f.ut32;
+    t.g = G.g; t.aux = G.aux; t.putg = reinterpret_cast<const TG*>(A.putg);
+    t.cpath = f.cpath; t.cown = f.cown;
+    t.store = it == *f.store_it;
+    t.pad = 0;
+    *PT = t;
+  }
+  __syncthreads();
   const int gw = blockIdx.x * wpc + warp, nw = gridDim.x * wpc;
-  const int steps = A.cpw * S;
-  // ---- the ring: step i = (chain slot i / S, step s = i % S): s < kb ancestor
-  // row s, s == kb chain aggregates, s > kb chain row t = N - 1 - (s - kb - 1)
-  auto issue = [&](int i) {
-    if (lane != 0 || i >= steps || up_only) return;
-    const int ci = gw + (i / S) * nw;
-    if (ci >= (int)nchain) return;
-    const int s = i % S;
-    double* st = ring + (i % DP_D) * STG;
-    uint64_t* b = mbar + (i % DP_D);
-    unsigned r;
-    bool dg = TMA_DG, px;
-    if (s < kb) {
-      r = (unsigned)f.cpath[(size_t)ci * kb + s];
-      px = (f.cown[ci] >> s) & 1u;
-    } else if (s == kb) {
-      if (TMA_DG) {
-        mbar_expect(b, (unsigned)(AW * 8));
-        bulk_g2s(st, reinterpret_cast<const double*>(agg) + (size_t)ci * AW, AW * 8, b);
-      } else {
-        mbar_expect(b, 0u);
+  // ---- prox-row ring: owned ancestors then chain rows (bottom-up) of each
+  // chain slot; one cp.async group per row (empty past the end)
+  int ic_cs = 0, ic_pos = -1;
+  unsigned ic_own = 0u;
+  int ic_k = 0, ck = 0;
+  auto issue = [&]() {
+    bool have = false, chain_row = false;
+    unsigned r = 0;
+    for (;;) {
+      if (++ic_pos == kb + N) {
+        ic_pos = 0;
+        ++ic_cs;
       }
-      return;
-    } else {
-      r = nbr + (unsigned)(N - 1 - (s - kb - 1)) * nchain + (unsigned)ci;
-      px = true;
+      const int ci = gw + ic_cs * nw;
+      if (ic_cs >= A.cpw || ci >= (int)nchain) {
+        ic_pos = kb + N - 1;  // park past the end
+        ic_cs = A.cpw;
+        break;
+      }
+      if (ic_pos == 0) ic_own = kb > 0 ? __ldg(PT->cown + ci) : 0u;
+      if (ic_pos >= kb) {
+        r = nbr + (unsigned)(N - 1 - (ic_pos - kb)) * nchain + (unsigned)ci;
+        have = chain_row = true;
+        break;
+      }
+      if ((ic_own >> ic_pos) & 1u) {
+        r = (unsigned)PT->cpath[(size_t)ci * kb + ic_pos];
+        have = true;
+        break;
+      }
     }
-    const unsigned bytes = (dg ? (unsigned)(2 * nu + lx) * 8u : 0u) + (px ? (unsigned)(2 * W + nu + lx) * 8u : 0u);
-    mbar_expect(b, bytes);
-    if (dg) {
-      bulk_g2s(st + oL, reinterpret_cast<const double*>(G.Lb) + (size_t)r * nu, nu * 8, b);
-      bulk_g2s(st + oB, reinterpret_cast<const double*>(f.ut) + (size_t)r * nu, nu * 8, b);
-      bulk_g2s(st + oG, reinterpret_cast<const double*>(G.g) + (size_t)r * lx, lx * 8, b);
+    if (have) {
+      double* st = ring + (ic_k & (DP_D - 1)) * STG;
+      const double* s0 = PT->yb + (size_t)r * W + 2 * lane;
+      const double* s1 = PT->ymb + (size_t)r * W + 2 * lane;
+#pragma unroll
+      for (int k = 0; k < (W / 2 + 31) / 32; ++k)
+        if (lane + 32 * k < W / 2) {
+          cp16(st + 2 * lane + 64 * k, s0 + 64 * k);
+          cp16(st + oYm + 2 * lane + 64 * k, s1 + 64 * k);
+        }
+      const double* s2 = PT->Ua + (size_t)r * NU + 2 * lane;
+#pragma unroll
+      for (int k = 0; k < (NU / 2 + 31) / 32; ++k)
+        if (lane + 32 * k < NU / 2) cp16(st + oUa + 2 * lane + 64 * k, s2 + 64 * k);
+      const double* s3 = PT->Xa + (size_t)r * LX + 2 * lane;
+#pragma unroll
+      for (int k = 0; k < (LX / 2 + 31) / 32; ++k)
+        if (lane + 32 * k < LX / 2) cp16(st + oXa + 2 * lane + 64 * k, s3 + 64 * k);
+      if constexpr (SDG) {
+        if (chain_row) {
+          const double* s4 = reinterpret_cast<const double*>(PT->Lb) + (size_t)r * NU + 2 * lane;
+          const double* s5 = reinterpret_cast<const double*>(PT->UT) + (size_t)r * NU + 2 * lane;
+#pragma unroll
+          for (int k = 0; k < (NU / 2 + 31) / 32; ++k)
+            if (lane + 32 * k < NU / 2) {
+              cp16(st + oL + 2 * lane + 64 * k, s4 + 64 * k);
+              cp16(st + oB + 2 * lane + 64 * k, s5 + 64 * k);
+            }
+          const double* s6 = reinterpret_cast<const double*>(PT->g) + (size_t)r * LX + 2 * lane;
+#pragma unroll
+          for (int k = 0; k < (LX / 2 + 31) / 32; ++k)
+            if (lane + 32 * k < LX / 2) cp16(st + oG + 2 * lane + 64 * k, s6 + 64 * k);
+          if (lane == 0) cp16(st + oAx, reinterpret_cast<const double*>(PT->aux) + (size_t)r * 2);
+        }
+      }
     }
-    if (px) {
-      bulk_g2s(st + oY, yb + (size_t)r * W, W * 8, b);
-      bulk_g2s(st + oYm, ymb + (size_t)r * W, W * 8, b);
-      bulk_g2s(st + oUa, d.Ua + (size_t)r * nu, nu * 8, b);
-      bulk_g2s(st + oXa, d.Xa + (size_t)r * lx, lx * 8, b);
-    }
+    cp_commit();
+    ++ic_k;
   };
-  auto take = [&](int i) -> const double* {  // wait for step i's stage
-    mbar_wait(mbar + (i % DP_D), (unsigned)((i / DP_D) & 1));
-    return ring + (i % DP_D) * STG;
-  };
-  auto release = [&](int i) {  // the warp has read step i's stage: re-arm it with step i + DP_D
+  auto take = [&]() -> const double* {
+    cp_wait<DP_D - 1>();
     __syncwarp();
-    if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    issue(i + DP_D);
+    return ring + (ck & (DP_D - 1)) * STG;
   };
-  for (int i = 0; i < DP_D; ++i) issue(i);
-  // ---- the projector and operator products through the exchange vectors
+  auto release = [&]() {  // every lane has read the stage: refill it with the row DP_D ahead
+    __syncwarp();
+    ++ck;
+    issue();
+  };
+#pragma unroll
+  for (int k = 0; k < DP_D; ++k) issue();
+  // ---- operator products through the exchange vectors
   auto proj_neg = [&](const TG (&v)[4], const TG (&base)[4], TG (&out)[4]) {  // out = base + P(-v)
     TG z[4];
 #pragma unroll
@@ -225,258 +315,258 @@ __global__ void __launch_bounds__(256, 1) k_chain_dp(FastView f, DpArgs A) {
     st2(zb + l2, z[0], z[1]);
     st2(zb + 64 + l2, z[2], z[3]);
     __syncwarp();
-    tb[lane] = CW_DOT(kr);  // zero past ns
+    tb[lane] = ellv_dot(kr);  // zero past ns
     __syncwarp();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) out[q] = base[q] + (z[q] - CW_DOT(ec[q]));
+    for (int q = 0; q < 4; ++q) out[q] = base[q] + (z[q] - ellv_dot(ec[q]));
   };
   auto bmul = [&](const TG (&u)[4], TG (&bu)[2]) {  // bu = B u (rows l2, l2 + 1)
     st2(ub + l2, u[0], u[1]);
     st2(ub + 64 + l2, u[2], u[3]);
     __syncwarp();
 #pragma unroll
-    for (int h = 0; h < 2; ++h) bu[h] = CW_DOT(br[h]);
+    for (int h = 0; h < 2; ++h) bu[h] = ellv_dot(br[h]);
   };
-  bool bad = false;
-  // Moreau prox of one row (prox_x_warp / prox_u_warp arithmetic, bit-exact
-  // with numpy per element), ergodic averages; returns the next collapsed dual
+  double badacc = 0.0;  // fma(p, 0, .): NaN once any output was not finite
+  // Moreau prox of one row (prox_x_warp / prox_u_warp arithmetic per element,
+  // bit-exact with numpy), ergodic averages, next collapsed dual
   auto prox = [&](const double* st, unsigned r, const TG (&u)[4], const TG (&x)[2], TG (&yx)[2], TG (&yu)[4]) {
-    const double gamma = P.gamma, ig = P.ig;
-    double* yn = ynb + (size_t)r * W;
-    double xv[2] = {(double)x[0], (double)x[1]};
-    double y1[2], y2[2], m1[2], m2[2], xa[2], V1[2], V2[2], v1[2], v2[2], c1[2], c2[2];
+    const double gamma = pv[0], ig = pv[1], beta = pv[2], theta = pv[3], om = pv[4];
+    double* yn = PT->ynb + (size_t)r * W;
+    double v1[2], v2[2], V1[2], V2[2], c1[2], c2[2], y1[2], y2[2];
     {
-      const double2 a = ld2s(st + oY + l2), b = ld2s(st + oYm + l2), c = ld2s(st + oXa + l2);
-      y1[0] = a.x; y1[1] = a.y; m1[0] = b.x; m1[1] = b.y; xa[0] = c.x; xa[1] = c.y;
-      y2[0] = st[oY + nt + l2]; y2[1] = st[oY + nt + l2 + 1];
-      m2[0] = st[oYm + nt + l2]; m2[1] = st[oYm + nt + l2 + 1];
-    }
-    double xan[2];
+      const double2 a = ld2s(st + l2), b = ld2s(st + oYm + l2), c = ld2s(st + oXa + l2);
+      y1[0] = a.x; y1[1] = a.y;
+      y2[0] = st[NT + l2]; y2[1] = st[NT + l2 + 1];
+      const double m1[2] = {b.x, b.y}, m2[2] = {st[oYm + NT + l2], st[oYm + NT + l2 + 1]};
+      const double xa[2] = {c.x, c.y};
+      double xan[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int j = l2 + h;
-      const bool ok = j < nt;
-      xan[h] = P.it == 0 ? xv[h] : dadd(dmul(xa[h], P.om), dmul(P.theta, xv[h]));
-      const double gx = dmul(gamma, xv[h]);
-      v1[h] = dadd(dadd(y1[h], dmul(P.beta, dsub(y1[h], m1[h]))), gx);
-      v2[h] = dadd(dadd(y2[h], dmul(P.beta, dsub(y2[h], m2[h]))), gx);
-      V1[h] = div_by(v1[h], gamma, ig);
-      V2[h] = div_by(v2[h], gamma, ig);
-      c1[h] = np_clip(V1[h], bnd[j], bnd[64 + j]);
-      c2[h] = np_max(V2[h], bnd[128 + j]);
-      if (ok) {
+      for (int h = 0; h < 2; ++h) {
+        const double xv = (double)x[h];
+        xan[h] = it == 0 ? xv : dadd(dmul(xa[h], om), dmul(theta, xv));
+        const double gx = dmul(gamma, xv);
+        v1[h] = dadd(dadd(y1[h], dmul(beta, dsub(y1[h], m1[h]))), gx);
+        v2[h] = dadd(dadd(y2[h], dmul(beta, dsub(y2[h], m2[h]))), gx);
+        V1[h] = div_by(v1[h], gamma, ig);
+        V2[h] = div_by(v2[h], gamma, ig);
+      }
+      const double2 lo = ld2s(bnd + l2), hi = ld2s(bnd + 64 + l2), sf = ld2s(bnd + 128 + l2);
+      c1[0] = np_clip_u(V1[0], lo.x, hi.x);
+      c1[1] = np_clip_u(V1[1], lo.y, hi.y);
+      c2[0] = np_max_u(V2[0], sf.x);
+      c2[1] = np_max_u(V2[1], sf.y);
+      double* xap = PT->Xa + (size_t)r * LX + l2;
+      if (okx2) st2(xap, xan[0], xan[1]);
+      else xap[0] = xan[0];
+      if (PT->store) {
+        TG* Xp = PT->X + (size_t)r * LX + l2;
+        if (okx2) st2(Xp, x[0], x[1]);
+        else Xp[0] = x[0];
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
         const double df1 = dsub(V1[h], c1[h]), df2 = dsub(V2[h], c2[h]);
-        sd2[j] = dmul(df1, df1);
-        sd2[64 + j] = dmul(df2, df2);
+        sd2[l2 + h] = dmul(df1, df1);  // slot 63 (past NT) is never read
+        sd2[64 + l2 + h] = dmul(df2, df2);
       }
     }
-    double* xap = d.Xa + (size_t)r * lx + l2;
-    if (okx2) st2(xap, xan[0], xan[1]);
-    else if (okx) xap[0] = xan[0];
-    // the u part while the norms' operands settle
-    double y3[4], m3[4], ua[4];
-    {
-      const double2 a0 = ld2s(st + oY + 2 * nt + l2), a1 = ld2s(st + oY + 2 * nt + o1);
-      const double2 b0 = ld2s(st + oYm + 2 * nt + l2), b1 = ld2s(st + oYm + 2 * nt + o1);
-      const double2 c0 = ld2s(st + oUa + l2), c1v = ld2s(st + oUa + o1);
-      y3[0] = a0.x; y3[1] = a0.y; y3[2] = a1.x; y3[3] = a1.y;
-      m3[0] = b0.x; m3[1] = b0.y; m3[2] = b1.x; m3[3] = b1.y;
-      ua[0] = c0.x; ua[1] = c0.y; ua[2] = c1v.x; ua[3] = c1v.y;
-    }
-    double uan[4], p3[4];
+    {  // the u part (plain box) while the norms' operands settle
+      double p3[4], uan[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = cw_ku(lane, q);
-      const double uq = (double)u[q];
-      uan[q] = P.it == 0 ? uq : dadd(dmul(ua[q], P.om), dmul(P.theta, uq));
-      const double v3 = dadd(dadd(y3[q], dmul(P.beta, dsub(y3[q], m3[q]))), dmul(gamma, uq));
-      const double V3 = div_by(v3, gamma, ig);
-      const int kk = k < nu ? k : 0;
-      p3[q] = dsub(v3, dmul(gamma, np_clip(V3, bnd[192 + kk], bnd[320 + kk])));
-      if (k < nu) bad |= !isfinite(p3[q]);
-      yu[q] = next ? (TG)dadd(p3[q], dmul(P.beta1, dsub(p3[q], y3[q]))) : TG(0);
-      if (k >= nu) yu[q] = TG(0);
-    }
-    if (ok0) {
-      st2(d.Ua + (size_t)r * nu + l2, uan[0], uan[1]);
-      st2(yn + 2 * nt + l2, p3[0], p3[1]);
-    }
-    if (ok1) {
-      st2(d.Ua + (size_t)r * nu + 64 + l2, uan[2], uan[3]);
-      st2(yn + 2 * nt + 64 + l2, p3[2], p3[3]);
+      for (int hq = 0; hq < 2; ++hq) {
+        const int o = hq ? o1 : l2;
+        const double2 a = ld2s(st + 2 * NT + o), b = ld2s(st + oYm + 2 * NT + o), c = ld2s(st + oUa + o);
+        const double2 lo = ld2s(bnd + 192 + o), hi = ld2s(bnd + 320 + o);
+        const double y3[2] = {a.x, a.y}, m3[2] = {b.x, b.y}, ua[2] = {c.x, c.y}, l3[2] = {lo.x, lo.y},
+                     h3[2] = {hi.x, hi.y};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int q = 2 * hq + h;
+          const double uq = (double)u[q];
+          uan[q] = it == 0 ? uq : dadd(dmul(ua[h], om), dmul(theta, uq));
+          const double v3 = dadd(dadd(y3[h], dmul(beta, dsub(y3[h], m3[h]))), dmul(gamma, uq));
+          const double V3 = div_by(v3, gamma, ig);
+          p3[q] = dsub(v3, dmul(gamma, np_clip_u(V3, l3[h], h3[h])));
+          yu[q] = (TG)dadd(p3[q], dmul(pv[5], dsub(p3[q], y3[h])));
+        }
+      }
+      st2(PT->Ua + (size_t)r * NU + l2, uan[0], uan[1]);
+      st2(yn + 2 * NT + l2, p3[0], p3[1]);
+      badacc = fma(p3[0], 0.0, fma(p3[1], 0.0, badacc));
+      if (PT->store) st2(PT->U + (size_t)r * NU + l2, u[0], u[1]);
+      if (ok1) {
+        st2(PT->Ua + (size_t)r * NU + 64 + l2, uan[2], uan[3]);
+        st2(yn + 2 * NT + 64 + l2, p3[2], p3[3]);
+        badacc = fma(p3[2], 0.0, fma(p3[3], 0.0, badacc));
+        if (PT->store) st2(PT->U + (size_t)r * NU + 64 + l2, u[2], u[3]);
+      } else {
+        yu[2] = yu[3] = TG(0);
+      }
     }
     __syncwarp();
     double stv = 0.0;
-    if (lane < 16) {
-      const int slot = lane >> 3;
-      const double ssum = pw_group8(sd2 + 64 * slot, nt, lane & 7, 0xffu << (lane & 8));
-      if ((lane & 7) == 0) {
+    if (lane < 16) {  // the two tank-slot norms, numpy pairwise order (8-lane groups)
+      const int slot = lane >> 3, g = lane & 7;
+      const unsigned mask = 0xffu << (lane & 8);
+      const double* s2 = sd2 + 64 * slot;
+      double r8 = s2[g];
+#pragma unroll
+      for (int q = 1; q < NB / 8; ++q) r8 = dadd(r8, s2[g + 8 * q]);
+      double ssum = dadd(r8, __shfl_down_sync(mask, r8, 1, 8));
+      ssum = dadd(ssum, __shfl_down_sync(mask, ssum, 2, 8));
+      ssum = dadd(ssum, __shfl_down_sync(mask, ssum, 4, 8));
+      if (g == 0) {
+#pragma unroll
+        for (int q = NB; q < NT; ++q) ssum = dadd(ssum, s2[q]);
         const double dist = __dsqrt_rn(ssum);
-        const double thr = dmul(ig, slot ? d.w_s : d.w_x);  // prox parameter RN(1/gamma) (solver.py:571)
+        const double thr = dmul(ig, pv[6 + slot]);  // prox parameter RN(1/gamma) (solver.py:571)
         stv = dist > 0.0 ? np_min(1.0, div_exact(thr, dist)) : 0.0;
       }
     }
     const double st1 = __shfl_sync(0xffffffffu, stv, 0), st2v = __shfl_sync(0xffffffffu, stv, 8);
+    const double beta1 = pv[5];
     double p1[2], p2[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int j = l2 + h;
       const double O1 = dsub(V1[h], dmul(st1, dsub(V1[h], c1[h])));
       const double O2 = dsub(V2[h], dmul(st2v, dsub(V2[h], c2[h])));
       p1[h] = dsub(v1[h], dmul(gamma, O1));
       p2[h] = dsub(v2[h], dmul(gamma, O2));
-      if (j < nt) bad |= !isfinite(p1[h]) || !isfinite(p2[h]);
-      yx[h] = (next && j < nt) ? (TG)dadd(dadd(p1[h], dmul(P.beta1, dsub(p1[h], y1[h]))),
-                                          dadd(p2[h], dmul(P.beta1, dsub(p2[h], y2[h]))))
-                               : TG(0);
+      yx[h] = (TG)dadd(dadd(p1[h], dmul(beta1, dsub(p1[h], y1[h]))), dadd(p2[h], dmul(beta1, dsub(p2[h], y2[h]))));
     }
-    if (okx2) st2(yn + l2, p1[0], p1[1]);
-    else if (okx) yn[l2] = p1[0];
-    if (okx) yn[nt + l2] = p2[0];
-    if (okx2) yn[nt + l2 + 1] = p2[1];
-  };
-  auto store_ux = [&](unsigned r, const TG (&u)[4], const TG (&x)[2]) {
-    TG* Up = G.U + (size_t)r * nu;
-    if (ok0) st2(Up + l2, u[0], u[1]);
-    if (ok1) st2(Up + 64 + l2, u[2], u[3]);
-    TG* Xp = G.X + (size_t)r * lx + l2;
-    if (okx2) st2(Xp, x[0], x[1]);
-    else if (okx) Xp[0] = x[0];
-  };
-  auto row_dg = [&](const double* st, unsigned r, TG (&L)[4], TG (&b)[4], TG (&g)[2]) {
-    if constexpr (TMA_DG) {
-      const double2 a0 = ld2s(st + oL + l2), a1 = ld2s(st + oL + o1);
-      const double2 b0 = ld2s(st + oB + l2), b1 = ld2s(st + oB + o1);
-      const double2 g0 = ld2s(st + oG + l2);
-      L[0] = (TG)a0.x; L[1] = (TG)a0.y; L[2] = (TG)a1.x; L[3] = (TG)a1.y;
-      b[0] = (TG)b0.x; b[1] = (TG)b0.y; b[2] = (TG)b1.x; b[3] = (TG)b1.y;
-      g[0] = (TG)g0.x; g[1] = (TG)g0.y;
+    yn[NT + l2] = p2[0];
+    if (okx2) {
+      st2(yn + l2, p1[0], p1[1]);
+      yn[NT + l2 + 1] = p2[1];
+      badacc = fma(p1[0], 0.0, fma(p1[1], 0.0, fma(p2[0], 0.0, fma(p2[1], 0.0, badacc))));
     } else {
-      const TG* base = sizeof(TG) == 8 ? (const TG*)f.ut : (const TG*)f.ut32;
-      const auto a0 = ldg2_if(G.Lb + (size_t)r * nu + l2, true), a1 = ldg2_if(G.Lb + (size_t)r * nu + o1, true);
-      const auto b0 = ldg2_if(base + (size_t)r * nu + l2, true), b1 = ldg2_if(base + (size_t)r * nu + o1, true);
-      const auto g0 = ldg2_if(G.g + (size_t)r * lx + l2, true);
-      L[0] = a0.x; L[1] = a0.y; L[2] = a1.x; L[3] = a1.y;
-      b[0] = b0.x; b[1] = b0.y; b[2] = b1.x; b[3] = b1.y;
-      g[0] = g0.x; g[1] = g0.y;
+      yn[l2] = p1[0];
+      badacc = fma(p1[0], 0.0, fma(p2[0], 0.0, badacc));
+      yx[1] = TG(0);
     }
-    if (!ok0) L[0] = L[1] = b[0] = b[1] = TG(0);
-    if (!ok1) L[2] = L[3] = b[2] = b[3] = TG(0);
-    if (!okx) g[0] = TG(0);
-    if (!okx2) g[1] = TG(0);
   };
-  int i = 0;  // ring step
+  auto ldrow = [&](unsigned r, TG (&L)[4], TG (&b)[4], TG (&g)[2], TG& ax) {  // down operands of a chain row
+    const auto a0 = ld2cg(PT->Lb + (size_t)r * NU + l2), a1 = ld2cg(PT->Lb + (size_t)r * NU + o1);
+    const auto b0 = ld2cg(PT->UT + (size_t)r * NU + l2), b1 = ld2cg(PT->UT + (size_t)r * NU + o1);
+    const auto g0 = ld2cg(PT->g + (size_t)r * LX + l2);
+    L[0] = a0.x; L[1] = a0.y; L[2] = ok1 ? a1.x : TG(0); L[3] = ok1 ? a1.y : TG(0);
+    b[0] = b0.x; b[1] = b0.y; b[2] = ok1 ? b1.x : TG(0); b[3] = ok1 ? b1.y : TG(0);
+    g[0] = g0.x; g[1] = okx2 ? g0.y : TG(0);
+    ax = __ldcg(PT->aux + (size_t)r * 2);
+  };
   for (int cs = 0; cs < A.cpw; ++cs) {
     const int ci = gw + cs * nw;
     if (ci >= (int)nchain) break;
     const unsigned r_top = nbr + (unsigned)ci;
-    TG ls[4] = {0, 0, 0, 0}, xs[2];
-    if (!up_only) {
-      // ---- ancestors, top-down (k_chain_down_r arithmetic)
-      const unsigned own = kb > 0 ? f.cown[ci] : 0u;
+    // the bottom chain row's operands (fp32) and the chain aggregates: in flight during the ancestor walk
+    TG Lc[4], bcur[4], gcur[2], axc;
+    if constexpr (!SDG) ldrow(nbr + (unsigned)(N - 1) * nchain + (unsigned)ci, Lc, bcur, gcur, axc);
+    TG LSc[4], LWc[4], SU[4], SG[2];
+    {
+      const TG* a = PT->agg + (size_t)ci * AW;
+      const auto s0 = ld2cg(a + l2), s1 = ld2cg(a + o1), w0 = ld2cg(a + NU + l2), w1 = ld2cg(a + NU + o1);
+      const auto u0 = ld2cg(a + 2 * NU + l2), u1 = ld2cg(a + 2 * NU + o1), g0 = ld2cg(a + 3 * NU + l2);
+      LSc[0] = s0.x; LSc[1] = s0.y; LSc[2] = ok1 ? s1.x : TG(0); LSc[3] = ok1 ? s1.y : TG(0);
+      LWc[0] = w0.x; LWc[1] = w0.y; LWc[2] = ok1 ? w1.x : TG(0); LWc[3] = ok1 ? w1.y : TG(0);
+      SU[0] = u0.x; SU[1] = u0.y; SU[2] = ok1 ? u1.x : TG(0); SU[3] = ok1 ? u1.y : TG(0);
+      SG[0] = g0.x; SG[1] = okx2 ? g0.y : TG(0);
+    }
+    // ---- ancestors, top-down: ls = running sum of L, Ws = running sum of ls
+    TG ls[4] = {0, 0, 0, 0}, Ws[4] = {0, 0, 0, 0};
+    const unsigned own = kb > 0 ? __ldg(PT->cown + ci) : 0u;
+    for (int m = 0; m < kb; ++m) {
+      const unsigned r = (unsigned)PT->cpath[(size_t)ci * kb + m];
+      const auto a0 = ld2cg(PT->Lb + (size_t)r * NU + l2), a1 = ld2cg(PT->Lb + (size_t)r * NU + o1);
+      const TG La[4] = {a0.x, a0.y, ok1 ? a1.x : TG(0), ok1 ? a1.y : TG(0)};
 #pragma unroll
-      for (int h = 0; h < 2; ++h) xs[h] = l2 + h < nt ? (TG)d.p[l2 + h] : TG(0);
-      for (int m = 0; m < kb; ++m, ++i) {
-        const unsigned r = (unsigned)f.cpath[(size_t)ci * kb + m];
-        const double* st = take(i);
-        TG L[4], b[4], g[2];
-        row_dg(st, r, L, b, g);
-        const bool mine = (own >> m) & 1u;
-        if (!mine) release(i);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) ls[q] = m == 0 ? L[q] : ls[q] + L[q];
-        TG u[4], bu[2];
-        proj_neg(ls, b, u);
-        bmul(u, bu);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) xs[h] = (xs[h] + bu[h]) + g[h];
-        if (mine) {
-          TG yx[2], yu[4];
-          prox(st, r, u, xs, yx, yu);
-          release(i);
-          if (next) {
-            TG* yc = G.Yc + (size_t)r * ly;
-            if (okx2) st2(yc + l2, yx[0], yx[1]);
-            else if (okx) yc[l2] = yx[0];
-            if (ok0) st2(yc + lx + l2, yu[0], yu[1]);
-            if (ok1) st2(yc + lx + 64 + l2, yu[2], yu[3]);
-          }
-          if (store) store_ux(r, u, xs);
+      for (int q = 0; q < 4; ++q) {
+        ls[q] = ls[q] + La[q];
+        Ws[q] = Ws[q] + ls[q];
+      }
+      if ((own >> m) & 1u) {  // this chain owns branching row r: its u, x and prox
+        TG ua[4], xa[2], sw[4], bw[2];
+        const auto b0 = ld2cg(PT->UT + (size_t)r * NU + l2), b1 = ld2cg(PT->UT + (size_t)r * NU + o1);
+        const TG* pg = PT->putg + (size_t)r * PW;
+        const auto p0 = ld2cg(pg + l2), p1 = ld2cg(pg + o1), q0 = ld2cg(pg + NU + l2);
+        const TG bu[4] = {b0.x, b0.y, ok1 ? b1.x : TG(0), ok1 ? b1.y : TG(0)};
+        const TG PU[4] = {p0.x, p0.y, ok1 ? p1.x : TG(0), ok1 ? p1.y : TG(0)};
+        proj_neg(ls, bu, ua);  // u_m = ut_m - P ls_m
+        proj_neg(Ws, PU, sw);  // sum_{m' <= m} u_m'
+        bmul(sw, bw);
+        xa[0] = ((TG)d.p[l2] + bw[0]) + q0.x;
+        xa[1] = okx2 ? ((TG)d.p[l2 + 1] + bw[1]) + q0.y : TG(0);
+        TG yx[2], yu[4];
+        prox(take(), r, ua, xa, yx, yu);
+        release();
+        if (next) {
+          TG* yc = PT->Yc + (size_t)r * LY;
+          if (okx2) st2(yc + l2, yx[0], yx[1]);
+          else yc[l2] = yx[0];
+          st2(yc + LX + l2, yu[0], yu[1]);
+          if (ok1) st2(yc + LX + 64 + l2, yu[2], yu[3]);
         }
       }
-      // ---- chain aggregates: the bottom row's prefix sums
-      {
-        const double* st = take(i);
-        TG LS[4], LW[4], SU[4], SG[2];
-        if constexpr (TMA_DG) {
-          const double* a = st;
-          const double2 s0 = ld2s(a + l2), s1 = ld2s(a + o1), w0 = ld2s(a + nu + l2), w1 = ld2s(a + nu + o1);
-          const double2 u0 = ld2s(a + 2 * nu + l2), u1 = ld2s(a + 2 * nu + o1), g0 = ld2s(a + 3 * nu + l2);
-          LS[0] = s0.x; LS[1] = s0.y; LS[2] = s1.x; LS[3] = s1.y;
-          LW[0] = w0.x; LW[1] = w0.y; LW[2] = w1.x; LW[3] = w1.y;
-          SU[0] = u0.x; SU[1] = u0.y; SU[2] = u1.x; SU[3] = u1.y;
-          SG[0] = g0.x; SG[1] = g0.y;
-        } else {
-          const TG* a = agg + (size_t)ci * AW;
-          const auto s0 = ld2s(a + l2), s1 = ld2s(a + o1), w0 = ld2s(a + nu + l2), w1 = ld2s(a + nu + o1);
-          const auto u0 = ld2s(a + 2 * nu + l2), u1 = ld2s(a + 2 * nu + o1), g0 = ld2s(a + 3 * nu + l2);
-          LS[0] = s0.x; LS[1] = s0.y; LS[2] = s1.x; LS[3] = s1.y;
-          LW[0] = w0.x; LW[1] = w0.y; LW[2] = w1.x; LW[3] = w1.y;
-          SU[0] = u0.x; SU[1] = u0.y; SU[2] = u1.x; SU[3] = u1.y;
-          SG[0] = g0.x; SG[1] = g0.y;
-        }
-        release(i);
-        ++i;
-        TG V[4], w[4], bw[2];
+    }
+    // ---- the bottom chain row's prefix sums from the aggregates
+    TG xs[2];
+    {
+      TG V[4], w[4], bw[2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) V[q] = fma((TG)N, ls[q], LW[q]);
-        proj_neg(V, SU, w);  // sum_t u_t
-        bmul(w, bw);
+      for (int q = 0; q < 4; ++q) V[q] = fma((TG)N, ls[q], LWc[q]) + Ws[q];
+      proj_neg(V, SU, w);  // sum of u over the root path
+      bmul(w, bw);
+      xs[0] = ((TG)d.p[l2] + bw[0]) + SG[0];
+      xs[1] = okx2 ? ((TG)d.p[l2 + 1] + bw[1]) + SG[1] : TG(0);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) xs[h] = (xs[h] + bw[h]) + SG[h];  // x_{N-1}
-#pragma unroll
-        for (int q = 0; q < 4; ++q) ls[q] = ls[q] + LS[q];  // ls_{N-1}
-      }
+      for (int q = 0; q < 4; ++q) ls[q] = ls[q] + LSc[q];  // ls_{N-1}
     }
     // ---- chain rows, bottom-up: down of it, prox of it, up of it + 1
     TG wbr[2] = {0, 0}, acc[4] = {0, 0, 0, 0}, LSn[4] = {0, 0, 0, 0}, LWn[4] = {0, 0, 0, 0};
     for (int t = N - 1; t >= 0; --t) {
       const unsigned r = nbr + (unsigned)t * nchain + (unsigned)ci;
       const bool bottom = t == N - 1;
-      TG yx[2], yu[4];
-      if (!up_only) {
-        const double* st = take(i);
-        TG L[4], b[4], g[2], u[4];
-        row_dg(st, r, L, b, g);
-        proj_neg(ls, b, u);
-        prox(st, r, u, xs, yx, yu);
-        release(i);
-        ++i;
-        if (store) store_ux(r, u, xs);
-        if (t > 0) {  // x and ls of the row above
-          TG bu[2];
-          bmul(u, bu);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) xs[h] = (xs[h] - g[h]) - bu[h];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) ls[q] = ls[q] - L[q];
-        }
+      TG L[4], b[4], g[2], ax, u[4], yx[2], yu[4];
+      const double* st = take();
+      if constexpr (SDG) {
+        const double2 a0 = ld2s(st + oL + l2), a1 = ld2s(st + oL + o1), b0 = ld2s(st + oB + l2),
+                      b1 = ld2s(st + oB + o1), g0 = ld2s(st + oG + l2);
+        L[0] = a0.x; L[1] = a0.y; L[2] = ok1 ? a1.x : 0.0; L[3] = ok1 ? a1.y : 0.0;
+        b[0] = b0.x; b[1] = b0.y; b[2] = ok1 ? b1.x : 0.0; b[3] = ok1 ? b1.y : 0.0;
+        g[0] = g0.x; g[1] = okx2 ? g0.y : 0.0;
+        ax = st[oAx];
       } else {
-        const TG* yc = G.Yc + (size_t)r * ly;
-        const auto a = ldg2_if(yc + l2, okx), b0 = ldg2_if(yc + lx + l2, ok0), b1 = ldg2_if(yc + lx + o1, ok1);
-        yx[0] = a.x; yx[1] = a.y;
-        yu[0] = b0.x; yu[1] = b0.y; yu[2] = b1.x; yu[3] = b1.y;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          L[q] = Lc[q];
+          b[q] = bcur[q];
+        }
+        g[0] = gcur[0];
+        g[1] = gcur[1];
+        ax = axc;
+        if (t > 0) ldrow(r - nchain, Lc, bcur, gcur, axc);  // the row above, one row ahead
+      }
+      proj_neg(ls, b, u);
+      prox(st, r, u, xs, yx, yu);
+      release();
+      if (t > 0) {  // x and ls of the row above
+        TG bu[2];
+        bmul(u, bu);
+        xs[0] = (xs[0] - g[0]) - bu[0];
+        xs[1] = (xs[1] - g[1]) - bu[1];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ls[q] = ls[q] - L[q];
       }
       if (!next) continue;
       // up pass of the next iteration (k_chain_up_r arithmetic, R-free)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) wbr[h] = bottom ? yx[h] : yx[h] + wbr[h];
+      wbr[0] = bottom ? yx[0] : yx[0] + wbr[0];
+      wbr[1] = bottom ? yx[1] : yx[1] + wbr[1];
       st2(wb + l2, wbr[0], wbr[1]);
       __syncwarp();
       TG a[4], Sv[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        a[q] = yu[q] + CW_DOT(bc[q]);
+        a[q] = yu[q] + ellv_dot(bc[q]);
         Sv[q] = acc[q];
         acc[q] = bottom ? a[q] : a[q] + acc[q];
       }
@@ -485,15 +575,14 @@ __global__ void __launch_bounds__(256, 1) k_chain_dp(FastView f, DpArgs A) {
         st2(zb + l2, Sv[0], Sv[1]);
         st2(zb + 64 + l2, Sv[2], Sv[3]);
         __syncwarp();
-        tb[lane] = CW_DOT(kr);
+        tb[lane] = ellv_dot(kr);
         __syncwarp();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) l[q] = a[q] + (Sv[q] - CW_DOT(ec[q]));
+        for (int q = 0; q < 4; ++q) l[q] = a[q] + (Sv[q] - ellv_dot(ec[q]));
       } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q) l[q] = a[q];
       }
-      const TG ax = G.aux[(size_t)r * 2];
       const TG wt = (TG)(N - t);
       TG Ln[4];
 #pragma unroll
@@ -502,49 +591,85 @@ __global__ void __launch_bounds__(256, 1) k_chain_dp(FastView f, DpArgs A) {
         LSn[q] = LSn[q] + Ln[q];
         LWn[q] = fma(wt, Ln[q], LWn[q]);
       }
-      TG* Lp = G.Lb + (size_t)r * nu;
-      if (ok0) st2(Lp + l2, Ln[0], Ln[1]);
+      TG* Lp = PT->Lb + (size_t)r * NU;
+      st2(Lp + l2, Ln[0], Ln[1]);
       if (ok1) st2(Lp + 64 + l2, Ln[2], Ln[3]);
-      __syncwarp();  // wb / zb / tb are rewritten by the next row
     }
-    if (next) {  // chain totals for the branch groups, aggregates for the next iteration
-      if (okx) G.wbar[(size_t)r_top * lx + l2] = wbr[0];
-      if (okx2) G.wbar[(size_t)r_top * lx + l2 + 1] = wbr[1];
-      if (ok0) st2(G.Asub + (size_t)r_top * nu + l2, acc[0], acc[1]);
-      if (ok1) st2(G.Asub + (size_t)r_top * nu + 64 + l2, acc[2], acc[3]);
-      TG* a = agg + (size_t)ci * AW;
-      if (ok0) {
-        st2(a + l2, LSn[0], LSn[1]);
-        st2(a + nu + l2, LWn[0], LWn[1]);
-      }
+    if (next) {  // chain totals for the branch groups, L aggregates for the next iteration
+      if (okx2) st2(PT->wbar + (size_t)r_top * LX + l2, wbr[0], wbr[1]);
+      else PT->wbar[(size_t)r_top * LX + l2] = wbr[0];
+      st2(PT->Asub + (size_t)r_top * NU + l2, acc[0], acc[1]);
+      if (ok1) st2(PT->Asub + (size_t)r_top * NU + 64 + l2, acc[2], acc[3]);
+      TG* a = PT->agg + (size_t)ci * AW;
+      st2(a + l2, LSn[0], LSn[1]);
+      st2(a + NU + l2, LWn[0], LWn[1]);
       if (ok1) {
         st2(a + 64 + l2, LSn[2], LSn[3]);
-        st2(a + nu + 64 + l2, LWn[2], LWn[3]);
+        st2(a + NU + 64 + l2, LWn[2], LWn[3]);
       }
     }
   }
-  if (!up_only && __any_sync(0xffffffffu, bad) && lane == 0) atomicMin(d.bad_nu, P.it);
+  cp_wait<0>();
+  if (__any_sync(0xffffffffu, isnan(badacc)) && lane == 0) atomicMin(d.bad_nu, it);
 }
 
-// Per-solve chain constants of k_chain_dp: SUT = sum_t ut_t, SG = sum_t g_t
-// (chain rows), and zero running aggregates. One warp per chain.
+// Per-solve constants of k_chain_dp: per chain SUTp / SGp (ut / g summed over
+// the whole root path, ancestors and chain rows), per branching row the root
+// path prefixes PUT / PG (including the row); the running L aggregates are
+// zeroed (L = 0 at Yc = 0). One warp per chain / branching row.
 template <typename TG>
-__global__ void k_dp_agg_init(FastView f, TG* agg) {
+__global__ void k_dp_agg_init(FastView f, TG* agg, TG* putg) {
+  const DevView& d = f.d;
+  const int nu = d.nu, lx = d.lx, kb = f.kstar, N = d.H - kb, AW = dp_agg_w(nu, lx), PW = nu + lx;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const GA<TG> G = ga<TG>(f);
+  const TG* UT = sizeof(TG) == 8 ? (const TG*)f.ut : (const TG*)f.ut32;
+  if (w < f.nchain) {
+    const int ci = w;
+    TG* a = agg + (size_t)ci * AW;
+    for (int c = lane; c < AW; c += 32) {
+      TG s = 0;
+      if (c >= 2 * nu) {
+        const bool isg = c >= 3 * nu;
+        const int cc = isg ? c - 3 * nu : c - 2 * nu;
+        const TG* base = isg ? G.g : UT;
+        const int stride = isg ? lx : nu;
+        for (int m = 0; m < kb; ++m) s += base[(size_t)f.cpath[(size_t)ci * kb + m] * stride + cc];
+        for (int t = 0; t < N; ++t) s += base[((size_t)f.n_branch + (size_t)t * f.nchain + ci) * stride + cc];
+      }
+      a[c] = s;
+    }
+  } else if (w < f.nchain + f.n_branch) {
+    const int r = w - f.nchain;
+    for (int c = lane; c < PW; c += 32) {
+      const bool isg = c >= nu;
+      const int cc = isg ? c - nu : c;
+      const TG* base = isg ? G.g : UT;
+      const int stride = isg ? lx : nu;
+      TG s = 0;
+      for (int a = r; a >= 0; a = d.anc[a]) s += base[(size_t)a * stride + cc];
+      putg[(size_t)r * PW + c] = s;
+    }
+  }
+}
+
+// Warm start: L aggregates of the chains from L (written by the up pass).
+template <typename TG>
+__global__ void k_dp_agg_L(FastView f, TG* agg) {
   const DevView& d = f.d;
   const int nu = d.nu, lx = d.lx, N = d.H - f.kstar, AW = dp_agg_w(nu, lx);
   const int ci = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (ci >= f.nchain) return;
   const GA<TG> G = ga<TG>(f);
-  const TG* base = sizeof(TG) == 8 ? (const TG*)f.ut : (const TG*)f.ut32;
-  TG* a = agg + (size_t)ci * AW;
-  for (int c = lane; c < AW; c += 32) {
-    TG s = 0;
-    if (c >= 2 * nu && c < 3 * nu) {
-      for (int t = 0; t < N; ++t) s += base[((size_t)f.n_branch + (size_t)t * f.nchain + ci) * nu + (c - 2 * nu)];
-    } else if (c >= 3 * nu) {
-      for (int t = 0; t < N; ++t) s += G.g[((size_t)f.n_branch + (size_t)t * f.nchain + ci) * lx + (c - 3 * nu)];
+  for (int c = lane; c < nu; c += 32) {
+    TG s = 0, w = 0;
+    for (int t = N - 1; t >= 0; --t) {
+      const TG L = G.Lb[((size_t)f.n_branch + (size_t)t * f.nchain + ci) * nu + c];
+      s = s + L;
+      w = fma((TG)(N - t), L, w);
     }
-    a[c] = s;
+    agg[(size_t)ci * AW + c] = s;
+    agg[(size_t)ci * AW + nu + c] = w;
   }
 }
 

@@ -80,16 +80,42 @@ def test_dp_uneven_tree_vs_oracle(monkeypatch):
     assert abs(res.objective - ref.objective) <= 1e-8 * (1 + abs(ref.objective))
 
 
-def test_dp_check_iterations_and_certificates_midway(monkeypatch):
-    """Convergence run: certificates between iteration chunks use scratch
-    buffers and must leave k_chain_dp's carried state (L, aggregates, chain
-    totals) intact: same iteration count and termination as the graph path."""
+def test_dp_certificates_between_chunks_leave_the_iteration_state_intact(monkeypatch):
+    """Check iterations run the certificate between iteration chunks; it uses
+    scratch buffers, so k_chain_dp's carried state (L, aggregates, chain
+    totals, branching rows' Yc) is untouched: 200 iterations in chunks of 25
+    with a certificate after each chunk are bit-identical to 200 without."""
+    inst = config_instance("C1")
+    out = []
+    for cert in (False, True):
+        cache = _cache(inst, monkeypatch, True)
+        ctx = cache._bind()
+        S._upload_bounds(ctx, inst)
+        th = S.theta_sequence(200)
+        be = S._beta_table(th)
+        ctx.call("wmpc_apg_begin", 1.0 / 2e9, 200, nat.ptr(th), nat.ptr(be))
+        for _ in range(8):
+            ctx.call("wmpc_apg_run", 25)
+            if cert:
+                S._certificate(ctx)
+        out.append(S._read(ctx, inst, True))
+    for a, b in zip(out[0], out[1]):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_dp_convergence_run_matches_graph_iteration(monkeypatch):
+    """A convergence run (checks every 25 iterations, certificates once the
+    residual is small): same termination and iteration count as the graph
+    path; iterates within the instance's own rounding-noise amplification
+    over 3,000 iterations (the oracle against itself with 1-ulp noise per
+    iteration: u0 6.4e-5, dual 1.6e-4 relative, measured on C1)."""
     inst = config_instance("C1")
     a, b = _pair(inst, monkeypatch, max_iter=3000, tol=2e-2, gap_check_every=25)
     assert a.termination == b.termination
     assert a.iterations == b.iterations
-    assert rel_err(a.u0, b.u0) <= 1e-9
-    assert rel_err(a.dual, b.dual) <= 1e-9
+    assert rel_err(a.u0, b.u0) <= 1e-3
+    assert rel_err(a.dual, b.dual) <= 1e-3
+    assert abs(a.objective - b.objective) <= 1e-6 * (1 + abs(b.objective))
 
 
 def test_dp_warm_start(monkeypatch):
@@ -104,7 +130,9 @@ def test_dp_warm_start(monkeypatch):
         assert rel_err(getattr(out[0], k), getattr(out[1], k)) <= 1e-10, k
 
 
-def test_dp_fp32_mode(monkeypatch):
+def test_dp_context_fp32_mode(monkeypatch):
+    """fp32 mode on a context configured for k_chain_dp runs the four-kernel
+    graph (k_chain_dp is fp64-only: measured slower in fp32)."""
     inst = config_instance("C2")
     a, b = _pair(inst, monkeypatch, max_iter=100, tol=1e-30, gamma=1 / 2e9, gap_check_every=101,
                  precision="fp32")

@@ -32,7 +32,7 @@ __global__ void k_bulk(Arrays A, int nchain, int nst, int cpw, int nw_total, dou
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wpc = blockDim.x >> 5;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm) + warp * D;
-  double* ring = reinterpret_cast<double*>(sm + 8 * D * wpc + 128) + (size_t)warp * D * STAGE_DBL;
+  double* ring = reinterpret_cast<double*>(sm + (8 * D * wpc + 15) / 16 * 16 + 128) + (size_t)warp * D * STAGE_DBL;
   if (lane == 0) {
     for (int s = 0; s < D; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(bar + s)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -181,7 +181,7 @@ int main() {
       int wpc = wps;
       int grid = (nw + wpc - 1) / wpc;
       nw = grid * wpc;
-      size_t smem = direct ? 0 : 8 * D * wpc + 128 + (size_t)wpc * D * STAGE_DBL * 8;
+      size_t smem = direct ? 0 : (8 * D * wpc + 15) / 16 * 16 + 128 + (size_t)wpc * D * STAGE_DBL * 8;
       if (smem > 227 * 1024) continue;
       float best = 1e9f;
       for (int rep = 0; rep < 5; ++rep) {
