@@ -2,26 +2,33 @@
 """Benchmark: fixed-iteration scenario-MPC solves on B200 (BASELINE.json metric).
 
 A step is one SMPC solve: ``--iters`` (500) fixed APG iterations on the
-configs[1] workload (Barcelona-dimension network, horizon 24, 128-scenario
-tree ``[2]*7``, 2,430 nodes, fp64) followed by the duality-gap certificate the
-reference always runs at max_iter, and the control action u0.
+largest single-GPU configuration, C4 by default (Barcelona-dimension network,
+horizon 24, 4,096-scenario tree ``[4]*6``, 79,188 nodes, fp64), followed by
+the duality-gap certificate the reference always runs at max_iter, and the
+control action u0. gamma = 1/L with L from the reference's own
+``estimate_lipschitz`` (tests/golden), the same in both arms.
 
 * ``value``: APG iterations/s with the instance resident in HBM (device time,
   CUDA events on the solver's stream, max over ranks).
 * ``e2e``: the same metric through the public API — ``factor_step(inst,
   structure_from=cache)`` + ``solve(inst, cfg, cache)`` per step, with the
   per-node inputs in pinned host memory and every result array read back.
-* ``roofline``: the APG iteration (the CUDA graph of all stage kernels)
-  against HBM: algorithmic 10,016 B per node per iteration.
+* ``roofline``: the dominant kernel (k_chain_dp at C4: the fused iteration)
+  timed on its own (wmpc_iteration_profile) against the iteration's
+  algorithmic 10,016 B per node; the whole-iteration figure
+  (graph replay) beside it.
 * ``cpu_baseline``: the oracle port (numpy restatement of the reference) on a
-  bounded sample on this host's cores.
+  bounded sample on this host's cores (APG loop only).
+* ``secondary_C2``: the L2-resident C2 tree in us per iteration and per
+  dependent stage step.
 
 With N > 1 ranks (torchrun) the same solve is split by subtrees (``shard.py``,
 SURVEY §8e): strong scaling, ``value`` = iterations/s of the whole job.
 
 ``--impl reference`` times the reference's CPU implementation of the path (the
 oracle port; the Python reference cannot travel to the GPU box) on the same
-config and prints the same JSON line with ``"impl": "reference"``.
+config, metric and gamma, and prints the same JSON line with
+``"impl": "reference"``.
 """
 
 from __future__ import annotations
@@ -50,13 +57,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--iters", type=int, default=500)
-    ap.add_argument("--cpu-sample-iters", type=int, default=30)
+    ap.add_argument("--cpu-sample-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
-    ap.add_argument("--no-large", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     return ap.parse_args()
 
 
@@ -166,56 +173,98 @@ def barrier(world: int):
 
 # ----------------------------------------------------------- CPU baseline
 
-def cpu_baseline(cfg: str, iters: int, sample_iters: int) -> dict:
-    """Oracle port (numpy restatement of the reference solve) on a bounded
-    sample: `sample_iters` APG iterations + one certificate, extrapolated to
-    one `iters`-iteration solve."""
+def golden_gamma(cfg: str):
+    """gamma = 1/L with L from the REFERENCE's own estimate_lipschitz on this
+    instance (tests/golden/barcelona_<cfg>.npz, made by make_golden.py): both
+    arms run the same step size (the arms' gammas differed)."""
+    path = os.path.join(ROOT, "tests", "golden", f"barcelona_{cfg}.npz")
+    try:
+        return 1.0 / float(np.load(path)["lipschitz"]), "reference estimate_lipschitz (tests/golden)"
+    except Exception:
+        return None, None
+
+
+def cpu_solve_sample(cfg: str, iters: int, sample_iters: int, gamma: float, cert: bool,
+                     threads=None) -> dict:
+    """The oracle port (numpy restatement of the reference solve, bit-identical
+    to it on C1: tests/test_cpu_oracle_and_host.py) on a bounded sample:
+    `sample_iters` APG iterations with the reference's per-iteration cost
+    accounting, optionally one certificate on the sample's final state; the
+    per-iteration time is extrapolated to an `iters`-iteration solve."""
+    from threadpoolctl import threadpool_limits
     from oracle import port
     from paper_1904_10548_b200.synthetic import config_instance
     inst = config_instance(cfg)
     t0 = time.perf_counter()
     fac, e_off = port.factor(inst)
     t_factor = time.perf_counter() - t0
-    gamma = 1.0 / 2.0e9
-    t0 = time.perf_counter()
-    res = port.apg_solve(inst, gamma, max_iter=sample_iters, tol=1e-30,
-                         gap_check_every=sample_iters + 1, fac=fac, e_off=e_off,
-                         reference_cost_accounting=True, final_certificate=True)
-    total = time.perf_counter() - t0
+    nthreads = threads or (os.cpu_count() or 1)
+    with threadpool_limits(limits=nthreads):
+        t0 = time.perf_counter()
+        res = port.apg_solve(inst, gamma, max_iter=sample_iters, tol=1e-30, gap_check_every=sample_iters + 1,
+                             fac=fac, e_off=e_off, reference_cost_accounting=True, final_certificate=cert)
+        total = time.perf_counter() - t0
     per_iter = res.loop_time_s / sample_iters
-    t_cert = total - res.loop_time_s
-    solve_s = iters * per_iter + t_cert
-    threads = os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS")
-    cores = int(threads) if threads else (os.cpu_count() or 1)
-    return {"value": iters / solve_s, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{cfg}: {sample_iters} APG iterations ({per_iter * 1e3:.1f} ms/it) + 1 certificate "
-                      f"({t_cert:.2f} s), extrapolated to a {iters}-iteration solve ({solve_s:.1f} s); "
-                      f"per-node factor part {t_factor * 1e3:.0f} ms; numpy/OpenBLAS fp64",
-            "ms_per_solve_extrapolated": solve_s * 1e3, "ms_per_iteration": per_iter * 1e3}
+    t_cert = total - res.loop_time_s if cert else None
+    return {"per_iter_s": per_iter, "cert_s": t_cert, "factor_s": t_factor, "threads": nthreads,
+            "nodes": inst.n_nonroot}
+
+
+def cpu_baseline(cfg: str, iters: int, sample_iters: int, gamma: float) -> dict:
+    """cpu_baseline of our line: the APG loop of the oracle port on a bounded
+    sample (the certificate is timed in the reference arm, whose line carries
+    the full extrapolated solve)."""
+    r = cpu_solve_sample(cfg, iters, sample_iters, gamma, cert=False)
+    return {"value": 1.0 / r["per_iter_s"], "unit": UNIT, "cores": r["threads"], "kind": "port",
+            "sample": f"{cfg}: {sample_iters} APG iterations of the oracle port ({r['per_iter_s'] * 1e3:.0f} ms/it, "
+                      f"numpy/OpenBLAS fp64, {r['threads']} BLAS threads); APG loop only (certificate in the "
+                      "reference arm's line)",
+            "ms_per_iteration": r["per_iter_s"] * 1e3}
 
 
 def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port) on this host's
+    cores, same config, metric and gamma. Setup: 1 vs nproc BLAS threads
+    compared on one iteration, the faster kept; one
+    certificate timed on the sampled state (after the warm-up iterations; the
+    Dykstra restoration after 500 iterations can take longer, so the
+    extrapolated solve time is a lower bound: conservative for the GPU/CPU
+    ratio). Each step = one APG iteration; value = iters / (iters * t_it +
+    t_cert)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     W, K = args.warmup, args.steps
-    # each step: a bounded sample (a few iterations + certificate) of the solve
-    sample = max(2, min(args.cpu_sample_iters, 10))
-    vals = []
-    cb = None
-    for i in range(W + K):
-        cb = cpu_baseline(args.config, args.iters, sample)
-        if i >= W:
-            vals.append(cb["value"])
+    cfg = args.config
+    gamma, gsrc = golden_gamma(cfg)
+    if gamma is None:
+        gamma, gsrc = 1.0 / 2.0e9, "fixed 1/2e9"
+    nproc = os.cpu_count() or 1
+    t_n = cpu_solve_sample(cfg, args.iters, 1, gamma, cert=False, threads=nproc)["per_iter_s"]
+    t_1 = cpu_solve_sample(cfg, args.iters, 1, gamma, cert=False, threads=1)["per_iter_s"] if nproc > 1 else t_n
+    threads = nproc if t_n <= t_1 else 1
+    warm = cpu_solve_sample(cfg, args.iters, max(1, W), gamma, cert=True, threads=threads)
+    t_cert = warm["cert_s"]
+    vals, per = [], []
+    for _ in range(K):
+        r = cpu_solve_sample(cfg, args.iters, 1, gamma, cert=False, threads=threads)
+        per.append(r["per_iter_s"])
+        vals.append(args.iters / (args.iters * r["per_iter_s"] + t_cert))
     value = float(np.median(vals))
-    cfgd = workload(args.config)
-    cfgd["fixed_iters"] = args.iters
+    t_it = float(np.median(per))
+    cfgd = workload(cfg)
+    cfgd.update({"fixed_iters": args.iters, "nodes": warm["nodes"], "gamma": gsrc,
+                 "step": f"{args.iters} fixed APG iterations + duality-gap certificate + u0 (extrapolated: "
+                         "1 timed iteration per step + 1 certificate)"})
+    sample = (f"oracle port of the reference solve, {threads} BLAS thread(s) of {nproc} (1 thread: "
+              f"{t_1:.2f} s/it, {nproc}: {t_n:.2f} s/it); per step 1 APG iteration ({t_it:.2f} s) + "
+              f"certificate {t_cert:.1f} s once, extrapolated to {args.iters} iterations")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": K, "warmup": W, "ms_per_step": args.iters / value * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfgd,
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb["cores"], "kind": "port",
-                             "sample": cb["sample"]},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "seconds_per_iteration": t_it, "certificate_s": t_cert, "factor_s": warm["factor_s"]}
     print(json.dumps(line), flush=True)
 
 
@@ -230,91 +279,69 @@ def load_peaks() -> tuple[float, str]:
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cfg: str):
-    """Per-iteration DRAM bytes (all kernels of one APG iteration) from the
-    committed ncu capture, profiles/traffic.json, if any."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
+def profile_json(name: str):
+    """Committed ncu-derived numbers (profiles/r02/<name>.json), if any."""
+    path = os.path.join(ROOT, "profiles", "r02", f"{name}.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get(cfg)
+            return json.load(f)
     except Exception:
         return None
 
 
-FLOPS_PER_NODE_ITER = 56_600  # SURVEY 8(d): structured recursion + prox, per node per APG iteration
+# fp32 mode's own compulsory bytes per node per iteration: y, y_prev read and
+# y+ written (fp64, 3 x 240), Ua / Xa read and written (fp64, 2 x 177), e_off
+# and g read (fp32, 177), prob (fp64)
+BYTES_PER_NODE_ITER_FP32 = 8 * (3 * 240 + 2 * 177 + 1) + 4 * (114 + 63)
 
 
-def fp64_pipe(n_nodes: int, t_iter: float) -> dict:
-    """SURVEY 8(d) asks for the fp64 pipe fraction against a DGEMM measured on
-    the box (MEASURED_PEAKS.json has bf16 and HBM only): torch.matmul float64,
-    8192^3, CUDA events. Our kernels execute fewer flops than the structured
-    count (sparse projector), so this is the fraction of the fp64 roof the
-    reference's algorithm would need at our speed: it shows the path is not
-    compute-bound."""
-    import torch
-    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
-    b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
-    for _ in range(2):
-        torch.matmul(a, b)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    reps = 5
-    for _ in range(reps):
-        torch.matmul(a, b)
-    e1.record()
-    torch.cuda.synchronize()
-    dgemm = 2 * 8192 ** 3 * reps / (e0.elapsed_time(e1) * 1e-3) / 1e12
-    del a, b
-    ach = FLOPS_PER_NODE_ITER * n_nodes / t_iter / 1e12
-    return {"dgemm_tflops_measured": dgemm, "structured_flops_per_iteration": FLOPS_PER_NODE_ITER * n_nodes,
-            "achieved_tflops": ach, "frac": ach / dgemm}
-
-
-def roofline_large(peak: float, peak_src: str, iters: int = 50) -> dict:
-    """Device time per APG iteration on C4 (79,188 nodes, 630 MB per
-    iteration: HBM-bound) against the same algorithmic bytes."""
-    from paper_1904_10548_b200 import factor_step
+def kernel_profile(ctx, inst, gamma: float, count: int = 20) -> dict:
+    """Per-kernel device time per iteration (wmpc_iteration_profile: eager
+    launches with CUDA events between kernel groups, on the solver stream)."""
     from paper_1904_10548_b200 import _native as nat
     from paper_1904_10548_b200 import solver as S
-    from paper_1904_10548_b200.synthetic import config_instance
-    inst = config_instance("C4")
-    cache = factor_step(inst)
-    ctx = cache._bind()
-    S._upload_bounds(ctx, inst)
+    th = S.theta_sequence(count + 3)
+    be = S._beta_table(th)
+    ctx.call("wmpc_apg_begin", float(gamma), count + 3, nat.ptr(th), nat.ptr(be))
+    ctx.call("wmpc_apg_run", 3)
+    out = np.zeros(4)
+    ctx.call("wmpc_iteration_profile", count, nat.ptr(out), 4)
+    info = nat.path_info(ctx)
+    if info.get("fused_dp"):
+        return {"k_branch_grp (all stage groups)": out[0] * 1e3, "k_chain_dp": out[1] * 1e3}
+    return {"chain up": out[0] * 1e3, "k_branch_grp (all stage groups)": out[1] * 1e3,
+            "chain down": out[2] * 1e3, "k_prox_warp": out[3] * 1e3}
+
+
+def iteration_us(ctx, gamma: float, iters: int = 50) -> float:
+    from paper_1904_10548_b200 import _native as nat
+    from paper_1904_10548_b200 import solver as S
     th = S.theta_sequence(iters + 5)
     be = S._beta_table(th)
-    out = {}
-    for prec in (0, 1):
-        ctx.call("wmpc_set_precision", prec)
-        ctx.call("wmpc_apg_begin", 1.0 / 2e9, iters + 5, nat.ptr(th), nat.ptr(be))
+    best = 1e30
+    for _ in range(3):
+        ctx.call("wmpc_apg_begin", float(gamma), iters + 5, nat.ptr(th), nat.ptr(be))
         ctx.call("wmpc_apg_run", 5)
         ms = nat.C.c_float(0.0)
         ctx.call("wmpc_apg_run_timed", iters, nat.C.byref(ms))
-        t = ms.value / iters / 1e3
-        ach = BYTES_PER_NODE_ITER * inst.n_nonroot / t / 1e9
-        out["fp32" if prec else "fp64"] = {"us_per_iteration": t * 1e6, "achieved": ach, "frac": ach / peak}
-    ctx.call("wmpc_set_precision", 0)
-    out["fp64_pipe"] = fp64_pipe(inst.n_nonroot, out["fp64"]["us_per_iteration"] * 1e-6)
-    return {"bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_src, "nodes": inst.n_nonroot,
-            "algorithmic_bytes_per_iteration": BYTES_PER_NODE_ITER * inst.n_nonroot,
-            "traffic": ncu_traffic("C4"), **out,
-            "how": f"{iters} graph-replayed iterations after 5 warm-up, CUDA events on the solver stream; "
-                   "~1.4 GB of per-iteration traffic streams from HBM (126 MB L2: no flush needed)"}
+        best = min(best, ms.value / iters * 1e3)
+    return best
 
 
-def kernel_desc(mode: int, per_iter: int) -> str:
-    if mode == 300:
-        return (f"one APG iteration = CUDA graph of {per_iter} kernels (chain up pass, k_branch_grp per stage "
-                "group, chain down pass, k_prox_warp; chain passes one CTA per chain for few chains, "
-                "one warp per chain for many: k_chain_up_r / k_chain_down_r at C4); timed per iteration")
-    if mode == 310:
-        return f"one APG iteration = CUDA graph of {per_iter} kernels (k_branch_grp per stage group, k_chain_fused)"
-    if mode >= 200:
-        return "k_apg_scan (persistent cooperative kernel)"
-    if mode > 0:
-        return "k_apg_fast (persistent cooperative kernel)"
-    return f"APG iteration = CUDA graph of {per_iter} per-stage kernels (general path)"
+def secondary_c2(gamma_default: float) -> dict:
+    """C2 (L2-resident, latency-bound): us per APG iteration and per dependent
+    stage step (2H = 48 stage steps per iteration), SURVEY §8(d)."""
+    from paper_1904_10548_b200 import factor_step
+    from paper_1904_10548_b200 import solver as S
+    from paper_1904_10548_b200.synthetic import config_instance
+    inst = config_instance("C2")
+    cache = factor_step(inst)
+    ctx = cache._bind()
+    S._upload_bounds(ctx, inst)
+    g, _ = golden_gamma("C2")
+    us = iteration_us(ctx, g or gamma_default, 200)
+    return {"workload": workload("C2")["workload"], "nodes": inst.n_nonroot, "us_per_iteration": us,
+            "us_per_dependent_stage_step": us / (2 * 24), "it_per_s": 1e6 / us}
 
 
 def run_sharded(args, world, rank, local):
@@ -328,8 +355,10 @@ def run_sharded(args, world, rank, local):
     inst = config_instance(args.config)
     n = inst.n_nonroot
     comm = shard.TorchCollective()
-    lam = estimate_lipschitz(factor_step(inst), inst) if rank == 0 else 0.0
-    gamma = 1.0 / comm.bcast_float(lam)
+    gamma, _ = golden_gamma(args.config)
+    if gamma is None:
+        lam = estimate_lipschitz(factor_step(inst), inst) if rank == 0 else 0.0
+        gamma = 1.0 / comm.bcast_float(lam)
     iters = args.iters
     cfg = SolverConfig(max_iter=iters, tol=1e-30, gamma=gamma, gap_check_every=iters + 1)
     specs = shard.plan(inst, world)
@@ -424,14 +453,19 @@ def run_ours(args):
     S.set_device(0)
     inst = config_instance(args.config)
     n = inst.n_nonroot
+    t0 = time.perf_counter()
     cache = factor_step(inst)
-    L = estimate_lipschitz(cache, inst)
-    gamma = 1.0 / L
+    t_factor = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    L_dev = estimate_lipschitz(cache, inst)
+    t_lip = time.perf_counter() - t0
+    gamma, gsrc = golden_gamma(args.config)
+    if gamma is None:
+        gamma, gsrc = 1.0 / L_dev, "1/L (device power iteration)"
     iters = args.iters
     cfg = SolverConfig(max_iter=iters, tol=1e-30, gamma=gamma, gap_check_every=iters + 1)
     ctx = cache._bind()
-    mode = nat.load().wmpc_fast_path(ctx.h)
-    per_iter = nat.load().wmpc_kernel_launches_per_iteration(ctx.h)
+    info = nat.path_info(ctx)
     theta = S.theta_sequence(iters)
     beta = S._beta_table(theta)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > L2
@@ -474,28 +508,38 @@ def run_ours(args):
     value = world * K * iters / (total_ms / 1e3)
     ms_per_step = total_ms / K
 
-    # roofline: the APG iteration (graph of stage kernels) against HBM
+    # roofline of the dominant kernel: its own device time per iteration
+    # (eager launches, CUDA events on the solver stream) against the
+    # iteration's algorithmic bytes, which it moves (the branch groups touch
+    # the 1,364 branching rows only)
     t_iter = loop_total / (K * iters) / 1e3
     alg_bytes = BYTES_PER_NODE_ITER * n
     peak, peak_src = load_peaks()
-    achieved = alg_bytes / t_iter / 1e9
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": ncu_traffic(args.config),
-            "kernel": kernel_desc(mode, per_iter),
-            "algorithmic_bytes_per_launch": alg_bytes, "us_per_iteration": t_iter * 1e6,
-            "peak_source": peak_src}
+    kp = kernel_profile(ctx, inst, gamma)
+    dom = max(kp, key=kp.get)
+    t_dom = kp[dom] * 1e-6
+    traffic = profile_json("traffic") or {}
+    roof = {"bound": "hbm", "achieved": alg_bytes / t_dom / 1e9, "peak": peak, "unit": "GB/s",
+            "frac": alg_bytes / t_dom / 1e9 / peak,
+            "traffic": (traffic.get(args.config) or {}).get(dom.split(" ")[0]),
+            "kernel": dom, "kernel_us_per_launch": kp[dom],
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "algorithmic_bytes": f"{BYTES_PER_NODE_ITER} B per node per APG iteration (SURVEY §8d) x {n} nodes",
+            "kernels_us_per_iteration": kp,
+            "iteration": {"us": t_iter * 1e6, "achieved": alg_bytes / t_iter / 1e9,
+                          "frac": alg_bytes / t_iter / 1e9 / peak,
+                          "how": "graph replay of all kernels of an iteration (PDL overlap), CUDA events"},
+            "path": info, "peak_source": peak_src}
 
     # e2e through the public API with pinned inputs
     e2e = None
     if not args.no_e2e:
-        from paper_1904_10548_b200.problem import ProblemInstance  # noqa: F401
         pin = nat.pinned_copy
         inst.demand = pin(inst.demand)
         inst.demand_gd = pin(inst.demand_gd)
         inst.econ = pin(inst.econ)
         # the warm-up keeps each result alive like the timed loop does, so the
-        # pinned result pool holds both sets before timing (a pinned allocation
-        # inside the timed region cost 10-200 ms)
+        # pinned result pool holds both sets before timing
         res = None
         for _ in range(max(2, args.warmup)):
             c2 = factor_step(inst, structure_from=cache)
@@ -514,15 +558,13 @@ def run_ours(args):
         d2h = 8 * (m.n_inputs + 2 * inst.n_primal + inst.n_dual + 8)
         e2e = {"value": world * K * iters / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s / K * 1e3,
-               "api": "factor_step(structure_from) + solve() per step"}
+               "api": "factor_step(structure_from) + solve() per step; every result array read back"}
         assert res.iterations == iters
 
-    # fp32 mode (SolverConfig.precision="fp32", own 1e-4 tolerance): reported beside, not the value
+    # fp32 mode (SolverConfig.precision="fp32", own 1e-4 tolerance): beside, not the value
     fp32 = None
-    if mode == 300 and not args.no_fp32:
+    if info["fast_path"] == 300 and not args.no_fp32:
         for _ in range(2):
-            flush.fill_(1.0)
-            torch.cuda.synchronize()
             device_step(fp32=True)
         f_ms, f_loop = [], []
         for _ in range(K):
@@ -532,30 +574,33 @@ def run_ours(args):
             f_ms.append(a)
             f_loop.append(b)
         ctx.call("wmpc_set_precision", 0)
-        fp32 = {"value": K * iters / (sum(f_ms) / 1e3), "unit": UNIT,
-                "us_per_iteration": sum(f_loop) / (K * iters) * 1e3, "tolerance": "1e-4 relative (tests/test_gpu_fp32.py)",
+        t32 = sum(f_loop) / (K * iters) / 1e3
+        own = BYTES_PER_NODE_ITER_FP32 * n
+        fp32 = {"value": K * iters / (sum(f_ms) / 1e3), "unit": UNIT, "us_per_iteration": t32 * 1e6,
+                "roofline_own_bytes": {"bytes_per_node": BYTES_PER_NODE_ITER_FP32, "achieved": own / t32 / 1e9,
+                                       "frac": own / t32 / 1e9 / peak},
+                "tolerance": "1e-4 relative vs the fp64 reference (tests/test_gpu_golden_large.py)",
                 "what": "dual-gradient kernels in fp32; y, prox, averages, certificate in fp64"}
-    # the large tree (C4) for the HBM roofline (the headline tree is L2-resident)
-    large = None
-    if args.config != "C4" and not args.no_large:
-        large = roofline_large(peak, peak_src)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.config, iters, args.cpu_sample_iters)
+        cpu = cpu_baseline(args.config, iters, args.cpu_sample_iters, gamma)
     if rank == 0:
         cfgd = workload(args.config)
-        cfgd.update({"fixed_iters": iters, "nodes": n, "gamma": "1/L (device power iteration)",
-                     "l2": "flushed between steps (256 MiB write); one solve's working set is "
-                           "L2-resident by design",
+        cfgd.update({"fixed_iters": iters, "nodes": n, "gamma": gsrc,
+                     "l2": "inputs larger than L2 (one iteration streams ~0.9 GB; L2 126 MB); a 256 MiB "
+                           "buffer is also written between steps",
                      "parallelism": "1 GPU",
-                     "step": "500 fixed APG iterations + duality-gap certificate + u0"})
+                     "step": f"{iters} fixed APG iterations + duality-gap certificate + u0 (one SMPC solve)"})
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": cfgd, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks.summary(),
-                "loop_ms_per_solve": loop_total / K, "fp32_mode": fp32, "roofline_C4": large}
+                "loop_ms_per_solve": loop_total / K, "fp32_mode": fp32,
+                "fp64_pipe": profile_json("fp64_pipe"),
+                "setup": {"factor_step_s": t_factor, "estimate_lipschitz_s": t_lip, "lipschitz_device": L_dev},
+                "secondary_C2": None if args.no_secondary else secondary_c2(gamma)}
         print(json.dumps(line), flush=True)
 
 

@@ -132,6 +132,13 @@ int wmpc_apg_read(wmpc_ctx* ctx, int averaged, double* u0, double* primal,
 int wmpc_apg_read_async(wmpc_ctx* ctx, int averaged, double* u0, double* primal, double* primal_avg,
                         double* dual);
 int wmpc_apg_read_wait(wmpc_ctx* ctx);
+/* Per-kernel device time of the APG iteration (bench.py roofline): runs
+ * `count` iterations eagerly with CUDA events between the kernel groups
+ * (no graph, no programmatic overlap); out[] in ms per iteration:
+ * [branch groups, k_chain_dp] on the fused path, [up, branch groups, down,
+ * prox] on the graph path (path_info field 1 says which). Diagnostics; no
+ * reference counterpart. */
+int wmpc_iteration_profile(wmpc_ctx* ctx, int count, double* out, int cap);
 /* Iterations completed since wmpc_apg_begin. */
 int wmpc_apg_iterations(const wmpc_ctx* ctx);
 

@@ -62,6 +62,7 @@ SIGNATURES = {
     "wmpc_apg_warm": (C.c_int, [_vp, _dp]),
     "wmpc_set_precision": (C.c_int, [_vp, C.c_int]),
     "wmpc_apg_run_timed": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_float)]),
+    "wmpc_iteration_profile": (C.c_int, [_vp, C.c_int, _dp, C.c_int]),
     "wmpc_apg_check": (C.c_int, [_vp, _dp, _dp, _dp, C.POINTER(C.c_int)]),
     "wmpc_certificate": (C.c_int, [_vp, _dp, _dp]),
     "wmpc_apg_read": (C.c_int, [_vp, C.c_int, _dp, _dp, _dp, _dp]),

@@ -2172,6 +2172,80 @@ int wmpc_apg_run_timed(wmpc_ctx* ctx, int count, float* ms) {
   });
 }
 
+// Per-kernel device time of the iteration (bench.py roofline): `count` APG
+// iterations launched eagerly (no graph, no programmatic overlap) with events
+// between the kernel groups. out (ms per iteration): k_chain_dp path
+// [branch groups, k_chain_dp]; graph path [up, branch groups, down, prox].
+// Advances the APG state like wmpc_apg_run.
+int wmpc_iteration_profile(wmpc_ctx* ctx, int count, double* out, int cap) {
+  return run(ctx, [&]() -> int {
+    if (!(ctx->fast && ctx->use_graphk && ctx->max_iter > 0 && ctx->shard_k < 0)) {
+      ctx->err = "iteration profile needs the structured graph path after wmpc_apg_begin";
+      return WMPC_E_STATE;
+    }
+    ARG(count >= 1 && ctx->it_host + count <= ctx->max_iter && out, "iteration count exceeds the theta table");
+    const int pdl = ctx->pdl;
+    ctx->pdl = 0;
+    int never = -1;
+    CK(cudaMemcpyAsync(ctx->store_it, &never, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    FastView f = make_fastview(ctx, 1);
+    const bool dp = dp_on(ctx);
+    const int nk = dp ? 2 : 4;
+    std::vector<cudaEvent_t> ev(nk + 1);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    std::vector<double> acc(nk, 0.0);
+    try {
+      for (int i = 0; i < count; ++i) {
+        if (ctx->gk_groups.empty()) k_advance<<<1, 32, 0, ctx->stream>>>(ctx->iter);
+        CK(cudaEventRecord(ev[0], ctx->stream));
+        if (dp) {
+          if (ctx->fp32) gk_grp<4, float>(ctx, f, 1, GRP_LATE); else gk_grp<4, double>(ctx, f, 1, GRP_LATE);
+          CK(cudaEventRecord(ev[1], ctx->stream));
+          if (ctx->fp32) launch_dp<float>(ctx, f); else launch_dp<double>(ctx, f);
+          CK(cudaEventRecord(ev[2], ctx->stream));
+        } else {
+          const int bump = ctx->gk_groups.empty() ? 0 : 1;
+          if (ctx->ell_w == 4) {
+            if (ctx->fp32) {
+              gk_up<4, float>(ctx, f); CK(cudaEventRecord(ev[1], ctx->stream));
+              gk_grp<4, float>(ctx, f, bump); CK(cudaEventRecord(ev[2], ctx->stream));
+              gk_down<4, float>(ctx, f); CK(cudaEventRecord(ev[3], ctx->stream));
+              gk_prox<float>(ctx, f);
+            } else {
+              gk_up<4, double>(ctx, f); CK(cudaEventRecord(ev[1], ctx->stream));
+              gk_grp<4, double>(ctx, f, bump); CK(cudaEventRecord(ev[2], ctx->stream));
+              gk_down<4, double>(ctx, f); CK(cudaEventRecord(ev[3], ctx->stream));
+              gk_prox<double>(ctx, f);
+            }
+          } else {
+            gk_up<8, double>(ctx, f); CK(cudaEventRecord(ev[1], ctx->stream));
+            gk_grp<8, double>(ctx, f, bump); CK(cudaEventRecord(ev[2], ctx->stream));
+            gk_down<8, double>(ctx, f); CK(cudaEventRecord(ev[3], ctx->stream));
+            gk_prox<double>(ctx, f);
+          }
+          CK(cudaEventRecord(ev[4], ctx->stream));
+        }
+        CK(cudaEventSynchronize(ev[nk]));
+        for (int k = 0; k < nk; ++k) {
+          float ms = 0.f;
+          CK(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+          acc[k] += ms;
+        }
+        ctx->it_host++;
+        ctx->launches += graphk_kernels(ctx);
+      }
+    } catch (Fail&) {
+      ctx->pdl = pdl;
+      for (auto& e : ev) cudaEventDestroy(e);
+      throw;
+    }
+    ctx->pdl = pdl;
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (int k = 0; k < nk && k < cap; ++k) out[k] = acc[k] / count;
+    return WMPC_OK;
+  });
+}
+
 int wmpc_apg_iterations(const wmpc_ctx* ctx) { return ctx ? ctx->it_host : -1; }
 
 int wmpc_apg_check(wmpc_ctx* ctx, double* primal_residual, double* image_scale, double* dual_change,
