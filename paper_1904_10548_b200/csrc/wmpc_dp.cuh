@@ -224,6 +224,9 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     *PT = t;
   }
   __syncthreads();
+  const DpPtrs<TG> Q = *PT;  // in registers (no spill at <= 8 warps per SM)
+  const double gamma = pv[0], ig = pv[1], beta = pv[2], theta = pv[3], om = pv[4], beta1 = pv[5];
+  const double w_x = pv[6], w_s = pv[7];
   const int gw = blockIdx.x * wpc + warp, nw = gridDim.x * wpc;
   // ---- prox-row ring: owned ancestors then chain rows (bottom-up) of each
   // chain slot; one cp.async group per row (empty past the end)
@@ -244,51 +247,51 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         ic_cs = A.cpw;
         break;
       }
-      if (ic_pos == 0) ic_own = kb > 0 ? __ldg(PT->cown + ci) : 0u;
+      if (ic_pos == 0) ic_own = kb > 0 ? __ldg(Q.cown + ci) : 0u;
       if (ic_pos >= kb) {
         r = nbr + (unsigned)(N - 1 - (ic_pos - kb)) * nchain + (unsigned)ci;
         have = chain_row = true;
         break;
       }
       if ((ic_own >> ic_pos) & 1u) {
-        r = (unsigned)PT->cpath[(size_t)ci * kb + ic_pos];
+        r = (unsigned)Q.cpath[(size_t)ci * kb + ic_pos];
         have = true;
         break;
       }
     }
     if (have) {
       double* st = ring + (ic_k & (DP_D - 1)) * STG;
-      const double* s0 = PT->yb + (size_t)r * W + 2 * lane;
-      const double* s1 = PT->ymb + (size_t)r * W + 2 * lane;
+      const double* s0 = Q.yb + (size_t)r * W + 2 * lane;
+      const double* s1 = Q.ymb + (size_t)r * W + 2 * lane;
 #pragma unroll
       for (int k = 0; k < (W / 2 + 31) / 32; ++k)
         if (lane + 32 * k < W / 2) {
           cp16(st + 2 * lane + 64 * k, s0 + 64 * k);
           cp16(st + oYm + 2 * lane + 64 * k, s1 + 64 * k);
         }
-      const double* s2 = PT->Ua + (size_t)r * NU + 2 * lane;
+      const double* s2 = Q.Ua + (size_t)r * NU + 2 * lane;
 #pragma unroll
       for (int k = 0; k < (NU / 2 + 31) / 32; ++k)
         if (lane + 32 * k < NU / 2) cp16(st + oUa + 2 * lane + 64 * k, s2 + 64 * k);
-      const double* s3 = PT->Xa + (size_t)r * LX + 2 * lane;
+      const double* s3 = Q.Xa + (size_t)r * LX + 2 * lane;
 #pragma unroll
       for (int k = 0; k < (LX / 2 + 31) / 32; ++k)
         if (lane + 32 * k < LX / 2) cp16(st + oXa + 2 * lane + 64 * k, s3 + 64 * k);
       if constexpr (SDG) {
         if (chain_row) {
-          const double* s4 = reinterpret_cast<const double*>(PT->Lb) + (size_t)r * NU + 2 * lane;
-          const double* s5 = reinterpret_cast<const double*>(PT->UT) + (size_t)r * NU + 2 * lane;
+          const double* s4 = reinterpret_cast<const double*>(Q.Lb) + (size_t)r * NU + 2 * lane;
+          const double* s5 = reinterpret_cast<const double*>(Q.UT) + (size_t)r * NU + 2 * lane;
 #pragma unroll
           for (int k = 0; k < (NU / 2 + 31) / 32; ++k)
             if (lane + 32 * k < NU / 2) {
               cp16(st + oL + 2 * lane + 64 * k, s4 + 64 * k);
               cp16(st + oB + 2 * lane + 64 * k, s5 + 64 * k);
             }
-          const double* s6 = reinterpret_cast<const double*>(PT->g) + (size_t)r * LX + 2 * lane;
+          const double* s6 = reinterpret_cast<const double*>(Q.g) + (size_t)r * LX + 2 * lane;
 #pragma unroll
           for (int k = 0; k < (LX / 2 + 31) / 32; ++k)
             if (lane + 32 * k < LX / 2) cp16(st + oG + 2 * lane + 64 * k, s6 + 64 * k);
-          if (lane == 0) cp16(st + oAx, reinterpret_cast<const double*>(PT->aux) + (size_t)r * 2);
+          if (lane == 0) cp16(st + oAx, reinterpret_cast<const double*>(Q.aux) + (size_t)r * 2);
         }
       }
     }
@@ -331,8 +334,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
   // Moreau prox of one row (prox_x_warp / prox_u_warp arithmetic per element,
   // bit-exact with numpy), ergodic averages, next collapsed dual
   auto prox = [&](const double* st, unsigned r, const TG (&u)[4], const TG (&x)[2], TG (&yx)[2], TG (&yu)[4]) {
-    const double gamma = pv[0], ig = pv[1], beta = pv[2], theta = pv[3], om = pv[4];
-    double* yn = PT->ynb + (size_t)r * W;
+    double* yn = Q.ynb + (size_t)r * W;
     double v1[2], v2[2], V1[2], V2[2], c1[2], c2[2], y1[2], y2[2];
     {
       const double2 a = ld2s(st + l2), b = ld2s(st + oYm + l2), c = ld2s(st + oXa + l2);
@@ -356,11 +358,11 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       c1[1] = np_clip_u(V1[1], lo.y, hi.y);
       c2[0] = np_max_u(V2[0], sf.x);
       c2[1] = np_max_u(V2[1], sf.y);
-      double* xap = PT->Xa + (size_t)r * LX + l2;
+      double* xap = Q.Xa + (size_t)r * LX + l2;
       if (okx2) st2(xap, xan[0], xan[1]);
       else xap[0] = xan[0];
-      if (PT->store) {
-        TG* Xp = PT->X + (size_t)r * LX + l2;
+      if (Q.store) {
+        TG* Xp = Q.X + (size_t)r * LX + l2;
         if (okx2) st2(Xp, x[0], x[1]);
         else Xp[0] = x[0];
       }
@@ -388,18 +390,18 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
           const double v3 = dadd(dadd(y3[h], dmul(beta, dsub(y3[h], m3[h]))), dmul(gamma, uq));
           const double V3 = div_by(v3, gamma, ig);
           p3[q] = dsub(v3, dmul(gamma, np_clip_u(V3, l3[h], h3[h])));
-          yu[q] = (TG)dadd(p3[q], dmul(pv[5], dsub(p3[q], y3[h])));
+          yu[q] = (TG)dadd(p3[q], dmul(beta1, dsub(p3[q], y3[h])));
         }
       }
-      st2(PT->Ua + (size_t)r * NU + l2, uan[0], uan[1]);
+      st2(Q.Ua + (size_t)r * NU + l2, uan[0], uan[1]);
       st2(yn + 2 * NT + l2, p3[0], p3[1]);
       badacc = fma(p3[0], 0.0, fma(p3[1], 0.0, badacc));
-      if (PT->store) st2(PT->U + (size_t)r * NU + l2, u[0], u[1]);
+      if (Q.store) st2(Q.U + (size_t)r * NU + l2, u[0], u[1]);
       if (ok1) {
-        st2(PT->Ua + (size_t)r * NU + 64 + l2, uan[2], uan[3]);
+        st2(Q.Ua + (size_t)r * NU + 64 + l2, uan[2], uan[3]);
         st2(yn + 2 * NT + 64 + l2, p3[2], p3[3]);
         badacc = fma(p3[2], 0.0, fma(p3[3], 0.0, badacc));
-        if (PT->store) st2(PT->U + (size_t)r * NU + 64 + l2, u[2], u[3]);
+        if (Q.store) st2(Q.U + (size_t)r * NU + 64 + l2, u[2], u[3]);
       } else {
         yu[2] = yu[3] = TG(0);
       }
@@ -420,12 +422,11 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
 #pragma unroll
         for (int q = NB; q < NT; ++q) ssum = dadd(ssum, s2[q]);
         const double dist = __dsqrt_rn(ssum);
-        const double thr = dmul(ig, pv[6 + slot]);  // prox parameter RN(1/gamma) (solver.py:571)
+        const double thr = dmul(ig, slot ? w_s : w_x);  // prox parameter RN(1/gamma) (solver.py:571)
         stv = dist > 0.0 ? np_min(1.0, div_exact(thr, dist)) : 0.0;
       }
     }
     const double st1 = __shfl_sync(0xffffffffu, stv, 0), st2v = __shfl_sync(0xffffffffu, stv, 8);
-    const double beta1 = pv[5];
     double p1[2], p2[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -447,13 +448,13 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     }
   };
   auto ldrow = [&](unsigned r, TG (&L)[4], TG (&b)[4], TG (&g)[2], TG& ax) {  // down operands of a chain row
-    const auto a0 = ld2cg(PT->Lb + (size_t)r * NU + l2), a1 = ld2cg(PT->Lb + (size_t)r * NU + o1);
-    const auto b0 = ld2cg(PT->UT + (size_t)r * NU + l2), b1 = ld2cg(PT->UT + (size_t)r * NU + o1);
-    const auto g0 = ld2cg(PT->g + (size_t)r * LX + l2);
+    const auto a0 = ld2cg(Q.Lb + (size_t)r * NU + l2), a1 = ld2cg(Q.Lb + (size_t)r * NU + o1);
+    const auto b0 = ld2cg(Q.UT + (size_t)r * NU + l2), b1 = ld2cg(Q.UT + (size_t)r * NU + o1);
+    const auto g0 = ld2cg(Q.g + (size_t)r * LX + l2);
     L[0] = a0.x; L[1] = a0.y; L[2] = ok1 ? a1.x : TG(0); L[3] = ok1 ? a1.y : TG(0);
     b[0] = b0.x; b[1] = b0.y; b[2] = ok1 ? b1.x : TG(0); b[3] = ok1 ? b1.y : TG(0);
     g[0] = g0.x; g[1] = okx2 ? g0.y : TG(0);
-    ax = __ldcg(PT->aux + (size_t)r * 2);
+    ax = __ldcg(Q.aux + (size_t)r * 2);
   };
   for (int cs = 0; cs < A.cpw; ++cs) {
     const int ci = gw + cs * nw;
@@ -464,7 +465,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     if constexpr (!SDG) ldrow(nbr + (unsigned)(N - 1) * nchain + (unsigned)ci, Lc, bcur, gcur, axc);
     TG LSc[4], LWc[4], SU[4], SG[2];
     {
-      const TG* a = PT->agg + (size_t)ci * AW;
+      const TG* a = Q.agg + (size_t)ci * AW;
       const auto s0 = ld2cg(a + l2), s1 = ld2cg(a + o1), w0 = ld2cg(a + NU + l2), w1 = ld2cg(a + NU + o1);
       const auto u0 = ld2cg(a + 2 * NU + l2), u1 = ld2cg(a + 2 * NU + o1), g0 = ld2cg(a + 3 * NU + l2);
       LSc[0] = s0.x; LSc[1] = s0.y; LSc[2] = ok1 ? s1.x : TG(0); LSc[3] = ok1 ? s1.y : TG(0);
@@ -474,10 +475,10 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     }
     // ---- ancestors, top-down: ls = running sum of L, Ws = running sum of ls
     TG ls[4] = {0, 0, 0, 0}, Ws[4] = {0, 0, 0, 0};
-    const unsigned own = kb > 0 ? __ldg(PT->cown + ci) : 0u;
+    const unsigned own = kb > 0 ? __ldg(Q.cown + ci) : 0u;
     for (int m = 0; m < kb; ++m) {
-      const unsigned r = (unsigned)PT->cpath[(size_t)ci * kb + m];
-      const auto a0 = ld2cg(PT->Lb + (size_t)r * NU + l2), a1 = ld2cg(PT->Lb + (size_t)r * NU + o1);
+      const unsigned r = (unsigned)Q.cpath[(size_t)ci * kb + m];
+      const auto a0 = ld2cg(Q.Lb + (size_t)r * NU + l2), a1 = ld2cg(Q.Lb + (size_t)r * NU + o1);
       const TG La[4] = {a0.x, a0.y, ok1 ? a1.x : TG(0), ok1 ? a1.y : TG(0)};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -486,8 +487,8 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       }
       if ((own >> m) & 1u) {  // this chain owns branching row r: its u, x and prox
         TG ua[4], xa[2], sw[4], bw[2];
-        const auto b0 = ld2cg(PT->UT + (size_t)r * NU + l2), b1 = ld2cg(PT->UT + (size_t)r * NU + o1);
-        const TG* pg = PT->putg + (size_t)r * PW;
+        const auto b0 = ld2cg(Q.UT + (size_t)r * NU + l2), b1 = ld2cg(Q.UT + (size_t)r * NU + o1);
+        const TG* pg = Q.putg + (size_t)r * PW;
         const auto p0 = ld2cg(pg + l2), p1 = ld2cg(pg + o1), q0 = ld2cg(pg + NU + l2);
         const TG bu[4] = {b0.x, b0.y, ok1 ? b1.x : TG(0), ok1 ? b1.y : TG(0)};
         const TG PU[4] = {p0.x, p0.y, ok1 ? p1.x : TG(0), ok1 ? p1.y : TG(0)};
@@ -500,7 +501,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         prox(take(), r, ua, xa, yx, yu);
         release();
         if (next) {
-          TG* yc = PT->Yc + (size_t)r * LY;
+          TG* yc = Q.Yc + (size_t)r * LY;
           if (okx2) st2(yc + l2, yx[0], yx[1]);
           else yc[l2] = yx[0];
           st2(yc + LX + l2, yu[0], yu[1]);
@@ -591,16 +592,16 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         LSn[q] = LSn[q] + Ln[q];
         LWn[q] = fma(wt, Ln[q], LWn[q]);
       }
-      TG* Lp = PT->Lb + (size_t)r * NU;
+      TG* Lp = Q.Lb + (size_t)r * NU;
       st2(Lp + l2, Ln[0], Ln[1]);
       if (ok1) st2(Lp + 64 + l2, Ln[2], Ln[3]);
     }
     if (next) {  // chain totals for the branch groups, L aggregates for the next iteration
-      if (okx2) st2(PT->wbar + (size_t)r_top * LX + l2, wbr[0], wbr[1]);
-      else PT->wbar[(size_t)r_top * LX + l2] = wbr[0];
-      st2(PT->Asub + (size_t)r_top * NU + l2, acc[0], acc[1]);
-      if (ok1) st2(PT->Asub + (size_t)r_top * NU + 64 + l2, acc[2], acc[3]);
-      TG* a = PT->agg + (size_t)ci * AW;
+      if (okx2) st2(Q.wbar + (size_t)r_top * LX + l2, wbr[0], wbr[1]);
+      else Q.wbar[(size_t)r_top * LX + l2] = wbr[0];
+      st2(Q.Asub + (size_t)r_top * NU + l2, acc[0], acc[1]);
+      if (ok1) st2(Q.Asub + (size_t)r_top * NU + 64 + l2, acc[2], acc[3]);
+      TG* a = Q.agg + (size_t)ci * AW;
       st2(a + l2, LSn[0], LSn[1]);
       st2(a + NU + l2, LWn[0], LWn[1]);
       if (ok1) {
