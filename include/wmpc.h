@@ -158,6 +158,10 @@ int wmpc_fast_path(const wmpc_ctx* ctx);
  * [12] kernels per iteration, [13] branching rows, [14] SMs. Returns the
  * number of fields (writes at most cap). No reference counterpart. */
 int wmpc_path_info(const wmpc_ctx* ctx, int* out, int cap);
+/* Programmatic dependent launch between the iteration kernels on (default) or
+ * off (plain stream order). Test hook: results must be bit-identical either
+ * way (tests/test_gpu_hazards.py). No reference counterpart. */
+int wmpc_set_pdl(wmpc_ctx* ctx, int on);
 
 /* Timing helpers for bench.py: run `count` iterations between CUDA events on
  * the context's stream; *ms = elapsed device time. */

@@ -72,6 +72,7 @@ SIGNATURES = {
     "wmpc_kernel_launches_per_iteration": (C.c_int, [_vp]),
     "wmpc_fast_path": (C.c_int, [_vp]),
     "wmpc_path_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.c_int]),
+    "wmpc_set_pdl": (C.c_int, [_vp, C.c_int]),
     "wmpc_profile_fast": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_int]),
     "wmpc_last_debug_ms": (C.c_float, [_vp]),
     "wmpc_debug_div": (C.c_int, [_dp, _dp, C.c_int, C.POINTER(C.c_uint64)]),

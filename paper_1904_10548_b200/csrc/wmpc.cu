@@ -17,7 +17,6 @@
 #include <vector>
 
 #include "wmpc.h"
-#include "wmpc_warp.cuh"
 #include "wmpc_scan.cuh"
 #include "wmpc_chainw.cuh"
 #include "wmpc_dp.cuh"
@@ -77,8 +76,6 @@ struct wmpc_ctx {
   bool fast = false;
   int kstar = 0, nchain = 0, fast_mc = 1, fast_cpc = 1, fast_gs = 1, fast_grid = 0;
   int fast_nrow = 2, fast_rec = 0, fast_enz = 0, fast_bnz = 0, fast_knz = 0;
-  int use_warp = 0, warp_nrow = 2;
-  size_t warp_smem = 0;
   int use_scan = 0, scan_work = 0;
   size_t scan_smem = 0;
   // graph-of-kernels scan path (wmpc_scan.cuh)
@@ -88,8 +85,7 @@ struct wmpc_ctx {
   unsigned long long* dk_mv = nullptr;
   int* dk_sweeps = nullptr;
   int* dk_fix = nullptr;                       // certificate Dykstra: per-node settled sweep (pass 1)
-  int use_graphk = 0, n_branch = 0, use_fused = 0, fused_pb = 1, fused_ring_off = 0, fused_threads = 1024;
-  size_t sm_fused = 0;
+  int use_graphk = 0, n_branch = 0;
   int* store_it = nullptr;
   int store_it_host = 0;
   double *Lb = nullptr, *Asub = nullptr;
@@ -108,11 +104,11 @@ struct wmpc_ctx {
   int n_rep_global = 0, shard_k = -1, kstar_min = 0;
   ncclComm_t nccl = nullptr;                   // subtree sharding: exchange inside the iteration graph
   size_t sm_up = 0, sm_grp = 0, sm_down = 0, sm_prox = 0;
-  int up_threads = 512, down_threads = 512, prox_warp = 1, use_pu = 0;
+  int up_threads = 512, down_threads = 512, prox_warp = 1;
   int fp32 = 0;                                 // SolverConfig.precision == "fp32"
   int pdl = 1;                                  // programmatic dependent launch between graph kernels
   int chain_occ = 0;                            // chain kernels: register cap for occupancy (many chains)
-  int chainw = 0, cw_pd = 2, cw_rd = 1;        // warp-per-chain kernels (wmpc_chainw.cuh), ring depth, rows ahead
+  int chainw = 0, cw_pd = 8;                   // warp-per-chain kernels (wmpc_chainw.cuh): 8-row ring or registers (1)
   int chainw32 = 0;                             // ... also in fp32 mode (register variant only)
   int rfree = 1;                                // R-free iteration form (graph path, unsharded, unfused)
   double* ut = nullptr;                         // u at Yc = 0 (rfree), per solve
@@ -123,7 +119,6 @@ struct wmpc_ctx {
         *f32_X = nullptr, *f32_eoff = nullptr, *f32_R = nullptr, *f32_g = nullptr, *f32_aux = nullptr,
         *f32_ell = nullptr;
   size_t ell_len = 0;
-  size_t sm_pu = 0;
   int *ell_cnt = nullptr, *ell_idx = nullptr;
   double* ell_val = nullptr;
   int ell_w = 4;
@@ -394,10 +389,6 @@ void launch_pdl(wmpc_ctx* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, 
   CK(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
-template <int WE>
-void gk_pu(wmpc_ctx* ctx, const FastView& f) {
-  k_chain_pu<WE><<<ctx->nchain, 256, ctx->sm_pu, ctx->stream>>>(f);
-}
 template <int WE, typename TG, int PD, bool RF>
 void cw_attrs1(wmpc_ctx* ctx) {
   CK(cudaFuncSetAttribute(k_chain_up_w<WE, TG, PD, RF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -414,11 +405,6 @@ template <int WE, typename TG, bool RF>
 void cw_up_r(wmpc_ctx* ctx, const FastView& f) {
   const dim3 grid((ctx->nchain + CW_WARPS - 1) / CW_WARPS), block(CW_WARPS * 32);
   const size_t sm = sizeof(TG) * (CW_WARPS * cw_up_warp_r() + (CW_SMV ? CW_UP_SLOTS * 32 : 0));
-  if (ctx->cw_rd == 2) {
-    if (ctx->ell_vf) launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 2, true>, grid, block, sm, f);
-    else launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 2, false>, grid, block, sm, f);
-    return;
-  }
   if (ctx->ell_vf) launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 1, true>, grid, block, sm, f);
   else launch_pdl(ctx, k_chain_up_r<WE, TG, RF, 1, false>, grid, block, sm, f);
 }
@@ -426,21 +412,12 @@ template <int WE, typename TG, bool RF>
 void cw_down_r(wmpc_ctx* ctx, const FastView& f) {
   const dim3 grid((ctx->nchain + CW_WARPS - 1) / CW_WARPS), block(CW_WARPS * 32);
   const size_t sm = sizeof(TG) * (CW_WARPS * cw_dn_warp_r() + (CW_SMV ? CW_DN_SLOTS * 32 : 0));
-  if (ctx->cw_rd == 2) {
-    if (ctx->ell_vf) launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 2, true>, grid, block, sm, f);
-    else launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 2, false>, grid, block, sm, f);
-    return;
-  }
   if (ctx->ell_vf) launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 1, true>, grid, block, sm, f);
   else launch_pdl(ctx, k_chain_down_r<WE, TG, RF, 1, false>, grid, block, sm, f);
 }
 template <int WE, typename TG>
 void gk_attrs_t(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
-  if constexpr (WE == 4) {
-    cw_attrs<WE, TG, 2>(ctx);
-    cw_attrs<WE, TG, 4>(ctx);
-    cw_attrs<WE, TG, 8>(ctx);
-  }
+  if constexpr (WE == 4 && sizeof(TG) == 8) cw_attrs<WE, TG, 8>(ctx);  // the ring: fp64 only
   CK(cudaFuncSetAttribute(k_chain_up<WE, TG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
   CK(cudaFuncSetAttribute(k_chain_down<WE, TG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
   CK(cudaFuncSetAttribute(k_chain_up<WE, TG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
@@ -451,7 +428,6 @@ template <int WE>
 void gk_attrs(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
   CK(cudaFuncSetAttribute(k_chain_rollout<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(sizeof(double) * (size_t)ctx->H * (ctx->nu + ctx->lx) + sizeof(int) * 32)));
-  if (ctx->sm_pu) CK(cudaFuncSetAttribute(k_chain_pu<WE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->sm_pu));
   gk_attrs_t<WE, double>(ctx, up, down, grp);
   gk_attrs_t<WE, float>(ctx, up, down, grp);
 }
@@ -473,15 +449,17 @@ template <int WE, typename TG = double>
 void gk_up(wmpc_ctx* ctx, const FastView& f) {
   if constexpr (WE == 4)
     if (ctx->chainw && (sizeof(TG) == 8 || ctx->chainw32)) {
-      // fp32: registers only (the 8-byte cp.async ring gave wrong results in fp32
-      // mode; the fp64 ring and both register variants are bit-identical to the
-      // CTA kernels: tests/test_gpu_fast_path.py)
-      const int pd = sizeof(TG) == 4 ? 1 : ctx->cw_pd;
-      if (pd == 8) cw_up<WE, TG, 8>(ctx, f);
-      else if (pd == 4) cw_up<WE, TG, 4>(ctx, f);
-      else if (pd == 1 && f.rfree) cw_up_r<WE, TG, true>(ctx, f);
-      else if (pd == 1) cw_up_r<WE, TG, false>(ctx, f);
-      else cw_up<WE, TG, 2>(ctx, f);
+      // the 8-row cp.async ring (fp64, 16-byte .cg copies) or rows streamed
+      // through registers; both bit-identical to the CTA kernels
+      // (tests/test_gpu_fast_path.py). fp32 mode: registers only (round 1's
+      // 8-byte cp.async.ca ring variant was deleted).
+      if constexpr (sizeof(TG) == 8)
+        if (ctx->cw_pd == 8) {
+          cw_up<WE, TG, 8>(ctx, f);
+          return;
+        }
+      if (f.rfree) cw_up_r<WE, TG, true>(ctx, f);
+      else cw_up_r<WE, TG, false>(ctx, f);
       return;
     }
   if (ctx->chain_occ)
@@ -500,14 +478,15 @@ void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump, int first_flags = 0) {
 }
 // fp64 only: in fp32 mode the four-kernel graph measured faster (C4 200 vs 258 us)
 bool dp_on(const wmpc_ctx* ctx) {
-  return ctx->use_dp && !ctx->fp32 && ctx->shard_k < 0 && ctx->rfree && !ctx->use_fused && !ctx->use_pu;
+  return ctx->use_dp && !ctx->fp32 && ctx->shard_k < 0 && ctx->rfree;
 }
 template <typename TG>
 void launch_dp(wmpc_ctx* ctx, const FastView& f) {
-  DpArgs a{sizeof(TG) == 8 ? (void*)ctx->dp_agg : (void*)ctx->dp_agg32,
-           sizeof(TG) == 8 ? (const void*)ctx->dp_putg : (const void*)ctx->dp_putg32, ctx->dp_cpw};
-  const dim3 grid(ctx->dp_grid), block(ctx->dp_wpc * 32);
-  launch_pdl(ctx, k_chain_dp<DP_NT, DP_NU, TG>, grid, block, ctx->dp_sm, f, a);
+  if constexpr (sizeof(TG) == 8) {  // fp64 only (dp_on)
+    DpArgs a{(void*)ctx->dp_agg, (const void*)ctx->dp_putg, ctx->dp_cpw};
+    const dim3 grid(ctx->dp_grid), block(ctx->dp_wpc * 32);
+    launch_pdl(ctx, k_chain_dp<DP_NT, DP_NU, double>, grid, block, ctx->dp_sm, f, a);
+  }
 }
 template <int WE>
 void gk_rep(wmpc_ctx* ctx, const FastView& f, int mode, int bump) {
@@ -519,12 +498,13 @@ template <int WE, typename TG = double>
 void gk_down(wmpc_ctx* ctx, const FastView& f) {
   if constexpr (WE == 4)
     if (ctx->chainw && (sizeof(TG) == 8 || ctx->chainw32)) {
-      const int pd = sizeof(TG) == 4 ? 1 : ctx->cw_pd;
-      if (pd == 8) cw_down<WE, TG, 8>(ctx, f);
-      else if (pd == 4) cw_down<WE, TG, 4>(ctx, f);
-      else if (pd == 1 && f.rfree) cw_down_r<WE, TG, true>(ctx, f);
-      else if (pd == 1) cw_down_r<WE, TG, false>(ctx, f);
-      else cw_down<WE, TG, 2>(ctx, f);
+      if constexpr (sizeof(TG) == 8)
+        if (ctx->cw_pd == 8) {
+          cw_down<WE, TG, 8>(ctx, f);
+          return;
+        }
+      if (f.rfree) cw_down_r<WE, TG, true>(ctx, f);
+      else cw_down_r<WE, TG, false>(ctx, f);
       return;
     }
   if (ctx->chain_occ)
@@ -541,13 +521,10 @@ void gk_prox(wmpc_ctx* ctx, const FastView& f) {
 }
 template <int WE, typename TG>
 void gk_iteration(wmpc_ctx* ctx, const FastView& f) {
-  // WMPC_SKIP (timing experiments only: results are wrong): letters u g d p drop kernels
-  const char* skip = getenv("WMPC_SKIP");
-  auto on = [&](char c) { return !skip || !std::strchr(skip, c); };
-  if (on('u')) gk_up<WE, TG>(ctx, f);
-  if (on('g')) gk_grp<WE, TG>(ctx, f, 1);
-  if (on('d')) gk_down<WE, TG>(ctx, f);
-  if (on('p')) gk_prox<TG>(ctx, f);
+  gk_up<WE, TG>(ctx, f);
+  gk_grp<WE, TG>(ctx, f, 1);
+  gk_down<WE, TG>(ctx, f);
+  gk_prox<TG>(ctx, f);
 }
 
 // Branching-region stage groups, bottom-up, with <= 32 items per row, and
@@ -627,9 +604,8 @@ void build_groups(wmpc_ctx* ctx, int k_rep, const int* acct) {
 #ifndef DP_WPS
 #define DP_WPS 7
 #endif
-template <typename TG>
 void dp_attr(wmpc_ctx* ctx, size_t sm) {
-  CK(cudaFuncSetAttribute(k_chain_dp<DP_NT, DP_NU, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  CK(cudaFuncSetAttribute(k_chain_dp<DP_NT, DP_NU, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
 }
 void configure_dp(wmpc_ctx* ctx) {
   ctx->use_dp = 0;
@@ -645,10 +621,9 @@ void configure_dp(wmpc_ctx* ctx) {
   const int nw = (nchain + cpw - 1) / cpw;
   const int wpc = std::min(DP_MAXT / 32, std::max(1, (nw + sms - 1) / sms));
   const int grid = (nw + wpc - 1) / wpc;
-  const size_t sm = std::max(dp_smem<double>(wpc, nt, nu, lx), dp_smem<float>(wpc, nt, nu, lx));
+  const size_t sm = dp_smem<double>(wpc, nt, nu, lx);
   if (sm > 227 * 1024) return;
-  dp_attr<double>(ctx, sm);
-  dp_attr<float>(ctx, sm);
+  dp_attr(ctx, sm);
   // ownership of the branching rows balanced over the persistent warps
   const int nwt = grid * wpc, nb = ctx->off[kstar];
   if (kstar > 0) {
@@ -823,17 +798,14 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
     ctx->ell_vf = 1;
     for (size_t i = 0; i < (size_t)(2 * nu + nt) * we && i < val.size(); ++i)
       ctx->ell_vf &= (double)(float)val[i] == val[i];
-    if (const char* e = getenv("WMPC_ELL_VF")) ctx->ell_vf &= e[0] != '0';
     ctx->ell_w = we;
     ctx->ell_len = val.size();
   }
   ctx->h_cptr = cptr;
   ctx->h_cidx = cidx;
-  if (const char* e = getenv("WMPC_GRP_ITEMS")) ctx->grp_items = std::max(1, atoi(e));
   // measured (us per iteration, 16 -> 64): C2 19.8 -> 22.6 (few chains: keep 16),
   // C3 52.4 -> 51.0, C4 269.7 -> 268.0
   ctx->grp_items_few = nchain > ctx->sms ? std::max(ctx->grp_items, 64) : ctx->grp_items;
-  if (const char* e = getenv("WMPC_GRP_FEW")) ctx->grp_items_few = std::max(1, atoi(e));
   build_groups(ctx, 0, nullptr);
   // chain root paths and ancestor ownership (first chain below a row writes it)
   std::vector<int> cpath((size_t)std::max(nchain * kstar, 1), 0);
@@ -876,21 +848,12 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   if (ctx->ut) cudaFree(ctx->ut);
   ctx->ut = nullptr;
   dalloc(ctx, &ctx->ut, (size_t)ctx->n * nu);
-  if (const char* e = getenv("WMPC_RFREE")) ctx->rfree = e[0] != '0';
-  {  // prox fused with the next up pass (k_chain_pu)
-    const int ra = ly + nu + 2;
-    ctx->sm_pu = sizeof(double) * ((size_t)nst * (ra + FAST_MAXNS) + (size_t)(256 / 64) * 128);
-    const char* e = getenv("WMPC_PU");
-    ctx->use_pu = e && e[0] == '1' && ctx->sm_pu <= cap && nt <= 64 && nu <= 128 ? 1 : 0;
-    if (ctx->sm_pu > cap) ctx->sm_pu = 0;
-  }
   if (ctx->ell_w == 4) gk_attrs<4>(ctx, up, down, grp);
   else gk_attrs<8>(ctx, up, down, grp);
   CK(cudaFuncSetAttribute(k_prox_nodes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prox));
   ctx->sm_up = up; ctx->sm_down = down; ctx->sm_grp = grp; ctx->sm_prox = prox;
   ctx->up_threads = ctx->down_threads = 512;  // measured: 512 beats 256 on C2 and C4
   ctx->chain_occ = ctx->nchain > 4 * ctx->sms ? 1 : 0;  // measured: C4 (4096 chains) +4 %; C2, C3 (<= 512) better without
-  if (const char* e = getenv("WMPC_PDL")) ctx->pdl = e[0] != '0';
   {  // warp-per-chain kernels (wmpc_chainw.cuh). Measured (us per iteration, CTA kernels ->
      // warp kernels): C2 128 chains 19.7 -> 27 (latency-bound: the CTA kernels run the
      // phases of all rows in parallel), C3 512 chains 55.4 -> 53.4 (8-row ring),
@@ -900,53 +863,15 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
     const int wps = (ctx->nchain + ctx->sms - 1) / std::max(ctx->sms, 1);
     ctx->chainw = ctx->nchain > 2 * ctx->sms ? 1 : 0;
     ctx->cw_pd = wps <= 4 ? 8 : 1;
-    ctx->cw_rd = 1;
-    if (const char* e = getenv("WMPC_CWPD")) ctx->cw_pd = atoi(e) >= 8 ? 8 : (atoi(e) >= 4 ? 4 : (atoi(e) >= 2 ? 2 : 1));
-    if (const char* e = getenv("WMPC_CWRD")) ctx->cw_rd = atoi(e) >= 2 ? 2 : 1;
+    // tests / tools force a variant: WMPC_CHAINW=0|1, WMPC_CWPD=1 (registers) | 8 (ring)
+    if (const char* e = getenv("WMPC_CWPD")) ctx->cw_pd = atoi(e) >= 8 ? 8 : 1;
     // fp32 mode (register variant only): C3 47 (CTA) vs 52 us, C4 279 vs 226 us
     ctx->chainw32 = wps > 4 ? 1 : 0;
     if (const char* e = getenv("WMPC_CHAINW")) ctx->chainw = ctx->chainw32 = e[0] == '1';
     if (!fits) ctx->chainw = ctx->chainw32 = 0;
   }
   configure_dp(ctx);
-  if (const char* e = getenv("WMPC_UPT")) ctx->up_threads = atoi(e) >= 512 ? 512 : 256;
-  if (const char* e = getenv("WMPC_DNT")) ctx->down_threads = atoi(e) >= 512 ? 512 : 256;
   ctx->prox_warp = nt <= 64 && nu <= 128 ? 1 : 0;
-  if (const char* e = getenv("WMPC_PROX")) ctx->prox_warp = std::string(e) == "warp" ? ctx->prox_warp : 0;
-  // fused chain kernel (down + prox + next up); pb rows per prox batch
-  {
-    ctx->use_fused = 0;
-    const char* ef = getenv("WMPC_FUSED");
-    const int rp = 2 * ctx->W + nu + lx;
-    auto layout = [&](int pb, int* ring_off) {
-      size_t dbl = (size_t)2 * H * nu + (size_t)H * lx + (size_t)H * FAST_MAXNS + (size_t)pb * 128 + 2 * pb + 2;
-      const size_t ints = ((H + 3) & ~3);
-      const size_t ring = (size_t)2 * pb * rp;
-      if (ring <= (size_t)H * nu) {
-        *ring_off = H * nu;
-        return dbl * sizeof(double) + ints * sizeof(int);
-      }
-      const size_t head = dbl * sizeof(double) + ints * sizeof(int);
-      *ring_off = (int)((head + 15) / 16 * 2);  // in doubles, 16-byte aligned
-      return (size_t)*ring_off * sizeof(double) + ring * sizeof(double);
-    };
-    const bool wide = ctx->nchain >= 2 * ctx->sms;  // many chains: occupancy over per-chain latency
-    int pb = wide ? std::max(1, (H * nu) / (2 * rp)) : 8;
-    int ft = wide ? 512 : 1024;
-    if (const char* e = getenv("WMPC_PB")) pb = std::max(1, atoi(e));
-    if (const char* e = getenv("WMPC_FT")) ft = std::min(1024, std::max(256, atoi(e) / 256 * 256));
-    ctx->fused_threads = ft;
-    pb = std::min(pb, nst);
-    int roff = 0;
-    const size_t fb = layout(pb, &roff);
-    if (ef && ef[0] == '1' && fb <= cap) {  // opt-in: slower than the 4-kernel graph on B200 so far
-      CK(cudaFuncSetAttribute(k_chain_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb));
-      ctx->sm_fused = fb;
-      ctx->fused_pb = pb;
-      ctx->fused_ring_off = roff;
-      ctx->use_fused = 1;
-    }
-  }
   ctx->blob16 = bl.bytes / 16;
   ctx->n_branch = nb;
   ctx->use_graphk = 1;
@@ -1038,10 +963,8 @@ void configure_fast(wmpc_ctx* ctx, const double* B, const double* E, const doubl
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev));
   ctx->sms = sms;
   int cpc = (nchain + sms - 1) / sms;
-  if (const char* e = getenv("WMPC_CPC")) cpc = std::max(cpc, atoi(e));
   int MC = 1;
   while (MC < 8 && MC < cpc) MC *= 2;
-  if (const char* e = getenv("WMPC_MC")) MC = std::min(8, std::max(MC, atoi(e)));
   int ngroups = (cpc + MC - 1) / MC;
   int gs = (cpc + ngroups - 1) / ngroups;
   ctx->kstar = kstar;  // fast_smem_bytes reads it
@@ -1051,7 +974,6 @@ void configure_fast(wmpc_ctx* ctx, const double* B, const double* E, const doubl
   int nrow = 0;
   for (int nr = 2; nr <= 8; ++nr)
     if (fast_smem_bytes(ctx, MC, nr, rec, cpc, enz, bnz) <= cap) nrow = nr;
-  if (const char* e = getenv("WMPC_NROW")) nrow = std::min(nrow, std::max(2, atoi(e)));
   if (nrow < 2) return;
   size_t smem = fast_smem_bytes(ctx, MC, nrow, rec, cpc, enz, bnz);
   switch (MC) {
@@ -1086,29 +1008,6 @@ void configure_fast(wmpc_ctx* ctx, const double* B, const double* E, const doubl
   ctx->fast_rec = rec;
   ctx->fast_enz = enz;
   ctx->fast_bnz = bnz;
-  // warp-per-chain variant (default when it fits)
-  {
-    auto wsm = [&](int nr) {
-      size_t dbl = (size_t)FW_WARPS * nr * rec + (size_t)FW_WARPS * FW_SCR + (3 * nt + 2 * nu) + (size_t)nu * ns +
-                   enz + 2 * (size_t)bnz;
-      size_t ints = (ns + 1) + enz + (nu + 1) + bnz + (nt + 1) + bnz + (H + 1);
-      return dbl * sizeof(double) + ints * sizeof(int) + 64;
-    };
-    int wn = 0;
-    for (int nr = 2; nr <= 8; ++nr)
-      if (wsm(nr) <= cap) wn = nr;
-    if (const char* e = getenv("WMPC_WARP_NROW")) wn = std::min(wn, std::max(2, atoi(e)));
-    const char* ek = getenv("WMPC_KERNEL");
-    bool want = ek && std::string(ek) == "warp";  // scan kernel is the default
-    if (wn >= 2 && want) {
-      ctx->warp_nrow = wn;
-      ctx->warp_smem = wsm(wn);
-      CK(cudaFuncSetAttribute(k_apg_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->warp_smem));
-      ctx->use_warp = 1;
-    } else {
-      ctx->use_warp = 0;
-    }
-  }
   // scan-form kernel (default when the chain fits in shared memory)
   {
     const int nst = H - kstar;
@@ -1160,8 +1059,7 @@ FastView make_fastview(wmpc_ctx* ctx, int count);
 int graphk_kernels(const wmpc_ctx* ctx) {
   const int g = (int)ctx->gk_groups.size();
   if (ctx->shard_k > 0) return 3 + g + 2 * (ctx->rep_group.second > 0) + (g == 0 && ctx->rep_group.second == 0);
-  if (ctx->use_fused || dp_on(ctx)) return g + 1 + (g == 0 ? 1 : 0);
-  if (ctx->use_pu) return g + 2 + (g == 0 ? 1 : 0);
+  if (dp_on(ctx)) return g + 1 + (g == 0 ? 1 : 0);
   return 3 + g + (g == 0 ? 1 : 0);
 }
 
@@ -1170,23 +1068,6 @@ void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
   cudaStream_t st = ctx->stream;
   const int nc = ctx->nchain;
   if (ctx->gk_groups.empty()) k_advance<<<1, 32, 0, st>>>(ctx->iter);  // else the first group kernel counts
-  if (ctx->use_fused) {  // up pass of iteration 0 runs in wmpc_apg_begin
-    if (ctx->ell_w == 4) gk_grp<4>(ctx, f, 1); else gk_grp<8>(ctx, f, 1);
-    k_chain_fused<<<nc, ctx->fused_threads, ctx->sm_fused, st>>>(f);
-    return;
-  }
-  if (ctx->use_pu) {  // up pass of iteration 0 runs in wmpc_apg_begin
-    if (ctx->ell_w == 4) {
-      gk_grp<4>(ctx, f, 1);
-      gk_down<4>(ctx, f);
-      gk_pu<4>(ctx, f);
-    } else {
-      gk_grp<8>(ctx, f, 1);
-      gk_down<8>(ctx, f);
-      gk_pu<8>(ctx, f);
-    }
-    return;
-  }
   if (dp_on(ctx)) {  // branch groups (the first reads Yc the previous k_chain_dp wrote) + k_chain_dp
     if (ctx->fp32) {
       gk_grp<4, float>(ctx, f, 1, GRP_LATE);
@@ -1343,15 +1224,13 @@ FastView make_fastview(wmpc_ctx* ctx, int count) {
   f.ell_val = ctx->ell_val;
   f.ell_w = ctx->ell_w;
   f.lb_prewait = ctx->gk_groups.empty() ? 0 : 1;
-  f.rfree = ctx->rfree && ctx->shard_k < 0 && !ctx->use_fused && !ctx->use_pu ? 1 : 0;
+  f.rfree = ctx->rfree && ctx->shard_k < 0 ? 1 : 0;
   f.ut = ctx->ut;
   f.ut32 = ctx->ut32;
   f.g32 = G32{ctx->f32_Yc, ctx->f32_Lb, ctx->f32_Asub, ctx->f32_wbar, ctx->f32_U, ctx->f32_X,
               ctx->f32_eoff, ctx->f32_R, ctx->f32_g, ctx->f32_aux, ctx->f32_ell};
   f.xbuf = ctx->xbuf;
   f.rep_gidx = ctx->rep_gidx;
-  f.pb = ctx->fused_pb;
-  f.ring_off = ctx->fused_ring_off;
   f.work_doubles = ctx->scan_work;
   return f;
 }
@@ -1370,14 +1249,6 @@ void launch_fast(wmpc_ctx* ctx, int count) {
       case 4: launch_scan_mc<4>(ctx, f); break;
       default: launch_scan_mc<8>(ctx, f); break;
     }
-    ctx->launches += 1;
-    return;
-  }
-  if (ctx->use_warp) {
-    f.nrow = ctx->warp_nrow;
-    void* args[] = {(void*)&f, (void*)&ctx->off_dev};
-    CK(cudaLaunchCooperativeKernel((void*)k_apg_warp, dim3(ctx->fast_grid), dim3(FW_THREADS), args, ctx->warp_smem,
-                                   ctx->stream));
     ctx->launches += 1;
     return;
   }
@@ -1837,11 +1708,20 @@ int wmpc_path_info(const wmpc_ctx* ctx, int* out, int cap) {
   return nv;
 }
 
+int wmpc_set_pdl(wmpc_ctx* ctx, int on) {
+  if (!ctx) return WMPC_E_ARG;
+  if (ctx->pdl != (on ? 1 : 0)) {
+    ctx->pdl = on ? 1 : 0;
+    ctx->gk_gamma = -1.0;  // recapture the iteration graphs
+  }
+  return WMPC_OK;
+}
+
 int wmpc_fast_path(const wmpc_ctx* ctx) {
   if (!ctx || !ctx->fast) return 0;
-  if (ctx->use_graphk) return ctx->use_fused ? 310 : (ctx->use_pu ? 320 : 300);
+  if (ctx->use_graphk) return 300;
   if (ctx->use_scan) return 200 + ctx->fast_mc;
-  return ctx->use_warp ? 100 + ctx->warp_nrow : ctx->fast_mc;
+  return ctx->fast_mc;
 }
 
 int wmpc_set_bounds(wmpc_ctx* ctx, const double* x_min, const double* x_max, const double* x_safe,
@@ -2085,12 +1965,6 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
           check_launch(ctx);
         }
         capture_graphk(ctx);
-        if (ctx->use_fused || ctx->use_pu) {  // up pass of iteration 0 (Yc = 0)
-          FastView f = make_fastview(ctx, 1);
-          if (ctx->ell_w == 4) gk_up<4>(ctx, f); else gk_up<8>(ctx, f);
-          ctx->launches++;
-          check_launch(ctx);
-        }
       }
       return WMPC_OK;  // persistent kernel: no graph
     }
@@ -2563,7 +2437,7 @@ int wmpc_set_precision(wmpc_ctx* ctx, int fp32) {
       ctx->fp32 = 0;
       return WMPC_OK;
     }
-    if (!ctx->fast || !ctx->use_graphk || ctx->use_fused || ctx->use_pu || ctx->shard_k >= 0) {
+    if (!ctx->fast || !ctx->use_graphk || ctx->shard_k >= 0) {
       ctx->err = "fp32 mode needs the structured graph path (A = I, W = cI), unsharded";
       return WMPC_E_STATE;
     }
@@ -2616,11 +2490,6 @@ int wmpc_apg_warm(wmpc_ctx* ctx, const double* y0) {
         k_dp_agg_L<double><<<nbk, 256, 0, ctx->stream>>>(f, ctx->dp_agg);
       }
       ctx->launches += 2;
-    }
-    if (ctx->fast && ctx->use_graphk && (ctx->use_fused || ctx->use_pu)) {  // the up pass of iteration 0
-      FastView f = make_fastview(ctx, 1);
-      if (ctx->ell_w == 4) gk_up<4>(ctx, f); else gk_up<8>(ctx, f);
-      ctx->launches++;
     }
     check_launch(ctx);
     sync(ctx);

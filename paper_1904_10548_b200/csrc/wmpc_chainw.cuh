@@ -14,8 +14,8 @@
 //     cp.async; every lane copies exactly the pairs it reads, so the ring needs
 //     no warp barrier (only the three small exchange vectors do: one
 //     __syncwarp per cross-lane product);
-//   * PD = 8 when chains are few (latency-bound: rows arrive 8 ahead), 2 when
-//     several waves of chains fill the GPU (HBM-bound, more warps per SM).
+//   * PD = 8 rows ahead (chains few per SM: latency-bound, C3); with many
+//     chains the register-streamed _r kernels below replace the ring.
 #pragma once
 #include <type_traits>
 
@@ -38,23 +38,20 @@ struct V2T<double> { using T = double2; };
 template <>
 struct V2T<float> { using T = float2; };
 
-// async copy of an element pair (16 B for double, 8 B for float)
+// async copy of an fp64 element pair (16-byte cp.async.cg: L2 only, so a
+// predecessor kernel's writes are never served from a stale L1 line)
 template <typename TG>
 __device__ __forceinline__ void cp_pair(TG* dst, const TG* src) {
-  if constexpr (sizeof(TG) == 8)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  static_assert(sizeof(TG) == 8, "the ring kernels are fp64-only (fp32 mode streams rows through registers)");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 // predicated form: nothing is read (the pair is zero-filled) when !ok; src must
 // still be a valid address
 template <typename TG>
 __device__ __forceinline__ void cp_pair_if(TG* dst, const TG* src, bool ok) {
-  const unsigned n = ok ? 2 * sizeof(TG) : 0u;
-  if constexpr (sizeof(TG) == 8)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(n) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(n) : "memory");
+  static_assert(sizeof(TG) == 8, "the ring kernels are fp64-only (fp32 mode streams rows through registers)");
+  const unsigned n = ok ? 16u : 0u;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(n) : "memory");
 }
 // ELL owner bound to one shared vector: entry addresses precomputed once
 template <int W, typename TG>

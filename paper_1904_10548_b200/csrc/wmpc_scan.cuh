@@ -860,319 +860,4 @@ __global__ void k_collapse(DevView d, const double* __restrict__ y, double* Yc) 
   }
 }
 
-// ---------------------------------------------------------------- k_chain_pu
-// Prox of iteration it fused with the up pass of iteration it+1, one CTA per
-// chain: warp pairs run the barrier-free warp prox over the chain rows (and
-// the ancestors this chain owns, whose Yc goes to HBM for k_branch_grp); the
-// chain rows' next collapsed dual Yc stays in shared memory and feeds the
-// suffix scans of k_chain_up directly (no Yc round trip through HBM).
-// Shared: rec nst x (ly + nu + 2) [Yc->wbar,a | R->S | aux], T nst x 32,
-// sd2 (warps/2) x 128.
-template <int WE>
-__global__ void __launch_bounds__(256) k_chain_pu(FastView f) {
-  const DevView& d = f.d;
-  const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly, ns = d.ns;
-  const int kb = f.kstar, nst = d.H - kb, ci = blockIdx.x;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int ra = ly + nu + 2;
-  double* rec = reinterpret_cast<double*>(smem_raw);
-  double* T = rec + (size_t)nst * ra;
-  double* sd2 = T + (size_t)nst * FAST_MAXNS;
-  const NodePtrs np = *d.np;
-  const ProxIt P = prox_it(f);
-  // R and aux of the chain rows arrive while the prox runs
-  FOR_RC(nst - 1, 6, (nu >> 1), t, k)
-    cp16(rec + (size_t)t * ra + ly + 2 * k, np.R + (size_t)chain_row(f, t, ci) * nu + 2 * k);
-  if (threadIdx.x < nst) cp16(rec + (size_t)threadIdx.x * ra + ly + nu, f.aux + (size_t)chain_row(f, threadIdx.x, ci) * 2);
-  cp_commit();
-  // ---- prox: owned ancestors, then chain rows; warp pair w takes rows w, w + pairs, ...
-  const unsigned own = kb > 0 ? f.cown[ci] : 0u;
-  const int pairs = blockDim.x >> 6, pw = threadIdx.x >> 6, role = (threadIdx.x >> 5) & 1;
-  const int n_own = __popc(own);
-  bool bad = false;
-  for (int p = pw; p < n_own + nst; p += pairs) {
-    int r;
-    double* yc;
-    if (p < n_own) {
-      unsigned w = own;
-      for (int c = 0; c < p; ++c) w &= w - 1;
-      r = f.cpath[(size_t)ci * kb + (__ffs(w) - 1)];
-      yc = d.Yc + (size_t)r * ly;
-    } else {
-      r = chain_row(f, p - n_own, ci);
-      yc = rec + (size_t)(p - n_own) * ra;
-    }
-    bad |= role == 0 ? prox_x_warp<double>(f, P, r, d.X + (size_t)r * lx, sd2 + (size_t)pw * 128, yc)
-                     : prox_u_warp<double>(f, P, r, d.U + (size_t)r * nu, yc);
-  }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicMin(d.bad_nu, P.it);
-  if (!P.next) return;
-  cp_wait<0>();
-  __syncthreads();
-  // ---- up pass of iteration it+1 (as k_chain_up, rec rows already hold Yc)
-  const int k = threadIdx.x & 127, tk = threadIdx.x >> 7, sk = blockDim.x >> 7;
-  const int i = threadIdx.x & 31, ti = threadIdx.x >> 5, si = blockDim.x >> 5;
-  if (threadIdx.x < nt) {
-    const int j = threadIdx.x;
-    double acc = 0.0;
-    for (int t = nst - 1; t >= 0; --t) {
-      const double yx = rec[(size_t)t * ra + j];
-      acc = t == nst - 1 ? yx : yx + acc;
-      rec[(size_t)t * ra + j] = acc;
-    }
-    d.wbar[(size_t)chain_row(f, 0, ci) * lx + j] = acc;
-  }
-  __syncthreads();
-  if (k < nu) {
-    const Ell<EllW<WE>::BC> bc = ell_load<EllW<WE>::BC>(f, own_bc(d, k));
-    for (int t = tk; t < nst; t += sk) {
-      double* R = rec + (size_t)t * ra;
-      double a = R[lx + k] + ell_dot(bc, R);
-      if (t < nst - 1) a = a + R[ly + k];
-      R[lx + k] = a;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < nu) {
-    double acc = 0.0;
-    for (int t = nst - 1; t >= 0; --t) {
-      double* R = rec + (size_t)t * ra;
-      R[ly + threadIdx.x] = acc;
-      const double a = R[lx + threadIdx.x];
-      acc = t == nst - 1 ? a : a + acc;
-    }
-    f.Asub[(size_t)chain_row(f, 0, ci) * nu + threadIdx.x] = acc;
-  }
-  __syncthreads();
-  if (i < ns) {
-    const Ell<EllW<WE>::KR> kr = ell_load<EllW<WE>::KR>(f, own_kr(d, i));
-    for (int t = ti; t < nst - 1; t += si) T[t * FAST_MAXNS + i] = ell_dot(kr, rec + (size_t)t * ra + ly);
-  }
-  __syncthreads();
-  if (k < nu) {
-    const Ell<EllW<WE>::EC> ec = ell_load<EllW<WE>::EC>(f, own_ec(d, k));
-    for (int t = tk; t < nst; t += sk) {
-      const double* R = rec + (size_t)t * ra;
-      const double a = R[lx + k];
-      const double l = t < nst - 1 ? a + (R[ly + k] - ell_dot(ec, T + t * FAST_MAXNS)) : a;
-      f.Lb[(size_t)chain_row(f, t, ci) * nu + k] = l * R[ly + nu];
-    }
-  }
-}
-
-// ---------------------------------------------------------------- k_chain_fused
-// One CTA per chain, three phases in shared memory:
-//   D  down pass of iteration it over the root path (as k_chain_down) -> u, x
-//   P  Moreau prox of the chain rows and of the ancestors this chain owns
-//      (records streamed through a 2-slot cp.async ring, pb rows per batch);
-//      the next collapsed dual Yc overwrites u, x in place
-//   U  up pass of iteration it+1 on the chain's Yc (as k_chain_up) -> L, wbar, Asub
-// so per chain node only y, y_prev, Ua, Xa, L, e_off, g, R move through HBM.
-// Shared (doubles): Z H x nu (L->z->u->Yu->a), E H x nu (e_off->Bu->ring->R->S),
-// G H x lx (g->x->Yx->wbar), T H x FAST_MAXNS, d2 pb x 128, stp 2pb, [ring], rows H.
-__device__ __forceinline__ void fused_issue(const FastView& f, double* slot, int rp, const int* grow, int bn, int it) {
-  const DevView& d = f.d;
-  const int W = d.W, nu = d.nu, lx = d.lx;
-  const double* y = ybuf(d, it);
-  const double* ym = ybuf(d, it + 2);
-  FOR_RC(bn, 7, (W >> 1), m, k) cp16(slot + (size_t)m * rp + 2 * k, y + (size_t)grow[m] * W + 2 * k);
-  FOR_RC(bn, 7, (W >> 1), m, k) cp16(slot + (size_t)m * rp + W + 2 * k, ym + (size_t)grow[m] * W + 2 * k);
-  if (it > 0) {
-    FOR_RC(bn, 6, (nu >> 1), m, k) cp16(slot + (size_t)m * rp + 2 * W + 2 * k, d.Ua + (size_t)grow[m] * nu + 2 * k);
-    FOR_RC(bn, 5, (lx >> 1), m, k) cp16(slot + (size_t)m * rp + 2 * W + nu + 2 * k, d.Xa + (size_t)grow[m] * lx + 2 * k);
-  }
-}
-__device__ __forceinline__ void fused_batch(int b, int n_own, unsigned own, int kb, int nst, int pb, int& m0, int& bn) {
-  if (b < n_own) {
-    unsigned w = own;
-    for (int i = 0; i < b; ++i) w &= w - 1;
-    m0 = __ffs(w) - 1;
-    bn = 1;
-  } else {
-    const int c = b - n_own;
-    m0 = kb + c * pb;
-    bn = min(pb, nst - c * pb);
-  }
-}
-
-__global__ void __launch_bounds__(1024) k_chain_fused(FastView f) {
-  const DevView& d = f.d;
-  const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly, W = d.W, ns = d.ns;
-  const int kb = f.kstar, H = d.H, nst = H - kb, ci = blockIdx.x, pb = f.pb;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* Z = reinterpret_cast<double*>(smem_raw);
-  double* E = Z + (size_t)H * nu;
-  double* G = E + (size_t)H * nu;
-  double* T = G + (size_t)H * lx;
-  double* d2 = T + (size_t)H * FAST_MAXNS;
-  double* stp = d2 + (size_t)pb * 128;
-  double* ring = reinterpret_cast<double*>(smem_raw) + f.ring_off;
-  const int rp = 2 * W + nu + lx;
-  int* rows = reinterpret_cast<int*>(stp + 2 * pb + 2);
-  const NodePtrs np = *d.np;
-  const Ops op = blob_ops(f, f.blob);
-  const int it = *d.iter - 1;
-  const bool has_next = it + 1 < f.max_iter;
-  const bool store = it == *f.store_it;
-  const unsigned own = kb > 0 ? f.cown[ci] : 0u;
-  unsigned long long* pc = f.prof && threadIdx.x == 0 ? f.prof + (size_t)ci * P_N : nullptr;
-  unsigned long long t0 = pc ? clk() : 0, tstart = t0;
-#define FSTEP(slot)                     \
-  if (pc) {                              \
-    const unsigned long long t_ = clk(); \
-    pc[slot] += t_ - t0;                 \
-    t0 = t_;                             \
-  }
-  if (threadIdx.x < H) {
-    const int m = threadIdx.x;
-    rows[m] = m < kb ? f.cpath[(size_t)ci * kb + m] : chain_row(f, m - kb, ci);
-  }
-  __syncthreads();
-  // ---- D: down pass
-  FOR_RC(H, 6, (nu >> 1), m, k) cp16(Z + (size_t)m * nu + 2 * k, f.Lb + (size_t)rows[m] * nu + 2 * k);
-  FOR_RC(H, 6, (nu >> 1), m, k) cp16(E + (size_t)m * nu + 2 * k, np.e_off + (size_t)rows[m] * nu + 2 * k);
-  FOR_RC(H, 5, (lx >> 1), m, k) cp16(G + (size_t)m * lx + 2 * k, np.g + (size_t)rows[m] * lx + 2 * k);
-  cp_commit();
-  cp_wait<0>();
-  __syncthreads();
-  FSTEP(1);
-  if (threadIdx.x < nu) {
-    const int k = threadIdx.x;
-    double ls = 0.0, es = d.q[k];
-    for (int m = 0; m < H; ++m) {
-      const double l = Z[m * nu + k];
-      ls = m == 0 ? l : ls + l;
-      Z[m * nu + k] = es - ls;
-      es = es + E[m * nu + k];
-    }
-  }
-  __syncthreads();
-  FOR_RC(H, 5, ns, m, i) {
-    const double* z = Z + (size_t)m * nu;
-    double v = 0.0;
-    for (int e = op.kptr[i]; e < op.kptr[i + 1]; ++e) v = fma(op.kval[e], z[op.kcol[e]], v);
-    T[m * FAST_MAXNS + i] = v;
-  }
-  __syncthreads();
-  FOR_NU(H, m, k) {
-    const double* tm = T + m * FAST_MAXNS;
-    double c = 0.0;
-    for (int e = op.ecp[k]; e < op.ecp[k + 1]; ++e) c = fma(op.ecv[e], tm[op.ecr[e]], c);
-    const double u = E[m * nu + k] + (Z[m * nu + k] - c);
-    Z[m * nu + k] = u;
-    if (store && (m >= kb || ((own >> m) & 1u))) d.U[(size_t)rows[m] * nu + k] = u;
-  }
-  __syncthreads();
-  FOR_NT(H, m, j) {
-    double bu = 0.0;
-    for (int e = op.brp[j]; e < op.brp[j + 1]; ++e) bu = fma(Z[m * nu + op.brc[e]], op.brv[e], bu);
-    E[m * nu + j] = bu;
-  }
-  __syncthreads();
-  if (threadIdx.x < nt) {
-    const int j = threadIdx.x;
-    double x = d.p[j];
-    for (int m = 0; m < H; ++m) {
-      x = (x + E[m * nu + j]) + G[m * lx + j];
-      G[m * lx + j] = x;
-      if (store && (m >= kb || ((own >> m) & 1u))) d.X[(size_t)rows[m] * lx + j] = x;
-    }
-  }
-  __syncthreads();
-  FSTEP(2);
-  // ---- P: prox of owned ancestors (one row per batch) and chain rows (pb per batch)
-  Ops pop = op;
-  pop.xmin = d.xmin;
-  pop.xmax = d.xmax;
-  pop.xsafe = d.xsafe;
-  pop.umin = d.umin;
-  pop.umax = d.umax;
-  RecOff o{};
-  o.y = 0;
-  o.ym = W;
-  o.ua = 2 * W;
-  o.xa = 2 * W + nu;
-  const int n_own = __popc(own);
-  const int nbat = n_own + (nst + pb - 1) / pb;
-  const double beta = d.beta[it], theta = d.theta[it], beta1 = has_next ? d.beta[it + 1] : 0.0;
-  {
-    int m0, bn;
-    fused_batch(0, n_own, own, kb, nst, pb, m0, bn);
-    fused_issue(f, ring, rp, rows + m0, bn, it);
-    cp_commit();
-  }
-  for (int b = 0; b < nbat; ++b) {
-    int m0, bn;
-    fused_batch(b, n_own, own, kb, nst, pb, m0, bn);
-    double* slot = ring + (size_t)(b & 1) * pb * rp;
-    if (b + 1 < nbat) {
-      int m1, bn1;
-      fused_batch(b + 1, n_own, own, kb, nst, pb, m1, bn1);
-      fused_issue(f, ring + (size_t)((b + 1) & 1) * pb * rp, rp, rows + m1, bn1, it);
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
-    FSTEP(3);
-    prox_rows(f, pop, rows + m0, bn, Z + (size_t)m0 * nu, nu, G + (size_t)m0 * lx, lx, slot, rp, d2, 128, stp, it, beta,
-              theta, beta1, has_next, o, G + (size_t)m0 * lx, lx, Z + (size_t)m0 * nu, nu);
-    if (m0 < kb && has_next) {  // owned ancestor: its collapsed dual goes to HBM for k_branch_grp
-      const size_t r = (size_t)rows[m0];
-      for (int j = threadIdx.x; j < nt; j += blockDim.x) d.Yc[r * ly + j] = G[m0 * lx + j];
-      for (int k = threadIdx.x; k < nu; k += blockDim.x) d.Yc[r * ly + lx + k] = Z[m0 * nu + k];
-    }
-    FSTEP(4);
-  }
-  if (!has_next) return;
-  // ---- U: up pass of the next iteration on the chain rows (smem rows kb..H-1)
-  double* Zc = Z + (size_t)kb * nu;  // Yu -> a
-  double* Gc = G + (size_t)kb * lx;  // Yx -> wbar
-  FOR_RC(nst - 1, 6, (nu >> 1), t, k) cp16(E + (size_t)t * nu + 2 * k, np.R + (size_t)chain_row(f, t, ci) * nu + 2 * k);
-  cp_commit();
-  if (threadIdx.x < nt) {  // wbar suffix scan (own column only: no barrier needed before)
-    const int j = threadIdx.x;
-    double acc = 0.0;
-    for (int t = nst - 1; t >= 0; --t) {
-      const double yx = Gc[t * lx + j];
-      acc = t == nst - 1 ? yx : yx + acc;
-      Gc[t * lx + j] = acc;
-    }
-    d.wbar[(size_t)chain_row(f, 0, ci) * lx + j] = acc;
-  }
-  cp_wait<0>();
-  __syncthreads();
-  FSTEP(5);
-  FOR_NU(nst, t, k) {  // a = (Yu + wbar B) + R
-    double bw = 0.0;
-    for (int e = op.bcp[k]; e < op.bcp[k + 1]; ++e) bw = fma(Gc[t * lx + op.bcr[e]], op.bcv[e], bw);
-    double a = Zc[t * nu + k] + bw;
-    if (t < nst - 1) a = a + E[t * nu + k];
-    Zc[t * nu + k] = a;
-  }
-  __syncthreads();
-  if (threadIdx.x < nu) {  // S_t = A_{t+1} (into E), A_0 -> Asub of the chain top
-    const int k = threadIdx.x;
-    double acc = 0.0;
-    for (int t = nst - 1; t >= 0; --t) {
-      E[t * nu + k] = acc;
-      const double a = Zc[t * nu + k];
-      acc = t == nst - 1 ? a : a + acc;
-    }
-    f.Asub[(size_t)chain_row(f, 0, ci) * nu + k] = acc;
-  }
-  __syncthreads();
-  proj_rows(d, op, E, E, T, nst - 1);
-  FOR_NU(nst, t, k) {
-    const double a = Zc[t * nu + k];
-    const double l = t < nst - 1 ? a + E[t * nu + k] : a;
-    const size_t r = (size_t)chain_row(f, t, ci);
-    f.Lb[r * nu + k] = l * f.aux[r * 2];
-  }
-  FSTEP(6);
-  if (pc) pc[0] += clk() - tstart;
-#undef FSTEP
-}
-
 }  // namespace wmpc

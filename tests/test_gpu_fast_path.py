@@ -115,16 +115,12 @@ def test_reciprocal_division_is_exact():
 
 
 # env switches of the kernel variants (graph: CTA-per-chain kernels; chainw:
-# warp-per-chain kernels with an 8- or 2-row shared-memory ring, or rows
+# warp-per-chain kernels with an 8-row shared-memory ring (fp64), or rows
 # streamed through registers)
 VARIANT_ENV = {
     "graph": {"WMPC_CHAINW": "0"},
-    "graph-fused": {"WMPC_FUSED": "1", "WMPC_CHAINW": "0"},
-    "graph-pu": {"WMPC_PU": "1", "WMPC_CHAINW": "0"},
     "graph-chainw8": {"WMPC_CHAINW": "1", "WMPC_CWPD": "8"},
-    "graph-chainw2": {"WMPC_CHAINW": "1", "WMPC_CWPD": "2"},
     "graph-chainwr": {"WMPC_CHAINW": "1", "WMPC_CWPD": "1"},
-    "graph-chainwr2": {"WMPC_CHAINW": "1", "WMPC_CWPD": "1", "WMPC_CWRD": "2"},
 }
 
 
@@ -141,8 +137,7 @@ def _with_env(env, fn):
                 os.environ[k] = v
 
 
-@pytest.mark.parametrize("kernel", ["graph", "graph-fused", "graph-pu", "graph-chainw8", "graph-chainw2",
-                                    "graph-chainwr", "graph-chainwr2", "scan", "cta", "warp"])
+@pytest.mark.parametrize("kernel", ["graph", "graph-chainw8", "graph-chainwr", "scan", "cta"])
 @pytest.mark.parametrize("cfg", ["C1", "C2"])
 def test_every_structured_kernel_matches_general(cfg, kernel):
     inst = config_instance(cfg)
@@ -151,14 +146,14 @@ def test_every_structured_kernel_matches_general(cfg, kernel):
     rf, mf = _with_env(env, lambda: _solve(inst, 40, gamma, True, gce=17))
     rg, _ = _solve(inst, 40, gamma, False, gce=17)
     # a variant whose shared-memory footprint does not fit falls back to the CTA kernel (1..99)
-    allowed = {"graph": [300], "graph-fused": [310], "graph-pu": [320], "scan": list(range(200, 300)) + list(range(1, 100)),
-               "warp": list(range(100, 200)) + list(range(1, 100)), "cta": list(range(1, 100))}.get(kernel, [300])
+    allowed = {"graph": [300], "scan": list(range(200, 300)) + list(range(1, 100)),
+               "cta": list(range(1, 100))}.get(kernel, [300])
     assert mf in allowed, mf
     for k in ("u0", "primal", "primal_avg", "dual"):
         assert rel_err(getattr(rf, k), getattr(rg, k)) <= 1e-11, k
 
 
-@pytest.mark.parametrize("variant", ["graph-chainw8", "graph-chainw2", "graph-chainwr", "graph-chainwr2"])
+@pytest.mark.parametrize("variant", ["graph-chainw8", "graph-chainwr"])
 @pytest.mark.parametrize("cfg,prec", [("C1", "fp64"), ("C3", "fp64"), ("C2", "fp32")])
 def test_chain_kernel_variants_bit_identical(cfg, prec, variant):
     """The warp-per-chain kernels (wmpc_chainw.cuh) do the per-element
