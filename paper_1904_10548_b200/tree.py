@@ -196,3 +196,29 @@ def uniform_tree(branching, horizon: int, n_demand: int, n_price: int,
         eps = np.zeros((n, n_demand + n_price))
     return ScenarioTree(horizon, n_demand, n_price, np.array(stage), np.array(anc),
                         np.array(prob), eps=eps)
+
+
+def random_tree(horizon: int, n_demand: int, n_price: int, branching_stages: int, max_children: int,
+                rng, eps: np.ndarray | None = None) -> ScenarioTree:
+    """BFS tree whose nodes in the first ``branching_stages`` stages have a
+    random number of children (1..max_children) with random split
+    probabilities, single-child chains below: the non-uniform shape of the
+    reference's fan-to-tree reduction (tree.py:320-392: bundles of scenarios
+    merge into nodes of unequal probability). Benchmarks and tests only."""
+    stage, anc, prob, frontier = [0], [-1], [1.0], [0]
+    for j in range(1, horizon + 1):
+        nxt = []
+        for parent in frontier:
+            k = int(rng.integers(1, max_children + 1)) if j <= branching_stages else 1
+            w = rng.random(k) + 0.25
+            w /= w.sum()
+            for c in range(k):
+                stage.append(j)
+                anc.append(parent)
+                prob.append(prob[parent] * (w[c] if k > 1 else 1.0))
+                nxt.append(len(stage) - 1)
+        frontier = nxt
+    n = len(stage)
+    if eps is None:
+        eps = np.zeros((n, n_demand + n_price))
+    return ScenarioTree(horizon, n_demand, n_price, np.array(stage), np.array(anc), np.array(prob), eps=eps)

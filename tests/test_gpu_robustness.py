@@ -1,0 +1,49 @@
+"""Shapes beyond the uniform Barcelona benchmark trees:
+* a non-uniform tree (random 1..k children with unequal probabilities over
+  the branching stages, the shape of the reference's fan-to-tree reduction,
+  tree.py:320-392), on the default kernels and on k_chain_dp;
+* a network whose flows join two mixing nodes (E E^T not diagonal, rows of
+  K = (E E^T)^{-1} E 40 wide): the ELL graph path declines it and the
+  structured persistent kernel (or the general path) runs;
+all against the oracle at the north_star's 1e-8 after fixed iterations."""
+
+from __future__ import annotations
+
+import pytest
+
+from conftest import rel_err
+from oracle import port
+from paper_1904_10548_b200 import SolverConfig, solve
+from paper_1904_10548_b200 import _native as nat
+from paper_1904_10548_b200 import solver as S
+from paper_1904_10548_b200.synthetic import barcelona_instance, fan_like_instance
+
+pytestmark = pytest.mark.gpu
+
+
+def _vs_oracle(inst, cache, it=80, gamma=1 / 3e9):
+    res = solve(inst, SolverConfig(max_iter=it, tol=1e-30, gamma=gamma, gap_check_every=it + 1), cache=cache)
+    ref = port.apg_solve(inst, gamma, max_iter=it, tol=1e-30, gap_check_every=it + 1,
+                         reference_cost_accounting=False)
+    for k in ("u0", "primal", "primal_avg", "dual"):
+        assert rel_err(getattr(res, k), getattr(ref, k)) <= 1e-8, k
+    assert abs(res.objective - ref.objective) <= 1e-8 * (1 + abs(ref.objective))
+    assert abs(res.duality_gap - ref.duality_gap) <= 1e-8 * (1 + abs(ref.duality_gap))
+
+
+@pytest.mark.parametrize("dp", [False, True])
+def test_non_uniform_tree_vs_oracle(dp, monkeypatch):
+    inst = fan_like_instance(seed=1, leaves_target=48, branching_stages=3, max_children=4, horizon=10)
+    monkeypatch.setenv("WMPC_DP", "1" if dp else "0")
+    cache = S._factor(inst, None, private=True)
+    info = nat.path_info(cache._bind())
+    assert info["fast_path"] == 300 and info["fused_dp"] == int(dp), info
+    _vs_oracle(inst, cache)
+
+
+def test_coupled_mixing_nodes_vs_oracle():
+    inst = barcelona_instance([2, 2, 2], mixing_links=8)
+    cache = S._factor(inst, None, private=True)
+    info = nat.path_info(cache._bind())
+    assert info["fast_path"] != 300, info  # wide K rows: not the ELL graph path
+    _vs_oracle(inst, cache, it=60)
