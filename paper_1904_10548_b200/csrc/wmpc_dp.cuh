@@ -139,6 +139,32 @@ __device__ __forceinline__ double pw_group8_64(const double* d2, int n, int lane
   return res;
 }
 
+// The kernel's sparse operators, register-light: a lane's 22 ELL entries
+// (slots: B by column q,e -> 2q+e; E by column q -> 8+q; K row e -> 12+e;
+// B by row h,e -> 16+3h+e) keep only their column index, 8 bits each, packed
+// four to a register (6 registers instead of 22 addresses); the values sit in
+// a per-CTA [slot][lane] table. A gather is BFE + LEA + 2 LDS + DFMA.
+struct DpOps {
+  unsigned pk[6];  // packed entry indices
+  unsigned vrow;   // shared address of this lane's value column (slot 0)
+  unsigned xb;     // shared address of the warp's exchange vectors
+};
+template <typename TG>
+__device__ __forceinline__ TG dp_gather(const DpOps& o, int slot0, int w, unsigned voff) {
+  TG x[8], v[8];
+#pragma unroll
+  for (int e = 0; e < w; ++e) {
+    const int sl = slot0 + e;
+    const unsigned idx = (o.pk[sl >> 2] >> (8 * (sl & 3))) & 0xffu;
+    x[e] = lds_t(o.xb + voff + idx * (unsigned)sizeof(TG), TG(0));
+    v[e] = lds_t(o.vrow + (unsigned)(sl * 32 * sizeof(TG)), TG(0));
+  }
+  TG s = 0;
+#pragma unroll
+  for (int e = 0; e < w; ++e) s = fma(v[e], x[e], s);
+  return s;
+}
+
 // Compile-time network dimensions (NT tanks, NU flows; the instantiated shape
 // is the Barcelona-dimension 63 / 114 network, other shapes run the graph
 // path): every offset and loop bound is a constant, so no dimension or index
@@ -187,22 +213,43 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     else v = i - 320 < NU ? d.umax[i - 320] : 0.0;
     bnd[i] = v;
   }
-  int voff = 0;
-  EllV<EllW<WE>::BC, TG, TG> bc[4];
-  EllV<EllW<WE>::EC, TG, TG> ec[4];
+  static_assert(EllW<WE>::BC == 2 && EllW<WE>::EC == 1 && EllW<WE>::KR == 4 && EllW<WE>::BR == 3, "slot map");
+  DpOps ops;
+  {
+    TG* vt = reinterpret_cast<TG*>(vtab);
+    unsigned pk[6] = {0, 0, 0, 0, 0, 0};
+    auto put = [&](int sl, int idx, TG val) {
+      pk[sl >> 2] |= ((unsigned)idx & 0xffu) << (8 * (sl & 3));
+      if (warp == 0) vt[sl * 32 + lane] = val;
+    };
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int k = cw_ku(lane, q);
-    bc[q] = ellv_bind<TG>(ell_own<EllW<WE>::BC, TG>(f, own_bc(d, k), k < NU), wb, vtab, voff, lane, warp == 0);
-    ec[q] = ellv_bind<TG>(ell_own<EllW<WE>::EC, TG>(f, own_ec(d, k), k < NU), tb, vtab, voff, lane, warp == 0);
+    for (int q = 0; q < 4; ++q) {
+      const int k = cw_ku(lane, q);
+      const Ell<2, TG> b = ell_own<2, TG>(f, own_bc(d, k), k < NU);
+      put(2 * q, b.idx[0], b.val[0]);
+      put(2 * q + 1, b.idx[1], b.val[1]);
+      const Ell<1, TG> e = ell_own<1, TG>(f, own_ec(d, k), k < NU);
+      put(8 + q, e.idx[0], e.val[0]);
+    }
+    const Ell<4, TG> kk = ell_own<4, TG>(f, own_kr(d, lane), lane < d.ns);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) put(12 + e, kk.idx[e], kk.val[e]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const Ell<3, TG> b = ell_own<3, TG>(f, own_br(d, l2 + h), l2 + h < NT);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) put(16 + 3 * h + e, b.idx[e], b.val[e]);
+    }
+#pragma unroll
+    for (int i = 0; i < 6; ++i) ops.pk[i] = pk[i];
+    ops.vrow = smem_u32(vt + lane);
+    ops.xb = smem_u32(wb);
   }
-  const EllV<EllW<WE>::KR, TG, TG> kr =
-      ellv_bind<TG>(ell_own<EllW<WE>::KR, TG>(f, own_kr(d, lane), lane < d.ns), zb, vtab, voff, lane, warp == 0);
-  EllV<EllW<WE>::BR, TG, TG> br[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-    br[h] = ellv_bind<TG>(ell_own<EllW<WE>::BR, TG>(f, own_br(d, l2 + h), l2 + h < NT), ub, vtab, voff, lane,
-                          warp == 0);
+  constexpr unsigned WB_OFF = 0, ZB_OFF = 64 * sizeof(TG), UB_OFF = 192 * sizeof(TG), TB_OFF = 320 * sizeof(TG);
+  auto G_bc = [&](int q) { return dp_gather<TG>(ops, 2 * q, 2, WB_OFF); };   // (B^T wb)_k
+  auto G_ec = [&](int q) { return dp_gather<TG>(ops, 8 + q, 1, TB_OFF); };   // (E^T tb)_k
+  auto G_kr = [&]() { return dp_gather<TG>(ops, 12, 4, ZB_OFF); };           // (K zb)_lane
+  auto G_br = [&](int h) { return dp_gather<TG>(ops, 16 + 3 * h, 3, UB_OFF); };  // (B ub)_j
   pdl_wait();  // L of the branching rows comes from the last group kernel; iter from the first
   pdl_trigger();
   const int it = *d.iter - 1;
@@ -318,17 +365,17 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     st2(zb + l2, z[0], z[1]);
     st2(zb + 64 + l2, z[2], z[3]);
     __syncwarp();
-    tb[lane] = ellv_dot(kr);  // zero past ns
+    tb[lane] = G_kr();  // zero past ns
     __syncwarp();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) out[q] = base[q] + (z[q] - ellv_dot(ec[q]));
+    for (int q = 0; q < 4; ++q) out[q] = base[q] + (z[q] - G_ec(q));
   };
   auto bmul = [&](const TG (&u)[4], TG (&bu)[2]) {  // bu = B u (rows l2, l2 + 1)
     st2(ub + l2, u[0], u[1]);
     st2(ub + 64 + l2, u[2], u[3]);
     __syncwarp();
 #pragma unroll
-    for (int h = 0; h < 2; ++h) bu[h] = ellv_dot(br[h]);
+    for (int h = 0; h < 2; ++h) bu[h] = G_br(h);
   };
   double badacc = 0.0;  // fma(p, 0, .): NaN once any output was not finite
   // Moreau prox of one row (prox_x_warp / prox_u_warp arithmetic per element,
@@ -567,7 +614,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       TG a[4], Sv[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        a[q] = yu[q] + ellv_dot(bc[q]);
+        a[q] = yu[q] + G_bc(q);
         Sv[q] = acc[q];
         acc[q] = bottom ? a[q] : a[q] + acc[q];
       }
@@ -576,10 +623,10 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         st2(zb + l2, Sv[0], Sv[1]);
         st2(zb + 64 + l2, Sv[2], Sv[3]);
         __syncwarp();
-        tb[lane] = ellv_dot(kr);
+        tb[lane] = G_kr();
         __syncwarp();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) l[q] = a[q] + (Sv[q] - ellv_dot(ec[q]));
+        for (int q = 0; q < 4; ++q) l[q] = a[q] + (Sv[q] - G_ec(q));
       } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q) l[q] = a[q];

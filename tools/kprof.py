@@ -31,5 +31,6 @@ res = {}
 fp32 = "--fp32" in sys.argv
 for cfg in [a for a in sys.argv[1:] if a.startswith("C")]:
     inst = config_instance(cfg)
-    res[cfg] = prof(factor_step(inst)._bind(), inst, fp32=fp32)
+    cache = factor_step(inst)  # keep the cache alive: its context dies with it
+    res[cfg] = prof(cache._bind(), inst, fp32=fp32)
 print(json.dumps(res))
