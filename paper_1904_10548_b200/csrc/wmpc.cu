@@ -483,7 +483,7 @@ bool dp_on(const wmpc_ctx* ctx) {
 template <typename TG>
 void launch_dp(wmpc_ctx* ctx, const FastView& f) {
   if constexpr (sizeof(TG) == 8) {  // fp64 only (dp_on)
-    DpArgs a{(void*)ctx->dp_agg, (const void*)ctx->dp_putg, ctx->dp_cpw};
+    DpArgs a{(void*)ctx->dp_agg, (const void*)ctx->dp_putg, ctx->dp_cpw, ctx->kstar * ctx->nu + dp_agg_w(ctx->nu, ctx->lx)};
     const dim3 grid(ctx->dp_grid), block(ctx->dp_wpc * 32);
     launch_pdl(ctx, k_chain_dp<DP_NT, DP_NU, double>, grid, block, ctx->dp_sm, f, a);
   }
@@ -621,7 +621,7 @@ void configure_dp(wmpc_ctx* ctx) {
   const int nw = (nchain + cpw - 1) / cpw;
   const int wpc = std::min(DP_MAXT / 32, std::max(1, (nw + sms - 1) / sms));
   const int grid = (nw + wpc - 1) / wpc;
-  const size_t sm = dp_smem<double>(wpc, nt, nu, lx);
+  const size_t sm = dp_smem<double>(wpc, nt, nu, lx, kstar);
   if (sm > 227 * 1024) return;
   dp_attr(ctx, sm);
   // ownership of the branching rows balanced over the persistent warps

@@ -66,6 +66,7 @@ struct DpArgs {
   void* agg;         // nchain x (3 nu + lx), TG: [LSc | LWc | SUTp | SGp]
   const void* putg;  // n_branch x (nu + lx), TG: root-path prefix sums [PUT | PG] of each branching row
   int cpw;           // chains per warp
+  int pro_w;         // doubles of a warp's chain-prologue scratch: kstar * nu + (3 nu + lx)
 };
 
 __host__ __device__ inline int dp_stage(int nt, int nu, int lx) { return 2 * (2 * nt + nu) + nu + lx; }
@@ -89,9 +90,10 @@ __host__ __device__ inline int dp_stage_t(int nt, int nu, int lx) {  // k_chain_
   return dp_stage(nt, nu, lx) + (sizeof(TG) == 8 ? 2 * nu + lx + 2 : 0);
 }
 template <typename TG>
-__host__ __device__ inline size_t dp_smem(int wpc, int nt, int nu, int lx) {
+__host__ __device__ inline size_t dp_smem(int wpc, int nt, int nu, int lx, int kstar) {
   return sizeof(double) * (DP_BND + 8 + DP_VSLOTS * 32) + sizeof(DpPtrs<TG>) +
-         (size_t)wpc * (sizeof(double) * (DP_D * (size_t)dp_stage_t<TG>(nt, nu, lx) + 128) + sizeof(TG) * DP_XCH);
+         (size_t)wpc * (sizeof(double) * (DP_D * (size_t)dp_stage_t<TG>(nt, nu, lx) + 128) + sizeof(TG) * DP_XCH) +
+         sizeof(double) * (size_t)wpc * ((size_t)kstar * nu + 3 * nu + lx);
 }
 
 template <typename TG>
@@ -196,6 +198,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
   const size_t wbytes = sizeof(double) * (DP_D * STG + 128) + sizeof(TG) * DP_XCH;
   double* ring = reinterpret_cast<double*>(wbase + warp * wbytes);
   double* sd2 = ring + DP_D * STG;  // 128
+  double* pro = reinterpret_cast<double*>(wbase + (size_t)wpc * wbytes) + (size_t)warp * A.pro_w;  // chain prologue
   TG* wb = reinterpret_cast<TG*>(sd2 + 128);  // 64
   TG* zb = wb + 64;                           // 128
   TG* ub = zb + 128;                          // 128
@@ -277,15 +280,18 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
   const int gw = blockIdx.x * wpc + warp, nw = gridDim.x * wpc;
   // ---- prox-row ring: owned ancestors then chain rows (bottom-up) of each
   // chain slot; one cp.async group per row (empty past the end)
-  int ic_cs = 0, ic_pos = -1;
+  int ic_cs = 0, ic_pos = -2;  // the first ++ lands on chain slot 0's prologue
   unsigned ic_own = 0u;
   int ic_k = 0, ck = 0;
+  // ring positions per chain: -1 the chain prologue (its ancestors' L rows and
+  // its aggregates, into the warp's scratch, not a stage), 0..kb-1 the owned
+  // ancestors, kb.. the chain rows bottom-up; one cp.async group each
   auto issue = [&]() {
     bool have = false, chain_row = false;
     unsigned r = 0;
     for (;;) {
       if (++ic_pos == kb + N) {
-        ic_pos = 0;
+        ic_pos = -1;
         ++ic_cs;
       }
       const int ci = gw + ic_cs * nw;
@@ -294,7 +300,21 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         ic_cs = A.cpw;
         break;
       }
-      if (ic_pos == 0) ic_own = kb > 0 ? __ldg(Q.cown + ci) : 0u;
+      if (ic_pos < 0) {  // prologue of chain ci
+        ic_own = kb > 0 ? __ldg(Q.cown + ci) : 0u;
+        for (int m = 0; m < kb; ++m) {
+          const double* sl = reinterpret_cast<const double*>(Q.Lb) + (size_t)Q.cpath[(size_t)ci * kb + m] * NU +
+                             2 * lane;
+#pragma unroll
+          for (int k = 0; k < (NU / 2 + 31) / 32; ++k)
+            if (lane + 32 * k < NU / 2) cp16(pro + m * NU + 2 * lane + 64 * k, sl + 64 * k);
+        }
+        const double* sa = reinterpret_cast<const double*>(Q.agg) + (size_t)ci * AW + 2 * lane;
+#pragma unroll
+        for (int k = 0; k < (AW / 2 + 31) / 32; ++k)
+          if (lane + 32 * k < AW / 2) cp16(pro + kb * NU + 2 * lane + 64 * k, sa + 64 * k);
+        break;
+      }
       if (ic_pos >= kb) {
         r = nbr + (unsigned)(N - 1 - (ic_pos - kb)) * nchain + (unsigned)ci;
         have = chain_row = true;
@@ -494,27 +514,19 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       yx[1] = TG(0);
     }
   };
-  auto ldrow = [&](unsigned r, TG (&L)[4], TG (&b)[4], TG (&g)[2], TG& ax) {  // down operands of a chain row
-    const auto a0 = ld2cg(Q.Lb + (size_t)r * NU + l2), a1 = ld2cg(Q.Lb + (size_t)r * NU + o1);
-    const auto b0 = ld2cg(Q.UT + (size_t)r * NU + l2), b1 = ld2cg(Q.UT + (size_t)r * NU + o1);
-    const auto g0 = ld2cg(Q.g + (size_t)r * LX + l2);
-    L[0] = a0.x; L[1] = a0.y; L[2] = ok1 ? a1.x : TG(0); L[3] = ok1 ? a1.y : TG(0);
-    b[0] = b0.x; b[1] = b0.y; b[2] = ok1 ? b1.x : TG(0); b[3] = ok1 ? b1.y : TG(0);
-    g[0] = g0.x; g[1] = okx2 ? g0.y : TG(0);
-    ax = __ldcg(Q.aux + (size_t)r * 2);
-  };
+
   for (int cs = 0; cs < A.cpw; ++cs) {
     const int ci = gw + cs * nw;
     if (ci >= (int)nchain) break;
     const unsigned r_top = nbr + (unsigned)ci;
-    // the bottom chain row's operands (fp32) and the chain aggregates: in flight during the ancestor walk
-    TG Lc[4], bcur[4], gcur[2], axc;
-    if constexpr (!SDG) ldrow(nbr + (unsigned)(N - 1) * nchain + (unsigned)ci, Lc, bcur, gcur, axc);
+    // the chain prologue (a ring group): its ancestors' L rows and its aggregates, in the scratch
+    take();
+    release();  // occupies no stage: the next group goes out right away
     TG LSc[4], LWc[4], SU[4], SG[2];
     {
-      const TG* a = Q.agg + (size_t)ci * AW;
-      const auto s0 = ld2cg(a + l2), s1 = ld2cg(a + o1), w0 = ld2cg(a + NU + l2), w1 = ld2cg(a + NU + o1);
-      const auto u0 = ld2cg(a + 2 * NU + l2), u1 = ld2cg(a + 2 * NU + o1), g0 = ld2cg(a + 3 * NU + l2);
+      const double* a = pro + kb * NU;
+      const double2 s0 = ld2s(a + l2), s1 = ld2s(a + o1), w0 = ld2s(a + NU + l2), w1 = ld2s(a + NU + o1);
+      const double2 u0 = ld2s(a + 2 * NU + l2), u1 = ld2s(a + 2 * NU + o1), g0 = ld2s(a + 3 * NU + l2);
       LSc[0] = s0.x; LSc[1] = s0.y; LSc[2] = ok1 ? s1.x : TG(0); LSc[3] = ok1 ? s1.y : TG(0);
       LWc[0] = w0.x; LWc[1] = w0.y; LWc[2] = ok1 ? w1.x : TG(0); LWc[3] = ok1 ? w1.y : TG(0);
       SU[0] = u0.x; SU[1] = u0.y; SU[2] = ok1 ? u1.x : TG(0); SU[3] = ok1 ? u1.y : TG(0);
@@ -525,7 +537,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     const unsigned own = kb > 0 ? __ldg(Q.cown + ci) : 0u;
     for (int m = 0; m < kb; ++m) {
       const unsigned r = (unsigned)Q.cpath[(size_t)ci * kb + m];
-      const auto a0 = ld2cg(Q.Lb + (size_t)r * NU + l2), a1 = ld2cg(Q.Lb + (size_t)r * NU + o1);
+      const double2 a0 = ld2s(pro + m * NU + l2), a1 = ld2s(pro + m * NU + o1);
       const TG La[4] = {a0.x, a0.y, ok1 ? a1.x : TG(0), ok1 ? a1.y : TG(0)};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -576,23 +588,13 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       const bool bottom = t == N - 1;
       TG L[4], b[4], g[2], ax, u[4], yx[2], yu[4];
       const double* st = take();
-      if constexpr (SDG) {
+      {
         const double2 a0 = ld2s(st + oL + l2), a1 = ld2s(st + oL + o1), b0 = ld2s(st + oB + l2),
                       b1 = ld2s(st + oB + o1), g0 = ld2s(st + oG + l2);
         L[0] = a0.x; L[1] = a0.y; L[2] = ok1 ? a1.x : 0.0; L[3] = ok1 ? a1.y : 0.0;
         b[0] = b0.x; b[1] = b0.y; b[2] = ok1 ? b1.x : 0.0; b[3] = ok1 ? b1.y : 0.0;
         g[0] = g0.x; g[1] = okx2 ? g0.y : 0.0;
         ax = st[oAx];
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          L[q] = Lc[q];
-          b[q] = bcur[q];
-        }
-        g[0] = gcur[0];
-        g[1] = gcur[1];
-        ax = axc;
-        if (t > 0) ldrow(r - nchain, Lc, bcur, gcur, axc);  // the row above, one row ahead
       }
       proj_neg(ls, b, u);
       prox(st, r, u, xs, yx, yu);
