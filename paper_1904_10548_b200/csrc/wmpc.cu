@@ -1129,10 +1129,10 @@ void launch_graphk(wmpc_ctx* ctx, int count) {
 // up/branch/down passes write U, X into Uc, Xc. phase 0: up to the exchange
 // point (sharded: partial sums in xbuf); phase 1: the rest; -1: both.
 template <int WE>
-void dual_eval_graph(wmpc_ctx* ctx, const double* y, int phase) {
+void dual_eval_graph(wmpc_ctx* ctx, const double* y, int phase, double* Uout = nullptr, double* Xout = nullptr) {
   FastView f = make_fastview(ctx, 1);
-  f.d.U = ctx->Uc;
-  f.d.X = ctx->Xc;
+  f.d.U = Uout ? Uout : ctx->Uc;
+  f.d.X = Xout ? Xout : ctx->Xc;
   f.rfree = 0;  // the minimiser of an arbitrary y: the full form with R
   if (dp_on(ctx)) {  // L, subtree totals and wbar are k_chain_dp's iteration state: use scratch
     f.Lb = ctx->dp_Lc;
@@ -1165,6 +1165,22 @@ void dual_eval_graph(wmpc_ctx* ctx, const double* y, int phase) {
     ctx->launches += 1 + (ctx->rep_group.second > 0);
   }
   check_launch(ctx);
+}
+
+// Dual-function minimiser (U, X) of a device-resident y for the public
+// dual_gradient and the power iteration: the graph kernels when the
+// structured path is bound (one launch per kernel of the iteration graph
+// instead of 2H per-stage launches), the general per-stage kernels otherwise.
+void dual_gradient_dev(wmpc_ctx* ctx, const double* y, double* Uout, double* Xout) {
+  if (ctx->fast && ctx->use_graphk && ctx->shard_k < 0) {
+    if (ctx->ell_w == 4) dual_eval_graph<4>(ctx, y, -1, Uout, Xout);
+    else dual_eval_graph<8>(ctx, y, -1, Uout, Xout);
+    return;
+  }
+  DevView d = view(ctx);
+  d.U = Uout;
+  d.X = Xout;
+  launch_dg(ctx, d, y, 0);
 }
 
 // x from u along every root path: one chain-parallel launch in graph mode
@@ -1764,7 +1780,7 @@ int wmpc_dual_gradient(wmpc_ctx* ctx, const double* y, double* z, double* value)
     DevView d = view(ctx);
     d.U = ctx->Uc;
     d.X = ctx->Xc;
-    launch_dg(ctx, d, ctx->ys, 0);
+    dual_gradient_dev(ctx, ctx->ys, ctx->Uc, ctx->Xc);
     ctx->launches++;
     k_join_primal<<<grid_for(n * ctx->P), 256, 0, ctx->stream>>>(ctx->n, ctx->nu, ctx->nt, ctx->lx, ctx->Uc, ctx->Xc,
                                                                    ctx->zbuf);
@@ -1806,7 +1822,7 @@ static void apply_operator(wmpc_ctx* ctx, const double* vsrc, double out[2]) {
   DevView d = view(ctx);
   d.U = ctx->Uc;
   d.X = ctx->Xc;
-  launch_dg(ctx, d, vsrc, 0);
+  dual_gradient_dev(ctx, vsrc, ctx->Uc, ctx->Xc);
   size_t len = (size_t)ctx->n * ctx->W;
   int nb = std::min(ctx->part_blocks, grid_for(len));
   ctx->launches++;
@@ -1820,10 +1836,7 @@ static void apply_operator(wmpc_ctx* ctx, const double* vsrc, double out[2]) {
 
 static void zero_dual_solution(wmpc_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->ys, 0, sizeof(double) * (size_t)ctx->n * ctx->W, ctx->stream));
-  DevView d = view(ctx);
-  d.U = ctx->U0;
-  d.X = ctx->X0;
-  launch_dg(ctx, d, ctx->ys, 0);
+  dual_gradient_dev(ctx, ctx->ys, ctx->U0, ctx->X0);
 }
 
 int wmpc_power_iteration(wmpc_ctx* ctx, const double* v0, double rel_tol, int max_iter, double* lam,
