@@ -400,7 +400,11 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
   double badacc = 0.0;  // fma(p, 0, .): NaN once any output was not finite
   // Moreau prox of one row (prox_x_warp / prox_u_warp arithmetic per element,
   // bit-exact with numpy), ergodic averages, next collapsed dual
-  auto prox = [&](const double* st, unsigned r, const TG (&u)[4], const TG (&x)[2], TG (&yx)[2], TG (&yu)[4]) {
+  // In the norms' shadow (the one long dependency chain of a row): bu = B u
+  // (the x recursion of the row above) and wn = -P lsn (the down pass of the
+  // row above: u = ut + wn, proj_neg's rounding).
+  auto prox = [&](const double* st, unsigned r, const TG (&u)[4], const TG (&x)[2], TG (&yx)[2], TG (&yu)[4],
+                  TG (&bu)[2], const TG (&lsn)[4], TG (&wn)[4]) {
     double* yn = Q.ynb + (size_t)r * W;
     double v1[2], v2[2], V1[2], V2[2], c1[2], c2[2], y1[2], y2[2];
     {
@@ -473,26 +477,35 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         yu[2] = yu[3] = TG(0);
       }
     }
+    st2(ub + l2, u[0], u[1]);
+    st2(ub + 64 + l2, u[2], u[3]);
+    TG zn[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) zn[q] = -lsn[q];
+    st2(zb + l2, zn[0], zn[1]);
+    st2(zb + 64 + l2, zn[2], zn[3]);
     __syncwarp();
-    double stv = 0.0;
-    if (lane < 16) {  // the two tank-slot norms, numpy pairwise order (8-lane groups)
-      const int slot = lane >> 3, g = lane & 7;
-      const unsigned mask = 0xffu << (lane & 8);
-      const double* s2 = sd2 + 64 * slot;
-      double r8 = s2[g];
+    // the two tank-slot norms, numpy pairwise order (8-lane groups; lanes 16-31
+    // repeat lanes 0-15 so the block has no branch and B u interleaves with it)
+    const int slot = (lane >> 3) & 1, g = lane & 7;
+    const double* s2 = sd2 + 64 * slot;
+    double r8 = s2[g];
 #pragma unroll
-      for (int q = 1; q < NB / 8; ++q) r8 = dadd(r8, s2[g + 8 * q]);
-      double ssum = dadd(r8, __shfl_down_sync(mask, r8, 1, 8));
-      ssum = dadd(ssum, __shfl_down_sync(mask, ssum, 2, 8));
-      ssum = dadd(ssum, __shfl_down_sync(mask, ssum, 4, 8));
-      if (g == 0) {
+    for (int q = 1; q < NB / 8; ++q) r8 = dadd(r8, s2[g + 8 * q]);
 #pragma unroll
-        for (int q = NB; q < NT; ++q) ssum = dadd(ssum, s2[q]);
-        const double dist = __dsqrt_rn(ssum);
-        const double thr = dmul(ig, slot ? w_s : w_x);  // prox parameter RN(1/gamma) (solver.py:571)
-        stv = dist > 0.0 ? np_min(1.0, div_exact(thr, dist)) : 0.0;
-      }
-    }
+    for (int h = 0; h < 2; ++h) bu[h] = G_br(h);
+    tb[lane] = G_kr();  // zero past ns
+    __syncwarp();
+    double ssum = dadd(r8, __shfl_down_sync(0xffffffffu, r8, 1, 8));
+    ssum = dadd(ssum, __shfl_down_sync(0xffffffffu, ssum, 2, 8));
+    ssum = dadd(ssum, __shfl_down_sync(0xffffffffu, ssum, 4, 8));
+#pragma unroll
+    for (int q = NB; q < NT; ++q) ssum = dadd(ssum, s2[q]);  // complete on g == 0 only
+    const double dist = __dsqrt_rn(ssum);
+    const double thr = dmul(ig, slot ? w_s : w_x);  // prox parameter RN(1/gamma) (solver.py:571)
+    const double stv = dist > 0.0 ? np_min(1.0, div_exact(thr, dist)) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) wn[q] = zn[q] - G_ec(q);
     const double st1 = __shfl_sync(0xffffffffu, stv, 0), st2v = __shfl_sync(0xffffffffu, stv, 8);
     double p1[2], p2[2];
 #pragma unroll
@@ -556,8 +569,8 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         bmul(sw, bw);
         xa[0] = ((TG)d.p[l2] + bw[0]) + q0.x;
         xa[1] = okx2 ? ((TG)d.p[l2 + 1] + bw[1]) + q0.y : TG(0);
-        TG yx[2], yu[4];
-        prox(take(), r, ua, xa, yx, yu);
+        TG yx[2], yu[4], bx[2], wx[4];
+        prox(take(), r, ua, xa, yx, yu, bx, ls, wx);
         release();
         if (next) {
           TG* yc = Q.Yc + (size_t)r * LY;
@@ -581,6 +594,19 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) ls[q] = ls[q] + LSc[q];  // ls_{N-1}
     }
+    TG wn[4];  // -P ls of the next row down the walk
+    {
+      TG z[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) z[q] = -ls[q];
+      st2(zb + l2, z[0], z[1]);
+      st2(zb + 64 + l2, z[2], z[3]);
+      __syncwarp();
+      tb[lane] = G_kr();
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) wn[q] = z[q] - G_ec(q);
+    }
     // ---- chain rows, bottom-up: down of it, prox of it, up of it + 1
     TG wbr[2] = {0, 0}, acc[4] = {0, 0, 0, 0}, LSn[4] = {0, 0, 0, 0}, LWn[4] = {0, 0, 0, 0};
     for (int t = N - 1; t >= 0; --t) {
@@ -596,16 +622,17 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         g[0] = g0.x; g[1] = okx2 ? g0.y : 0.0;
         ax = st[oAx];
       }
-      proj_neg(ls, b, u);
-      prox(st, r, u, xs, yx, yu);
+      TG bu[2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        u[q] = b[q] + wn[q];
+        ls[q] = ls[q] - L[q];  // ls of the row above
+      }
+      prox(st, r, u, xs, yx, yu, bu, ls, wn);
       release();
-      if (t > 0) {  // x and ls of the row above
-        TG bu[2];
-        bmul(u, bu);
+      if (t > 0) {  // x of the row above
         xs[0] = (xs[0] - g[0]) - bu[0];
         xs[1] = (xs[1] - g[1]) - bu[1];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) ls[q] = ls[q] - L[q];
       }
       if (!next) continue;
       // up pass of the next iteration (k_chain_up_r arithmetic, R-free)
