@@ -53,7 +53,7 @@ namespace wmpc {
 #endif
 constexpr int DP_D = DP_D_N;   // ring stages per warp
 constexpr int DP_BND = 448;    // bounds table: xmin 64 | xmax 64 | xsafe 64 | umin 128 | umax 128
-constexpr int DP_XCH = 352;    // per-warp exchange vectors (TG): wb 64 | zb 128 | ub 128 | tb 32
+constexpr int DP_XCH = 512;    // per-warp exchange vectors (TG): wb 64 | zb 128 | ub 128 | tb 32 | zb2 128 | tb2 32
 constexpr int DP_VSLOTS = 22;  // operator value table: bc 8 | ec 4 | kr 4 | br 6 (x 32 lanes)
 #ifndef DP_MAXT
 #define DP_MAXT 256  // up to 8 warps per CTA, one CTA per SM
@@ -167,6 +167,28 @@ __device__ __forceinline__ TG dp_gather(const DpOps& o, int slot0, int w, unsign
   return s;
 }
 
+// the same entries applied to two exchange vectors (one value load per entry)
+template <typename TG>
+__device__ __forceinline__ void dp_gather2(const DpOps& o, int slot0, int w, unsigned voff, unsigned voff2, TG& s,
+                                           TG& s2) {
+  TG x[8], x2[8], v[8];
+#pragma unroll
+  for (int e = 0; e < w; ++e) {
+    const int sl = slot0 + e;
+    const unsigned idx = (o.pk[sl >> 2] >> (8 * (sl & 3))) & 0xffu;
+    x[e] = lds_t(o.xb + voff + idx * (unsigned)sizeof(TG), TG(0));
+    x2[e] = lds_t(o.xb + voff2 + idx * (unsigned)sizeof(TG), TG(0));
+    v[e] = lds_t(o.vrow + (unsigned)(sl * 32 * sizeof(TG)), TG(0));
+  }
+  s = 0;
+  s2 = 0;
+#pragma unroll
+  for (int e = 0; e < w; ++e) {
+    s = fma(v[e], x[e], s);
+    s2 = fma(v[e], x2[e], s2);
+  }
+}
+
 // Compile-time network dimensions (NT tanks, NU flows; the instantiated shape
 // is the Barcelona-dimension 63 / 114 network, other shapes run the graph
 // path): every offset and loop bound is a constant, so no dimension or index
@@ -203,6 +225,8 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
   TG* zb = wb + 64;                           // 128
   TG* ub = zb + 128;                          // 128
   TG* tb = ub + 128;                          // 32
+  TG* zb2 = tb + 32;                          // 128
+  TG* tb2 = zb2 + 128;                        // 32
   const int l2 = 2 * lane;
   const bool ok1 = 64 + l2 < NU, okx2 = l2 + 1 < NT;  // ok0 (l2 < NU) and okx (l2 < NT) hold for every lane
   const int o1 = ok1 ? 64 + l2 : l2;                   // second u pair (a valid in-row offset when absent)
@@ -248,7 +272,8 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     ops.vrow = smem_u32(vt + lane);
     ops.xb = smem_u32(wb);
   }
-  constexpr unsigned WB_OFF = 0, ZB_OFF = 64 * sizeof(TG), UB_OFF = 192 * sizeof(TG), TB_OFF = 320 * sizeof(TG);
+  constexpr unsigned WB_OFF = 0, ZB_OFF = 64 * sizeof(TG), UB_OFF = 192 * sizeof(TG), TB_OFF = 320 * sizeof(TG),
+                     ZB2_OFF = 352 * sizeof(TG), TB2_OFF = 480 * sizeof(TG);
   auto G_bc = [&](int q) { return dp_gather<TG>(ops, 2 * q, 2, WB_OFF); };   // (B^T wb)_k
   auto G_ec = [&](int q) { return dp_gather<TG>(ops, 8 + q, 1, TB_OFF); };   // (E^T tb)_k
   auto G_kr = [&]() { return dp_gather<TG>(ops, 12, 4, ZB_OFF); };           // (K zb)_lane
@@ -404,7 +429,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
   // (the x recursion of the row above) and wn = -P lsn (the down pass of the
   // row above: u = ut + wn, proj_neg's rounding).
   auto prox = [&](const double* st, unsigned r, const TG (&u)[4], const TG (&x)[2], TG (&yx)[2], TG (&yu)[4],
-                  TG (&bu)[2], const TG (&lsn)[4], TG (&wn)[4]) {
+                  TG (&bu)[2], const TG (&lsn)[4], TG (&wn)[4], const TG (&sv)[4], TG (&ps)[4]) {
     double* yn = Q.ynb + (size_t)r * W;
     double v1[2], v2[2], V1[2], V2[2], c1[2], c2[2], y1[2], y2[2];
     {
@@ -484,6 +509,8 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     for (int q = 0; q < 4; ++q) zn[q] = -lsn[q];
     st2(zb + l2, zn[0], zn[1]);
     st2(zb + 64 + l2, zn[2], zn[3]);
+    st2(zb2 + l2, sv[0], sv[1]);
+    st2(zb2 + 64 + l2, sv[2], sv[3]);
     __syncwarp();
     // the two tank-slot norms, numpy pairwise order (8-lane groups; lanes 16-31
     // repeat lanes 0-15 so the block has no branch and B u interleaves with it)
@@ -494,7 +521,12 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     for (int q = 1; q < NB / 8; ++q) r8 = dadd(r8, s2[g + 8 * q]);
 #pragma unroll
     for (int h = 0; h < 2; ++h) bu[h] = G_br(h);
-    tb[lane] = G_kr();  // zero past ns
+    {
+      TG k1, k2;
+      dp_gather2<TG>(ops, 12, 4, ZB_OFF, ZB2_OFF, k1, k2);  // (K zb, K zb2)_lane, zero past ns
+      tb[lane] = k1;
+      tb2[lane] = k2;
+    }
     __syncwarp();
     double ssum = dadd(r8, __shfl_down_sync(0xffffffffu, r8, 1, 8));
     ssum = dadd(ssum, __shfl_down_sync(0xffffffffu, ssum, 2, 8));
@@ -505,7 +537,12 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     const double thr = dmul(ig, slot ? w_s : w_x);  // prox parameter RN(1/gamma) (solver.py:571)
     const double stv = dist > 0.0 ? np_min(1.0, div_exact(thr, dist)) : 0.0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) wn[q] = zn[q] - G_ec(q);
+    for (int q = 0; q < 4; ++q) {
+      TG e1, e2;
+      dp_gather2<TG>(ops, 8 + q, 1, TB_OFF, TB2_OFF, e1, e2);
+      wn[q] = zn[q] - e1;
+      ps[q] = sv[q] - e2;  // P sv
+    }
     const double st1 = __shfl_sync(0xffffffffu, stv, 0), st2v = __shfl_sync(0xffffffffu, stv, 8);
     double p1[2], p2[2];
 #pragma unroll
@@ -569,8 +606,8 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         bmul(sw, bw);
         xa[0] = ((TG)d.p[l2] + bw[0]) + q0.x;
         xa[1] = okx2 ? ((TG)d.p[l2 + 1] + bw[1]) + q0.y : TG(0);
-        TG yx[2], yu[4], bx[2], wx[4];
-        prox(take(), r, ua, xa, yx, yu, bx, ls, wx);
+        TG yx[2], yu[4], bx[2], wx[4], px[4];
+        prox(take(), r, ua, xa, yx, yu, bx, ls, wx, ls, px);
         release();
         if (next) {
           TG* yc = Q.Yc + (size_t)r * LY;
@@ -628,7 +665,8 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         u[q] = b[q] + wn[q];
         ls[q] = ls[q] - L[q];  // ls of the row above
       }
-      prox(st, r, u, xs, yx, yu, bu, ls, wn);
+      TG pS[4];  // P (sum of a below), for the up pass
+      prox(st, r, u, xs, yx, yu, bu, ls, wn, acc, pS);
       release();
       if (t > 0) {  // x of the row above
         xs[0] = (xs[0] - g[0]) - bu[0];
@@ -640,25 +678,12 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       wbr[1] = bottom ? yx[1] : yx[1] + wbr[1];
       st2(wb + l2, wbr[0], wbr[1]);
       __syncwarp();
-      TG a[4], Sv[4];
+      TG a[4], l[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         a[q] = yu[q] + G_bc(q);
-        Sv[q] = acc[q];
         acc[q] = bottom ? a[q] : a[q] + acc[q];
-      }
-      TG l[4];
-      if (!bottom) {
-        st2(zb + l2, Sv[0], Sv[1]);
-        st2(zb + 64 + l2, Sv[2], Sv[3]);
-        __syncwarp();
-        tb[lane] = G_kr();
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 4; ++q) l[q] = a[q] + (Sv[q] - G_ec(q));
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) l[q] = a[q];
+        l[q] = bottom ? a[q] : a[q] + pS[q];
       }
       const TG wt = (TG)(N - t);
       TG Ln[4];
