@@ -69,7 +69,29 @@ struct DpArgs {
   int pro_w;         // doubles of a warp's chain-prologue scratch: kstar * nu + (3 nu + lx)
 };
 
-__host__ __device__ inline int dp_stage(int nt, int nu, int lx) { return 2 * (2 * nt + nu) + nu + lx; }
+// Ring stage layout (doubles): every region starts on a 128-byte boundary so
+// a warp's 512-byte cp.async rows and its 16-byte-per-lane reads take the
+// minimum number of shared-memory wavefronts.
+struct DpStage {
+  int oYm, oUa, oXa, oL, oB, oG, oAx, stg;
+};
+__host__ __device__ constexpr int dp_p16(int x) { return (x + 15) & ~15; }
+template <typename TG>
+__host__ __device__ constexpr DpStage dp_stage_layout(int nt, int nu, int lx) {
+  DpStage s{};
+  const int w = 2 * nt + nu;
+  s.oYm = dp_p16(w);
+  s.oUa = s.oYm + dp_p16(w);
+  s.oXa = s.oUa + dp_p16(nu);
+  s.oL = s.oXa + dp_p16(lx);
+  s.oB = s.oL + dp_p16(nu);
+  s.oG = s.oB + dp_p16(nu);
+  s.oAx = s.oG + dp_p16(lx);
+  s.stg = sizeof(TG) == 8 ? dp_p16(s.oAx + 2) : s.oL;
+  return s;
+}
+constexpr int DP_SD2 = 72;  // second tank-slot norm buffer (bank offset 16 from the first)
+constexpr int DP_SD2W = 144;
 __host__ __device__ inline int dp_agg_w(int nu, int lx) { return 3 * nu + lx; }
 // Per-CTA pointer block of k_chain_dp in shared memory: under register
 // pressure the compiler re-reads these from shared memory (short latency)
@@ -86,13 +108,10 @@ struct alignas(16) DpPtrs {
 };
 
 template <typename TG>
-__host__ __device__ inline int dp_stage_t(int nt, int nu, int lx) {  // k_chain_dp's ring stage (doubles)
-  return dp_stage(nt, nu, lx) + (sizeof(TG) == 8 ? 2 * nu + lx + 2 : 0);
-}
-template <typename TG>
 __host__ __device__ inline size_t dp_smem(int wpc, int nt, int nu, int lx, int kstar) {
-  return sizeof(double) * (DP_BND + 8 + DP_VSLOTS * 32) + sizeof(DpPtrs<TG>) +
-         (size_t)wpc * (sizeof(double) * (DP_D * (size_t)dp_stage_t<TG>(nt, nu, lx) + 128) + sizeof(TG) * DP_XCH) +
+  return 128 + sizeof(double) * (DP_BND + 8 + DP_VSLOTS * 32) + sizeof(DpPtrs<TG>) +
+         (size_t)wpc * (sizeof(double) * (DP_D * (size_t)dp_stage_layout<TG>(nt, nu, lx).stg + DP_SD2W) +
+                        sizeof(TG) * DP_XCH) +
          sizeof(double) * (size_t)wpc * ((size_t)kstar * nu + 3 * nu + lx);
 }
 
@@ -202,8 +221,10 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
   // operands [L NU | ut NU | g LX | aux 2] (fp32 rows are not 16-byte multiples:
   // those come through registers one row ahead)
   constexpr bool SDG = sizeof(TG) == 8;
-  constexpr int oYm = W, oUa = 2 * W, oXa = 2 * W + NU, oL = 2 * W + NU + LX, oB = oL + NU, oG = oB + NU,
-                oAx = oG + LX, STG = SDG ? oAx + 2 : oL;
+  constexpr DpStage SL = dp_stage_layout<TG>(NT, NU, LX);
+  constexpr int oYm = SL.oYm, oUa = SL.oUa, oXa = SL.oXa, oL = SL.oL, oB = SL.oB, oG = SL.oG, oAx = SL.oAx,
+                STG = SL.stg;
+  static_assert(!SDG || (oYm % 16 == 0 && STG % 16 == 0), "128-byte regions");
   constexpr int AW = 3 * NU + LX, PW = NU + LX;
   constexpr int WE = 4;
   constexpr int NB = NT - NT % 8;  // pairwise-sum block part of a tank norm
@@ -216,12 +237,12 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
   double* pv = bnd + DP_BND;                                 // 8: gamma, 1/gamma, beta, theta, 1-theta, beta1, w_x, w_s
   DpPtrs<TG>* PT = reinterpret_cast<DpPtrs<TG>*>(pv + 8);
   unsigned char* vtab = reinterpret_cast<unsigned char*>(PT + 1);  // DP_VSLOTS x 32 doubles
-  unsigned char* wbase = vtab + 8 * DP_VSLOTS * 32;
-  const size_t wbytes = sizeof(double) * (DP_D * STG + 128) + sizeof(TG) * DP_XCH;
+  unsigned char* wbase = smem_raw + ((vtab + 8 * DP_VSLOTS * 32 - smem_raw + 127) & ~(size_t)127);
+  const size_t wbytes = sizeof(double) * (DP_D * STG + DP_SD2W) + sizeof(TG) * DP_XCH;
   double* ring = reinterpret_cast<double*>(wbase + warp * wbytes);
-  double* sd2 = ring + DP_D * STG;  // 128
+  double* sd2 = ring + DP_D * STG;  // DP_SD2W: tank-slot squares at 0 and DP_SD2
   double* pro = reinterpret_cast<double*>(wbase + (size_t)wpc * wbytes) + (size_t)warp * A.pro_w;  // chain prologue
-  TG* wb = reinterpret_cast<TG*>(sd2 + 128);  // 64
+  TG* wb = reinterpret_cast<TG*>(sd2 + DP_SD2W);  // 64
   TG* zb = wb + 64;                           // 128
   TG* ub = zb + 128;                          // 128
   TG* tb = ub + 128;                          // 32
@@ -466,7 +487,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       for (int h = 0; h < 2; ++h) {
         const double df1 = dsub(V1[h], c1[h]), df2 = dsub(V2[h], c2[h]);
         sd2[l2 + h] = dmul(df1, df1);  // slot 63 (past NT) is never read
-        sd2[64 + l2 + h] = dmul(df2, df2);
+        sd2[DP_SD2 + l2 + h] = dmul(df2, df2);
       }
     }
     {  // the u part (plain box) while the norms' operands settle
@@ -515,7 +536,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     // the two tank-slot norms, numpy pairwise order (8-lane groups; lanes 16-31
     // repeat lanes 0-15 so the block has no branch and B u interleaves with it)
     const int slot = (lane >> 3) & 1, g = lane & 7;
-    const double* s2 = sd2 + 64 * slot;
+    const double* s2 = sd2 + DP_SD2 * slot;
     double r8 = s2[g];
 #pragma unroll
     for (int q = 1; q < NB / 8; ++q) r8 = dadd(r8, s2[g + 8 * q]);
