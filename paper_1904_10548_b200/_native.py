@@ -135,7 +135,8 @@ class NativeError(RuntimeError):
 
 
 PATH_FIELDS = ("fast_path", "fused_dp", "chainw", "ring_depth", "branch_groups", "nchain", "kstar",
-               "ell_vf", "fp32", "dp_wpc", "dp_grid", "dp_cpw", "kernels_per_iteration", "n_branch", "sms")
+               "ell_vf", "fp32", "dp_wpc", "dp_grid", "dp_cpw", "kernels_per_iteration", "n_branch", "sms",
+               "dp_sib")
 
 
 def path_info(ctx: "Context") -> dict:

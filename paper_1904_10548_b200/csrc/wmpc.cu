@@ -125,6 +125,7 @@ struct wmpc_ctx {
   int ell_vf = 0;                               // B, E ELL values exact in fp32 (WMPC_ELL_VF=0 disables)
   // fused one-kernel iteration for many chains (wmpc_dp.cuh)
   int use_dp = 0, dp_wpc = 0, dp_grid = 0, dp_cpw = 1;
+  int dp_sib = 0;  // k_chain_dp runs the up pass of the stage-(kstar-1) rows (gk_groups[0] skipped)
   size_t dp_sm = 0;
   double* dp_agg = nullptr;  // nchain x (3 nu + lx): [LSc | LWc | SUTp | SGp]
   float* dp_agg32 = nullptr;
@@ -467,9 +468,12 @@ void gk_up(wmpc_ctx* ctx, const FastView& f) {
   else
     launch_pdl(ctx, k_chain_up<WE, TG, false>, dim3(ctx->nchain), dim3(ctx->up_threads), ctx->sm_up, f);
 }
+// stage groups [g0, g1) of gk_groups (g1 < 0: to the end)
 template <int WE, typename TG = double>
-void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump, int first_flags = 0) {
-  for (const auto& g : ctx->gk_groups) {
+void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump, int first_flags = 0, int g0 = 0, int g1 = -1) {
+  const int ng = (int)ctx->gk_groups.size();
+  for (int gi = g0; gi < (g1 < 0 ? ng : std::min(g1, ng)); ++gi) {
+    const auto& g = ctx->gk_groups[gi];
     launch_pdl(ctx, k_branch_grp<WE, TG>, dim3(g.second), dim3(GRP_THREADS), ctx->sm_grp, f, g.first, bump,
                (int)GRP_FULL | first_flags);
     bump = 0;
@@ -483,7 +487,8 @@ bool dp_on(const wmpc_ctx* ctx) {
 template <typename TG>
 void launch_dp(wmpc_ctx* ctx, const FastView& f) {
   if constexpr (sizeof(TG) == 8) {  // fp64 only (dp_on)
-    DpArgs a{(void*)ctx->dp_agg, (const void*)ctx->dp_putg, ctx->dp_cpw, ctx->kstar * ctx->nu + dp_agg_w(ctx->nu, ctx->lx)};
+    DpArgs a{(void*)ctx->dp_agg, (const void*)ctx->dp_putg, ctx->dp_cpw,
+             ctx->kstar * ctx->nu + dp_agg_w(ctx->nu, ctx->lx), ctx->dp_sib};
     const dim3 grid(ctx->dp_grid), block(ctx->dp_wpc * 32);
     launch_pdl(ctx, k_chain_dp<DP_NT, DP_NU, double>, grid, block, ctx->dp_sm, f, a);
   }
@@ -609,6 +614,7 @@ void dp_attr(wmpc_ctx* ctx, size_t sm) {
 }
 void configure_dp(wmpc_ctx* ctx) {
   ctx->use_dp = 0;
+  ctx->dp_sib = 0;
   const int nt = ctx->nt, nu = ctx->nu, lx = ctx->lx, nchain = ctx->nchain, kstar = ctx->kstar;
   const bool fits = ctx->ell_w == 4 && nt == DP_NT && nu == DP_NU && ctx->ns <= 32 && kstar <= 30;
   // many chains per SM (C4: 4,096 chains, 27.7 per SM: 236 vs 256 us per iteration); at C3 (512 chains,
@@ -640,14 +646,23 @@ void configure_dp(wmpc_ctx* ctx) {
         if (hi[a] < 0) continue;
         int best = lo[a];
         for (int i = lo[a]; i < hi[a]; ++i) {
-          const int ci = cntw[i % nwt], cb = cntw[best % nwt];
+          const int ci = cntw[i / cpw], cb = cntw[best / cpw];
           if (ci < cb || (ci == cb && cntc[i] < cntc[best])) best = i;
         }
-        cntw[best % nwt]++;
+        cntw[best / cpw]++;
         cntc[best]++;
         cown[best] |= 1u << st;
       }
     upload_vec(ctx, &ctx->cown, cown);
+    // the stage-(kstar-1) rows' up pass moves into k_chain_dp when each such
+    // row's chains are all on one warp (contiguous chains per warp) and that
+    // stage is exactly the first branch group (identical item lists)
+    bool sib = ctx->gk_groups.size() >= 2 && ctx->gk_groups[0].first == ctx->off[kstar - 1] &&
+               ctx->gk_groups[0].second == ctx->off[kstar] - ctx->off[kstar - 1];
+    for (int a = ctx->off[kstar - 1]; sib && a < ctx->off[kstar]; ++a)
+      sib = hi[a] > 0 && lo[a] / cpw == (hi[a] - 1) / cpw;
+    ctx->dp_sib = sib ? 1 : 0;
+    if (const char* e = getenv("WMPC_DP_SIB")) ctx->dp_sib &= e[0] != '0';
   }
   const size_t aw = (size_t)nchain * dp_agg_w(nu, lx);
   if (ctx->dp_agg) cudaFree(ctx->dp_agg);
@@ -1059,7 +1074,7 @@ FastView make_fastview(wmpc_ctx* ctx, int count);
 int graphk_kernels(const wmpc_ctx* ctx) {
   const int g = (int)ctx->gk_groups.size();
   if (ctx->shard_k > 0) return 3 + g + 2 * (ctx->rep_group.second > 0) + (g == 0 && ctx->rep_group.second == 0);
-  if (dp_on(ctx)) return g + 1 + (g == 0 ? 1 : 0);
+  if (dp_on(ctx)) return g - ctx->dp_sib + 1 + (g == 0 ? 1 : 0);
   return 3 + g + (g == 0 ? 1 : 0);
 }
 
@@ -1073,7 +1088,7 @@ void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
       gk_grp<4, float>(ctx, f, 1, GRP_LATE);
       launch_dp<float>(ctx, f);
     } else {
-      gk_grp<4, double>(ctx, f, 1, GRP_LATE);
+      gk_grp<4, double>(ctx, f, 1, GRP_LATE, ctx->dp_sib);
       launch_dp<double>(ctx, f);
     }
     return;
@@ -1718,7 +1733,8 @@ int wmpc_path_info(const wmpc_ctx* ctx, int* out, int cap) {
                    ctx->dp_cpw,
                    wmpc_kernel_launches_per_iteration(ctx),
                    ctx->n_branch,
-                   ctx->sms};
+                   ctx->sms,
+                   g && dp_on(ctx) ? ctx->dp_sib : 0};
   const int nv = (int)(sizeof(v) / sizeof(v[0]));
   for (int i = 0; i < cap && i < nv; ++i) out[i] = v[i];
   return nv;
@@ -2086,7 +2102,7 @@ int wmpc_iteration_profile(wmpc_ctx* ctx, int count, double* out, int cap) {
         if (ctx->gk_groups.empty()) k_advance<<<1, 32, 0, ctx->stream>>>(ctx->iter);
         CK(cudaEventRecord(ev[0], ctx->stream));
         if (dp) {
-          if (ctx->fp32) gk_grp<4, float>(ctx, f, 1, GRP_LATE); else gk_grp<4, double>(ctx, f, 1, GRP_LATE);
+          if (ctx->fp32) gk_grp<4, float>(ctx, f, 1, GRP_LATE); else gk_grp<4, double>(ctx, f, 1, GRP_LATE, ctx->dp_sib);
           CK(cudaEventRecord(ev[1], ctx->stream));
           if (ctx->fp32) launch_dp<float>(ctx, f); else launch_dp<double>(ctx, f);
           CK(cudaEventRecord(ev[2], ctx->stream));
@@ -2500,9 +2516,10 @@ int wmpc_apg_warm(wmpc_ctx* ctx, const double* y0) {
         k_dp_agg_L<float><<<nbk, 256, 0, ctx->stream>>>(f, ctx->dp_agg32);
       } else {
         gk_up<4, double>(ctx, f);
+        if (ctx->dp_sib) gk_grp<4, double>(ctx, f, 0, 0, 0, 1);  // the stage k_chain_dp finishes itself
         k_dp_agg_L<double><<<nbk, 256, 0, ctx->stream>>>(f, ctx->dp_agg);
       }
-      ctx->launches += 2;
+      ctx->launches += 2 + ctx->dp_sib;
     }
     check_launch(ctx);
     sync(ctx);

@@ -67,6 +67,8 @@ struct DpArgs {
   const void* putg;  // n_branch x (nu + lx), TG: root-path prefix sums [PUT | PG] of each branching row
   int cpw;           // chains per warp
   int pro_w;         // doubles of a warp's chain-prologue scratch: kstar * nu + (3 nu + lx)
+  int sib;           // 1: a warp's chains hold every chain of their stage-(kstar-1) parents, whose
+                     // up pass (k_branch_grp's first stage group) the warp runs after its last child
 };
 
 // Ring stage layout (doubles): every region starts on a 128-byte boundary so
@@ -323,7 +325,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
   const DpPtrs<TG> Q = *PT;  // in registers (no spill at <= 8 warps per SM)
   const double gamma = pv[0], ig = pv[1], beta = pv[2], theta = pv[3], om = pv[4], beta1 = pv[5];
   const double w_x = pv[6], w_s = pv[7];
-  const int gw = blockIdx.x * wpc + warp, nw = gridDim.x * wpc;
+  const int gw = blockIdx.x * wpc + warp;
   // ---- prox-row ring: owned ancestors then chain rows (bottom-up) of each
   // chain slot; one cp.async group per row (empty past the end)
   int ic_cs = 0, ic_pos = -2;  // the first ++ lands on chain slot 0's prologue
@@ -340,7 +342,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         ic_pos = -1;
         ++ic_cs;
       }
-      const int ci = gw + ic_cs * nw;
+      const int ci = gw * A.cpw + ic_cs;
       if (ic_cs >= A.cpw || ci >= (int)nchain) {
         ic_pos = kb + N - 1;  // park past the end
         ic_cs = A.cpw;
@@ -586,8 +588,9 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     }
   };
 
+  int sib0 = gw * A.cpw;  // first chain of the current stage-(kstar-1) parent
   for (int cs = 0; cs < A.cpw; ++cs) {
-    const int ci = gw + cs * nw;
+    const int ci = gw * A.cpw + cs;
     if (ci >= (int)nchain) break;
     const unsigned r_top = nbr + (unsigned)ci;
     // the chain prologue (a ring group): its ancestors' L rows and its aggregates, in the scratch
@@ -729,6 +732,55 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       if (ok1) {
         st2(a + 64 + l2, LSn[2], LSn[3]);
         st2(a + NU + 64 + l2, LWn[2], LWn[3]);
+      }
+    }
+    if (A.sib && next) {  // after the parent's last chain: its up pass (k_branch_grp arithmetic, R-free,
+                          // no branching descendants: W2 = 0), from its own Yc and the chains' totals
+      const unsigned p = (unsigned)Q.cpath[(size_t)ci * kb + kb - 1];
+      const int cn = ci + 1;
+      const bool fin = cs + 1 >= A.cpw || cn >= (int)nchain || (unsigned)Q.cpath[(size_t)cn * kb + kb - 1] != p;
+      if (fin) {
+        // this warp wrote every operand below (same lanes, same addresses)
+        TG W1[2] = {0, 0}, Su[4] = {0, 0, 0, 0};
+        for (int c = sib0; c <= ci; ++c) {
+          const size_t rt = nbr + (size_t)c;
+          const auto w = ld2cg(Q.wbar + rt * LX + l2);
+          const auto s0 = ld2cg(Q.Asub + rt * NU + l2), s1 = ld2cg(Q.Asub + rt * NU + o1);
+          W1[0] += w.x;
+          W1[1] += okx2 ? w.y : TG(0);
+          Su[0] += s0.x; Su[1] += s0.y; Su[2] += ok1 ? s1.x : TG(0); Su[3] += ok1 ? s1.y : TG(0);
+        }
+        const TG* yc = Q.Yc + (size_t)p * LY;
+        const auto ox = ld2cg(yc + l2), ou0 = ld2cg(yc + LX + l2), ou1 = ld2cg(yc + LX + o1);
+        W1[0] = ox.x + W1[0];
+        W1[1] = okx2 ? ox.y + W1[1] : TG(0);
+        const TG yu[4] = {ou0.x, ou0.y, ok1 ? ou1.x : TG(0), ok1 ? ou1.y : TG(0)};
+        const TG axp = Q.aux[(size_t)p * 2];
+        __syncwarp();  // every lane is past the last row's reads of wb
+        st2(wb + l2, W1[0], W1[1]);
+        st2(zb + l2, Su[0], Su[1]);
+        st2(zb + 64 + l2, Su[2], Su[3]);
+        __syncwarp();
+        TG a[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a[q] = yu[q] + G_bc(q);
+        tb[lane] = G_kr();
+        __syncwarp();
+        TG Lp[4], Ap[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          Lp[q] = (a[q] + (Su[q] - G_ec(q))) * axp;
+          Ap[q] = a[q] + Su[q];
+        }
+        if (okx2) st2(Q.wbar + (size_t)p * LX + l2, W1[0], W1[1]);
+        else Q.wbar[(size_t)p * LX + l2] = W1[0];
+        st2(Q.Lb + (size_t)p * NU + l2, Lp[0], Lp[1]);
+        st2(Q.Asub + (size_t)p * NU + l2, Ap[0], Ap[1]);
+        if (ok1) {
+          st2(Q.Lb + (size_t)p * NU + 64 + l2, Lp[2], Lp[3]);
+          st2(Q.Asub + (size_t)p * NU + 64 + l2, Ap[2], Ap[3]);
+        }
+        sib0 = cn;
       }
     }
   }
