@@ -289,6 +289,19 @@ def profile_json(name: str):
         return None
 
 
+def ncu_digest(name: str):
+    """Headline numbers of the committed ncu summary of the dominant kernel
+    (tools/ncu_summary.py), or None."""
+    d = profile_json(name)
+    if not d:
+        return None
+    keep = ("duration", "dram_bytes", "dram_pct_of_peak", "ipc_per_sm", "issue_active_pct", "fp64_pipe_active_pct",
+            "warps_active_per_sm", "registers", "stalls_per_issued_instruction")
+    out = {k: (d[k]["value"] if isinstance(d[k], dict) and "value" in d[k] else d[k]) for k in keep if k in d}
+    out["source"] = f"profiles/r02/{name}.json ({d.get('how', '')})"
+    return out
+
+
 # fp32 mode's own compulsory bytes per node per iteration: y, y_prev read and
 # y+ written (fp64, 3 x 240), Ua / Xa read and written (fp64, 2 x 177), e_off
 # and g read (fp32, 177), prob (fp64)
@@ -598,7 +611,7 @@ def run_ours(args):
                 "config": cfgd, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clocks.summary(),
                 "loop_ms_per_solve": loop_total / K, "fp32_mode": fp32,
-                "fp64_pipe": profile_json("fp64_pipe"),
+                "ncu": ncu_digest(f"ncu_{dom.split(' ')[0]}_{args.config}"),
                 "setup": {"factor_step_s": t_factor, "estimate_lipschitz_s": t_lip, "lipschitz_device": L_dev},
                 "secondary_C2": None if args.no_secondary else secondary_c2(gamma)}
         print(json.dumps(line), flush=True)
