@@ -156,7 +156,8 @@ int wmpc_fast_path(const wmpc_ctx* ctx);
  * groups, [5] chains, [6] first chain stage, [7] B/E values as float, [8] fp32
  * mode, [9] k_chain_dp warps per CTA, [10] its grid, [11] chains per warp,
  * [12] kernels per iteration, [13] branching rows, [14] SMs, [15] k_chain_dp
- * runs the lowest branching stage's up pass itself. Returns the
+ * runs the lowest branching stage's up pass itself, [16] k_chain_dp's
+ * upper-segment rows per chain (0: one warp per whole chain). Returns the
  * number of fields (writes at most cap). No reference counterpart. */
 int wmpc_path_info(const wmpc_ctx* ctx, int* out, int cap);
 /* Programmatic dependent launch between the iteration kernels on (default) or

@@ -136,7 +136,7 @@ class NativeError(RuntimeError):
 
 PATH_FIELDS = ("fast_path", "fused_dp", "chainw", "ring_depth", "branch_groups", "nchain", "kstar",
                "ell_vf", "fp32", "dp_wpc", "dp_grid", "dp_cpw", "kernels_per_iteration", "n_branch", "sms",
-               "dp_sib")
+               "dp_sib", "dp_segm")
 
 
 def path_info(ctx: "Context") -> dict:

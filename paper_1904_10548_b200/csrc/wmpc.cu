@@ -128,9 +128,10 @@ struct wmpc_ctx {
   int dp_sib = 0;  // k_chain_dp runs the up pass of the stage-(kstar-1) rows (gk_groups[0] skipped)
   size_t dp_sm = 0;
   double* dp_agg = nullptr;  // nchain x (3 nu + lx): [LSc | LWc | SUTp | SGp]
-  float* dp_agg32 = nullptr;
   double* dp_putg = nullptr;  // n_branch x (nu + lx): root-path prefixes [PUT | PG]
-  float* dp_putg32 = nullptr;
+  int dp_segm = 0;            // > 0: segmented chains (upper rows [0, dp_segm) on their own warp)
+  double *dp_aggu = nullptr, *dp_corr = nullptr, *dp_segx = nullptr, *dp_auxs = nullptr;  // see DpArgs
+  int* dp_flag = nullptr;
   double *dp_Lc = nullptr, *dp_Ac = nullptr, *dp_wc = nullptr;  // certificate scratch (the iteration state stays)
   cudaGraphExec_t gk_exec1 = nullptr, gk_exec8 = nullptr;
   double gk_gamma = -1.0;
@@ -484,14 +485,12 @@ void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump, int first_flags = 0, int
 bool dp_on(const wmpc_ctx* ctx) {
   return ctx->use_dp && !ctx->fp32 && ctx->shard_k < 0 && ctx->rfree;
 }
-template <typename TG>
-void launch_dp(wmpc_ctx* ctx, const FastView& f) {
-  if constexpr (sizeof(TG) == 8) {  // fp64 only (dp_on)
-    DpArgs a{(void*)ctx->dp_agg, (const void*)ctx->dp_putg, ctx->dp_cpw,
-             ctx->kstar * ctx->nu + dp_agg_w(ctx->nu, ctx->lx), ctx->dp_sib};
-    const dim3 grid(ctx->dp_grid), block(ctx->dp_wpc * 32);
-    launch_pdl(ctx, k_chain_dp<DP_NT, DP_NU, double>, grid, block, ctx->dp_sm, f, a);
-  }
+void launch_dp(wmpc_ctx* ctx, const FastView& f) {  // fp64 only (dp_on)
+  DpArgs a{(void*)ctx->dp_agg, (const void*)ctx->dp_putg, ctx->dp_cpw,
+           dp_pro_w(ctx->kstar, ctx->nu, ctx->lx, ctx->dp_segm > 0), ctx->dp_segm, (void*)ctx->dp_aggu,
+           (void*)ctx->dp_corr, (void*)ctx->dp_segx, ctx->dp_flag, (const void*)ctx->dp_auxs, ctx->dp_sib};
+  const dim3 grid(ctx->dp_grid), block(ctx->dp_wpc * 32);
+  launch_pdl(ctx, k_chain_dp<DP_NT, DP_NU, double>, grid, block, ctx->dp_sm, f, a);
 }
 template <int WE>
 void gk_rep(wmpc_ctx* ctx, const FastView& f, int mode, int bump) {
@@ -615,19 +614,33 @@ void dp_attr(wmpc_ctx* ctx, size_t sm) {
 void configure_dp(wmpc_ctx* ctx) {
   ctx->use_dp = 0;
   ctx->dp_sib = 0;
+  ctx->dp_segm = 0;
   const int nt = ctx->nt, nu = ctx->nu, lx = ctx->lx, nchain = ctx->nchain, kstar = ctx->kstar;
   const bool fits = ctx->ell_w == 4 && nt == DP_NT && nu == DP_NU && ctx->ns <= 32 && kstar <= 30;
+  const int sms = std::max(ctx->sms, 1), N = ctx->H - kstar;
   // many chains per SM (C4: 4,096 chains, 27.7 per SM: 236 vs 256 us per iteration); at C3 (512 chains,
-  // 3.5 per SM) one warp per chain is latency-bound (116 vs 52 us): the graph path stays
-  bool want = fits && nchain >= 8 * ctx->sms;
+  // 3.5 per SM) one warp per whole chain is latency-bound (51 vs 52 us): segmented chains (two warps
+  // per chain) where every pair fits in one wave
+  // (measured, us per iteration: C3 graph 52.1, whole chains 50.0, segmented 42.5 with 10 of 19 rows
+  // up; C2, 128 chains: graph 19.4, segmented 28.0, whole 42.2)
+  const bool many = nchain >= 8 * sms;
+  const bool few = 2 * nchain <= sms * DP_WPS && N >= 6 && kstar > 0;
+  const bool seg_default = few && nchain >= 2 * sms;
+  bool want = fits && (many || seg_default);
   if (const char* e = getenv("WMPC_DP")) want = fits && e[0] == '1';
   if (!want) return;
-  const int sms = std::max(ctx->sms, 1);
-  const int cpw = (nchain + sms * DP_WPS - 1) / (sms * DP_WPS);
-  const int nw = (nchain + cpw - 1) / cpw;
+  int segm = few && !many && seg_default ? (N + 1) / 2 : 0;
+  if (few && !many) {
+    if (const char* e = getenv("WMPC_DP_SEG")) segm = e[0] == '1' ? (N + 1) / 2 : 0;
+    if (const char* e = getenv("WMPC_DP_SEGM")) segm = std::min(std::max(atoi(e), 1), N - 1);
+  }
+  const int lanes = segm > 0 ? 2 : 1;  // warps per chain slot
+  const int cpw = (lanes * nchain + sms * DP_WPS - 1) / (sms * DP_WPS);
+  const int nw = lanes * ((nchain + cpw - 1) / cpw);
   const int wpc = std::min(DP_MAXT / 32, std::max(1, (nw + sms - 1) / sms));
   const int grid = (nw + wpc - 1) / wpc;
-  const size_t sm = dp_smem<double>(wpc, nt, nu, lx, kstar);
+  if (segm > 0 && grid > sms) return;  // the upper warps wait for the lower ones: one resident wave
+  const size_t sm = dp_smem<double>(wpc, nt, nu, lx, kstar, segm > 0);
   if (sm > 227 * 1024) return;
   dp_attr(ctx, sm);
   // ownership of the branching rows balanced over the persistent warps
@@ -657,7 +670,7 @@ void configure_dp(wmpc_ctx* ctx) {
     // the stage-(kstar-1) rows' up pass moves into k_chain_dp when each such
     // row's chains are all on one warp (contiguous chains per warp) and that
     // stage is exactly the first branch group (identical item lists)
-    bool sib = ctx->gk_groups.size() >= 2 && ctx->gk_groups[0].first == ctx->off[kstar - 1] &&
+    bool sib = segm == 0 && ctx->gk_groups.size() >= 2 && ctx->gk_groups[0].first == ctx->off[kstar - 1] &&
                ctx->gk_groups[0].second == ctx->off[kstar] - ctx->off[kstar - 1];
     for (int a = ctx->off[kstar - 1]; sib && a < ctx->off[kstar]; ++a)
       sib = hi[a] > 0 && lo[a] / cpw == (hi[a] - 1) / cpw;
@@ -665,18 +678,23 @@ void configure_dp(wmpc_ctx* ctx) {
     if (const char* e = getenv("WMPC_DP_SIB")) ctx->dp_sib &= e[0] != '0';
   }
   const size_t aw = (size_t)nchain * dp_agg_w(nu, lx);
-  if (ctx->dp_agg) cudaFree(ctx->dp_agg);
-  if (ctx->dp_agg32) cudaFree(ctx->dp_agg32);
-  ctx->dp_agg = nullptr;
-  ctx->dp_agg32 = nullptr;
+  for (double** p : {&ctx->dp_agg, &ctx->dp_putg, &ctx->dp_aggu, &ctx->dp_corr, &ctx->dp_segx, &ctx->dp_auxs}) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+  }
+  if (ctx->dp_flag) cudaFree(ctx->dp_flag);
+  ctx->dp_flag = nullptr;
   dalloc(ctx, &ctx->dp_agg, aw);
-  dalloc(ctx, &ctx->dp_agg32, aw);
-  if (ctx->dp_putg) cudaFree(ctx->dp_putg);
-  if (ctx->dp_putg32) cudaFree(ctx->dp_putg32);
-  ctx->dp_putg = nullptr;
-  ctx->dp_putg32 = nullptr;
   dalloc(ctx, &ctx->dp_putg, (size_t)std::max(nb, 1) * (nu + lx));
-  dalloc(ctx, &ctx->dp_putg32, (size_t)std::max(nb, 1) * (nu + lx));
+  if (segm > 0) {
+    dalloc(ctx, &ctx->dp_aggu, aw);
+    dalloc(ctx, &ctx->dp_corr, (size_t)nchain * 2 * nu);
+    dalloc(ctx, &ctx->dp_segx, (size_t)nchain * (lx + nu));
+    dalloc(ctx, &ctx->dp_auxs, (size_t)nchain * 4);
+    CK(cudaMalloc(&ctx->dp_flag, sizeof(int) * nchain));
+    CK(cudaMemset(ctx->dp_flag, 0, sizeof(int) * nchain));
+  }
+  ctx->dp_segm = segm;
   if (!ctx->dp_Lc) {
     dalloc(ctx, &ctx->dp_Lc, (size_t)ctx->n * nu);
     dalloc(ctx, &ctx->dp_wc, (size_t)ctx->n * lx);
@@ -1084,13 +1102,8 @@ void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
   const int nc = ctx->nchain;
   if (ctx->gk_groups.empty()) k_advance<<<1, 32, 0, st>>>(ctx->iter);  // else the first group kernel counts
   if (dp_on(ctx)) {  // branch groups (the first reads Yc the previous k_chain_dp wrote) + k_chain_dp
-    if (ctx->fp32) {
-      gk_grp<4, float>(ctx, f, 1, GRP_LATE);
-      launch_dp<float>(ctx, f);
-    } else {
-      gk_grp<4, double>(ctx, f, 1, GRP_LATE, ctx->dp_sib);
-      launch_dp<double>(ctx, f);
-    }
+    gk_grp<4, double>(ctx, f, 1, GRP_LATE, ctx->dp_sib);
+    launch_dp(ctx, f);
     return;
   }
   if (ctx->fp32) {
@@ -1324,7 +1337,7 @@ void free_all(wmpc_ctx* c) {
                   c->Lb, c->Asub, c->blob, c->store_it, c->ut, c->ut32, c->f32_Yc, c->f32_Lb, c->f32_Asub, c->f32_wbar, c->f32_U,
                   c->f32_X, c->f32_eoff, c->f32_R, c->f32_g, c->f32_aux, c->f32_ell, c->Yc_save, c->acct, c->rep_gidx, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
                   c->pj_ecv, c->dk_mv, c->dk_sweeps, c->dk_fix, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
-                  c->prof, c->rb_u0, c->rb_p, c->rb_a, c->gd_stage, c->dp_agg, c->dp_agg32, c->dp_putg, c->dp_putg32, c->dp_Lc,
+                  c->prof, c->rb_u0, c->rb_p, c->rb_a, c->gd_stage, c->dp_agg, c->dp_putg, c->dp_aggu, c->dp_corr, c->dp_segx, c->dp_auxs, c->dp_flag, c->dp_Lc,
                   c->dp_Ac, c->dp_wc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1734,7 +1747,8 @@ int wmpc_path_info(const wmpc_ctx* ctx, int* out, int cap) {
                    wmpc_kernel_launches_per_iteration(ctx),
                    ctx->n_branch,
                    ctx->sms,
-                   g && dp_on(ctx) ? ctx->dp_sib : 0};
+                   g && dp_on(ctx) ? ctx->dp_sib : 0,
+                   g && dp_on(ctx) ? ctx->dp_segm : 0};
   const int nv = (int)(sizeof(v) / sizeof(v[0]));
   for (int i = 0; i < cap && i < nv; ++i) out[i] = v[i];
   return nv;
@@ -1983,14 +1997,12 @@ int wmpc_apg_begin(wmpc_ctx* ctx, double gamma, int max_iter, const double* thet
           FastView f1 = make_fastview(ctx, 1);
           const int nbk = ((ctx->nchain + ctx->n_branch) * 32 + 255) / 256;
           ctx->launches++;
-          if (ctx->fp32) {
-            CK(cudaMemsetAsync(ctx->f32_Lb, 0, sizeof(float) * n * ctx->nu, ctx->stream));
-            CK(cudaMemsetAsync(ctx->f32_Asub, 0, sizeof(float) * na, ctx->stream));
-            CK(cudaMemsetAsync(ctx->f32_wbar, 0, sizeof(float) * n * ctx->lx, ctx->stream));
-            k_dp_agg_init<float><<<nbk, 256, 0, ctx->stream>>>(f1, ctx->dp_agg32, ctx->dp_putg32);
-          } else {
-            k_dp_agg_init<double><<<nbk, 256, 0, ctx->stream>>>(f1, ctx->dp_agg, ctx->dp_putg);
+          if (ctx->dp_segm > 0) {  // segmented chains: corrections 0, handshake flags reset
+            CK(cudaMemsetAsync(ctx->dp_corr, 0, sizeof(double) * ctx->nchain * 2 * ctx->nu, ctx->stream));
+            CK(cudaMemsetAsync(ctx->dp_flag, 0, sizeof(int) * ctx->nchain, ctx->stream));
           }
+          k_dp_agg_init<<<nbk, 256, 0, ctx->stream>>>(f1, ctx->dp_agg, ctx->dp_putg, ctx->dp_aggu, ctx->dp_auxs,
+                                                      ctx->dp_segm);
           check_launch(ctx);
         }
         capture_graphk(ctx);
@@ -2102,9 +2114,9 @@ int wmpc_iteration_profile(wmpc_ctx* ctx, int count, double* out, int cap) {
         if (ctx->gk_groups.empty()) k_advance<<<1, 32, 0, ctx->stream>>>(ctx->iter);
         CK(cudaEventRecord(ev[0], ctx->stream));
         if (dp) {
-          if (ctx->fp32) gk_grp<4, float>(ctx, f, 1, GRP_LATE); else gk_grp<4, double>(ctx, f, 1, GRP_LATE, ctx->dp_sib);
+          gk_grp<4, double>(ctx, f, 1, GRP_LATE, ctx->dp_sib);
           CK(cudaEventRecord(ev[1], ctx->stream));
-          if (ctx->fp32) launch_dp<float>(ctx, f); else launch_dp<double>(ctx, f);
+          launch_dp(ctx, f);
           CK(cudaEventRecord(ev[2], ctx->stream));
         } else {
           const int bump = ctx->gk_groups.empty() ? 0 : 1;
@@ -2511,14 +2523,9 @@ int wmpc_apg_warm(wmpc_ctx* ctx, const double* y0) {
     if (ctx->fast && ctx->use_graphk && dp_on(ctx)) {  // L, aggregates and chain totals of iteration 0
       FastView f = make_fastview(ctx, 1);  // the up pass of Yc(0) (R-free), then the L aggregates
       const int nbk = (ctx->nchain * 32 + 255) / 256;
-      if (ctx->fp32) {
-        gk_up<4, float>(ctx, f);
-        k_dp_agg_L<float><<<nbk, 256, 0, ctx->stream>>>(f, ctx->dp_agg32);
-      } else {
-        gk_up<4, double>(ctx, f);
-        if (ctx->dp_sib) gk_grp<4, double>(ctx, f, 0, 0, 0, 1);  // the stage k_chain_dp finishes itself
-        k_dp_agg_L<double><<<nbk, 256, 0, ctx->stream>>>(f, ctx->dp_agg);
-      }
+      gk_up<4, double>(ctx, f);
+      if (ctx->dp_sib) gk_grp<4, double>(ctx, f, 0, 0, 0, 1);  // the stage k_chain_dp finishes itself
+      k_dp_agg_L<<<nbk, 256, 0, ctx->stream>>>(f, ctx->dp_agg, ctx->dp_aggu, ctx->dp_segm);
       ctx->launches += 2 + ctx->dp_sib;
     }
     check_launch(ctx);

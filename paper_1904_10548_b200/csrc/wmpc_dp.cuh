@@ -66,7 +66,21 @@ struct DpArgs {
   void* agg;         // nchain x (3 nu + lx), TG: [LSc | LWc | SUTp | SGp]
   const void* putg;  // n_branch x (nu + lx), TG: root-path prefix sums [PUT | PG] of each branching row
   int cpw;           // chains per warp
-  int pro_w;         // doubles of a warp's chain-prologue scratch: kstar * nu + (3 nu + lx)
+  int pro_w;         // doubles of a warp's chain-prologue scratch: kstar * nu + (3 nu + lx) [+ 2 nu]
+  // Segmented chains (few chains per SM): seg_m > 0 splits every chain into an
+  // upper segment (rows [0, seg_m), warp 2p) and a lower one ([seg_m, N),
+  // warp 2p + 1) walked at the same time. The lower segment's L rows are
+  // final; the upper segment stores its rows' L without the lower segment's
+  // contribution (base) and, once the lower warp has published its totals,
+  // the per-chain correction L_t = base_t + aux_t (c0 + n_t c1), n_t = seg_m - 1 - t
+  // (applied where the rows are read next iteration), its corrected
+  // aggregates and the chain-top totals.
+  int seg_m;
+  void* aggu;   // nchain x (3 nu + lx): [LS_U | LW_U | SUT_U | SG_U] (upper segment; LW weights seg_m - t)
+  void* corr;   // nchain x 2 nu: [c0 | c1]
+  void* segx;   // nchain x (lx + nu): the lower segment's [sum yx | sum a]
+  int* flag;    // nchain: iteration + 1 once segx holds that iteration's totals
+  const void* auxs;  // nchain x 4: sums over upper rows of aux, n aux, (m - t) aux, (m - t) n aux
   int sib;           // 1: a warp's chains hold every chain of their stage-(kstar-1) parents, whose
                      // up pass (k_branch_grp's first stage group) the warp runs after its last child
 };
@@ -109,14 +123,25 @@ struct alignas(16) DpPtrs {
   int store, pad;
 };
 
+__host__ __device__ inline int dp_pro_w(int kstar, int nu, int lx, bool seg) {
+  return kstar * nu + 3 * nu + lx + (seg ? 2 * nu : 0);
+}
 template <typename TG>
-__host__ __device__ inline size_t dp_smem(int wpc, int nt, int nu, int lx, int kstar) {
+__host__ __device__ inline size_t dp_smem(int wpc, int nt, int nu, int lx, int kstar, bool seg = false) {
   return 128 + sizeof(double) * (DP_BND + 8 + DP_VSLOTS * 32) + sizeof(DpPtrs<TG>) +
          (size_t)wpc * (sizeof(double) * (DP_D * (size_t)dp_stage_layout<TG>(nt, nu, lx).stg + DP_SD2W) +
                         sizeof(TG) * DP_XCH) +
-         sizeof(double) * (size_t)wpc * ((size_t)kstar * nu + 3 * nu + lx);
+         sizeof(double) * (size_t)wpc * (size_t)dp_pro_w(kstar, nu, lx, seg);
 }
 
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 template <typename TG>
 __device__ __forceinline__ typename V2T<TG>::T ld2s(const TG* p) {  // aligned pair (shared or global)
   return *reinterpret_cast<const typename V2T<TG>::T*>(p);
@@ -326,6 +351,10 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
   const double gamma = pv[0], ig = pv[1], beta = pv[2], theta = pv[3], om = pv[4], beta1 = pv[5];
   const double w_x = pv[6], w_s = pv[7];
   const int gw = blockIdx.x * wpc + warp;
+  // whole chains (seg -1), or the upper (0) / lower (1) segment of a warp pair's chains
+  const bool segd = A.seg_m > 0;
+  const int seg = segd ? (gw & 1) : -1, gp = segd ? (gw >> 1) : gw;
+  const int t_lo = seg == 1 ? A.seg_m : 0, t_hi = seg == 0 ? A.seg_m : N, NR = t_hi - t_lo;
   // ---- prox-row ring: owned ancestors then chain rows (bottom-up) of each
   // chain slot; one cp.async group per row (empty past the end)
   int ic_cs = 0, ic_pos = -2;  // the first ++ lands on chain slot 0's prologue
@@ -338,18 +367,18 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     bool have = false, chain_row = false;
     unsigned r = 0;
     for (;;) {
-      if (++ic_pos == kb + N) {
+      if (++ic_pos == kb + NR) {
         ic_pos = -1;
         ++ic_cs;
       }
-      const int ci = gw * A.cpw + ic_cs;
+      const int ci = gp * A.cpw + ic_cs;
       if (ic_cs >= A.cpw || ci >= (int)nchain) {
-        ic_pos = kb + N - 1;  // park past the end
+        ic_pos = kb + NR - 1;  // park past the end
         ic_cs = A.cpw;
         break;
       }
       if (ic_pos < 0) {  // prologue of chain ci
-        ic_own = kb > 0 ? __ldg(Q.cown + ci) : 0u;
+        ic_own = kb > 0 && seg <= 0 ? __ldg(Q.cown + ci) : 0u;
         for (int m = 0; m < kb; ++m) {
           const double* sl = reinterpret_cast<const double*>(Q.Lb) + (size_t)Q.cpath[(size_t)ci * kb + m] * NU +
                              2 * lane;
@@ -357,14 +386,24 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
           for (int k = 0; k < (NU / 2 + 31) / 32; ++k)
             if (lane + 32 * k < NU / 2) cp16(pro + m * NU + 2 * lane + 64 * k, sl + 64 * k);
         }
-        const double* sa = reinterpret_cast<const double*>(Q.agg) + (size_t)ci * AW + 2 * lane;
+        // aggregates: the chain's (whole / lower segment) or the upper segment's;
+        // segmented: then the upper segment's corrections [c0 | c1] (upper) or
+        // its corrected [LS_U | LW_U] (lower)
+        const double* sa = reinterpret_cast<const double*>(seg == 0 ? A.aggu : Q.agg) + (size_t)ci * AW + 2 * lane;
 #pragma unroll
         for (int k = 0; k < (AW / 2 + 31) / 32; ++k)
           if (lane + 32 * k < AW / 2) cp16(pro + kb * NU + 2 * lane + 64 * k, sa + 64 * k);
+        if (segd) {
+          const double* sc = seg == 0 ? reinterpret_cast<const double*>(A.corr) + (size_t)ci * 2 * NU + 2 * lane
+                                      : reinterpret_cast<const double*>(A.aggu) + (size_t)ci * AW + 2 * lane;
+#pragma unroll
+          for (int k = 0; k < (NU + 31) / 32; ++k)
+            if (lane + 32 * k < NU) cp16(pro + kb * NU + AW + 2 * lane + 64 * k, sc + 64 * k);
+        }
         break;
       }
       if (ic_pos >= kb) {
-        r = nbr + (unsigned)(N - 1 - (ic_pos - kb)) * nchain + (unsigned)ci;
+        r = nbr + (unsigned)(t_hi - 1 - (ic_pos - kb)) * nchain + (unsigned)ci;
         have = chain_row = true;
         break;
       }
@@ -588,9 +627,9 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     }
   };
 
-  int sib0 = gw * A.cpw;  // first chain of the current stage-(kstar-1) parent
+  int sib0 = gp * A.cpw;  // first chain of the current stage-(kstar-1) parent
   for (int cs = 0; cs < A.cpw; ++cs) {
-    const int ci = gw * A.cpw + cs;
+    const int ci = gp * A.cpw + cs;
     if (ci >= (int)nchain) break;
     const unsigned r_top = nbr + (unsigned)ci;
     // the chain prologue (a ring group): its ancestors' L rows and its aggregates, in the scratch
@@ -605,10 +644,22 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       LWc[0] = w0.x; LWc[1] = w0.y; LWc[2] = ok1 ? w1.x : TG(0); LWc[3] = ok1 ? w1.y : TG(0);
       SU[0] = u0.x; SU[1] = u0.y; SU[2] = ok1 ? u1.x : TG(0); SU[3] = ok1 ? u1.y : TG(0);
       SG[0] = g0.x; SG[1] = okx2 ? g0.y : TG(0);
+      if (seg == 1) {  // lower segment: whole-chain aggregates from both segments' (the upper's corrected)
+        const double2 su0 = ld2s(a + AW + l2), su1 = ld2s(a + AW + o1), wu0 = ld2s(a + AW + NU + l2),
+                      wu1 = ld2s(a + AW + NU + o1);
+        const TG LSu[4] = {su0.x, su0.y, ok1 ? su1.x : TG(0), ok1 ? su1.y : TG(0)};
+        const TG LWu[4] = {wu0.x, wu0.y, ok1 ? wu1.x : TG(0), ok1 ? wu1.y : TG(0)};
+        const TG dn = (TG)(N - A.seg_m);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          LWc[q] = fma(dn, LSu[q], LWc[q] + LWu[q]);
+          LSc[q] = LSu[q] + LSc[q];
+        }
+      }
     }
     // ---- ancestors, top-down: ls = running sum of L, Ws = running sum of ls
     TG ls[4] = {0, 0, 0, 0}, Ws[4] = {0, 0, 0, 0};
-    const unsigned own = kb > 0 ? __ldg(Q.cown + ci) : 0u;
+    const unsigned own = kb > 0 && seg <= 0 ? __ldg(Q.cown + ci) : 0u;
     for (int m = 0; m < kb; ++m) {
       const unsigned r = (unsigned)Q.cpath[(size_t)ci * kb + m];
       const double2 a0 = ld2s(pro + m * NU + l2), a1 = ld2s(pro + m * NU + o1);
@@ -647,13 +698,13 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     {
       TG V[4], w[4], bw[2];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) V[q] = fma((TG)N, ls[q], LWc[q]) + Ws[q];
+      for (int q = 0; q < 4; ++q) V[q] = fma((TG)t_hi, ls[q], LWc[q]) + Ws[q];
       proj_neg(V, SU, w);  // sum of u over the root path
       bmul(w, bw);
       xs[0] = ((TG)d.p[l2] + bw[0]) + SG[0];
       xs[1] = okx2 ? ((TG)d.p[l2 + 1] + bw[1]) + SG[1] : TG(0);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) ls[q] = ls[q] + LSc[q];  // ls_{N-1}
+      for (int q = 0; q < 4; ++q) ls[q] = ls[q] + LSc[q];  // ls of the warp's bottom row
     }
     TG wn[4];  // -P ls of the next row down the walk
     {
@@ -670,9 +721,9 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     }
     // ---- chain rows, bottom-up: down of it, prox of it, up of it + 1
     TG wbr[2] = {0, 0}, acc[4] = {0, 0, 0, 0}, LSn[4] = {0, 0, 0, 0}, LWn[4] = {0, 0, 0, 0};
-    for (int t = N - 1; t >= 0; --t) {
+    for (int t = t_hi - 1; t >= t_lo; --t) {
       const unsigned r = nbr + (unsigned)t * nchain + (unsigned)ci;
-      const bool bottom = t == N - 1;
+      const bool bottom = t == t_hi - 1;
       TG L[4], b[4], g[2], ax, u[4], yx[2], yu[4];
       const double* st = take();
       {
@@ -682,6 +733,15 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         b[0] = b0.x; b[1] = b0.y; b[2] = ok1 ? b1.x : 0.0; b[3] = ok1 ? b1.y : 0.0;
         g[0] = g0.x; g[1] = okx2 ? g0.y : 0.0;
         ax = st[oAx];
+        if (seg == 0) {  // upper segment: L_t = base_t + aux_t (c0 + n_t c1) (previous iteration's correction)
+          const double* cb = pro + kb * NU + AW;
+          const double2 c00 = ld2s(cb + l2), c01 = ld2s(cb + o1), c10 = ld2s(cb + NU + l2), c11 = ld2s(cb + NU + o1);
+          const TG c0[4] = {c00.x, c00.y, c01.x, c01.y}, c1[4] = {c10.x, c10.y, c11.x, c11.y};
+          const TG nt = (TG)(t_hi - 1 - t);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < 2 || ok1) L[q] = fma(ax, fma(nt, c1[q], c0[q]), L[q]);
+        }
       }
       TG bu[2];
 #pragma unroll
@@ -692,7 +752,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       TG pS[4];  // P (sum of a below), for the up pass
       prox(st, r, u, xs, yx, yu, bu, ls, wn, acc, pS);
       release();
-      if (t > 0) {  // x of the row above
+      if (t > t_lo) {  // x of the row above
         xs[0] = (xs[0] - g[0]) - bu[0];
         xs[1] = (xs[1] - g[1]) - bu[1];
       }
@@ -709,7 +769,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         acc[q] = bottom ? a[q] : a[q] + acc[q];
         l[q] = bottom ? a[q] : a[q] + pS[q];
       }
-      const TG wt = (TG)(N - t);
+      const TG wt = (TG)(t_hi - t);  // LW weight from the warp's bottom row
       TG Ln[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -721,7 +781,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       st2(Lp + l2, Ln[0], Ln[1]);
       if (ok1) st2(Lp + 64 + l2, Ln[2], Ln[3]);
     }
-    if (next) {  // chain totals for the branch groups, L aggregates for the next iteration
+    if (next && seg < 0) {  // chain totals for the branch groups, L aggregates for the next iteration
       if (okx2) st2(Q.wbar + (size_t)r_top * LX + l2, wbr[0], wbr[1]);
       else Q.wbar[(size_t)r_top * LX + l2] = wbr[0];
       st2(Q.Asub + (size_t)r_top * NU + l2, acc[0], acc[1]);
@@ -733,6 +793,92 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         st2(a + 64 + l2, LSn[2], LSn[3]);
         st2(a + NU + 64 + l2, LWn[2], LWn[3]);
       }
+    }
+    if (next && seg == 1) {  // lower segment: its totals to the upper warp, its L aggregates
+      TG* sx = reinterpret_cast<TG*>(A.segx) + (size_t)ci * (LX + NU);
+      if (okx2) st2(sx + l2, wbr[0], wbr[1]);
+      else sx[l2] = wbr[0];
+      st2(sx + LX + l2, acc[0], acc[1]);
+      if (ok1) st2(sx + LX + 64 + l2, acc[2], acc[3]);
+      TG* a = Q.agg + (size_t)ci * AW;
+      st2(a + l2, LSn[0], LSn[1]);
+      st2(a + NU + l2, LWn[0], LWn[1]);
+      if (ok1) {
+        st2(a + 64 + l2, LSn[2], LSn[3]);
+        st2(a + NU + 64 + l2, LWn[2], LWn[3]);
+      }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release_gpu(A.flag + ci, it + 1);
+    }
+    if (next && seg == 0) {  // upper segment: wait for the lower one, then the corrections
+      const int* fl = A.flag + ci;
+      for (long long k = 0; ld_acquire_gpu(fl) < it + 1; ++k) {
+        __nanosleep(128);
+        if (k > (1ll << 24)) {  // never expected (both warps are resident): fail loudly, not hang
+          if (lane == 0) atomicMin(d.bad_nu, it);
+          break;
+        }
+      }
+      __syncwarp();
+      const TG* sx = reinterpret_cast<const TG*>(A.segx) + (size_t)ci * (LX + NU);
+      const auto wd = ld2cg(sx + l2), d0 = ld2cg(sx + LX + l2), d1 = ld2cg(sx + LX + o1);
+      const TG WBd[2] = {wd.x, okx2 ? wd.y : TG(0)};
+      const TG AD[4] = {d0.x, d0.y, ok1 ? d1.x : TG(0), ok1 ? d1.y : TG(0)};
+      st2(wb + l2, WBd[0], WBd[1]);  // every lane is past the last row's reads (the wait's syncwarp)
+      __syncwarp();
+      TG c[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c[q] = G_bc(q);  // c = B' WB_D
+      st2(zb + l2, c[0], c[1]);
+      st2(zb + 64 + l2, c[2], c[3]);
+      st2(zb2 + l2, AD[0], AD[1]);
+      st2(zb2 + 64 + l2, AD[2], AD[3]);
+      __syncwarp();
+      {
+        TG k1, k2;
+        dp_gather2<TG>(ops, 12, 4, ZB_OFF, ZB2_OFF, k1, k2);
+        tb[lane] = k1;
+        tb2[lane] = k2;
+      }
+      __syncwarp();
+      TG c0[4], c1[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        TG e1, e2;
+        dp_gather2<TG>(ops, 8 + q, 1, TB_OFF, TB2_OFF, e1, e2);
+        c1[q] = c[q] - e1;             // P c
+        c0[q] = c[q] + (AD[q] - e2);   // c + P A_D
+      }
+      TG* cr = reinterpret_cast<TG*>(A.corr) + (size_t)ci * 2 * NU;
+      st2(cr + l2, c0[0], c0[1]);
+      st2(cr + NU + l2, c1[0], c1[1]);
+      if (ok1) {
+        st2(cr + 64 + l2, c0[2], c0[3]);
+        st2(cr + NU + 64 + l2, c1[2], c1[3]);
+      }
+      const TG* as = reinterpret_cast<const TG*>(A.auxs) + (size_t)ci * 4;
+      const TG A0 = as[0], A1 = as[1], A2 = as[2], A3 = as[3];
+      const TG mm = (TG)A.seg_m;
+      TG* au = reinterpret_cast<TG*>(A.aggu) + (size_t)ci * AW;
+      TG LSu[4], LWu[4], At[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        LSu[q] = LSn[q] + (A0 * c0[q] + A1 * c1[q]);
+        LWu[q] = LWn[q] + (A2 * c0[q] + A3 * c1[q]);
+        At[q] = fma(mm, c[q], acc[q]) + AD[q];
+      }
+      st2(au + l2, LSu[0], LSu[1]);
+      st2(au + NU + l2, LWu[0], LWu[1]);
+      if (ok1) {
+        st2(au + 64 + l2, LSu[2], LSu[3]);
+        st2(au + NU + 64 + l2, LWu[2], LWu[3]);
+      }
+      const TG Wt[2] = {wbr[0] + WBd[0], wbr[1] + WBd[1]};
+      if (okx2) st2(Q.wbar + (size_t)r_top * LX + l2, Wt[0], Wt[1]);
+      else Q.wbar[(size_t)r_top * LX + l2] = Wt[0];
+      st2(Q.Asub + (size_t)r_top * NU + l2, At[0], At[1]);
+      if (ok1) st2(Q.Asub + (size_t)r_top * NU + 64 + l2, At[2], At[3]);
     }
     if (A.sib && next) {  // after the parent's last chain: its up pass (k_branch_grp arithmetic, R-free,
                           // no branching descendants: W2 = 0), from its own Yc and the chains' totals
@@ -791,28 +937,49 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
 // Per-solve constants of k_chain_dp: per chain SUTp / SGp (ut / g summed over
 // the whole root path, ancestors and chain rows), per branching row the root
 // path prefixes PUT / PG (including the row); the running L aggregates are
-// zeroed (L = 0 at Yc = 0). One warp per chain / branching row.
+// zeroed (L = 0 at Yc = 0). Segmented chains (segm > 0): also the upper
+// segment's SUT_U / SG_U (ancestors + rows [0, segm)) and its aux sums
+// [sum aux, sum n aux, sum (segm - t) aux, sum (segm - t) n aux], n = segm - 1 - t.
+// One warp per chain / branching row.
 template <typename TG>
-__global__ void k_dp_agg_init(FastView f, TG* agg, TG* putg) {
+__global__ void k_dp_agg_init(FastView f, TG* agg, TG* putg, TG* aggu, TG* auxs, int segm) {
   const DevView& d = f.d;
   const int nu = d.nu, lx = d.lx, kb = f.kstar, N = d.H - kb, AW = dp_agg_w(nu, lx), PW = nu + lx;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const GA<TG> G = ga<TG>(f);
   const TG* UT = sizeof(TG) == 8 ? (const TG*)f.ut : (const TG*)f.ut32;
+  auto crow = [&](int ci, int t) { return (size_t)f.n_branch + (size_t)t * f.nchain + ci; };
   if (w < f.nchain) {
     const int ci = w;
-    TG* a = agg + (size_t)ci * AW;
-    for (int c = lane; c < AW; c += 32) {
-      TG s = 0;
-      if (c >= 2 * nu) {
-        const bool isg = c >= 3 * nu;
-        const int cc = isg ? c - 3 * nu : c - 2 * nu;
-        const TG* base = isg ? G.g : UT;
-        const int stride = isg ? lx : nu;
-        for (int m = 0; m < kb; ++m) s += base[(size_t)f.cpath[(size_t)ci * kb + m] * stride + cc];
-        for (int t = 0; t < N; ++t) s += base[((size_t)f.n_branch + (size_t)t * f.nchain + ci) * stride + cc];
+    for (int part = 0; part < (segm > 0 ? 2 : 1); ++part) {
+      const int tend = part == 0 ? N : segm;
+      TG* a = (part == 0 ? agg : aggu) + (size_t)ci * AW;
+      for (int c = lane; c < AW; c += 32) {
+        TG s = 0;
+        if (c >= 2 * nu) {
+          const bool isg = c >= 3 * nu;
+          const int cc = isg ? c - 3 * nu : c - 2 * nu;
+          const TG* base = isg ? G.g : UT;
+          const int stride = isg ? lx : nu;
+          for (int m = 0; m < kb; ++m) s += base[(size_t)f.cpath[(size_t)ci * kb + m] * stride + cc];
+          for (int t = 0; t < tend; ++t) s += base[crow(ci, t) * stride + cc];
+        }
+        a[c] = s;
       }
-      a[c] = s;
+    }
+    if (segm > 0 && lane == 0) {
+      TG s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+      for (int t = 0; t < segm; ++t) {
+        const TG ax = G.aux[crow(ci, t) * 2], n = (TG)(segm - 1 - t), wt = (TG)(segm - t);
+        s0 += ax;
+        s1 += n * ax;
+        s2 += wt * ax;
+        s3 += wt * n * ax;
+      }
+      auxs[(size_t)ci * 4] = s0;
+      auxs[(size_t)ci * 4 + 1] = s1;
+      auxs[(size_t)ci * 4 + 2] = s2;
+      auxs[(size_t)ci * 4 + 3] = s3;
     }
   } else if (w < f.nchain + f.n_branch) {
     const int r = w - f.nchain;
@@ -828,23 +995,29 @@ __global__ void k_dp_agg_init(FastView f, TG* agg, TG* putg) {
   }
 }
 
-// Warm start: L aggregates of the chains from L (written by the up pass).
+// Warm start: L aggregates of the chains from L (written by the up pass; the
+// segment corrections are zero): [LS | LW] over rows [segm, N) with weights
+// N - t into agg and, segmented, over rows [0, segm) with weights segm - t into aggu.
 template <typename TG>
-__global__ void k_dp_agg_L(FastView f, TG* agg) {
+__global__ void k_dp_agg_L(FastView f, TG* agg, TG* aggu, int segm) {
   const DevView& d = f.d;
   const int nu = d.nu, lx = d.lx, N = d.H - f.kstar, AW = dp_agg_w(nu, lx);
   const int ci = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (ci >= f.nchain) return;
   const GA<TG> G = ga<TG>(f);
-  for (int c = lane; c < nu; c += 32) {
-    TG s = 0, w = 0;
-    for (int t = N - 1; t >= 0; --t) {
-      const TG L = G.Lb[((size_t)f.n_branch + (size_t)t * f.nchain + ci) * nu + c];
-      s = s + L;
-      w = fma((TG)(N - t), L, w);
+  for (int part = 0; part < (segm > 0 ? 2 : 1); ++part) {
+    const int t0 = part == 0 ? segm : 0, t1 = part == 0 ? N : segm;
+    TG* a = (part == 0 ? agg : aggu) + (size_t)ci * AW;
+    for (int c = lane; c < nu; c += 32) {
+      TG s = 0, w = 0;
+      for (int t = t1 - 1; t >= t0; --t) {
+        const TG L = G.Lb[((size_t)f.n_branch + (size_t)t * f.nchain + ci) * nu + c];
+        s = s + L;
+        w = fma((TG)(t1 - t), L, w);
+      }
+      a[c] = s;
+      a[nu + c] = w;
     }
-    agg[(size_t)ci * AW + c] = s;
-    agg[(size_t)ci * AW + nu + c] = w;
   }
 }
 

@@ -117,10 +117,10 @@ def test_reciprocal_division_is_exact():
 # env switches of the kernel variants (graph: CTA-per-chain kernels; chainw:
 # warp-per-chain kernels with an 8-row shared-memory ring (fp64), or rows
 # streamed through registers)
-VARIANT_ENV = {
-    "graph": {"WMPC_CHAINW": "0"},
-    "graph-chainw8": {"WMPC_CHAINW": "1", "WMPC_CWPD": "8"},
-    "graph-chainwr": {"WMPC_CHAINW": "1", "WMPC_CWPD": "1"},
+VARIANT_ENV = {  # (k_chain_dp off: it is the C3 / C4 default)
+    "graph": {"WMPC_DP": "0", "WMPC_CHAINW": "0"},
+    "graph-chainw8": {"WMPC_DP": "0", "WMPC_CHAINW": "1", "WMPC_CWPD": "8"},
+    "graph-chainwr": {"WMPC_DP": "0", "WMPC_CHAINW": "1", "WMPC_CWPD": "1"},
 }
 
 

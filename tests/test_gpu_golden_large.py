@@ -64,6 +64,7 @@ def _solve_vs_golden(name, precision="fp64", tol=TOL):
 def test_c3_500_iterations_production_path_vs_reference_golden():
     info, errs = _solve_vs_golden("C3")
     assert info["fast_path"] == 300, info
+    assert info["fused_dp"] == 1 and info["dp_segm"] > 0, info  # the C3 default: segmented k_chain_dp
     bad = {k: v for k, v in errs.items() if not v <= TOL}
     assert not bad, (bad, info)
 

@@ -27,9 +27,10 @@ pytestmark = pytest.mark.gpu
 
 MODES = {  # name: (config, env, precision)
     "graph-c1": ("C1", {}, "fp64"),
-    "ring-c3": ("C3", {}, "fp64"),
-    "registers-c3": ("C3", {"WMPC_CHAINW": "1", "WMPC_CWPD": "1"}, "fp64"),
-    "dp-c3": ("C3", {"WMPC_DP": "1"}, "fp64"),
+    "ring-c3": ("C3", {"WMPC_DP": "0"}, "fp64"),
+    "registers-c3": ("C3", {"WMPC_DP": "0", "WMPC_CHAINW": "1", "WMPC_CWPD": "1"}, "fp64"),
+    "dp-whole-c3": ("C3", {"WMPC_DP": "1", "WMPC_DP_SEG": "0"}, "fp64"),
+    "dp-segmented-c3": ("C3", {}, "fp64"),  # the C3 default: two warps per chain, flag handshake
     "graph-fp32-c2": ("C2", {}, "fp32"),
     "registers-fp32-c3": ("C3", {"WMPC_CHAINW": "1", "WMPC_CWPD": "1"}, "fp32"),
 }
