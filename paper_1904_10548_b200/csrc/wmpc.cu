@@ -2216,11 +2216,12 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
       CK(cudaMemsetAsync(ctx->dk_mv, 0, sizeof(unsigned long long) * 512, ctx->stream));
       const int nbw = (ctx->n + 7) / 8;
       ctx->launches += 3;
-      launch_dyk(ctx, nbw, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 1,
-                                                ctx->dk_fix);
-      k_dyk_count<<<1, 512, 0, ctx->stream>>>(ctx->dk_mv, 500, ctx->scal + 8, ctx->dk_sweeps);
-      launch_dyk(ctx, nbw, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 2,
-                                                ctx->dk_fix);
+      launch_dyk(ctx, nbw, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 3, ctx->dk_fix,
+                 (const double*)(ctx->scal + 8));
+      k_dyk_count_bits<<<1, 512, 0, ctx->stream>>>(reinterpret_cast<const unsigned*>(ctx->dk_mv), 500,
+                                                   ctx->dk_sweeps);
+      launch_dyk(ctx, nbw, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 2, ctx->dk_fix,
+                 (const double*)(ctx->scal + 8));
     }
     // 2. rollout (problem.py:207-218)
     rollout(ctx, d, ctx->Uf, ctx->Xf);
@@ -2659,7 +2660,7 @@ int wmpc_cert_dykstra(wmpc_ctx* ctx, int max_sweeps, double* mv) {
       CK(cudaMemsetAsync(ctx->dk_mv, 0, sizeof(unsigned long long) * 512, ctx->stream));
       ctx->launches++;
       launch_dyk(ctx, (ctx->n + 7) / 8, po, d, po, ctx->Ua, nullptr, ctx->dk_mv, ctx->dk_sweeps,
-                                                            max_sweeps, 1, nullptr);
+                 max_sweeps, 1, nullptr, (const double*)nullptr);
       check_launch(ctx);
       d2h(ctx, bits.data(), ctx->dk_mv, sizeof(unsigned long long) * max_sweeps);
       sync(ctx);
@@ -2700,7 +2701,7 @@ int wmpc_cert_terms(wmpc_ctx* ctx, int sweeps, double* terms) {
       DykOps po = dyk_ops(ctx);
       ctx->launches++;
       launch_dyk(ctx, (ctx->n + 7) / 8, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, sweeps,
-                                                            2, nullptr);
+                 2, nullptr, (const double*)nullptr);
     }
     rollout(ctx, d, ctx->Uf, ctx->Xf);
     check_launch(ctx);

@@ -775,17 +775,26 @@ constexpr int DYK_MAXQ = 4;  // nu <= 128
 #ifndef DYK_WPB
 #define DYK_WPB 4  // nodes (warps) per CTA (measured: 4 beats 8 and 2 by 3-5 % at C3)
 #endif
+// pass 3: pass 1 for the local certificate, with the stop threshold already
+// known (*tol): instead of the per-sweep maximum, each node votes whether
+// any of its movements exceeds it (the same test as k_dyk_count's max <= tol,
+// NaN counting as exceeding) into a per-sweep bit mask (mv as 32-bit words,
+// one atomicOr per node and 32 sweeps).
 template <bool ELL>
 __global__ void __launch_bounds__(DYK_WPB * 32) k_dyk_warp(DevView d, DykOps po, const double* __restrict__ u_in,
                                                   double* __restrict__ u_out, unsigned long long* mv,
-                                                  const int* sweeps_in, int max_sweeps, int pass, int* fix) {
+                                                  const int* sweeps_in, int max_sweeps, int pass, int* fix,
+                                                  const double* tol) {
   __shared__ double sA[DYK_WPB][128];
   __shared__ double sT[DYK_WPB][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * DYK_WPB + warp;
   if (r >= d.n) return;
   const int nu = d.nu, ns = d.ns;
-  const int nsw = pass == 1 ? max_sweeps : *sweeps_in;
+  const int nsw = pass != 2 ? max_sweeps : *sweeps_in;
+  const double thr = pass == 3 ? *tol : 0.0;
+  unsigned* bad_words = reinterpret_cast<unsigned*>(mv);
+  unsigned wbits = 0u;
   if (pass == 2 && fix && nsw >= fix[r]) return;  // pass 1 already left the answer in u_out
   int settled = nsw;
   double cur[DYK_MAXQ], pc[DYK_MAXQ], qc[DYK_MAXQ], c[DYK_MAXQ], lo[DYK_MAXQ], hi[DYK_MAXQ];
@@ -897,20 +906,27 @@ __global__ void __launch_bounds__(DYK_WPB * 32) k_dyk_warp(DevView d, DykOps po,
         cur[q] = nx;
       }
     }
-    // warp max of a nonnegative double (NaN largest, as np.max propagates it)
-    // on its bit pattern: high words, then low words among the top holders
-    {
+    if (pass == 3) {
+      wbits |= (__any_sync(0xffffffffu, !(moved <= thr)) ? 1u : 0u) << (s & 31);
+      if ((s & 31) == 31) {
+        if (lane == 0 && wbits) atomicOr(bad_words + (s >> 5), wbits);
+        wbits = 0u;
+      }
+    } else if (pass == 1) {
+      // warp max of a nonnegative double (NaN largest, as np.max propagates it)
+      // on its bit pattern: high words, then low words among the top holders
       const unsigned long long bits = (unsigned long long)__double_as_longlong(moved);
       const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(bits >> 32));
       const unsigned lo = __reduce_max_sync(0xffffffffu, (unsigned)(bits >> 32) == hi ? (unsigned)bits : 0u);
       const unsigned long long mb = ((unsigned long long)hi << 32) | lo;
-      if (pass == 1 && lane == 0 && mb != 0ull) atomicMax(mv + s, mb);
+      if (lane == 0 && mb != 0ull) atomicMax(mv + s, mb);
     }
     bool stop = false;
     if constexpr (CHECK) stop = __all_sync(0xffffffffu, same);  // every later sweep repeats it
     __syncwarp();
     return stop;
   };
+  int s_end = nsw;
   for (int s = 0; s < nsw; ++s) {
     const bool chk = (s & 3) == 3;
     const bool stop = fast ? (chk ? sweep(s, std::true_type{}, std::true_type{})
@@ -919,16 +935,33 @@ __global__ void __launch_bounds__(DYK_WPB * 32) k_dyk_warp(DevView d, DykOps po,
                                   : sweep(s, std::false_type{}, std::false_type{}));
     if (stop) {
       settled = s;
+      s_end = s + 1;
       break;
     }
   }
-  if (pass == 1 && fix && lane == 0) fix[r] = settled;
+  if (pass == 3 && lane == 0 && wbits) atomicOr(bad_words + ((s_end - 1) >> 5), wbits);
+  if (pass != 2 && fix && lane == 0) fix[r] = settled;
   if (pass == 2 || (fix && u_out)) {
 #pragma unroll
     for (int q = 0; q < DYK_MAXQ; ++q) {
       const int k = lane + 32 * q;
       if (k < nu) u_out[(size_t)r * nu + k] = cur[q];
     }
+  }
+}
+
+// Global sweep count from pass 3's bit mask: first sweep no node voted for.
+__global__ void k_dyk_count_bits(const unsigned* bad, int max_sweeps, int* sweeps) {
+  __shared__ int smin[32];
+  int best = max_sweeps;
+  for (int s = threadIdx.x; s < max_sweeps; s += blockDim.x)
+    if (!((bad[s >> 5] >> (s & 31)) & 1u)) best = min(best, s + 1);
+  for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) smin[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = min(best, smin[w]);
+    *sweeps = best;
   }
 }
 
