@@ -84,7 +84,7 @@ struct wmpc_ctx {
   double *pj_kv = nullptr, *pj_ecv = nullptr;
   unsigned long long* dk_mv = nullptr;
   int* dk_sweeps = nullptr;
-  int* dk_fix = nullptr;                       // certificate Dykstra: per-node settled sweep (pass 1)
+  int* dk_fix = nullptr;                       // certificate Dykstra: settled sweep per node (k_dyk_warp) or per (node, coupling row) (k_dyk_block)
   int use_graphk = 0, n_branch = 0;
   int* store_it = nullptr;
   int store_it_host = 0;
@@ -1597,7 +1597,7 @@ int wmpc_set_structure(wmpc_ctx* ctx, const double* A, const double* B, const do
       upload_vec(ctx, &ctx->pj_ecv, ecv);
       if (!ctx->dk_mv) dalloc(ctx, &ctx->dk_mv, 512);
       if (!ctx->dk_sweeps) dalloc(ctx, &ctx->dk_sweeps, 1);
-      if (!ctx->dk_fix) dalloc(ctx, &ctx->dk_fix, (size_t)n);
+      if (!ctx->dk_fix) dalloc(ctx, &ctx->dk_fix, (size_t)n * std::max(ctx->ns, 1));  // per node or (node, row)
     }
     sync(ctx);
     configure_fast(ctx, B, E, e_pinv, T, D, cptr, cidx);
@@ -2216,12 +2216,22 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
       CK(cudaMemsetAsync(ctx->dk_mv, 0, sizeof(unsigned long long) * 512, ctx->stream));
       const int nbw = (ctx->n + 7) / 8;
       ctx->launches += 3;
-      launch_dyk(ctx, nbw, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 3, ctx->dk_fix,
-                 (const double*)(ctx->scal + 8));
-      k_dyk_count_bits<<<1, 512, 0, ctx->stream>>>(reinterpret_cast<const unsigned*>(ctx->dk_mv), 500,
-                                                   ctx->dk_sweeps);
-      launch_dyk(ctx, nbw, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 2, ctx->dk_fix,
-                 (const double*)(ctx->scal + 8));
+      unsigned* bad = reinterpret_cast<unsigned*>(ctx->dk_mv);
+      if (po.eidx) {  // block-diagonal coupling: one thread per (node, coupling row)
+        const long long nthr = (long long)ctx->n * (ctx->ns + ctx->nu);
+        const int gb = (int)((nthr + 255) / 256);
+        k_dyk_block<3><<<gb, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, bad, ctx->dk_sweeps, 500, ctx->dk_fix,
+                                                   (const double*)(ctx->scal + 8));
+        k_dyk_count_bits<<<1, 512, 0, ctx->stream>>>(bad, 500, ctx->dk_sweeps);
+        k_dyk_block<2><<<gb, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, bad, ctx->dk_sweeps, 500, ctx->dk_fix,
+                                                   (const double*)(ctx->scal + 8));
+      } else {
+        launch_dyk(ctx, nbw, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 3, ctx->dk_fix,
+                   (const double*)(ctx->scal + 8));
+        k_dyk_count_bits<<<1, 512, 0, ctx->stream>>>(bad, 500, ctx->dk_sweeps);
+        launch_dyk(ctx, nbw, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 2, ctx->dk_fix,
+                   (const double*)(ctx->scal + 8));
+      }
     }
     // 2. rollout (problem.py:207-218)
     rollout(ctx, d, ctx->Uf, ctx->Xf);

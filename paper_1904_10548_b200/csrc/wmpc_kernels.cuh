@@ -950,6 +950,129 @@ __global__ void __launch_bounds__(DYK_WPB * 32) k_dyk_warp(DevView d, DykOps po,
   }
 }
 
+// Dykstra with the structured operators (DykOps ELL copy: every E column has
+// at most one entry, so E E^T is diagonal and the affine projection splits
+// into independent blocks, one per coupling row j: the coordinates of K row j):
+// one THREAD per (node, block) runs the sweeps of its <= 4 coordinates in
+// registers, no shared-memory exchange; one thread per (node, coordinate
+// outside every block) does the box part (a fixed point after the first
+// sweep). Per element the same arithmetic as k_dyk_warp (the K-row sum over
+// the row's entries in ELL order; k_dyk_warp also adds the zero padding
+// slots, which can only change the sign of a zero sum). pass 3 votes into the
+// per-sweep bit mask against *tol and stores each block's settled sweep in
+// fix; pass 2 recomputes the blocks that had not settled by the global count.
+template <int PASS>
+__global__ void __launch_bounds__(256) k_dyk_block(DevView d, DykOps po, const double* __restrict__ u_in,
+                                                   double* __restrict__ u_out, unsigned* bad_words,
+                                                   const int* sweeps_in, int max_sweeps, int* fix,
+                                                   const double* tol) {
+  const int nu = d.nu, ns = d.ns;
+  const long long nb = (long long)d.n * ns;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int nsw = PASS == 3 ? max_sweeps : *sweeps_in;
+  const double thr = PASS == 3 ? *tol : 0.0;
+  if (tid >= nb) {  // a coordinate outside every block: clip, fixed after sweep 0
+    if (tid >= nb + (long long)d.n * nu) return;
+    const long long c = tid - nb;
+    const int r = (int)(c / nu), k = (int)(c - (long long)r * nu);
+    if (po.eval[(size_t)(po.ec0 + k) * po.ew] != 0.0) return;  // in a block
+    if (PASS == 2) return;  // pass 3 wrote the answer (any global count >= 1)
+    const double x0 = u_in[(size_t)r * nu + k];
+    const double x1 = np_clip(x0, d.umin[k], d.umax[k]);
+    u_out[(size_t)r * nu + k] = x1;
+    const bool bad = !(np_max(0.0, fabs(x1 - x0)) <= thr);
+    const unsigned am = __activemask();
+    if (__any_sync(am, bad) && lane == __ffs(am) - 1) atomicOr(bad_words, 1u);
+    return;
+  }
+  const int r = (int)(tid / ns), j = (int)(tid - (long long)r * ns);
+  if (PASS == 2 && nsw >= fix[tid]) return;  // pass 3 left the answer in u_out
+  constexpr int W = 4;
+  int kk[W];
+  double kv[W], ev[W], cur[W], pc[W], qc[W], c[W], lo[W], hi[W];
+  int cnt = 0;
+  const double* sh = d.np->shift + (size_t)r * ns;
+  bool fin = true;
+#pragma unroll
+  for (int e = 0; e < W; ++e) {
+    const size_t o = (size_t)(po.kr0 + j) * po.ew + e;
+    const double v = po.eval[o];
+    const int k = po.eidx[o];
+    const bool ok = v != 0.0;  // zero-padded slots past the row's entries
+    cnt += ok;
+    kk[e] = ok ? k : 0;
+    kv[e] = ok ? v : 0.0;
+    ev[e] = ok ? po.eval[(size_t)(po.ec0 + k) * po.ew] : 0.0;
+    cur[e] = ok ? u_in[(size_t)r * nu + k] : 0.0;
+    pc[e] = qc[e] = 0.0;
+    double cc = 0.0;
+    if (ok)
+      for (int i = 0; i < ns; ++i) cc = fma(d.e_pinv[(size_t)k * ns + i], sh[i], cc);
+    c[e] = cc;
+    lo[e] = ok ? d.umin[k] : 0.0;
+    hi[e] = ok ? d.umax[k] : 0.0;
+    fin &= fabs(cur[e]) <= 1e150 && fabs(c[e]) <= 1e150 && fabs(kv[e]) <= 1e150 && fabs(ev[e]) <= 1e150;
+  }
+  int settled = nsw, s_end = nsw;
+  unsigned wbits = 0u;
+  for (int s = 0; s < nsw; ++s) {
+    double A[W], t = 0.0;
+#pragma unroll
+    for (int e = 0; e < W; ++e) A[e] = cur[e] + pc[e];
+#pragma unroll
+    for (int e = 0; e < W; ++e)
+      if (e < cnt) t = fma(kv[e], A[e], t);
+    double moved = 0.0;
+    bool same = true;
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      if (e >= cnt) continue;
+      const double corr = fma(ev[e], t, 0.0);
+      const double a = A[e] - (corr + c[e]);
+      const double pn = A[e] - a;
+      const double v = a + qc[e];
+      double nx;
+      if (fin) {
+        const double m = v > lo[e] ? v : lo[e];
+        nx = m < hi[e] ? m : hi[e];
+        moved = fmax(moved, fabs(nx - cur[e]));
+      } else {
+        nx = np_clip(v, lo[e], hi[e]);
+        moved = np_max(moved, fabs(nx - cur[e]));
+      }
+      const double qn = v - nx;
+      same &= nx == cur[e] && pn == pc[e] && qn == qc[e];
+      pc[e] = pn;
+      qc[e] = qn;
+      cur[e] = nx;
+    }
+    if (PASS == 3) {  // own votes; OR-reduced over whichever lanes arrive together (a union either way)
+      wbits |= (!(moved <= thr) ? 1u : 0u) << (s & 31);
+      if ((s & 31) == 31) {
+        const unsigned am = __activemask();
+        const unsigned w = __reduce_or_sync(am, wbits);
+        if (lane == __ffs(am) - 1 && w) atomicOr(bad_words + (s >> 5), w);
+        wbits = 0u;
+      }
+    }
+    if ((s & 3) == 3 && same) {  // every later sweep repeats it (k_dyk_warp's test, per block)
+      settled = s;
+      s_end = s + 1;
+      break;
+    }
+  }
+  if (PASS == 3) {
+    const unsigned am = __activemask();  // threads leaving here together: one of them flushes
+    const unsigned w = __reduce_or_sync(am, wbits);
+    if (lane == __ffs(am) - 1 && w) atomicOr(bad_words + ((s_end - 1) >> 5), w);
+    fix[tid] = settled;
+  }
+#pragma unroll
+  for (int e = 0; e < W; ++e)
+    if (e < cnt) u_out[(size_t)r * nu + kk[e]] = cur[e];
+}
+
 // Global sweep count from pass 3's bit mask: first sweep no node voted for.
 __global__ void k_dyk_count_bits(const unsigned* bad, int max_sweeps, int* sweeps) {
   __shared__ int smin[32];
