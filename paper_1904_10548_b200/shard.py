@@ -380,7 +380,12 @@ class ShardedSolver:
 
     def solve(self, config: S.SolverConfig | None = None, results: str = "all") -> S.SolverResult:
         """``solve`` (solver.py:398-543) over the shards; every rank returns the
-        full result (``results="u0"``: only u0 and the scalars)."""
+        full result (``results="u0"``: only u0 and the scalars).
+
+        With ``config.gamma`` None the Lipschitz constant is estimated once,
+        on rank 0, over the whole tree (factor step + device power iteration
+        on one GPU) and broadcast: a tree that does not fit one GPU needs an
+        explicit ``config.gamma`` (or a precomputed ``self.lipschitz``)."""
         import time
         config = config or S.SolverConfig()
         comm, shards, instance = self.comm, self.shards, self.instance
