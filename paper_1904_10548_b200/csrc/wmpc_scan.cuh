@@ -403,46 +403,32 @@ __global__ void __launch_bounds__(GRP_THREADS) k_branch_grp(FastView f, int r0, 
 #pragma unroll
     for (int i = 0; i < 4; ++i) su[i] += vu[q][i];
   }
-  // rows with more than MQ items per warp: batches of BQ items with every
-  // load in flight before the sums (same per-warp order as one at a time);
-  // predecessor-written rows through L2 (ld.global.cg)
-  constexpr int BQ = 4;
-  for (int eb = e0 + warp + NW * MQ; eb < e1; eb += NW * BQ) {
-    TG x2[BQ][2], u4[BQ][4], wb[BQ];
+  for (int e = e0 + warp + NW * MQ; e < e1; e += NW) {  // rows with more than MQ items per warp
+    const int item = f.gi_item[e];
+    const size_t row = (size_t)(item >> 1);
+    const bool fr = item & 1;
+    const TG w = (TG)f.gi_w[e];
+    const TG* px = fr ? G.wbar + row * lx : G.Yc + row * ly;
+    TG x2[2], u4[4];
 #pragma unroll
-    for (int b = 0; b < BQ; ++b) {
-      const int e = eb + NW * b;
-      const bool ok = e < e1;
-      const int item = ok ? f.gi_item[e] : 0;
-      const size_t row = (size_t)(item >> 1);
-      const bool fr = item & 1;
-      wb[b] = ok ? (TG)f.gi_w[e] : TG(0);
-      const TG* px = fr ? G.wbar + row * lx : G.Yc + row * ly;
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int c = lane + 32 * i;
-        x2[b][i] = ok && c < nt ? __ldcg(px + c) : TG(0);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int c = lane + 32 * i;
-        u4[b][i] = ok && c < nu ? (fr ? __ldcg(G.Asub + row * nu + c)
-                                      : (withR ? __ldcg(G.Yc + row * ly + lx + c) + __ldcg(G.R + row * nu + c)
-                                               : __ldcg(G.Yc + row * ly + lx + c)))
-                                : TG(0);
-      }
+    for (int i = 0; i < 2; ++i) {
+      const int c = lane + 32 * i;
+      x2[i] = c < nt ? px[c] : TG(0);
     }
 #pragma unroll
-    for (int b = 0; b < BQ; ++b) {
-      if (eb + NW * b >= e1) break;
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        s1[i] += x2[b][i];
-        s2[i] = fma(wb[b], x2[b][i], s2[i]);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) su[i] += u4[b][i];
+    for (int i = 0; i < 4; ++i) {
+      const int c = lane + 32 * i;
+      u4[i] = c < nu ? (fr ? G.Asub[row * nu + c]
+                           : (withR ? G.Yc[row * ly + lx + c] + G.R[row * nu + c] : G.Yc[row * ly + lx + c]))
+                     : TG(0);
     }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      s1[i] += x2[i];
+      s2[i] = fma(w, x2[i], s2[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) su[i] += u4[i];
   }
   TG* pw = part + warp * 256;
 #pragma unroll
