@@ -2218,7 +2218,7 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
       ctx->launches += 3;
       unsigned* bad = reinterpret_cast<unsigned*>(ctx->dk_mv);
       if (po.eidx) {  // block-diagonal coupling: one thread per (node, coupling row)
-        const long long nthr = (long long)ctx->n * (ctx->ns + ctx->nu);
+        const long long nthr = (long long)((ctx->n + 31) / 32) * 32 * ctx->ns + (long long)ctx->n * ctx->nu;
         const int gb = (int)((nthr + 255) / 256);
         k_dyk_block<3><<<gb, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, bad, ctx->dk_sweeps, 500, ctx->dk_fix,
                                                    (const double*)(ctx->scal + 8));

@@ -967,7 +967,10 @@ __global__ void __launch_bounds__(256) k_dyk_block(DevView d, DykOps po, const d
                                                    const int* sweeps_in, int max_sweeps, int* fix,
                                                    const double* tol) {
   const int nu = d.nu, ns = d.ns;
-  const long long nb = (long long)d.n * ns;
+  // block threads: warp w takes coupling row j = w % ns of 32 consecutive nodes
+  // (warp-uniform operator entries and slot counts), then one thread per
+  // (node, input) for the inputs outside every block
+  const long long nb = (long long)((d.n + 31) / 32) * 32 * ns;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int nsw = PASS == 3 ? max_sweeps : *sweeps_in;
@@ -986,8 +989,11 @@ __global__ void __launch_bounds__(256) k_dyk_block(DevView d, DykOps po, const d
     if (__any_sync(am, bad) && lane == __ffs(am) - 1) atomicOr(bad_words, 1u);
     return;
   }
-  const int r = (int)(tid / ns), j = (int)(tid - (long long)r * ns);
-  if (PASS == 2 && nsw >= fix[tid]) return;  // pass 3 left the answer in u_out
+  const long long w = tid >> 5;
+  const int j = (int)(w % ns), r = (int)((w / ns) * 32 + lane);
+  if (r >= d.n) return;
+  const long long fi = (long long)r * ns + j;
+  if (PASS == 2 && nsw >= fix[fi]) return;  // pass 3 left the answer in u_out
   constexpr int W = 4;
   int kk[W];
   double kv[W], ev[W], cur[W], pc[W], qc[W], c[W], lo[W], hi[W];
@@ -1016,7 +1022,9 @@ __global__ void __launch_bounds__(256) k_dyk_block(DevView d, DykOps po, const d
   }
   int settled = nsw, s_end = nsw;
   unsigned wbits = 0u;
-  for (int s = 0; s < nsw; ++s) {
+  // one sweep; CHECK: the exact fixed-point test (every 4th sweep, as k_dyk_warp)
+  auto sweep = [&](int s, auto check_tag) -> bool {
+    constexpr bool CHECK = decltype(check_tag)::value;
     double A[W], t = 0.0;
 #pragma unroll
     for (int e = 0; e < W; ++e) A[e] = cur[e] + pc[e];
@@ -1036,13 +1044,13 @@ __global__ void __launch_bounds__(256) k_dyk_block(DevView d, DykOps po, const d
       if (fin) {
         const double m = v > lo[e] ? v : lo[e];
         nx = m < hi[e] ? m : hi[e];
-        moved = fmax(moved, fabs(nx - cur[e]));
+        if (PASS == 3) moved = fmax(moved, fabs(nx - cur[e]));
       } else {
         nx = np_clip(v, lo[e], hi[e]);
-        moved = np_max(moved, fabs(nx - cur[e]));
+        if (PASS == 3) moved = np_max(moved, fabs(nx - cur[e]));
       }
       const double qn = v - nx;
-      same &= nx == cur[e] && pn == pc[e] && qn == qc[e];
+      if (CHECK) same &= nx == cur[e] && pn == pc[e] && qn == qc[e];
       pc[e] = pn;
       qc[e] = qn;
       cur[e] = nx;
@@ -1051,12 +1059,15 @@ __global__ void __launch_bounds__(256) k_dyk_block(DevView d, DykOps po, const d
       wbits |= (!(moved <= thr) ? 1u : 0u) << (s & 31);
       if ((s & 31) == 31) {
         const unsigned am = __activemask();
-        const unsigned w = __reduce_or_sync(am, wbits);
-        if (lane == __ffs(am) - 1 && w) atomicOr(bad_words + (s >> 5), w);
+        const unsigned wv = __reduce_or_sync(am, wbits);
+        if (lane == __ffs(am) - 1 && wv) atomicOr(bad_words + (s >> 5), wv);
         wbits = 0u;
       }
     }
-    if ((s & 3) == 3 && same) {  // every later sweep repeats it (k_dyk_warp's test, per block)
+    return CHECK && same;  // every later sweep repeats it
+  };
+  for (int s = 0; s < nsw; ++s) {
+    if (((s & 3) == 3 ? sweep(s, std::true_type{}) : sweep(s, std::false_type{}))) {
       settled = s;
       s_end = s + 1;
       break;
@@ -1064,9 +1075,9 @@ __global__ void __launch_bounds__(256) k_dyk_block(DevView d, DykOps po, const d
   }
   if (PASS == 3) {
     const unsigned am = __activemask();  // threads leaving here together: one of them flushes
-    const unsigned w = __reduce_or_sync(am, wbits);
-    if (lane == __ffs(am) - 1 && w) atomicOr(bad_words + ((s_end - 1) >> 5), w);
-    fix[tid] = settled;
+    const unsigned wv = __reduce_or_sync(am, wbits);
+    if (lane == __ffs(am) - 1 && wv) atomicOr(bad_words + ((s_end - 1) >> 5), wv);
+    fix[fi] = settled;
   }
 #pragma unroll
   for (int e = 0; e < W; ++e)
