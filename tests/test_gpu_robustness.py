@@ -31,14 +31,35 @@ def _vs_oracle(inst, cache, it=80, gamma=1 / 3e9):
     assert abs(res.duality_gap - ref.duality_gap) <= 1e-8 * (1 + abs(ref.duality_gap))
 
 
-@pytest.mark.parametrize("dp", [False, True])
-def test_non_uniform_tree_vs_oracle(dp, monkeypatch):
+@pytest.mark.parametrize("mode", ["graph", "dp", "dp-segmented"])
+def test_non_uniform_tree_vs_oracle(mode, monkeypatch):
     inst = fan_like_instance(seed=1, leaves_target=48, branching_stages=3, max_children=4, horizon=10)
-    monkeypatch.setenv("WMPC_DP", "1" if dp else "0")
+    monkeypatch.setenv("WMPC_DP", "0" if mode == "graph" else "1")
+    monkeypatch.setenv("WMPC_DP_SEG", "1" if mode == "dp-segmented" else "0")
     cache = S._factor(inst, None, private=True)
     info = nat.path_info(cache._bind())
-    assert info["fast_path"] == 300 and info["fused_dp"] == int(dp), info
+    assert info["fast_path"] == 300 and info["fused_dp"] == int(mode != "graph"), info
+    assert (info["dp_segm"] > 0) == (mode == "dp-segmented"), info
     _vs_oracle(inst, cache)
+
+
+def test_non_uniform_c3_scale_default_path_vs_graph(monkeypatch):
+    """A fan-like tree of ~400 scenarios (2-3 chains per SM: the segmented
+    k_chain_dp by default) against the graph iteration after 150 iterations."""
+    inst = fan_like_instance(seed=2, leaves_target=400, branching_stages=5, max_children=5)
+    out, infos = [], []
+    for env in ({}, {"WMPC_DP": "0"}):
+        for k in ("WMPC_DP", "WMPC_DP_SEG"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        cache = S._factor(inst, None, private=True)
+        infos.append(nat.path_info(cache._bind()))
+        out.append(solve(inst, SolverConfig(max_iter=150, tol=1e-30, gamma=1 / 3e9, gap_check_every=151),
+                         cache=cache))
+    assert infos[1]["fused_dp"] == 0, infos
+    for k in ("u0", "primal", "primal_avg", "dual"):
+        assert rel_err(getattr(out[0], k), getattr(out[1], k)) <= 1e-10, (k, infos[0])
 
 
 def test_coupled_mixing_nodes_vs_oracle():
