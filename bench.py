@@ -357,6 +357,25 @@ def secondary_c2(gamma_default: float) -> dict:
             "us_per_dependent_stage_step": us / (2 * 24), "it_per_s": 1e6 / us}
 
 
+def secondary_c3(gamma_default: float) -> dict:
+    """C3 (512 scenarios: the segmented k_chain_dp by default): us per APG
+    iteration, graph replay, and the kernel selection."""
+    from paper_1904_10548_b200 import factor_step
+    from paper_1904_10548_b200 import _native as nat
+    from paper_1904_10548_b200 import solver as S
+    from paper_1904_10548_b200.synthetic import config_instance
+    inst = config_instance("C3")
+    cache = factor_step(inst)
+    ctx = cache._bind()
+    S._upload_bounds(ctx, inst)
+    g, _ = golden_gamma("C3")
+    us = iteration_us(ctx, g or gamma_default, 200)
+    info = nat.path_info(ctx)
+    return {"workload": workload("C3")["workload"], "nodes": inst.n_nonroot, "us_per_iteration": us,
+            "it_per_s": 1e6 / us, "bytes_frac_of_hbm": BYTES_PER_NODE_ITER * inst.n_nonroot / (us * 1e-6) / 1e9
+            / load_peaks()[0], "fused_dp": info.get("fused_dp"), "dp_segm": info.get("dp_segm")}
+
+
 def run_sharded(args, world, rank, local):
     """N > 1: one solve split by subtrees over the ranks (shard.py), strong scaling."""
     import torch
@@ -613,7 +632,8 @@ def run_ours(args):
                 "loop_ms_per_solve": loop_total / K, "fp32_mode": fp32,
                 "ncu": ncu_digest(f"ncu_{dom.split(' ')[0]}_{args.config}"),
                 "setup": {"factor_step_s": t_factor, "estimate_lipschitz_s": t_lip, "lipschitz_device": L_dev},
-                "secondary_C2": None if args.no_secondary else secondary_c2(gamma)}
+                "secondary_C2": None if args.no_secondary else secondary_c2(gamma),
+                "secondary_C3": None if args.no_secondary else secondary_c3(gamma)}
         print(json.dumps(line), flush=True)
 
 
