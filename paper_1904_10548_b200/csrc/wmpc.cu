@@ -84,6 +84,7 @@ struct wmpc_ctx {
   double *pj_kv = nullptr, *pj_ecv = nullptr;
   unsigned long long* dk_mv = nullptr;
   int* dk_sweeps = nullptr;
+  int* dk_list = nullptr;                      // block Dykstra pass 2: [count | block indices]
   int* dk_fix = nullptr;                       // certificate Dykstra: settled sweep per node (k_dyk_warp) or per (node, coupling row) (k_dyk_block)
   int use_graphk = 0, n_branch = 0;
   int* store_it = nullptr;
@@ -1336,7 +1337,7 @@ void free_all(wmpc_ctx* c) {
                   c->e_ptr, c->e_col, c->e_val, c->aux,
                   c->Lb, c->Asub, c->blob, c->store_it, c->ut, c->ut32, c->f32_Yc, c->f32_Lb, c->f32_Asub, c->f32_wbar, c->f32_U,
                   c->f32_X, c->f32_eoff, c->f32_R, c->f32_g, c->f32_aux, c->f32_ell, c->Yc_save, c->acct, c->rep_gidx, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
-                  c->pj_ecv, c->dk_mv, c->dk_sweeps, c->dk_fix, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
+                  c->pj_ecv, c->dk_mv, c->dk_sweeps, c->dk_fix, c->dk_list, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
                   c->prof, c->rb_u0, c->rb_p, c->rb_a, c->gd_stage, c->dp_agg, c->dp_putg, c->dp_aggu, c->dp_corr, c->dp_segx, c->dp_auxs, c->dp_flag, c->dp_Lc,
                   c->dp_Ac, c->dp_wc};
   for (void* p : ptrs)
@@ -1598,6 +1599,7 @@ int wmpc_set_structure(wmpc_ctx* ctx, const double* A, const double* B, const do
       if (!ctx->dk_mv) dalloc(ctx, &ctx->dk_mv, 512);
       if (!ctx->dk_sweeps) dalloc(ctx, &ctx->dk_sweeps, 1);
       if (!ctx->dk_fix) dalloc(ctx, &ctx->dk_fix, (size_t)n * std::max(ctx->ns, 1));  // per node or (node, row)
+      if (!ctx->dk_list) dalloc(ctx, &ctx->dk_list, (size_t)n * std::max(ctx->ns, 1) + 1);  // [count | blocks]
     }
     sync(ctx);
     configure_fast(ctx, B, E, e_pinv, T, D, cptr, cidx);
@@ -2223,8 +2225,14 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
         k_dyk_block<3><<<gb, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, bad, ctx->dk_sweeps, 500, ctx->dk_fix,
                                                    (const double*)(ctx->scal + 8));
         k_dyk_count_bits<<<1, 512, 0, ctx->stream>>>(bad, 500, ctx->dk_sweeps);
-        k_dyk_block<2><<<gb, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, bad, ctx->dk_sweeps, 500, ctx->dk_fix,
-                                                   (const double*)(ctx->scal + 8));
+        // pass 2 over the blocks not settled by the global count, compacted
+        const long long nblk = (long long)ctx->n * ctx->ns;
+        CK(cudaMemsetAsync(ctx->dk_list, 0, sizeof(int), ctx->stream));
+        k_dyk_compact<<<(int)((nblk + 255) / 256), 256, 0, ctx->stream>>>(ctx->dk_fix, nblk, ctx->dk_sweeps,
+                                                                         ctx->dk_list + 1, ctx->dk_list);
+        k_dyk_redo<<<std::min((int)((nblk + 255) / 256), ctx->sms * 8), 256, 0, ctx->stream>>>(
+            d, po, ctx->Ua, ctx->Uf, ctx->dk_sweeps, ctx->dk_list + 1, ctx->dk_list);
+        ctx->launches += 2;
       } else {
         launch_dyk(ctx, nbw, po, d, po, ctx->Ua, ctx->Uf, ctx->dk_mv, ctx->dk_sweeps, 500, 3, ctx->dk_fix,
                    (const double*)(ctx->scal + 8));

@@ -961,39 +961,13 @@ __global__ void __launch_bounds__(DYK_WPB * 32) k_dyk_warp(DevView d, DykOps po,
 // slots, which can only change the sign of a zero sum). pass 3 votes into the
 // per-sweep bit mask against *tol and stores each block's settled sweep in
 // fix; pass 2 recomputes the blocks that had not settled by the global count.
+// One (node r, coupling row j) block through nsw sweeps (k_dyk_block / k_dyk_redo).
 template <int PASS>
-__global__ void __launch_bounds__(256) k_dyk_block(DevView d, DykOps po, const double* __restrict__ u_in,
-                                                   double* __restrict__ u_out, unsigned* bad_words,
-                                                   const int* sweeps_in, int max_sweeps, int* fix,
-                                                   const double* tol) {
+__device__ __forceinline__ void dyk_block_run(const DevView& d, const DykOps& po, const double* __restrict__ u_in,
+                                              double* __restrict__ u_out, unsigned* bad_words, int nsw,
+                                              double thr, int* fix, int r, int j, int lane) {
   const int nu = d.nu, ns = d.ns;
-  // block threads: warp w takes coupling row j = w % ns of 32 consecutive nodes
-  // (warp-uniform operator entries and slot counts), then one thread per
-  // (node, input) for the inputs outside every block
-  const long long nb = (long long)((d.n + 31) / 32) * 32 * ns;
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int nsw = PASS == 3 ? max_sweeps : *sweeps_in;
-  const double thr = PASS == 3 ? *tol : 0.0;
-  if (tid >= nb) {  // a coordinate outside every block: clip, fixed after sweep 0
-    if (tid >= nb + (long long)d.n * nu) return;
-    const long long c = tid - nb;
-    const int r = (int)(c / nu), k = (int)(c - (long long)r * nu);
-    if (po.eval[(size_t)(po.ec0 + k) * po.ew] != 0.0) return;  // in a block
-    if (PASS == 2) return;  // pass 3 wrote the answer (any global count >= 1)
-    const double x0 = u_in[(size_t)r * nu + k];
-    const double x1 = np_clip(x0, d.umin[k], d.umax[k]);
-    u_out[(size_t)r * nu + k] = x1;
-    const bool bad = !(np_max(0.0, fabs(x1 - x0)) <= thr);
-    const unsigned am = __activemask();
-    if (__any_sync(am, bad) && lane == __ffs(am) - 1) atomicOr(bad_words, 1u);
-    return;
-  }
-  const long long w = tid >> 5;
-  const int j = (int)(w % ns), r = (int)((w / ns) * 32 + lane);
-  if (r >= d.n) return;
   const long long fi = (long long)r * ns + j;
-  if (PASS == 2 && nsw >= fix[fi]) return;  // pass 3 left the answer in u_out
   constexpr int W = 4;
   int kk[W];
   double kv[W], ev[W], cur[W], pc[W], qc[W], c[W], lo[W], hi[W];
@@ -1082,6 +1056,63 @@ __global__ void __launch_bounds__(256) k_dyk_block(DevView d, DykOps po, const d
 #pragma unroll
   for (int e = 0; e < W; ++e)
     if (e < cnt) u_out[(size_t)r * nu + kk[e]] = cur[e];
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(256) k_dyk_block(DevView d, DykOps po, const double* __restrict__ u_in,
+                                                   double* __restrict__ u_out, unsigned* bad_words,
+                                                   const int* sweeps_in, int max_sweeps, int* fix,
+                                                   const double* tol) {
+  const int nu = d.nu, ns = d.ns;
+  // block threads: warp w takes coupling row j = w % ns of 32 consecutive nodes
+  // (warp-uniform operator entries and slot counts), then one thread per
+  // (node, input) for the inputs outside every block
+  const long long nb = (long long)((d.n + 31) / 32) * 32 * ns;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int nsw = PASS == 3 ? max_sweeps : *sweeps_in;
+  const double thr = PASS == 3 ? *tol : 0.0;
+  if (tid >= nb) {  // a coordinate outside every block: clip, fixed after sweep 0
+    if (tid >= nb + (long long)d.n * nu) return;
+    const long long c = tid - nb;
+    const int r = (int)(c / nu), k = (int)(c - (long long)r * nu);
+    if (po.eval[(size_t)(po.ec0 + k) * po.ew] != 0.0) return;  // in a block
+    if (PASS == 2) return;  // pass 3 wrote the answer (any global count >= 1)
+    const double x0 = u_in[(size_t)r * nu + k];
+    const double x1 = np_clip(x0, d.umin[k], d.umax[k]);
+    u_out[(size_t)r * nu + k] = x1;
+    const bool bad = !(np_max(0.0, fabs(x1 - x0)) <= thr);
+    const unsigned am = __activemask();
+    if (__any_sync(am, bad) && lane == __ffs(am) - 1) atomicOr(bad_words, 1u);
+    return;
+  }
+  const long long w = tid >> 5;
+  const int j = (int)(w % ns), r = (int)((w / ns) * 32 + lane);
+  if (r >= d.n) return;
+  dyk_block_run<PASS>(d, po, u_in, u_out, bad_words, nsw, thr, fix, r, j, lane);
+}
+
+// Pass 2 over the compacted blocks that had not settled by the global count.
+__global__ void __launch_bounds__(256) k_dyk_redo(DevView d, DykOps po, const double* __restrict__ u_in,
+                                                  double* __restrict__ u_out, const int* sweeps_in,
+                                                  const int* list, const int* count) {
+  const int nsw = *sweeps_in, cnt = *count, ns = d.ns;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
+    const int fi = list[t];
+    dyk_block_run<2>(d, po, u_in, u_out, nullptr, nsw, 0.0, nullptr, fi / ns, fi % ns, threadIdx.x & 31);
+  }
+}
+
+// The blocks pass 2 must recompute: settled after the global count (or never).
+__global__ void k_dyk_compact(const int* fix, long long nblk, const int* sweeps_in, int* list, int* count) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool need = i < nblk && *sweeps_in < fix[i];
+  const unsigned m = __ballot_sync(0xffffffffu, need);
+  int base = 0;
+  const int lane = threadIdx.x & 31;
+  if (lane == 0 && m) base = atomicAdd(count, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (need) list[base + __popc(m & ((1u << lane) - 1u))] = (int)i;
 }
 
 // Global sweep count from pass 3's bit mask: first sweep no node voted for.
