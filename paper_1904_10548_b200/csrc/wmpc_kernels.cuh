@@ -1058,8 +1058,11 @@ __device__ __forceinline__ void dyk_block_run(const DevView& d, const DykOps& po
     if (e < cnt) u_out[(size_t)r * nu + kk[e]] = cur[e];
 }
 
+#ifndef DYK_MINB
+#define DYK_MINB 3  // 80 registers, 24 warps per SM (measured: C3 certificate 0.45-0.47 vs 0.47-0.55 ms at 1, C4 2.2 vs 2.4-3.3)
+#endif
 template <int PASS>
-__global__ void __launch_bounds__(256) k_dyk_block(DevView d, DykOps po, const double* __restrict__ u_in,
+__global__ void __launch_bounds__(256, DYK_MINB) k_dyk_block(DevView d, DykOps po, const double* __restrict__ u_in,
                                                    double* __restrict__ u_out, unsigned* bad_words,
                                                    const int* sweeps_in, int max_sweeps, int* fix,
                                                    const double* tol) {
