@@ -25,4 +25,4 @@ for target in (25, 50, 100, 250, 500, 1000, 2500, 5000):
     for _ in range(3):
         t0 = time.perf_counter(); g = S._certificate(ctx); ts.append(time.perf_counter() - t0)
     out.append(f"{target}:{min(ts)*1e3:.2f}ms")
-print(cfg, os.environ.get("WMPC_DYK_CHUNK", "1"), " ".join(out))
+print(cfg, " ".join(out))
