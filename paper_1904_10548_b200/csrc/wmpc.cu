@@ -839,7 +839,10 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   ctx->h_cidx = cidx;
   // measured (us per iteration, 16 -> 64): C2 19.8 -> 22.6 (few chains: keep 16),
   // C3 52.4 -> 51.0, C4 269.7 -> 268.0
-  ctx->grp_items_few = nchain > ctx->sms ? std::max(ctx->grp_items, 64) : ctx->grp_items;
+#ifndef GRP_FEW_CAP
+#define GRP_FEW_CAP 32  // round 2, k_chain_dp paths (us per iteration, 64 -> 32): C3 42.8 -> 40.8, C4 191.7 -> 191.1
+#endif
+  ctx->grp_items_few = nchain > ctx->sms ? std::max(ctx->grp_items, GRP_FEW_CAP) : ctx->grp_items;
   build_groups(ctx, 0, nullptr);
   // chain root paths and ancestor ownership (first chain below a row writes it)
   std::vector<int> cpath((size_t)std::max(nchain * kstar, 1), 0);
