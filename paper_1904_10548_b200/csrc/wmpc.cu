@@ -114,7 +114,10 @@ struct wmpc_ctx {
   int rfree = 1;                                // R-free iteration form (graph path, unsharded, unfused)
   double* ut = nullptr;                         // u at Yc = 0 (rfree), per solve
   float* ut32 = nullptr;
-  int grp_items = 16;                           // max items per row in one branching stage group (measured)
+#ifndef GRP_ITEMS_CAP
+#define GRP_ITEMS_CAP 16
+#endif
+  int grp_items = GRP_ITEMS_CAP;                           // max items per row in one branching stage group (measured)
   int grp_items_few = 16;                       // ... when the stage has at most one row per SM
   float *f32_Yc = nullptr, *f32_Lb = nullptr, *f32_Asub = nullptr, *f32_wbar = nullptr, *f32_U = nullptr,
         *f32_X = nullptr, *f32_eoff = nullptr, *f32_R = nullptr, *f32_g = nullptr, *f32_aux = nullptr,

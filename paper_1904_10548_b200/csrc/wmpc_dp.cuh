@@ -58,6 +58,9 @@ constexpr int DP_VSLOTS = 22;  // operator value table: bc 8 | ec 4 | kr 4 | br 
 #ifndef DP_MAXT
 #define DP_MAXT 256  // up to 8 warps per CTA, one CTA per SM
 #endif
+#ifndef DP_SEG_NOOWN
+#define DP_SEG_NOOWN 1  // segmented chains: the segment that does not run the owned branching rows' prox
+#endif
 #ifndef DP_MAXREG
 #define DP_MAXREG 255  // <= 8 warps per SM: 2 per sub-partition, no spills (measured: 7 warps x 224 regs 236 us vs 10 warps x 168 regs (spills) 349 us at C4)
 #endif
@@ -378,7 +381,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         break;
       }
       if (ic_pos < 0) {  // prologue of chain ci
-        ic_own = kb > 0 && seg <= 0 ? __ldg(Q.cown + ci) : 0u;
+        ic_own = kb > 0 && seg != DP_SEG_NOOWN ? __ldg(Q.cown + ci) : 0u;
         for (int m = 0; m < kb; ++m) {
           const double* sl = reinterpret_cast<const double*>(Q.Lb) + (size_t)Q.cpath[(size_t)ci * kb + m] * NU +
                              2 * lane;
@@ -659,7 +662,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     }
     // ---- ancestors, top-down: ls = running sum of L, Ws = running sum of ls
     TG ls[4] = {0, 0, 0, 0}, Ws[4] = {0, 0, 0, 0};
-    const unsigned own = kb > 0 && seg <= 0 ? __ldg(Q.cown + ci) : 0u;
+    const unsigned own = kb > 0 && seg != DP_SEG_NOOWN ? __ldg(Q.cown + ci) : 0u;
     for (int m = 0; m < kb; ++m) {
       const unsigned r = (unsigned)Q.cpath[(size_t)ci * kb + m];
       const double2 a0 = ld2s(pro + m * NU + l2), a1 = ld2s(pro + m * NU + o1);
