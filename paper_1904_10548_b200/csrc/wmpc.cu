@@ -626,11 +626,12 @@ void configure_dp(wmpc_ctx* ctx) {
   // 3.5 per SM) one warp per whole chain is latency-bound (51 vs 52 us): segmented chains (two warps
   // per chain) where every pair fits in one wave
   // (measured, us per iteration: C3 graph 52.1, whole chains 50.0, segmented 42.5 with 10 of 19 rows
-  // up; C2, 128 chains: graph 19.4, segmented 28.0, whole 42.2)
+  // up; C2, 128 chains: graph 19.4, segmented 28.0, whole 42.2; 1,024 chains [4,4,4,4,2,2]: graph 95.8,
+  // whole chains 62.4; [8,8,8,2]: 100.2 vs 63.8): k_chain_dp from 2 chains per SM
   const bool many = nchain >= 8 * sms;
   const bool few = 2 * nchain <= sms * DP_WPS && N >= 6 && kstar > 0;
   const bool seg_default = few && nchain >= 2 * sms;
-  bool want = fits && (many || seg_default);
+  bool want = fits && nchain >= 2 * sms;
   if (const char* e = getenv("WMPC_DP")) want = fits && e[0] == '1';
   if (!want) return;
   int segm = few && !many && seg_default ? (N + 1) / 2 : 0;
