@@ -84,6 +84,8 @@ struct wmpc_ctx {
   double *pj_kv = nullptr, *pj_ecv = nullptr;
   unsigned long long* dk_mv = nullptr;
   int* dk_sweeps = nullptr;
+  int* dk_free = nullptr;                      // inputs in no coupling row (E column empty)
+  int dk_nfree = 0;
   int* dk_list = nullptr;                      // block Dykstra pass 2: [count | block indices]
   int* dk_fix = nullptr;                       // certificate Dykstra: settled sweep per node (k_dyk_warp) or per (node, coupling row) (k_dyk_block)
   int use_graphk = 0, n_branch = 0;
@@ -322,7 +324,8 @@ double gconj_value(wmpc_ctx* ctx, const DevView& d, const double* y) {
 // Dykstra operators: CSR always; the structured path's ELL copy (width 4,
 // zero-padded, the same entries) keeps them in registers across the sweeps.
 DykOps dyk_ops(const wmpc_ctx* ctx) {
-  DykOps po{ctx->pj_kp, ctx->pj_kc, ctx->pj_ecp, ctx->pj_ecr, ctx->pj_kv, ctx->pj_ecv, nullptr, nullptr, 0, 0, 0};
+  DykOps po{ctx->pj_kp, ctx->pj_kc, ctx->pj_ecp, ctx->pj_ecr, ctx->pj_kv, ctx->pj_ecv, nullptr, nullptr, 0, 0, 0,
+            ctx->dk_free, ctx->dk_nfree};
   if (ctx->fast && ctx->use_graphk && ctx->ell_idx && ctx->ell_w == 4) {
     po.eidx = ctx->ell_idx;
     po.eval = ctx->ell_val;
@@ -1344,7 +1347,7 @@ void free_all(wmpc_ctx* c) {
                   c->e_ptr, c->e_col, c->e_val, c->aux,
                   c->Lb, c->Asub, c->blob, c->store_it, c->ut, c->ut32, c->f32_Yc, c->f32_Lb, c->f32_Asub, c->f32_wbar, c->f32_U,
                   c->f32_X, c->f32_eoff, c->f32_R, c->f32_g, c->f32_aux, c->f32_ell, c->Yc_save, c->acct, c->rep_gidx, c->ell_cnt, c->ell_idx, c->ell_val, c->pj_kp, c->pj_kc, c->pj_ecp, c->pj_ecr, c->pj_kv,
-                  c->pj_ecv, c->dk_mv, c->dk_sweeps, c->dk_fix, c->dk_list, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
+                  c->pj_ecv, c->dk_mv, c->dk_sweeps, c->dk_fix, c->dk_list, c->dk_free, c->gi_ptr, c->gi_item, c->gi_w, c->cpath, c->cown,
                   c->prof, c->rb_u0, c->rb_p, c->rb_a, c->gd_stage, c->dp_agg, c->dp_putg, c->dp_aggu, c->dp_corr, c->dp_segx, c->dp_auxs, c->dp_flag, c->dp_Lc,
                   c->dp_Ac, c->dp_wc};
   for (void* p : ptrs)
@@ -1607,6 +1610,14 @@ int wmpc_set_structure(wmpc_ctx* ctx, const double* A, const double* B, const do
       if (!ctx->dk_sweeps) dalloc(ctx, &ctx->dk_sweeps, 1);
       if (!ctx->dk_fix) dalloc(ctx, &ctx->dk_fix, (size_t)n * std::max(ctx->ns, 1));  // per node or (node, row)
       if (!ctx->dk_list) dalloc(ctx, &ctx->dk_list, (size_t)n * std::max(ctx->ns, 1) + 1);  // [count | blocks]
+      {
+        std::vector<int> fr;
+        for (int k = 0; k < nu; ++k)
+          if (ecp[k + 1] == ecp[k]) fr.push_back(k);
+        ctx->dk_nfree = (int)fr.size();
+        if (fr.empty()) fr.push_back(0);
+        upload_vec(ctx, &ctx->dk_free, fr);
+      }
     }
     sync(ctx);
     configure_fast(ctx, B, E, e_pinv, T, D, cptr, cidx);
@@ -2227,7 +2238,7 @@ int wmpc_certificate(wmpc_ctx* ctx, double* gap, double* objective) {
       ctx->launches += 3;
       unsigned* bad = reinterpret_cast<unsigned*>(ctx->dk_mv);
       if (po.eidx) {  // block-diagonal coupling: one thread per (node, coupling row)
-        const long long nthr = (long long)((ctx->n + 31) / 32) * 32 * ctx->ns + (long long)ctx->n * ctx->nu;
+        const long long nthr = (long long)((ctx->n + 31) / 32) * 32 * ctx->ns;
         const int gb = (int)((nthr + 255) / 256);
         k_dyk_block<3><<<gb, 256, 0, ctx->stream>>>(d, po, ctx->Ua, ctx->Uf, bad, ctx->dk_sweeps, 500, ctx->dk_fix,
                                                    (const double*)(ctx->scal + 8));

@@ -763,6 +763,8 @@ struct DykOps {
   const int* eidx;
   const double* eval;
   int ew, ec0, kr0;
+  const int* freek;  // inputs in no coupling row (E column empty), nfree of them
+  int nfree;
 };
 constexpr int DYK_MAXQ = 4;  // nu <= 128
 // fix (optional): pass 1 stores its final state in u_out and, per node, the
@@ -954,9 +956,9 @@ __global__ void __launch_bounds__(DYK_WPB * 32) k_dyk_warp(DevView d, DykOps po,
 // at most one entry, so E E^T is diagonal and the affine projection splits
 // into independent blocks, one per coupling row j: the coordinates of K row j):
 // one THREAD per (node, block) runs the sweeps of its <= 4 coordinates in
-// registers, no shared-memory exchange; one thread per (node, coordinate
-// outside every block) does the box part (a fixed point after the first
-// sweep). Per element the same arithmetic as k_dyk_warp (the K-row sum over
+// registers, no shared-memory exchange; the inputs outside every block are
+// box-only (a fixed point after the first sweep) and clipped by the node's
+// block threads. Per element the same arithmetic as k_dyk_warp (the K-row sum over
 // the row's entries in ELL order; k_dyk_warp also adds the zero padding
 // slots, which can only change the sign of a zero sum). pass 3 votes into the
 // per-sweep bit mask against *tol and stores each block's settled sweep in
@@ -996,6 +998,18 @@ __device__ __forceinline__ void dyk_block_run(const DevView& d, const DykOps& po
   }
   int settled = nsw, s_end = nsw;
   unsigned wbits = 0u;
+  if (PASS == 3) {  // the node's inputs outside every block, shared over its ns block threads:
+                    // clip = their state after any sweep count >= 1; movement counts in sweep 0
+    double moved0 = 0.0;
+    for (int i = j; i < po.nfree; i += ns) {
+      const int k = po.freek[i];
+      const double x0 = u_in[(size_t)r * nu + k];
+      const double x1 = np_clip(x0, d.umin[k], d.umax[k]);
+      u_out[(size_t)r * nu + k] = x1;
+      moved0 = np_max(moved0, fabs(x1 - x0));
+    }
+    wbits = !(moved0 <= thr) ? 1u : 0u;
+  }
   // one sweep; CHECK: the exact fixed-point test (every 4th sweep, as k_dyk_warp)
   auto sweep = [&](int s, auto check_tag) -> bool {
     constexpr bool CHECK = decltype(check_tag)::value;
@@ -1067,28 +1081,15 @@ __global__ void __launch_bounds__(256, DYK_MINB) k_dyk_block(DevView d, DykOps p
                                                    const int* sweeps_in, int max_sweeps, int* fix,
                                                    const double* tol) {
   const int nu = d.nu, ns = d.ns;
-  // block threads: warp w takes coupling row j = w % ns of 32 consecutive nodes
-  // (warp-uniform operator entries and slot counts), then one thread per
-  // (node, input) for the inputs outside every block
+  // warp w takes coupling row j = w % ns of 32 consecutive nodes (warp-uniform
+  // operator entries and slot counts); each block thread also clips its share
+  // of the node's inputs outside every block
   const long long nb = (long long)((d.n + 31) / 32) * 32 * ns;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int nsw = PASS == 3 ? max_sweeps : *sweeps_in;
   const double thr = PASS == 3 ? *tol : 0.0;
-  if (tid >= nb) {  // a coordinate outside every block: clip, fixed after sweep 0
-    if (tid >= nb + (long long)d.n * nu) return;
-    const long long c = tid - nb;
-    const int r = (int)(c / nu), k = (int)(c - (long long)r * nu);
-    if (po.eval[(size_t)(po.ec0 + k) * po.ew] != 0.0) return;  // in a block
-    if (PASS == 2) return;  // pass 3 wrote the answer (any global count >= 1)
-    const double x0 = u_in[(size_t)r * nu + k];
-    const double x1 = np_clip(x0, d.umin[k], d.umax[k]);
-    u_out[(size_t)r * nu + k] = x1;
-    const bool bad = !(np_max(0.0, fabs(x1 - x0)) <= thr);
-    const unsigned am = __activemask();
-    if (__any_sync(am, bad) && lane == __ffs(am) - 1) atomicOr(bad_words, 1u);
-    return;
-  }
+  if (tid >= nb) return;
   const long long w = tid >> 5;
   const int j = (int)(w % ns), r = (int)((w / ns) * 32 + lane);
   if (r >= d.n) return;
