@@ -647,7 +647,7 @@ void configure_dp(wmpc_ctx* ctx) {
   const int nw = lanes * ((nchain + cpw - 1) / cpw);
   const int wpc = std::min(DP_MAXT / 32, std::max(1, (nw + sms - 1) / sms));
   const int grid = (nw + wpc - 1) / wpc;
-  if (segm > 0 && grid > sms) return;  // the upper warps wait for the lower ones: one resident wave
+  if (segm > 0 && grid > sms) return;  // segments pay in one resident wave only (not reached: few chains)
   const size_t sm = dp_smem<double>(wpc, nt, nu, lx, kstar, segm > 0);
   if (sm > 227 * 1024) return;
   dp_attr(ctx, sm);
@@ -697,7 +697,7 @@ void configure_dp(wmpc_ctx* ctx) {
   if (segm > 0) {
     dalloc(ctx, &ctx->dp_aggu, aw);
     dalloc(ctx, &ctx->dp_corr, (size_t)nchain * 2 * nu);
-    dalloc(ctx, &ctx->dp_segx, (size_t)nchain * (lx + nu));
+    dalloc(ctx, &ctx->dp_segx, (size_t)nchain * DP_SXW(nu, lx));
     dalloc(ctx, &ctx->dp_auxs, (size_t)nchain * 4);
     CK(cudaMalloc(&ctx->dp_flag, sizeof(int) * nchain));
     CK(cudaMemset(ctx->dp_flag, 0, sizeof(int) * nchain));

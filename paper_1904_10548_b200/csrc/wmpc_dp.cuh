@@ -81,8 +81,8 @@ struct DpArgs {
   int seg_m;
   void* aggu;   // nchain x (3 nu + lx): [LS_U | LW_U | SUT_U | SG_U] (upper segment; LW weights seg_m - t)
   void* corr;   // nchain x 2 nu: [c0 | c1]
-  void* segx;   // nchain x (lx + nu): the lower segment's [sum yx | sum a]
-  int* flag;    // nchain: iteration + 1 once segx holds that iteration's totals
+  void* segx;   // nchain x DP_SXW: [lower: sum yx | sum a] [upper: sum yx | sum a | LS base | LW base]
+  int* flag;    // nchain arrival counters (0 -> 1 -> 0 each iteration: the second warp corrects)
   const void* auxs;  // nchain x 4: sums over upper rows of aux, n aux, (m - t) aux, (m - t) n aux
   int sib;           // 1: a warp's chains hold every chain of their stage-(kstar-1) parents, whose
                      // up pass (k_branch_grp's first stage group) the warp runs after its last child
@@ -112,6 +112,7 @@ __host__ __device__ constexpr DpStage dp_stage_layout(int nt, int nu, int lx) {
 constexpr int DP_SD2 = 72;  // second tank-slot norm buffer (bank offset 16 from the first)
 constexpr int DP_SD2W = 144;
 __host__ __device__ inline int dp_agg_w(int nu, int lx) { return 3 * nu + lx; }
+__host__ __device__ constexpr int DP_SXW(int nu, int lx) { return 2 * lx + 4 * nu; }
 // Per-CTA pointer block of k_chain_dp in shared memory: under register
 // pressure the compiler re-reads these from shared memory (short latency)
 // instead of re-loading the bound node-state pointers from global memory.
@@ -137,14 +138,6 @@ __host__ __device__ inline size_t dp_smem(int wpc, int nt, int nu, int lx, int k
          sizeof(double) * (size_t)wpc * (size_t)dp_pro_w(kstar, nu, lx, seg);
 }
 
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 template <typename TG>
 __device__ __forceinline__ typename V2T<TG>::T ld2s(const TG* p) {  // aligned pair (shared or global)
   return *reinterpret_cast<const typename V2T<TG>::T*>(p);
@@ -797,91 +790,132 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         st2(a + NU + 64 + l2, LWn[2], LWn[3]);
       }
     }
-    if (next && seg == 1) {  // lower segment: its totals to the upper warp, its L aggregates
-      TG* sx = reinterpret_cast<TG*>(A.segx) + (size_t)ci * (LX + NU);
-      if (okx2) st2(sx + l2, wbr[0], wbr[1]);
-      else sx[l2] = wbr[0];
-      st2(sx + LX + l2, acc[0], acc[1]);
-      if (ok1) st2(sx + LX + 64 + l2, acc[2], acc[3]);
-      TG* a = Q.agg + (size_t)ci * AW;
-      st2(a + l2, LSn[0], LSn[1]);
-      st2(a + NU + l2, LWn[0], LWn[1]);
-      if (ok1) {
-        st2(a + 64 + l2, LSn[2], LSn[3]);
-        st2(a + NU + 64 + l2, LWn[2], LWn[3]);
-      }
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) st_release_gpu(A.flag + ci, it + 1);
-    }
-    if (next && seg == 0) {  // upper segment: wait for the lower one, then the corrections
-      const int* fl = A.flag + ci;
-      for (long long k = 0; ld_acquire_gpu(fl) < it + 1; ++k) {
-        __nanosleep(128);
-        if (k > (1ll << 24)) {  // never expected (both warps are resident): fail loudly, not hang
-          if (lane == 0) atomicMin(d.bad_nu, it);
-          break;
+    if (next && seg >= 0) {  // segmented: the second warp of the pair to finish applies the lower totals
+                             // to the upper rows (no waiting: any order). A warp that finds its partner
+                             // done (counter 1 -> 0) needs no record of its own; otherwise it publishes
+                             // its totals (fenced) and arrives (0 -> 1, or 1 -> 0 if the partner came
+                             // in between: then it is the second after all).
+      TG* sx = reinterpret_cast<TG*>(A.segx) + (size_t)ci * DP_SXW(NU, LX);
+      TG* own = sx + (seg == 1 ? 0 : LX + NU);  // [lower: wbar | a] [upper: wbar | a | LS base | LW base]
+      if (seg == 1) {  // the lower segment's L rows are final: its aggregates in any case
+        TG* ag = Q.agg + (size_t)ci * AW;
+        st2(ag + l2, LSn[0], LSn[1]);
+        st2(ag + NU + l2, LWn[0], LWn[1]);
+        if (ok1) {
+          st2(ag + 64 + l2, LSn[2], LSn[3]);
+          st2(ag + NU + 64 + l2, LWn[2], LWn[3]);
         }
       }
-      __syncwarp();
-      const TG* sx = reinterpret_cast<const TG*>(A.segx) + (size_t)ci * (LX + NU);
-      const auto wd = ld2cg(sx + l2), d0 = ld2cg(sx + LX + l2), d1 = ld2cg(sx + LX + o1);
-      const TG WBd[2] = {wd.x, okx2 ? wd.y : TG(0)};
-      const TG AD[4] = {d0.x, d0.y, ok1 ? d1.x : TG(0), ok1 ? d1.y : TG(0)};
-      st2(wb + l2, WBd[0], WBd[1]);  // every lane is past the last row's reads (the wait's syncwarp)
-      __syncwarp();
-      TG c[4];
+      unsigned* cnt = reinterpret_cast<unsigned*>(A.flag) + ci;
+      unsigned second = 0u;
+      if (lane == 0) second = atomicCAS(cnt, 1u, 0u) == 1u;
+      second = __shfl_sync(0xffffffffu, second, 0);
+      if (!second) {
+        if (okx2) st2(own + l2, wbr[0], wbr[1]);
+        else own[l2] = wbr[0];
+        st2(own + LX + l2, acc[0], acc[1]);
+        if (ok1) st2(own + LX + 64 + l2, acc[2], acc[3]);
+        if (seg == 0) {
+          TG* ag = own + LX + NU;
+          st2(ag + l2, LSn[0], LSn[1]);
+          st2(ag + NU + l2, LWn[0], LWn[1]);
+          if (ok1) {
+            st2(ag + 64 + l2, LSn[2], LSn[3]);
+            st2(ag + NU + 64 + l2, LWn[2], LWn[3]);
+          }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) second = atomicInc(cnt, 1u) == 1u;  // 0 -> 1 (first), 1 -> 0 (second)
+        second = __shfl_sync(0xffffffffu, second, 0);
+      }
+      __syncwarp();  // every lane is past the last row's reads of the exchange vectors
+      if (second) {
+        __threadfence();
+        const TG* lo = sx;
+        const TG* up = sx + LX + NU;
+        auto pair4 = [&](const TG* v, TG (&o)[4]) {
+          const auto p0 = ld2cg(v + l2), p1 = ld2cg(v + o1);
+          o[0] = p0.x; o[1] = p0.y; o[2] = ok1 ? p1.x : TG(0); o[3] = ok1 ? p1.y : TG(0);
+        };
+        // this warp's own totals from registers, the other segment's from its record (the same bits)
+        TG WBd[2], WBu[2], AD[4], AU[4], LSb[4], LWb[4];
+        if (seg == 1) {
+          const auto wu = ld2cg(up + l2);
+          WBu[0] = wu.x; WBu[1] = okx2 ? wu.y : TG(0);
+          pair4(up + LX, AU);
+          pair4(up + LX + NU, LSb);
+          pair4(up + LX + 2 * NU, LWb);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) c[q] = G_bc(q);  // c = B' WB_D
-      st2(zb + l2, c[0], c[1]);
-      st2(zb + 64 + l2, c[2], c[3]);
-      st2(zb2 + l2, AD[0], AD[1]);
-      st2(zb2 + 64 + l2, AD[2], AD[3]);
-      __syncwarp();
-      {
-        TG k1, k2;
-        dp_gather2<TG>(ops, 12, 4, ZB_OFF, ZB2_OFF, k1, k2);
-        tb[lane] = k1;
-        tb2[lane] = k2;
-      }
-      __syncwarp();
-      TG c0[4], c1[4];
+          for (int q = 0; q < 4; ++q) AD[q] = acc[q];
+          WBd[0] = wbr[0]; WBd[1] = okx2 ? wbr[1] : TG(0);
+        } else {
+          const auto wd = ld2cg(lo + l2);
+          WBd[0] = wd.x; WBd[1] = okx2 ? wd.y : TG(0);
+          pair4(lo + LX, AD);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        TG e1, e2;
-        dp_gather2<TG>(ops, 8 + q, 1, TB_OFF, TB2_OFF, e1, e2);
-        c1[q] = c[q] - e1;             // P c
-        c0[q] = c[q] + (AD[q] - e2);   // c + P A_D
-      }
-      TG* cr = reinterpret_cast<TG*>(A.corr) + (size_t)ci * 2 * NU;
-      st2(cr + l2, c0[0], c0[1]);
-      st2(cr + NU + l2, c1[0], c1[1]);
-      if (ok1) {
-        st2(cr + 64 + l2, c0[2], c0[3]);
-        st2(cr + NU + 64 + l2, c1[2], c1[3]);
-      }
-      const TG* as = reinterpret_cast<const TG*>(A.auxs) + (size_t)ci * 4;
-      const TG A0 = as[0], A1 = as[1], A2 = as[2], A3 = as[3];
-      const TG mm = (TG)A.seg_m;
-      TG* au = reinterpret_cast<TG*>(A.aggu) + (size_t)ci * AW;
-      TG LSu[4], LWu[4], At[4];
+          for (int q = 0; q < 4; ++q) {
+            AU[q] = acc[q];
+            LSb[q] = LSn[q];
+            LWb[q] = LWn[q];
+          }
+          WBu[0] = wbr[0]; WBu[1] = okx2 ? wbr[1] : TG(0);
+        }
+        st2(wb + l2, WBd[0], WBd[1]);
+        __syncwarp();
+        TG c[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        LSu[q] = LSn[q] + (A0 * c0[q] + A1 * c1[q]);
-        LWu[q] = LWn[q] + (A2 * c0[q] + A3 * c1[q]);
-        At[q] = fma(mm, c[q], acc[q]) + AD[q];
+        for (int q = 0; q < 4; ++q) c[q] = G_bc(q);  // c = B' WB_D
+        st2(zb + l2, c[0], c[1]);
+        st2(zb + 64 + l2, c[2], c[3]);
+        st2(zb2 + l2, AD[0], AD[1]);
+        st2(zb2 + 64 + l2, AD[2], AD[3]);
+        __syncwarp();
+        {
+          TG k1, k2;
+          dp_gather2<TG>(ops, 12, 4, ZB_OFF, ZB2_OFF, k1, k2);
+          tb[lane] = k1;
+          tb2[lane] = k2;
+        }
+        __syncwarp();
+        TG c0[4], c1[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          TG e1, e2;
+          dp_gather2<TG>(ops, 8 + q, 1, TB_OFF, TB2_OFF, e1, e2);
+          c1[q] = c[q] - e1;             // P c
+          c0[q] = c[q] + (AD[q] - e2);   // c + P A_D
+        }
+        TG* cr = reinterpret_cast<TG*>(A.corr) + (size_t)ci * 2 * NU;
+        st2(cr + l2, c0[0], c0[1]);
+        st2(cr + NU + l2, c1[0], c1[1]);
+        if (ok1) {
+          st2(cr + 64 + l2, c0[2], c0[3]);
+          st2(cr + NU + 64 + l2, c1[2], c1[3]);
+        }
+        const TG* as = reinterpret_cast<const TG*>(A.auxs) + (size_t)ci * 4;
+        const TG A0 = as[0], A1 = as[1], A2 = as[2], A3 = as[3];
+        const TG mm = (TG)A.seg_m;
+        TG* au = reinterpret_cast<TG*>(A.aggu) + (size_t)ci * AW;
+        TG LSu[4], LWu[4], At[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          LSu[q] = LSb[q] + (A0 * c0[q] + A1 * c1[q]);
+          LWu[q] = LWb[q] + (A2 * c0[q] + A3 * c1[q]);
+          At[q] = fma(mm, c[q], AU[q]) + AD[q];
+        }
+        st2(au + l2, LSu[0], LSu[1]);
+        st2(au + NU + l2, LWu[0], LWu[1]);
+        if (ok1) {
+          st2(au + 64 + l2, LSu[2], LSu[3]);
+          st2(au + NU + 64 + l2, LWu[2], LWu[3]);
+        }
+        const TG Wt[2] = {WBu[0] + WBd[0], WBu[1] + WBd[1]};
+        if (okx2) st2(Q.wbar + (size_t)r_top * LX + l2, Wt[0], Wt[1]);
+        else Q.wbar[(size_t)r_top * LX + l2] = Wt[0];
+        st2(Q.Asub + (size_t)r_top * NU + l2, At[0], At[1]);
+        if (ok1) st2(Q.Asub + (size_t)r_top * NU + 64 + l2, At[2], At[3]);
       }
-      st2(au + l2, LSu[0], LSu[1]);
-      st2(au + NU + l2, LWu[0], LWu[1]);
-      if (ok1) {
-        st2(au + 64 + l2, LSu[2], LSu[3]);
-        st2(au + NU + 64 + l2, LWu[2], LWu[3]);
-      }
-      const TG Wt[2] = {wbr[0] + WBd[0], wbr[1] + WBd[1]};
-      if (okx2) st2(Q.wbar + (size_t)r_top * LX + l2, Wt[0], Wt[1]);
-      else Q.wbar[(size_t)r_top * LX + l2] = Wt[0];
-      st2(Q.Asub + (size_t)r_top * NU + l2, At[0], At[1]);
-      if (ok1) st2(Q.Asub + (size_t)r_top * NU + 64 + l2, At[2], At[3]);
     }
     if (A.sib && next) {  // after the parent's last chain: its up pass (k_branch_grp arithmetic, R-free,
                           // no branching descendants: W2 = 0), from its own Yc and the chains' totals
