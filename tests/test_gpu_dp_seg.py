@@ -1,11 +1,11 @@
 """k_chain_dp with segmented chains (DpArgs.seg_m, csrc/wmpc_dp.cuh): two warps
 per chain walk the upper and lower rows at the same time; the upper warp
 stores its rows' L without the lower segment's contribution and applies the
-per-chain correction L_t = base_t + aux_t (c0 + n_t c1) once the lower warp
-has published its totals. Same quantities as the reference recursion
+per-chain correction L_t = base_t + aux_t (c0 + n_t c1), written by whichever
+warp of the pair finishes second (a per-chain counter, no waiting). Same quantities as the reference recursion
 (solver.py:242-290) in real arithmetic, different rounding: 1e-10 against
 the graph iteration, 1e-8 against the oracle; bit-identical under
-reordering of the warps' handshake (PDL on/off, repeated runs)."""
+reordering of the pair's completion (PDL on/off, repeated runs)."""
 
 from __future__ import annotations
 
@@ -94,7 +94,7 @@ def _state(ctx, inst, iters, chunks, cert):
 
 def test_segmented_certificates_between_chunks(monkeypatch):
     """The certificate between chunks leaves the carried state (base rows,
-    corrections, aggregates, handshake flags) intact: bit-identical."""
+    corrections, aggregates, pair counters) intact: bit-identical."""
     inst = config_instance("C2")
     ca, cb = _cache(inst, monkeypatch, "seg"), _cache(inst, monkeypatch, "seg")  # held: they own the contexts
     a = _state(ca._bind(), inst, 200, 8, False)
@@ -104,9 +104,9 @@ def test_segmented_certificates_between_chunks(monkeypatch):
 
 
 def test_segmented_handshake_is_deterministic(monkeypatch):
-    """The upper warp waits for the lower one through a flag: the arithmetic
-    never depends on who arrives first, with or without programmatic
-    dependent launch."""
+    """Either warp of a pair may apply the correction (whichever finishes
+    second): the arithmetic never depends on which, with or without
+    programmatic dependent launch."""
     inst = config_instance("C3")
     outs = []
     for pdl in (1, 1, 0):
