@@ -459,6 +459,14 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     issue();
   };
 #pragma unroll
+  if constexpr (SDG) {  // zero padding of the L / ut regions (the copies fill [0, NU) only)
+    static_assert(oB - oL >= 128 && oG - oB >= 128, "128-wide L / ut regions");
+    constexpr int PADN = 128 - NU;
+    for (int i = lane; i < DP_D * 2 * PADN; i += 32) {
+      const int stg = i / (2 * PADN), w = (i / PADN) & 1, j = i % PADN;
+      ring[stg * STG + (w ? oB : oL) + NU + j] = 0.0;
+    }
+  }
   for (int k = 0; k < DP_D; ++k) issue();
   // ---- operator products through the exchange vectors
   auto proj_neg = [&](const TG (&v)[4], const TG (&base)[4], TG (&out)[4]) {  // out = base + P(-v)
@@ -500,7 +508,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const double xv = (double)x[h];
-        xan[h] = it == 0 ? xv : dadd(dmul(xa[h], om), dmul(theta, xv));
+        xan[h] = dadd(dmul(xa[h], om), dmul(theta, xv));  // iteration 0: Xa = 0, om = 0, theta = 1
         const double gx = dmul(gamma, xv);
         v1[h] = dadd(dadd(y1[h], dmul(beta, dsub(y1[h], m1[h]))), gx);
         v2[h] = dadd(dadd(y2[h], dmul(beta, dsub(y2[h], m2[h]))), gx);
@@ -540,7 +548,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
         for (int h = 0; h < 2; ++h) {
           const int q = 2 * hq + h;
           const double uq = (double)u[q];
-          uan[q] = it == 0 ? uq : dadd(dmul(ua[h], om), dmul(theta, uq));
+          uan[q] = dadd(dmul(ua[h], om), dmul(theta, uq));  // iteration 0: Ua = 0, om = 0, theta = 1
           const double v3 = dadd(dadd(y3[h], dmul(beta, dsub(y3[h], m3[h]))), dmul(gamma, uq));
           const double V3 = div_by(v3, gamma, ig);
           p3[q] = dsub(v3, dmul(gamma, np_clip_u(V3, l3[h], h3[h])));
@@ -723,10 +731,11 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       TG L[4], b[4], g[2], ax, u[4], yx[2], yu[4];
       const double* st = take();
       {
-        const double2 a0 = ld2s(st + oL + l2), a1 = ld2s(st + oL + o1), b0 = ld2s(st + oB + l2),
-                      b1 = ld2s(st + oB + o1), g0 = ld2s(st + oG + l2);
-        L[0] = a0.x; L[1] = a0.y; L[2] = ok1 ? a1.x : 0.0; L[3] = ok1 ? a1.y : 0.0;
-        b[0] = b0.x; b[1] = b0.y; b[2] = ok1 ? b1.x : 0.0; b[3] = ok1 ? b1.y : 0.0;
+        // the L / ut regions are 128 wide with zero padding past NU: no masks
+        const double2 a0 = ld2s(st + oL + l2), a1 = ld2s(st + oL + 64 + l2), b0 = ld2s(st + oB + l2),
+                      b1 = ld2s(st + oB + 64 + l2), g0 = ld2s(st + oG + l2);
+        L[0] = a0.x; L[1] = a0.y; L[2] = a1.x; L[3] = a1.y;
+        b[0] = b0.x; b[1] = b0.y; b[2] = b1.x; b[3] = b1.y;
         g[0] = g0.x; g[1] = okx2 ? g0.y : 0.0;
         ax = st[oAx];
         if (seg == 0) {  // upper segment: L_t = base_t + aux_t (c0 + n_t c1) (previous iteration's correction)
