@@ -1110,7 +1110,6 @@ int graphk_kernels(const wmpc_ctx* ctx) {
 // One APG iteration of the graph-of-kernels path, enqueued on ctx->stream.
 void enqueue_graphk_iteration(wmpc_ctx* ctx, const FastView& f) {
   cudaStream_t st = ctx->stream;
-  const int nc = ctx->nchain;
   if (ctx->gk_groups.empty()) k_advance<<<1, 32, 0, st>>>(ctx->iter);  // else the first group kernel counts
   if (dp_on(ctx)) {  // branch groups (the first reads Yc the previous k_chain_dp wrote) + k_chain_dp
     gk_grp<4, double>(ctx, f, 1, GRP_LATE, ctx->dp_sib);

@@ -523,11 +523,6 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       double* xap = Q.Xa + (size_t)r * LX + l2;
       if (okx2) st2(xap, xan[0], xan[1]);
       else xap[0] = xan[0];
-      if (Q.store) {
-        TG* Xp = Q.X + (size_t)r * LX + l2;
-        if (okx2) st2(Xp, x[0], x[1]);
-        else Xp[0] = x[0];
-      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const double df1 = dsub(V1[h], c1[h]), df2 = dsub(V2[h], c2[h]);
@@ -558,15 +553,20 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       st2(Q.Ua + (size_t)r * NU + l2, uan[0], uan[1]);
       st2(yn + 2 * NT + l2, p3[0], p3[1]);
       badacc = fma(p3[0], 0.0, fma(p3[1], 0.0, badacc));
-      if (Q.store) st2(Q.U + (size_t)r * NU + l2, u[0], u[1]);
       if (ok1) {
         st2(Q.Ua + (size_t)r * NU + 64 + l2, uan[2], uan[3]);
         st2(yn + 2 * NT + 64 + l2, p3[2], p3[3]);
         badacc = fma(p3[2], 0.0, fma(p3[3], 0.0, badacc));
-        if (Q.store) st2(Q.U + (size_t)r * NU + 64 + l2, u[2], u[3]);
       } else {
         yu[2] = yu[3] = TG(0);
       }
+    }
+    if (Q.store) {  // the chunk's last iteration: U, X of the row reach HBM (one uniform branch)
+      TG* Xp = Q.X + (size_t)r * LX + l2;
+      if (okx2) st2(Xp, x[0], x[1]);
+      else Xp[0] = x[0];
+      st2(Q.U + (size_t)r * NU + l2, u[0], u[1]);
+      if (ok1) st2(Q.U + (size_t)r * NU + 64 + l2, u[2], u[3]);
     }
     st2(ub + l2, u[0], u[1]);
     st2(ub + 64 + l2, u[2], u[3]);
@@ -727,7 +727,6 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
     TG wbr[2] = {0, 0}, acc[4] = {0, 0, 0, 0}, LSn[4] = {0, 0, 0, 0}, LWn[4] = {0, 0, 0, 0};
     for (int t = t_hi - 1; t >= t_lo; --t) {
       const unsigned r = nbr + (unsigned)t * nchain + (unsigned)ci;
-      const bool bottom = t == t_hi - 1;
       TG L[4], b[4], g[2], ax, u[4], yx[2], yu[4];
       const double* st = take();
       {
@@ -763,16 +762,18 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
       }
       if (!next) continue;
       // up pass of the next iteration (k_chain_up_r arithmetic, R-free)
-      wbr[0] = bottom ? yx[0] : yx[0] + wbr[0];
-      wbr[1] = bottom ? yx[1] : yx[1] + wbr[1];
+      // wbr, acc start at zero and pS = P 0 = 0 at the bottom row: the sums need no
+      // bottom-row case (up to the sign of an exact zero)
+      wbr[0] = yx[0] + wbr[0];
+      wbr[1] = yx[1] + wbr[1];
       st2(wb + l2, wbr[0], wbr[1]);
       __syncwarp();
       TG a[4], l[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         a[q] = yu[q] + G_bc(q);
-        acc[q] = bottom ? a[q] : a[q] + acc[q];
-        l[q] = bottom ? a[q] : a[q] + pS[q];
+        acc[q] = a[q] + acc[q];
+        l[q] = a[q] + pS[q];
       }
       const TG wt = (TG)(t_hi - t);  // LW weight from the warp's bottom row
       TG Ln[4];
