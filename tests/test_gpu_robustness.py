@@ -68,3 +68,24 @@ def test_coupled_mixing_nodes_vs_oracle():
     info = nat.path_info(cache._bind())
     assert info["fast_path"] != 300, info  # wide K rows: not the ELL graph path
     _vs_oracle(inst, cache, it=60)
+
+
+@pytest.mark.parametrize("seed", [3, 4, 5])
+@pytest.mark.parametrize("mode", ["dp", "dp-segmented"])
+def test_random_trees_dp_modes_vs_graph(seed, mode, monkeypatch):
+    """Random non-uniform trees (1..5 children over 4 branching stages, ragged
+    chain counts per parent) through the forced k_chain_dp modes against the
+    graph iteration: 100 iterations, 1e-10."""
+    inst = fan_like_instance(seed=seed, leaves_target=150, branching_stages=4, max_children=5, horizon=14)
+    out = []
+    for env in ({"WMPC_DP": "1", "WMPC_DP_SEG": "1" if mode == "dp-segmented" else "0"}, {"WMPC_DP": "0"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        cache = S._factor(inst, None, private=True)
+        info = nat.path_info(cache._bind())
+        if env["WMPC_DP"] == "1":
+            assert info["fused_dp"] == 1 and (info["dp_segm"] > 0) == (mode == "dp-segmented"), info
+        out.append(solve(inst, SolverConfig(max_iter=100, tol=1e-30, gamma=1 / 3e9, gap_check_every=101),
+                         cache=cache))
+    for k in ("u0", "primal", "primal_avg", "dual"):
+        assert rel_err(getattr(out[0], k), getattr(out[1], k)) <= 1e-10, k
