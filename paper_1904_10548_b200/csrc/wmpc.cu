@@ -106,7 +106,7 @@ struct wmpc_ctx {
   double* xbuf = nullptr;                      // exchange buffer (caller-owned device memory)
   int n_rep_global = 0, shard_k = -1, kstar_min = 0;
   ncclComm_t nccl = nullptr;                   // subtree sharding: exchange inside the iteration graph
-  size_t sm_up = 0, sm_grp = 0, sm_down = 0, sm_prox = 0;
+  size_t sm_up = 0, sm_grp = 0, sm_grp128 = 0, sm_down = 0, sm_prox = 0;
   int up_threads = 512, down_threads = 512, prox_warp = 1;
   int fp32 = 0;                                 // SolverConfig.precision == "fp32"
   int pdl = 1;                                  // programmatic dependent launch between graph kernels
@@ -432,6 +432,7 @@ void gk_attrs_t(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
   CK(cudaFuncSetAttribute(k_chain_up<WE, TG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)up));
   CK(cudaFuncSetAttribute(k_chain_down<WE, TG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)down));
   CK(cudaFuncSetAttribute(k_branch_grp<WE, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grp));
+  CK(cudaFuncSetAttribute(k_branch_grp<WE, TG, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grp));
 }
 template <int WE>
 void gk_attrs(wmpc_ctx* ctx, size_t up, size_t down, size_t grp) {
@@ -476,14 +477,19 @@ void gk_up(wmpc_ctx* ctx, const FastView& f) {
   else
     launch_pdl(ctx, k_chain_up<WE, TG, false>, dim3(ctx->nchain), dim3(ctx->up_threads), ctx->sm_up, f);
 }
+bool dp_on(const wmpc_ctx* ctx);
 // stage groups [g0, g1) of gk_groups (g1 < 0: to the end)
 template <int WE, typename TG = double>
 void gk_grp(wmpc_ctx* ctx, const FastView& f, int bump, int first_flags = 0, int g0 = 0, int g1 = -1) {
   const int ng = (int)ctx->gk_groups.size();
   for (int gi = g0; gi < (g1 < 0 ? ng : std::min(g1, ng)); ++gi) {
     const auto& g = ctx->gk_groups[gi];
-    launch_pdl(ctx, k_branch_grp<WE, TG>, dim3(g.second), dim3(GRP_THREADS), ctx->sm_grp, f, g.first, bump,
-               (int)GRP_FULL | first_flags);
+    if (dp_on(ctx))  // 4-warp CTAs next to k_chain_dp
+      launch_pdl(ctx, k_branch_grp<WE, TG, 128>, dim3(g.second), dim3(128), ctx->sm_grp128, f, g.first, bump,
+                 (int)GRP_FULL | first_flags);
+    else
+      launch_pdl(ctx, k_branch_grp<WE, TG>, dim3(g.second), dim3(GRP_THREADS), ctx->sm_grp, f, g.first, bump,
+                 (int)GRP_FULL | first_flags);
     bump = 0;
     first_flags = 0;
   }
@@ -778,6 +784,7 @@ void configure_graphk(wmpc_ctx* ctx, const std::vector<int>& cptr, const std::ve
   const size_t cap = 227 * 1024;
   const size_t up = sizeof(double) * (size_t)nst * (ly + nu + 2 + FAST_MAXNS);
   const size_t grp = sizeof(double) * ((size_t)(GRP_THREADS / 32) * 256 + 2 * lx + 2 * nu + FAST_MAXNS);
+  ctx->sm_grp128 = sizeof(double) * ((size_t)(128 / 32) * 256 + 2 * lx + 2 * nu + FAST_MAXNS);
   const size_t down = sizeof(double) * (size_t)H * (2 * nu + lx + FAST_MAXNS) + sizeof(int) * ((H + 3) & ~3);
   const size_t prox = sizeof(double) * ((size_t)SC_NPB * (ctx->fast_rec + nu + lx + 2) + 3 * nt + 2 * nu) +
                       sizeof(int) * SC_NPB + 16;

@@ -320,12 +320,14 @@ __global__ void __launch_bounds__(512, OCC ? 3 : 1) k_chain_up(FastView f) {
 // immediate predecessor (k_chain_dp runs the branching rows' prox), so every
 // Yc load waits for it.
 enum { GRP_FULL = 0, GRP_PARTIAL = 1, GRP_FINISH = 2, GRP_LATE = 4 };
-template <int WE, typename TG>
-__global__ void __launch_bounds__(GRP_THREADS) k_branch_grp(FastView f, int r0, int bump, int mode) {
+// GT: threads per CTA (>= 128, one per u element); 128 on the k_chain_dp paths (measured: C3 41.6 -> 40.3 us),
+// 256 on the graph path (C2 19.4 vs 20.4 with 128)
+template <int WE, typename TG, int GT = GRP_THREADS>
+__global__ void __launch_bounds__(GT) k_branch_grp(FastView f, int r0, int bump, int mode) {
   const DevView& d = f.d;
   const int nt = d.nt, nu = d.nu, lx = d.lx, ly = d.ly;
   const int r = r0 + blockIdx.x;
-  constexpr int NW = GRP_THREADS / 32;
+  constexpr int NW = GT / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   TG* part = reinterpret_cast<TG*>(smem_raw);  // NW x 256: [s1 64 | s2 64 | su 128]
   TG* W1 = part + NW * 256;  // lx
