@@ -74,10 +74,10 @@ struct DpArgs {
   // upper segment (rows [0, seg_m), warp 2p) and a lower one ([seg_m, N),
   // warp 2p + 1) walked at the same time. The lower segment's L rows are
   // final; the upper segment stores its rows' L without the lower segment's
-  // contribution (base) and, once the lower warp has published its totals,
+  // contribution (base). Whichever warp of the pair finishes second writes
   // the per-chain correction L_t = base_t + aux_t (c0 + n_t c1), n_t = seg_m - 1 - t
-  // (applied where the rows are read next iteration), its corrected
-  // aggregates and the chain-top totals.
+  // (applied where the rows are read next iteration), the upper segment's
+  // corrected aggregates and the chain-top totals.
   int seg_m;
   void* aggu;   // nchain x (3 nu + lx): [LS_U | LW_U | SUT_U | SG_U] (upper segment; LW weights seg_m - t)
   void* corr;   // nchain x 2 nu: [c0 | c1]
