@@ -734,7 +734,7 @@ __global__ void __maxnreg__(DP_MAXREG) k_chain_dp(FastView f, DpArgs A) {
                       b1 = ld2s(st + oB + 64 + l2), g0 = ld2s(st + oG + l2);
         L[0] = a0.x; L[1] = a0.y; L[2] = a1.x; L[3] = a1.y;
         b[0] = b0.x; b[1] = b0.y; b[2] = b1.x; b[3] = b1.y;
-        g[0] = g0.x; g[1] = okx2 ? g0.y : 0.0;
+        g[0] = g0.x; g[1] = g0.y;  // (the padding column of g is zero: k_pad_rows)
         ax = st[oAx];
         if (seg == 0) {  // upper segment: L_t = base_t + aux_t (c0 + n_t c1) (previous iteration's correction)
           const double* cb = pro + kb * NU + AW;
