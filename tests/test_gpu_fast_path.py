@@ -174,3 +174,19 @@ def test_chain_kernel_variants_bit_identical(cfg, prec, variant):
     for k in ("u0", "primal", "primal_avg", "dual"):
         np.testing.assert_array_equal(getattr(ra, k), getattr(rb, k), err_msg=k)
     assert ra.duality_gap == rb.duality_gap and ra.objective == rb.objective
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_block_dykstra_certificate_matches_general(cfg):
+    """The certificate's Dykstra restoration: one thread per (node, coupling
+    row) block on the structured path (k_dyk_block) against one warp per node
+    over the CSR operators on the general path (k_dyk_warp): the same sweep
+    count rule and per-element arithmetic, so the gap and the objective agree
+    to rounding."""
+    inst = config_instance(cfg)
+    gamma = 1.0 / 2e9
+    rf, mf = _solve(inst, 200, gamma, True)
+    rg, mg = _solve(inst, 200, gamma, False)
+    assert mf == 300 and mg == 0, (mf, mg)
+    assert abs(rf.duality_gap - rg.duality_gap) <= 1e-10 * (1 + abs(rg.duality_gap))
+    assert abs(rf.objective - rg.objective) <= 1e-12 * (1 + abs(rg.objective))

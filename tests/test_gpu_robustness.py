@@ -89,3 +89,22 @@ def test_random_trees_dp_modes_vs_graph(seed, mode, monkeypatch):
                          cache=cache))
     for k in ("u0", "primal", "primal_avg", "dual"):
         assert rel_err(getattr(out[0], k), getattr(out[1], k)) <= 1e-10, k
+
+
+def test_1024_chain_default_whole_chain_dp_vs_graph(monkeypatch):
+    """3.5-8 chains per SM: k_chain_dp with one warp per whole chain by default
+    ([4,4,4,4,2,2], 1,024 chains), against the graph iteration."""
+    inst = barcelona_instance([4, 4, 4, 4, 2, 2], seed=2)
+    out, infos = [], []
+    for env in ({}, {"WMPC_DP": "0"}):
+        for k in ("WMPC_DP", "WMPC_DP_SEG", "WMPC_DP_SEGM"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        cache = S._factor(inst, None, private=True)
+        infos.append(nat.path_info(cache._bind()))
+        out.append(solve(inst, SolverConfig(max_iter=100, tol=1e-30, gamma=1 / 3e9, gap_check_every=101),
+                         cache=cache))
+    assert infos[0]["fused_dp"] == 1 and infos[0]["dp_segm"] == 0 and infos[1]["fused_dp"] == 0, infos
+    for k in ("u0", "primal", "primal_avg", "dual"):
+        assert rel_err(getattr(out[0], k), getattr(out[1], k)) <= 1e-10, k
